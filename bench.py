@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""bench.py -- split evaluations/s (scenario x tour) of the B200 Split-DP hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl spdp|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1], DESIGN §Input recipe): "C2", an X-n101-shaped
+CVRPSD instance, n = 100 customers, one giant tour, 10^6 correlated-demand
+scenarios per GPU (weak scaling: rank r owns global scenarios
+[r 10^6, (r+1) 10^6)).  One step = one pass of the hot path over the resident
+demand set: tour prep (a2) + masked min-plus sweep with per-scenario costs
+(a5) + fused SAA partial (a6) (+ the int64 all-reduce of the partial, a7, at
+N > 1).  Timed with CUDA events on the launching stream, max over ranks.
+The demand set (200 MB/GPU) is larger than L2, so every step streams it from HBM.
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+import bench_config  # noqa: E402
+
+METRIC = "split evals/sec (scenario x tour) at n=100, S=1M per GPU"
+UNIT = "scenario-tour evals/s"
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": HBM_FALLBACK_GBS, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ALU peak for one integer add-min per Eq. (3) candidate:
+# 148 SMs x 4 SMSPs x 16 lanes/clk (ALU pipe, one VIMNMX per lane every clk/16)
+ALU_LANES_PER_SM_CLK = 64
+N_SM = 148
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def ncu_traffic(config_name: str):
+    """dram bytes per sweep launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_sweep_%s.json" % config_name)
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The reference arm of this tier: the CPU oracle (plain C, OpenMP over scenarios) on the
+    host cores, on the same workload/metric; each step is a bounded sample of it."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = synth.config_instance(args.config)
+    inst = cfg["inst"]
+    S_full = cfg["S"]
+    threads = oracle.num_threads()
+    # size the per-step sample for ~1 s of oracle work (bounded; whole run stays within minutes)
+    S_probe = 20_000
+    dem = oracle.gen_demands(cfg["model"], 0, S_probe, threads=threads)
+    t0 = time.perf_counter()
+    oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], threads=threads)
+    per = (time.perf_counter() - t0) / S_probe
+    S_ref = int(min(S_full, max(S_probe, 1.0 / max(per, 1e-9))))
+    dem = oracle.gen_demands(cfg["model"], 0, S_ref, threads=threads)
+    for _ in range(args.warmup):
+        oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        c = oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], threads=threads)
+        oracle.saa(c)
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    value = S_ref / t
+    sample = "first %d of the %d scenarios of %s per step (oracle split + SAA, demands pre-generated)" % (
+        S_ref, S_full, args.config)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": args.config, "n": cfg["n"], "S_per_step": S_ref, "Q": cfg["Q"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="spdp", choices=["spdp", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-rows", action="store_true", help="skip the per-row (C3/C4/C5/gen) measurements")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--window-hint", type=int, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2511_18022_b200 as spdp
+    from paper_2511_18022_b200 import dist as pdist
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+
+    cfg = synth.config_instance(args.config)
+    inst, n, Q = cfg["inst"], cfg["n"], cfg["Q"]
+    S_cfg = cfg["S"]
+    if args.scaling == "weak":
+        S_loc, s_begin = S_cfg, rank * S_cfg
+        S_glob = S_cfg * world
+    else:
+        s_begin, s_end = pdist.shard_range(S_cfg, rank, world)
+        S_loc, S_glob = s_end - s_begin, S_cfg
+    hint = args.window_hint if args.window_hint is not None else bench_config.HINT[args.config]
+
+    demand = spdp.gen_demands(cfg["model"], s_begin, S_loc, device=dev)
+    tour = torch.from_numpy(inst["tour"]).to(dev)
+    dist = torch.from_numpy(inst["dist"]).to(dev)
+    cost = torch.empty(S_loc, dtype=torch.int32, device=dev)
+    partial = torch.zeros(6, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        spdp.split_eval(tour, dist, demand, Q, S=S_loc, window_hint=hint, cost=cost, partial=partial)
+        if world > 1:
+            pdist.allreduce_partials(partial)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # algorithmic work: Eq. (3) candidates sum_i (i - mask(i)) from the standalone mask kernel (untimed)
+    m = spdp.split_mask(tour, demand, Q, S=S_loc)
+    idx = torch.arange(1, n + 1, device=dev, dtype=torch.int64).unsqueeze(1)
+    cand = int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item())
+    del m
+    torch.cuda.synchronize(dev)
+
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    props = torch.cuda.get_device_properties(dev)
+    try:
+        smi_id = "%08X:%02X:%02X.0" % (props.pci_domain_id, props.pci_bus_id, props.pci_device_id)
+    except AttributeError:
+        smi_id = str(local)
+    sampler = ClockSampler(smi_id)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    t_start.record(stream)
+    for k in range(args.steps):
+        spdp.set_profile_events(ev_s[k], ev_e[k])
+        step()
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    spdp.set_profile_events()
+    if world > 1:
+        tdist.barrier()
+    # keep sampling clocks under the same load for >= 1 s so the record is meaningful
+    soak_end = time.perf_counter() + 1.0
+    while time.perf_counter() < soak_end:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+
+    ms_step = t_start.elapsed_time(t_end) / args.steps
+    sweep_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev_s, ev_e))
+    if world > 1:
+        ms_step = pdist.max_over_ranks(ms_step, device=dev)
+        sweep_ms = pdist.max_over_ranks(sweep_ms, device=dev)
+    value = S_glob * 1.0 / (ms_step / 1e3)
+
+    pk = peaks()
+    bytes_alg = n * S_loc * 2 + S_loc * 4  # demand stream (u16, read once) + per-scenario costs (i32)
+    hbm_achieved = bytes_alg / (sweep_ms / 1e3) / 1e9
+    alu_peak = N_SM * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6  # candidates/s
+    alu_achieved = cand / (sweep_ms / 1e3)
+    t_hbm = bytes_alg / (pk["hbm_gbs"] * 1e9)
+    t_alu = cand / alu_peak
+    if t_hbm >= t_alu:
+        roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": hbm_achieved / pk["hbm_gbs"]}
+    else:
+        roof = {"bound": "alu", "achieved": alu_achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tcand/s",
+                "frac": alu_achieved / alu_peak}
+    roof.update({"traffic": ncu_traffic(args.config), "kernel": "split_sweep_kernel", "kernel_ms": sweep_ms,
+                 "bytes_alg_per_launch": bytes_alg, "candidates_per_launch": cand,
+                 "hbm_frac": hbm_achieved / pk["hbm_gbs"], "alu_frac": alu_achieved / alu_peak,
+                 "peak_source": pk["source"], "sweep_share_of_step": sweep_ms / ms_step})
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": "%s: X-n101-shaped CVRPSD, n=%d, Q=%d, %d correlated-demand scenarios per GPU "
+                                   "(cv=0.3, rho=0.5), 1 giant tour" % (args.config, n, Q, S_loc),
+                       "n": n, "S_per_gpu": S_loc, "S_global": S_glob, "T": 1, "window_hint": hint,
+                       "l2": "inputs larger than L2 (demand %.0f MB/GPU > 126 MB)" % (n * S_loc * 2 / 1e6),
+                       "parallelism": "scenario-sharded dp%d, 1 int64 all-reduce/step" % world},
+            "roofline": roof, "clocks": clocks, "gpu_launches": 3 * args.steps}
+
+    # ------------------------------------------------------------------ e2e through the C-ABI host entry
+    if not args.no_e2e:
+        dem_h = torch.empty(demand.shape, dtype=torch.int16, pin_memory=True)
+        dem_h.copy_(demand)
+        cost_h = torch.empty(S_loc, dtype=torch.int32, pin_memory=True)
+        tour_h, dist_h = np.ascontiguousarray(inst["tour"]), np.ascontiguousarray(inst["dist"])
+        for _ in range(2):
+            spdp.split_eval_host(tour_h, dist_h, dem_h, Q, S=S_loc, cost_h=cost_h, window_hint=hint, device=dev)
+        ke = max(3, min(args.steps, 20))
+        if world > 1:
+            tdist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            est = spdp.split_eval_host(tour_h, dist_h, dem_h, Q, S=S_loc, cost_h=cost_h, window_hint=hint,
+                                       device=dev)
+        te = (time.perf_counter() - t0) / ke
+        if world > 1:
+            te = pdist.max_over_ranks(te, device=dev)
+        line["e2e"] = {"value": S_glob / te, "unit": UNIT,
+                       "h2d_bytes_per_step": int(dem_h.numel() * 2 + tour_h.nbytes + dist_h.nbytes),
+                       "d2h_bytes_per_step": int(S_loc * 4 + 48), "ms_per_step": te * 1e3,
+                       "api": "spdp_split_eval_host (pinned host demand, costs + SAA estimate back)",
+                       "saa_mean": est["mean"]}
+
+    # ------------------------------------------------------------------ per-row measurements (rank 0, N=1)
+    if rank == 0 and world == 1 and not args.no_rows:
+        line["rows"] = measure_rows(spdp, torch, dev, pk)
+
+    # ------------------------------------------------------------------ oracle cpu_baseline (rank 0, N=1)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, cost, S_loc, spdp, partial)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
+def _time_events(fn, torch, dev, iters=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize(dev)
+    return a.elapsed_time(b) / iters
+
+
+def measure_rows(spdp, torch, dev, pk):
+    """One measurement per other hot-path row (device time, CUDA events)."""
+    rows = {}
+    # a1: scenario generation at C2 size
+    cfg2 = synth.config_instance("C2")
+    out = spdp.empty_demand(cfg2["n"], cfg2["S"], dev)
+    ms = _time_events(lambda: spdp.gen_demands(cfg2["model"], 0, cfg2["S"], device=dev, out=out), torch, dev)
+    rows["a1_gen_C2"] = {"ms": ms, "demands_per_s": cfg2["n"] * cfg2["S"] / (ms / 1e3),
+                         "write_GBps": cfg2["n"] * cfg2["S"] * 2 / (ms / 1e3) / 1e9}
+    del out
+    # a8: batched tours (C3) and a5 at n=1000 (C4, 1 GPU)
+    for name in ("C3", "C4"):
+        cfg = synth.config_instance(name)
+        inst = cfg["inst"]
+        d = spdp.gen_demands(cfg["model"], 0, cfg["S"], device=dev)
+        tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
+        dist = torch.from_numpy(inst["dist"]).to(dev)
+        part = torch.zeros((cfg["T"], 6), dtype=torch.int64, device=dev)
+        h = bench_config.HINT[name]
+        fn = lambda: spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, partial=part,
+                                           window_hint=h)
+        ms = _time_events(fn, torch, dev, iters=3)
+        m = spdp.split_mask(tours[0].contiguous(), d, inst["Q"], S=cfg["S"])
+        idx = torch.arange(1, cfg["n"] + 1, device=dev, dtype=torch.int64).unsqueeze(1)
+        cand0 = int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item())
+        del m
+        alu_peak = N_SM * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6
+        cand = cand0 * cfg["T"]  # tours differ by a few moves: window statistics ~ tour 0
+        rows["a8_batch_%s" % name if cfg["T"] > 1 else "a5_%s" % name] = {
+            "ms": ms, "evals_per_s": cfg["T"] * cfg["S"] / (ms / 1e3), "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
+            "candidates_est": cand, "alu_frac_est": cand / (ms / 1e3) / alu_peak}
+        del d
+    # a9/a10: IRP (C5)
+    c5 = synth.irp_config()
+    irp = c5["irp"]
+    d = spdp.gen_demands(c5["model"], 0, c5["S"], device=dev)
+    costb = torch.empty(c5["S"], dtype=torch.int64, device=dev)
+    fn = lambda: spdp.irp_dp(irp["visit"], irp["cust"], d, irp["H"], irp["M"], S=c5["S"], cost=costb)
+    ms = _time_events(fn, torch, dev, iters=3)
+    rows["a9_a10_irp_C5"] = {"ms": ms, "scenarios_per_s": c5["S"] / (ms / 1e3),
+                             "states_per_s": c5["S"] * irp["M"] * irp["H"] * 101 / (ms / 1e3)}
+    return rows
+
+
+def cpu_baseline(cfg, cost_dev, S, spdp, partial_dev):
+    import oracle
+    inst = cfg["inst"]
+    threads = oracle.num_threads()
+    dem = oracle.gen_demands(cfg["model"], 0, S, threads=threads)
+    t0 = time.perf_counter()
+    want = oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], threads=threads)
+    w = oracle.saa(want)
+    t = time.perf_counter() - t0
+    got = cost_dev.cpu().numpy().astype(np.int64)
+    parity = bool(np.array_equal(got, want))
+    est = spdp.saa_mean(partial_dev)
+    return {"value": S / t, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": "all %d scenarios of the timed workload, once (oracle split + SAA; demands pre-generated "
+                      "by the oracle's own generator)" % S,
+            "seconds": t, "parity_all_costs_bit_exact": parity, "saa_mean_equal": est["mean"] == w["mean"]}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

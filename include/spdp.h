@@ -1,0 +1,216 @@
+/*
+ * spdp.h -- C-ABI of the B200-native scenario-parallel Split DP library
+ * (libspdp.so), the hot path of arXiv 2511.18022:
+ *   second-stage evaluation of a first-stage giant tour over up to millions of
+ *   demand scenarios (§2), by the masked Split DP of Eq. (1)-(3)
+ *   (§3), reduced to the sample-average-approximation (SAA)
+ *   statistics of the expected recourse cost.
+ *
+ * Citations: PAPER:n = line n of the paper text; SPEC:n = line n of the
+ * companion spec; SURVEY §x = /root/repo/SURVEY.md; DESIGN Rk = reading k in
+ * DESIGN.md.
+ *
+ * Conventions (all entry points)
+ *  - Plain C types only.  Array arguments are caller-owned DEVICE pointers
+ *    unless the name ends in _h (host pointer).  The library never allocates
+ *    or frees caller memory; scratch comes from the caller's workspace `ws`
+ *    (size from spdp_workspace_bytes), which must not be used concurrently by
+ *    two calls.
+ *  - All device work is enqueued asynchronously on `stream` (a cudaStream_t;
+ *    NULL = legacy default stream).  Exceptions: spdp_saa_mean (host only),
+ *    spdp_split_eval_host (synchronizes `stream` before returning) and any
+ *    call with SPDP_F_VALIDATE (synchronizes to read back the check).
+ *  - Return value: SPDP_OK, or an error code; spdp_last_error() then returns a
+ *    thread-local message.  Usage errors are detected on the host before
+ *    anything is enqueued.
+ *  - Index conventions: customers are 1..n, node 0 is the depot, node n+1 (the
+ *    return depot) is node 0 (DESIGN R6).  A tour is a permutation
+ *    sigma_1..sigma_n of 1..n (int32 [n]).  dist is int32 [(n+1)*(n+1)]
+ *    row-major, dist[a*(n+1)+b] = c_{a,b} >= 0.
+ *  - Demand matrix: uint16 [n][ld], row c-1 holds customer c, column j holds
+ *    scenario j (scenario-minor so a warp's loads are coalesced, PAPER:151;
+ *    DESIGN R19).  ld >= S, ld % 8 == 0, pointer 16-byte aligned.  The DP
+ *    reads q^omega_{sigma_k} = demand[(sigma_k - 1)*ld + j] (tour order,
+ *    PAPER:92; DESIGN R1).
+ *  - Costs are exact integers (int32); an infeasible scenario (some single
+ *    demand > Q, so Eq. (2)'s set is empty, DESIGN R4) gets SPDP_INFEASIBLE.
+ *    Results are bit-identical for every launch configuration and shard
+ *    count.
+ */
+#ifndef SPDP_H
+#define SPDP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SPDP_API __attribute__((visibility("default")))
+#else
+#define SPDP_API
+#endif
+
+typedef struct CUstream_st* spdp_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    SPDP_OK = 0,
+    SPDP_E_USAGE = 2,    /* bad argument (null pointer, size, alignment, workspace too small) */
+    SPDP_E_DATA = 3,     /* bad data: tour not a permutation, negative/oversized costs,
+                            SAA over zero feasible scenarios */
+    SPDP_E_RESOURCE = 4, /* problem too large for the kernels (e.g. n > SPDP_MAX_N) */
+    SPDP_E_CUDA = 5      /* CUDA launch / runtime error */
+} spdp_status;
+
+#define SPDP_INFEASIBLE INT32_MAX   /* cost sentinel */
+#define SPDP_MAX_N 16384            /* largest tour length the sweep kernels accept */
+
+/* flags */
+#define SPDP_F_VALIDATE 1u          /* check tour permutation, dist >= 0 and the int32 range
+                                       bound on the device; synchronizes; E_DATA on failure */
+
+/* Summable SAA partial.  Every field is an int64 that adds
+ * elementwise, so partials of disjoint scenario sets combine by a plain SUM
+ * (e.g. an NCCL all-reduce over ranks) and the result is exact and
+ * independent of the summation order.  sum = sum of feasible costs;
+ * sum of squares = sumsq_hi * 2^32 + sumsq_lo where sumsq_lo / sumsq_hi are
+ * the sums of the low / high 32-bit halves of each cost^2.  48 bytes. */
+typedef struct {
+    int64_t n_feas, n_infeas, sum, sumsq_lo, sumsq_hi, reserved;
+} spdp_saa_partial;
+
+/* SAA estimate (PAPER:264 z_m): mean and unbiased variance of
+ * the feasible scenario costs, std_err = sqrt(var/m), ci95 = mean -+ 1.96 std_err. */
+typedef struct {
+    int64_t m, infeasible;
+    double mean, var, std_err, ci95_lo, ci95_hi;
+} spdp_saa_estimate;
+
+/* Counter-based demand model (DESIGN R14).  For global
+ * scenario s and customer c (1..n), u = Philox4x32-10(ctr = (lo32 s, hi32 s,
+ * c, stream_tag), key = (lo32 seed, hi32 seed)):
+ *   kind 0 fixed:       q = mu_c
+ *   kind 1 uniform-int: q = lo + ((u0 * (hi - lo + 1)) >> 32), lo = mu*lo_pm/1000, hi = mu*hi_pm/1000
+ *   kind 2 correlated:  q = mu + floor((mu*(A_fx*z_s + B_fx*z_sc) + D/2) / D), D = 37837*2^16,
+ *                       z = sum_j (u_j >> 16) - 131070 (Irwin-Hall(4)); z_s uses counter c = 0
+ * then q = clamp(q, 0, q_cap).  `nominal` is a DEVICE pointer [n]. */
+typedef struct {
+    int32_t kind;
+    int32_t n;
+    const uint16_t* nominal;
+    int32_t lo_pm, hi_pm;
+    int64_t A_fx, B_fx;
+    int32_t q_cap;
+    uint32_t stream_tag;
+    uint64_t seed;
+} spdp_demand_model;
+
+/* IRP customer parameters (DESIGN R21): capacity U, max
+ * delivery X per visit, initial inventory I0, holding h, lost-sale b and
+ * per-unit delivery c costs; all >= 0 and I0 <= U. */
+typedef struct {
+    int32_t U, X, I0, h, b, c;
+} spdp_irp_customer;
+
+/* Library version (major*10000 + minor*100 + patch). */
+SPDP_API int spdp_version(void);
+
+/* Thread-local message for the last non-OK status of this thread. */
+SPDP_API const char* spdp_last_error(void);
+
+/* Measurement hook (bench.py): when both are non-NULL, every subsequent
+ * spdp_split_eval / spdp_split_eval_batch / spdp_irp_dp call made by THIS
+ * thread records `start_event` immediately before and `stop_event`
+ * immediately after its dominant kernel (the sweep / IRP kernel), on the call's
+ * stream.  Both are cudaEvent_t.  Pass NULL, NULL to clear.  Thread-local. */
+SPDP_API void spdp_set_profile_events(void* start_event, void* stop_event);
+
+/* Workspace bytes needed by spdp_split_eval / spdp_split_eval_batch for T tours
+ * of n customers over S scenarios (T = 1 for spdp_split_eval). */
+SPDP_API size_t spdp_workspace_bytes(int32_t n, int64_t S, int32_t T);
+
+/* a1. Scenario generation: demand[(c-1)*ld + j] = q of customer c in global
+ * scenario s_begin + j, j in [0, S).  Bit-identical to the host definition
+ * above for any (s_begin, S) split, so ranks generate their own shards.
+ * model: HOST pointer to the struct (its `nominal` is a device pointer). */
+SPDP_API spdp_status spdp_gen_demands(const spdp_demand_model* model, int64_t s_begin, int64_t S,
+                             uint16_t* demand, int64_t ld, spdp_stream_t stream);
+
+/* a3. Tour-order demand prefix sums ("prefix-sum operations";
+ * SPEC:127-135): prefix[i*S + j] = sum_{k<=i} q^j_{sigma_k}, i = 0..n
+ * (uint32 [n+1][S], scenario-minor). */
+SPDP_API spdp_status spdp_demand_prefix(const int32_t* tour, int32_t n, const uint16_t* demand, int64_t ld,
+                               int64_t S, uint32_t* prefix, spdp_stream_t stream);
+
+/* a4. Masks, Eq. (2): mask[(i-1)*S + j] = min{p < i : sum_{k=p+1}^{i}
+ * q^j_{sigma_k} <= Q}, or -1 when q^j_{sigma_i} > Q (DESIGN R4).  int32 [n][S]. */
+SPDP_API spdp_status spdp_split_mask(const int32_t* tour, int32_t n, const uint16_t* demand, int64_t ld,
+                            int64_t S, int32_t Q, int32_t* mask, spdp_stream_t stream);
+
+/* a2+a5+a6. Split evaluation of one giant tour over S scenarios:
+ *   f(0) = 0,  f(i) = min_{mask(i) <= p <= i-1} f(p) + c_{0,sigma_{p+1}}
+ *                     + sum_{k=p+1}^{i-1} c_{sigma_k,sigma_{k+1}} + c_{sigma_i,0}
+ *   cost[j] = f(n) of scenario j  (int32 [S], may be NULL)
+ *   partial = SAA partial over the S scenarios (DEVICE pointer to ONE
+ *             spdp_saa_partial, may be NULL), overwritten (not accumulated).
+ * Q >= 1.  window_hint: expected maximum window width i - mask(i) (0 = sample
+ * the data to choose); it only selects the kernel variant, never the result:
+ * scenarios whose window exceeds the variant's register ring are finished by
+ * a general transition-parallel kernel.  The int32 range bound is
+ * 3*n*max(dist) + max(dist) < 2^31 (checked with SPDP_F_VALIDATE). */
+SPDP_API spdp_status spdp_split_eval(const int32_t* tour, const int32_t* dist, int32_t n,
+                            const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                            int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
+                            void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream);
+
+/* a8. Batched tours (tour x scenario x transition parallelism): T tours
+ * [T][n] over the same demand set.  cost [T][S] (may be NULL), partial [T]
+ * (may be NULL), one SAA partial per tour. */
+SPDP_API spdp_status spdp_split_eval_batch(const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,
+                                  const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                                  int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
+                                  void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream);
+
+/* a6 standalone: SAA partial of a cost vector (SPDP_INFEASIBLE entries are
+ * counted in n_infeas and excluded).  partial: DEVICE pointer to one struct. */
+SPDP_API spdp_status spdp_saa_reduce(const int32_t* cost, int64_t S, spdp_saa_partial* partial,
+                            spdp_stream_t stream);
+
+/* a6 finalize (host, synchronous): estimate from a (possibly all-reduced)
+ * partial.  E_DATA when n_feas == 0. */
+SPDP_API spdp_status spdp_saa_mean(const spdp_saa_partial* partial_h, spdp_saa_estimate* out_h);
+
+/* End-to-end entry with HOST buffers: copies tour/dist/demand host->device
+ * (pinned host memory recommended), runs spdp_split_eval, copies the partial
+ * (and cost_h if non-NULL) back and finalizes the estimate.  Synchronizes
+ * `stream`.  demand_h is [n][ld_h] uint16 (ld_h >= S).  ws must hold
+ * spdp_host_workspace_bytes(n, S) bytes of DEVICE memory. */
+SPDP_API size_t spdp_host_workspace_bytes(int32_t n, int64_t S);
+SPDP_API spdp_status spdp_split_eval_host(const int32_t* tour_h, const int32_t* dist_h, int32_t n,
+                                 const uint16_t* demand_h, int64_t ld_h, int64_t S, int32_t Q,
+                                 int32_t* cost_h, spdp_saa_estimate* est_h, int32_t window_hint,
+                                 void* ws, size_t ws_bytes, spdp_stream_t stream);
+
+/* a9+a10. Inventory-routing recourse DP (model SURVEY §8(c6), DESIGN R21):
+ * per scenario j and customer m, V_0[I0] = 0, and for t = 0..H-1
+ *   W_t[y]     = min_{I in [max(0, y - z_{m,t} X), y]} V_t[I] + c (y - I)          (delivery)
+ *   V_{t+1}[J] = W_t[J + d] + h J                       for J >= 1, J + d <= U     (demand d)
+ *   V_{t+1}[0] = min_{y <= min(d, U)} W_t[y] + b (d - y)
+ * cost[j] = sum_m min_J V_H[J] (int64 [S], overwritten).  visit_h: HOST uint8 [M][H]
+ * (z_{m,t}); cust_h: HOST array [M]; both are copied into `ws` (size from
+ * spdp_irp_workspace_bytes).  demand: uint16 [H*M][ld], row t*M + m.
+ * U <= 1023 and H (c X + h U + b 65535) < 2^29 (else E_RESOURCE).
+ * partial (may be NULL): SAA partial of the S costs (DEVICE pointer). */
+SPDP_API size_t spdp_irp_workspace_bytes(int32_t H, int32_t M, int64_t S);
+SPDP_API spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_customer* cust_h, int32_t H, int32_t M,
+                        const uint16_t* demand, int64_t ld, int64_t S, int64_t* cost,
+                        spdp_saa_partial* partial, void* ws, size_t ws_bytes, uint32_t flags,
+                        spdp_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPDP_H */

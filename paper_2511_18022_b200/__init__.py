@@ -1,0 +1,337 @@
+"""paper_2511_18022_b200 -- B200-native scenario-parallel Split DP (arXiv 2511.18022).
+
+Thin Python binding over the C-ABI library ``libspdp.so`` (declared in
+``include/spdp.h``): argument marshalling only.  Every step of the hot path
+runs in the CUDA kernels of ``csrc/``; PyTorch supplies device memory, the
+current stream and (in ``dist``) process groups.  There is no CPU fallback:
+importing this package without the built library raises ImportError, and
+calling a kernel entry point without a CUDA device raises SpdpError.
+
+Names follow the paper: ``split_eval`` evaluates Eq. (1)-(3)
+for every scenario, ``saa_mean`` finalizes the SAA statistics,
+``irp_dp`` runs the inventory-routing recourse DP (DESIGN R21).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspdp.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        "paper_2511_18022_b200: %s is missing -- build it with "
+        "`python -m paper_2511_18022_b200.build` (nvcc, sm_100a). There is no CPU fallback." % LIB_PATH)
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+SPDP_OK, SPDP_E_USAGE, SPDP_E_DATA, SPDP_E_RESOURCE, SPDP_E_CUDA = 0, 2, 3, 4, 5
+INFEASIBLE = 2**31 - 1
+F_VALIDATE = 1
+MAX_N = 16384
+
+SYMBOLS = (
+    "spdp_version", "spdp_last_error", "spdp_workspace_bytes", "spdp_gen_demands", "spdp_demand_prefix",
+    "spdp_split_mask", "spdp_split_eval", "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean",
+    "spdp_host_workspace_bytes", "spdp_split_eval_host", "spdp_irp_workspace_bytes", "spdp_irp_dp",
+    "spdp_set_profile_events",
+)
+
+
+class SaaPartial(ctypes.Structure):
+    _fields_ = [("n_feas", ctypes.c_int64), ("n_infeas", ctypes.c_int64), ("sum", ctypes.c_int64),
+                ("sumsq_lo", ctypes.c_int64), ("sumsq_hi", ctypes.c_int64), ("reserved", ctypes.c_int64)]
+
+
+class SaaEstimate(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("infeasible", ctypes.c_int64), ("mean", ctypes.c_double),
+                ("var", ctypes.c_double), ("std_err", ctypes.c_double), ("ci95_lo", ctypes.c_double),
+                ("ci95_hi", ctypes.c_double)]
+
+
+class DemandModel(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("n", ctypes.c_int32), ("nominal", ctypes.c_void_p),
+                ("lo_pm", ctypes.c_int32), ("hi_pm", ctypes.c_int32), ("A_fx", ctypes.c_int64),
+                ("B_fx", ctypes.c_int64), ("q_cap", ctypes.c_int32), ("stream_tag", ctypes.c_uint32),
+                ("seed", ctypes.c_uint64)]
+
+
+class IrpCustomer(ctypes.Structure):
+    _fields_ = [("U", ctypes.c_int32), ("X", ctypes.c_int32), ("I0", ctypes.c_int32), ("h", ctypes.c_int32),
+                ("b", ctypes.c_int32), ("c", ctypes.c_int32)]
+
+
+def _sig():
+    P, i32, i64, u32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t
+    st = ctypes.c_int
+    L = _lib
+    L.spdp_version.restype = ctypes.c_int
+    L.spdp_set_profile_events.argtypes = [P, P]
+    L.spdp_set_profile_events.restype = None
+    L.spdp_last_error.restype = ctypes.c_char_p
+    L.spdp_workspace_bytes.argtypes = [i32, i64, i32]
+    L.spdp_workspace_bytes.restype = sz
+    L.spdp_host_workspace_bytes.argtypes = [i32, i64]
+    L.spdp_host_workspace_bytes.restype = sz
+    L.spdp_irp_workspace_bytes.argtypes = [i32, i32, i64]
+    L.spdp_irp_workspace_bytes.restype = sz
+    L.spdp_gen_demands.argtypes = [ctypes.POINTER(DemandModel), i64, i64, P, i64, P]
+    L.spdp_demand_prefix.argtypes = [P, i32, P, i64, i64, P, P]
+    L.spdp_split_mask.argtypes = [P, i32, P, i64, i64, i32, P, P]
+    L.spdp_split_eval.argtypes = [P, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
+    L.spdp_split_eval_batch.argtypes = [P, i32, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
+    L.spdp_saa_reduce.argtypes = [P, i64, P, P]
+    L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
+    L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
+    L.spdp_irp_dp.argtypes = [P, ctypes.POINTER(IrpCustomer), i32, i32, P, i64, i64, P, P, P, sz, u32, P]
+    for name in ("spdp_gen_demands", "spdp_demand_prefix", "spdp_split_mask", "spdp_split_eval",
+                 "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean", "spdp_split_eval_host",
+                 "spdp_irp_dp"):
+        getattr(L, name).restype = st
+
+
+_sig()
+
+
+class SpdpError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib.spdp_last_error().decode(errors="replace")
+        super().__init__("%s failed (status %d): %s" % (where, status, msg))
+        self.status = status
+
+
+def _check(rc: int, where: str):
+    if rc != SPDP_OK:
+        raise SpdpError(rc, where)
+
+
+def set_profile_events(start=None, stop=None):
+    """Record torch.cuda.Event pair (start, stop) around the dominant kernel of the next calls
+    on this thread (the sweep / IRP kernel); call with no arguments to clear."""
+    if start is None or stop is None:
+        _lib.spdp_set_profile_events(None, None)
+    else:
+        _lib.spdp_set_profile_events(ctypes.c_void_p(start.cuda_event), ctypes.c_void_p(stop.cuda_event))
+
+
+def version() -> int:
+    return int(_lib.spdp_version())
+
+
+def lib():
+    """The raw ctypes handle of libspdp.so."""
+    return _lib
+
+
+# ------------------------------------------------------------------ torch plumbing
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_ptr(t, what: str):
+    torch = _torch()
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError("%s must be a CUDA tensor (the kernels have no CPU path)" % what)
+    if not t.is_contiguous():
+        raise ValueError("%s must be contiguous" % what)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+_WS = {}
+
+
+def workspace(nbytes: int, device, tag: str = "split"):
+    """Cached per-device scratch buffer (torch uint8), grown on demand."""
+    torch = _torch()
+    dev = torch.device(device)
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), tag)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+        _WS[key] = buf
+    return buf
+
+
+def workspace_bytes(n: int, S: int, T: int = 1) -> int:
+    return int(_lib.spdp_workspace_bytes(n, S, T))
+
+
+def padded_ld(S: int) -> int:
+    return (S + 7) // 8 * 8
+
+
+def empty_demand(n: int, S: int, device):
+    """u16 demand matrix [n][ld] (stored as torch.int16), ld = S rounded up to 8."""
+    torch = _torch()
+    return torch.zeros((n, padded_ld(S)), dtype=torch.int16, device=device)
+
+
+# ------------------------------------------------------------------ a1
+def gen_demands(model: dict, s_begin: int, S: int, device="cuda", out=None):
+    """Generate the demand shard [n][ld] for global scenarios [s_begin, s_begin+S)."""
+    torch = _torch()
+    nominal = torch.as_tensor(np.ascontiguousarray(model["nominal"], dtype=np.uint16).view(np.int16),
+                              device=device)
+    n = nominal.shape[0]
+    if out is None:
+        out = empty_demand(n, S, device)
+    m = DemandModel(kind=int(model["kind"]), n=n, nominal=nominal.data_ptr(), lo_pm=int(model.get("lo_pm", 0)),
+                    hi_pm=int(model.get("hi_pm", 0)), A_fx=int(model.get("A_fx", 0)), B_fx=int(model.get("B_fx", 0)),
+                    q_cap=int(model["q_cap"]), stream_tag=int(model.get("stream_tag", 0)), seed=int(model["seed"]))
+    _check(_lib.spdp_gen_demands(ctypes.byref(m), int(s_begin), int(S), _dev_ptr(out, "out"), out.shape[1],
+                                 _stream(out.device)), "spdp_gen_demands")
+    out._spdp_nominal = nominal  # keep alive until the stream has consumed it
+    return out
+
+
+# ------------------------------------------------------------------ a3 / a4
+def demand_prefix(tour, demand, S: int | None = None):
+    torch = _torch()
+    n, ld = demand.shape
+    S = ld if S is None else S
+    out = torch.empty((n + 1, S), dtype=torch.int32, device=demand.device)
+    _check(_lib.spdp_demand_prefix(_dev_ptr(tour, "tour"), n, _dev_ptr(demand, "demand"), ld, S,
+                                   _dev_ptr(out, "prefix"), _stream(demand.device)), "spdp_demand_prefix")
+    return out
+
+
+def split_mask(tour, demand, Q: int, S: int | None = None):
+    torch = _torch()
+    n, ld = demand.shape
+    S = ld if S is None else S
+    out = torch.empty((n, S), dtype=torch.int32, device=demand.device)
+    _check(_lib.spdp_split_mask(_dev_ptr(tour, "tour"), n, _dev_ptr(demand, "demand"), ld, S, int(Q),
+                                _dev_ptr(out, "mask"), _stream(demand.device)), "spdp_split_mask")
+    return out
+
+
+# ------------------------------------------------------------------ a2 + a5 + a6
+def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool = True,
+               want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None, partial=None):
+    """Per-scenario split costs (int32 [S], INFEASIBLE sentinel) and the SAA partial (int64 [6])."""
+    torch = _torch()
+    n, ld = demand.shape
+    S = ld if S is None else S
+    dev = demand.device
+    if want_cost and cost is None:
+        cost = torch.empty(S, dtype=torch.int32, device=dev)
+    if want_partial and partial is None:
+        partial = torch.zeros(6, dtype=torch.int64, device=dev)
+    nb = workspace_bytes(n, S, 1)
+    ws = workspace(nb, dev)
+    _check(_lib.spdp_split_eval(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld, S,
+                                int(Q), _dev_ptr(cost, "cost") if want_cost else None,
+                                _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
+                                ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_VALIDATE if validate else 0,
+                                _stream(dev)), "spdp_split_eval")
+    return cost, partial
+
+
+def split_eval_batch(tours, dist, demand, Q: int, S: int | None = None, want_cost: bool = True,
+                     want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None,
+                     partial=None):
+    """T tours [T][n] over one demand set: costs int32 [T][S] and partials int64 [T][6]."""
+    torch = _torch()
+    n, ld = demand.shape
+    T = tours.shape[0]
+    S = ld if S is None else S
+    dev = demand.device
+    if want_cost and cost is None:
+        cost = torch.empty((T, S), dtype=torch.int32, device=dev)
+    if want_partial and partial is None:
+        partial = torch.zeros((T, 6), dtype=torch.int64, device=dev)
+    ws = workspace(workspace_bytes(n, S, T), dev)
+    _check(_lib.spdp_split_eval_batch(_dev_ptr(tours, "tours"), T, _dev_ptr(dist, "dist"), n,
+                                      _dev_ptr(demand, "demand"), ld, S, int(Q),
+                                      _dev_ptr(cost, "cost") if want_cost else None,
+                                      _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
+                                      ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_VALIDATE if validate else 0,
+                                      _stream(dev)), "spdp_split_eval_batch")
+    return cost, partial
+
+
+def saa_reduce(cost, partial=None):
+    torch = _torch()
+    if partial is None:
+        partial = torch.zeros(6, dtype=torch.int64, device=cost.device)
+    _check(_lib.spdp_saa_reduce(_dev_ptr(cost, "cost"), cost.numel(), _dev_ptr(partial, "partial"),
+                                _stream(cost.device)), "spdp_saa_reduce")
+    return partial
+
+
+def saa_mean(partial) -> dict:
+    """Host finalize of an SAA partial (int64[6] tensor/array, any device)."""
+    arr = partial.detach().cpu().numpy() if hasattr(partial, "detach") else np.asarray(partial)
+    arr = np.ascontiguousarray(arr, dtype=np.int64).reshape(6)
+    p = SaaPartial(*[int(v) for v in arr])
+    e = SaaEstimate()
+    _check(_lib.spdp_saa_mean(ctypes.byref(p), ctypes.byref(e)), "spdp_saa_mean")
+    return {"m": e.m, "infeasible": e.infeasible, "mean": e.mean, "var": e.var, "stderr": e.std_err,
+            "ci95_lo": e.ci95_lo, "ci95_hi": e.ci95_hi}
+
+
+def host_workspace_bytes(n: int, S: int) -> int:
+    return int(_lib.spdp_host_workspace_bytes(n, S))
+
+
+def split_eval_host(tour_h, dist_h, demand_h, Q: int, S: int | None = None, cost_h=None, window_hint: int = 0,
+                    device="cuda"):
+    """End-to-end call with HOST buffers (numpy or pinned torch CPU tensors): H2D copy, kernels,
+    D2H of the estimate (and of cost_h if given).  Returns the SAA estimate dict."""
+    torch = _torch()
+
+    def hptr(a, what):
+        if a is None:
+            return None
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda or not a.is_contiguous():
+                raise ValueError("%s must be a contiguous CPU tensor" % what)
+            return ctypes.c_void_p(a.data_ptr())
+        a = np.asarray(a)
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("%s must be C-contiguous" % what)
+        return a.ctypes.data_as(ctypes.c_void_p)
+
+    n, ld = demand_h.shape
+    S = ld if S is None else S
+    ws = workspace(host_workspace_bytes(n, S), device, tag="host")
+    e = SaaEstimate()
+    _check(_lib.spdp_split_eval_host(hptr(tour_h, "tour"), hptr(dist_h, "dist"), n, hptr(demand_h, "demand"), ld, S,
+                                     int(Q), hptr(cost_h, "cost"), ctypes.byref(e), int(window_hint),
+                                     ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(torch.device(device))),
+           "spdp_split_eval_host")
+    return {"m": e.m, "infeasible": e.infeasible, "mean": e.mean, "var": e.var, "stderr": e.std_err,
+            "ci95_lo": e.ci95_lo, "ci95_hi": e.ci95_hi}
+
+
+# ------------------------------------------------------------------ a9 + a10
+def irp_dp(visit, cust, demand, H: int, M: int, S: int | None = None, want_partial: bool = True, cost=None,
+           partial=None):
+    """IRP recourse cost per scenario (int64 [S]); visit u8 [M][H] and cust int32 [M][6] on the host."""
+    torch = _torch()
+    ld = demand.shape[1]
+    S = ld if S is None else S
+    dev = demand.device
+    visit = np.ascontiguousarray(visit, dtype=np.uint8)
+    cust = np.ascontiguousarray(cust, dtype=np.int32)
+    carr = (IrpCustomer * M)(*[IrpCustomer(*[int(v) for v in row]) for row in cust])
+    if cost is None:
+        cost = torch.empty(S, dtype=torch.int64, device=dev)
+    if want_partial and partial is None:
+        partial = torch.zeros(6, dtype=torch.int64, device=dev)
+    ws = workspace(int(_lib.spdp_irp_workspace_bytes(H, M, S)), dev, tag="irp")
+    _check(_lib.spdp_irp_dp(visit.ctypes.data_as(ctypes.c_void_p), carr, H, M, _dev_ptr(demand, "demand"), ld, S,
+                            _dev_ptr(cost, "cost"), _dev_ptr(partial, "partial") if want_partial else None,
+                            ctypes.c_void_p(ws.data_ptr()), ws.numel(), 0, _stream(dev)), "spdp_irp_dp")
+    return cost, partial

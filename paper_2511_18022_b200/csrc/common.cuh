@@ -1,0 +1,91 @@
+// common.cuh -- shared device/host helpers of libspdp (product code; never
+// includes or links anything under oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spdp.h"
+
+namespace spdp {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// Thread-local error message (spdp_last_error).
+void set_error(const char* fmt, ...);
+spdp_status fail(spdp_status st, const char* fmt, ...);
+spdp_status cuda_check(cudaError_t e, const char* what);
+spdp_status last_launch(const char* what);
+
+// spdp_set_profile_events hook: record around the dominant kernel if set.
+void prof_begin(cudaStream_t st);
+void prof_end(cudaStream_t st);
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Streaming 16-bit load that does not allocate in L1 (each demand row is
+// read once per tour by a given warp).
+__device__ __forceinline__ uint32_t ld_stream_u16(const uint16_t* p) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+    return (uint32_t)v;
+}
+
+// Warp + block reduction of the SAA partial fields.
+struct Part {
+    long long n_feas, n_infeas, sum, sq_lo, sq_hi;
+};
+
+__device__ __forceinline__ void part_add_cost(Part& p, long long c, bool feasible) {
+    if (feasible) {
+        unsigned long long sq = (unsigned long long)c * (unsigned long long)c;
+        p.n_feas += 1;
+        p.sum += c;
+        p.sq_lo += (long long)(sq & 0xffffffffull);
+        p.sq_hi += (long long)(sq >> 32);
+    } else {
+        p.n_infeas += 1;
+    }
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+__device__ __forceinline__ Part warp_sum(Part p) {
+    p.n_feas = warp_sum_ll(p.n_feas);
+    p.n_infeas = warp_sum_ll(p.n_infeas);
+    p.sum = warp_sum_ll(p.sum);
+    p.sq_lo = warp_sum_ll(p.sq_lo);
+    p.sq_hi = warp_sum_ll(p.sq_hi);
+    return p;
+}
+
+// Block-wide sum; result valid in thread 0.  smem must hold blockDim/32 Parts.
+__device__ __forceinline__ Part block_sum(Part p, Part* smem) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    p = warp_sum(p);
+    if (lane == 0) smem[wid] = p;
+    __syncthreads();
+    Part r{0, 0, 0, 0, 0};
+    if (wid == 0) {
+        if (lane < nw) r = smem[lane];
+        r = warp_sum(r);
+    }
+    return r;
+}
+
+__device__ __forceinline__ void part_store(spdp_saa_partial* dst, const Part& p) {
+    dst->n_feas = p.n_feas;
+    dst->n_infeas = p.n_infeas;
+    dst->sum = p.sum;
+    dst->sumsq_lo = p.sq_lo;
+    dst->sumsq_hi = p.sq_hi;
+    dst->reserved = 0;
+}
+
+}  // namespace spdp

@@ -1,0 +1,242 @@
+// irp.cu -- a9/a10: inventory-routing recourse DP (PAPER:7 names the
+// application and its "three-dimensional GPU parallelism"; the model is
+// SURVEY §8(c6), DESIGN R21).
+//
+// Per scenario s and customer m, forward over periods t = 0..H-1 with state I
+// (inventory) in [0, U]:
+//   step A (delivery, masked min-plus over the band I in [y - z X, y]):
+//       W[y] = min_I V[I] + c (y - I) = c y + min_I (V[I] - c I)
+//   step B (demand d, lost sales):
+//       V'[J] = W[J + d] + h J            (1 <= J, J + d <= U)
+//       V'[0] = b d + min_{y <= min(d,U)} (W[y] - b y)
+// cost_s = sum_m min_J V_H[J].
+//
+// Parallel layout (the "3-D" of PAPER:7): (scenario x customer) -> warps,
+// inventory state y -> lanes (K consecutive states per lane, in registers),
+// the band of step A -> a warp prefix-min scan when X >= U (the band is
+// [0, y]) or an explicit band loop otherwise; periods are the sequential
+// layers.  A warp takes a tile of 32 scenarios of one customer: the tile's
+// demands [H][32] are staged in shared memory with coalesced loads.
+#include <climits>
+
+#include "common.cuh"
+
+namespace spdp {
+
+constexpr int32_t kIrpInf = 1 << 30;  // "unreachable"; all real values are < 2^29 (host check)
+
+struct IrpCust {
+    int32_t U, X, I0, h, b, c;
+};
+
+template <int K>
+__global__ void __launch_bounds__(128) irp_kernel(const uint8_t* __restrict__ visit, const IrpCust* __restrict__ cust,
+                                                  int H, int M, const uint16_t* __restrict__ demand, int64_t ld,
+                                                  int64_t S, long long* __restrict__ cost) {
+    extern __shared__ unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // per warp: demand tile [H][32] u16, then W buffer [32*K] int32
+    uint16_t* dtile = reinterpret_cast<uint16_t*>(smem_raw) + (size_t)wid * (H * 32 + 2 * 32 * K);
+    int32_t* wbuf = reinterpret_cast<int32_t*>(dtile + H * 32);
+    const int64_t ntile = (S + 31) / 32;
+    const int64_t ntask = ntile * M;
+    for (int64_t task = (int64_t)blockIdx.x * nw + wid; task < ntask; task += (int64_t)gridDim.x * nw) {
+        const int m = (int)(task % M);
+        const int64_t s0 = (task / M) * 32;
+        const IrpCust p = cust[m];
+        for (int t = 0; t < H; ++t) {
+            const int64_t s = s0 + lane;
+            dtile[t * 32 + lane] = (s < S) ? demand[((int64_t)t * M + m) * ld + s] : (uint16_t)0;
+        }
+        __syncwarp();
+        const int jmax = (int)((S - s0) < 32 ? (S - s0) : 32);
+        for (int j = 0; j < jmax; ++j) {
+            int32_t v[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int y = lane * K + k;
+                v[k] = (y == p.I0) ? 0 : kIrpInf;
+            }
+            for (int t = 0; t < H; ++t) {
+                const int d = dtile[t * 32 + j];
+                const bool vis = visit[(int64_t)m * H + t] != 0;
+                // ---- step A
+                if (vis && p.X > 0) {
+                    if (p.X >= p.U) {
+                        // band [0, y]: prefix-min of V[I] - c I, then + c y
+                        int32_t run = kIrpInf;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const int y = lane * K + k;
+                            const int32_t a = (v[k] >= kIrpInf) ? kIrpInf : v[k] - p.c * y;
+                            run = min(run, a);
+                            v[k] = run;  // lane-local inclusive prefix-min
+                        }
+                        int32_t carry = run;  // inclusive scan of lane totals
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int32_t u = __shfl_up_sync(kFull, carry, o);
+                            if (lane >= o) carry = min(carry, u);
+                        }
+                        int32_t excl = __shfl_up_sync(kFull, carry, 1);
+                        if (lane == 0) excl = kIrpInf;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const int y = lane * K + k;
+                            const int32_t mn = min(v[k], excl);
+                            v[k] = (mn >= kIrpInf / 2) ? kIrpInf : mn + p.c * y;
+                        }
+                    } else {
+                        // explicit band [max(0, y - X), y] (DESIGN: general X < U path)
+#pragma unroll
+                        for (int k = 0; k < K; ++k) wbuf[lane * K + k] = v[k];
+                        __syncwarp();
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const int y = lane * K + k;
+                            int32_t best = kIrpInf;
+                            if (y <= p.U) {
+                                for (int I = max(0, y - p.X); I <= y; ++I) {
+                                    const int32_t a = wbuf[I];
+                                    if (a < kIrpInf) best = min(best, a + p.c * (y - I));
+                                }
+                            }
+                            v[k] = best;
+                        }
+                        __syncwarp();
+                    }
+                }
+                // states above U are never reachable
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    if (lane * K + k > p.U) v[k] = kIrpInf;
+                // ---- step B
+                int32_t m0 = kIrpInf;  // min_{y <= min(d,U)} W[y] - b y
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int y = lane * K + k;
+                    wbuf[y] = v[k];
+                    if (y <= d && v[k] < kIrpInf) m0 = min(m0, v[k] - p.b * y);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) m0 = min(m0, __shfl_xor_sync(kFull, m0, o));
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int J = lane * K + k;
+                    int32_t nv;
+                    if (J == 0) {
+                        nv = (m0 >= kIrpInf) ? kIrpInf : m0 + p.b * d;
+                    } else if (J + d <= p.U) {
+                        const int32_t wv = wbuf[J + d];
+                        nv = (wv >= kIrpInf) ? kIrpInf : wv + p.h * J;
+                    } else {
+                        nv = kIrpInf;
+                    }
+                    v[k] = nv;
+                }
+                __syncwarp();
+            }
+            int32_t best = kIrpInf;
+#pragma unroll
+            for (int k = 0; k < K; ++k) best = min(best, v[k]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
+            if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&cost[s0 + j]), (unsigned long long)best);
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(256) irp_reduce_kernel(const long long* __restrict__ cost, int64_t S,
+                                                         spdp_saa_partial* __restrict__ partial) {
+    __shared__ Part red[8];
+    Part p{0, 0, 0, 0, 0};
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x)
+        part_add_cost(p, cost[s], true);
+    Part r = block_sum(p, red);
+    if (threadIdx.x == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&partial->n_feas), (unsigned long long)r.n_feas);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sum), (unsigned long long)r.sum);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_lo), (unsigned long long)r.sq_lo);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_hi), (unsigned long long)r.sq_hi);
+    }
+}
+
+template <int K>
+static spdp_status launch_irp(const uint8_t* visit, const IrpCust* cust, int H, int M, const uint16_t* demand,
+                              int64_t ld, int64_t S, long long* cost, cudaStream_t st) {
+    const int warps = 4;
+    const size_t smem = (size_t)warps * (sizeof(uint16_t) * H * 32 + sizeof(int32_t) * 32 * K);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(irp_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(irp)");
+        attr_set = true;
+    }
+    const int64_t ntask = ((S + 31) / 32) * M;
+    int64_t blocks = ceil_div(ntask, warps);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    prof_begin(st);
+    irp_kernel<K><<<(unsigned)blocks, warps * 32, smem, st>>>(visit, cust, H, M, demand, ld, S, cost);
+    spdp_status rc = last_launch("irp_kernel");
+    prof_end(st);
+    return rc;
+}
+
+}  // namespace spdp
+
+using namespace spdp;
+
+extern "C" size_t spdp_irp_workspace_bytes(int32_t H, int32_t M, int64_t S) {
+    (void)S;
+    if (H < 1 || M < 1) return 0;
+    return align_up(sizeof(IrpCust) * (size_t)M, 256) + align_up((size_t)M * (size_t)H, 256);
+}
+
+extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_customer* cust_h, int32_t H, int32_t M,
+                                   const uint16_t* demand, int64_t ld, int64_t S, int64_t* cost,
+                                   spdp_saa_partial* partial, void* ws, size_t ws_bytes, uint32_t flags,
+                                   spdp_stream_t stream) {
+    (void)flags;
+    if (H < 1 || M < 1 || S < 1) return fail(SPDP_E_USAGE, "spdp_irp_dp: H, M, S must be >= 1");
+    if (!visit_h || !cust_h || !demand || !cost || !ws) return fail(SPDP_E_USAGE, "spdp_irp_dp: NULL pointer");
+    if (ld < S) return fail(SPDP_E_USAGE, "spdp_irp_dp: ld < S");
+    if (ws_bytes < spdp_irp_workspace_bytes(H, M, S)) return fail(SPDP_E_USAGE, "spdp_irp_dp: workspace too small");
+    int Umax = 0;
+    for (int m = 0; m < M; ++m) {
+        const spdp_irp_customer& c = cust_h[m];
+        if (c.U < 0 || c.X < 0 || c.I0 < 0 || c.I0 > c.U || c.h < 0 || c.b < 0 || c.c < 0)
+            return fail(SPDP_E_DATA, "spdp_irp_dp: customer %d has invalid parameters", m);
+        // every reachable value <= H (c X + h U + b 65535) must stay below 2^29
+        const long long bound = (long long)H * ((long long)c.c * c.X + (long long)c.h * c.U + (long long)c.b * 65535LL);
+        if (bound >= (1LL << 29)) return fail(SPDP_E_RESOURCE, "spdp_irp_dp: cost bound %lld exceeds int32 kernel range", bound);
+        Umax = c.U > Umax ? c.U : Umax;
+    }
+    if (Umax + 1 > 32 * 32) return fail(SPDP_E_RESOURCE, "spdp_irp_dp: U=%d > 1023", Umax);
+    cudaStream_t st = (cudaStream_t)stream;
+    char* w = static_cast<char*>(ws);
+    IrpCust* dcust = reinterpret_cast<IrpCust*>(w);
+    uint8_t* dvisit = reinterpret_cast<uint8_t*>(w + align_up(sizeof(IrpCust) * (size_t)M, 256));
+    spdp_status rc;
+    if ((rc = cuda_check(cudaMemcpyAsync(dcust, cust_h, sizeof(IrpCust) * M, cudaMemcpyHostToDevice, st), "H2D cust"))) return rc;
+    if ((rc = cuda_check(cudaMemcpyAsync(dvisit, visit_h, (size_t)M * H, cudaMemcpyHostToDevice, st), "H2D visit"))) return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(cost, 0, sizeof(int64_t) * (size_t)S, st), "memset cost"))) return rc;
+    long long* c = reinterpret_cast<long long*>(cost);
+    const int need = Umax + 1;
+    if (need <= 32) rc = launch_irp<1>(dvisit, dcust, H, M, demand, ld, S, c, st);
+    else if (need <= 64) rc = launch_irp<2>(dvisit, dcust, H, M, demand, ld, S, c, st);
+    else if (need <= 128) rc = launch_irp<4>(dvisit, dcust, H, M, demand, ld, S, c, st);
+    else if (need <= 256) rc = launch_irp<8>(dvisit, dcust, H, M, demand, ld, S, c, st);
+    else if (need <= 512) rc = launch_irp<16>(dvisit, dcust, H, M, demand, ld, S, c, st);
+    else rc = launch_irp<32>(dvisit, dcust, H, M, demand, ld, S, c, st);
+    if (rc) return rc;
+    if (partial) {
+        if ((rc = cuda_check(cudaMemsetAsync(partial, 0, sizeof(spdp_saa_partial), st), "memset partial"))) return rc;
+        int64_t blocks = ceil_div(S, 256 * 8);
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        irp_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(c, S, partial);
+        if ((rc = last_launch("irp_reduce_kernel"))) return rc;
+    }
+    return SPDP_OK;
+}

@@ -1,0 +1,42 @@
+"""Short driver for ncu: a few C2 steps (or --config C3/C4, --irp) through the C-ABI."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+import bench_config
+import paper_2511_18022_b200 as spdp
+import synth
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2")
+ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--hint", type=int, default=None)
+ap.add_argument("--irp", action="store_true")
+a = ap.parse_args()
+dev = torch.device("cuda", 0)
+if a.irp:
+    c5 = synth.irp_config()
+    irp = c5["irp"]
+    d = spdp.gen_demands(c5["model"], 0, c5["S"], device=dev)
+    for _ in range(a.iters):
+        spdp.irp_dp(irp["visit"], irp["cust"], d, irp["H"], irp["M"], S=c5["S"])
+else:
+    cfg = synth.config_instance(a.config)
+    inst = cfg["inst"]
+    d = spdp.gen_demands(cfg["model"], 0, cfg["S"], device=dev)
+    tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
+    dist = torch.from_numpy(inst["dist"]).to(dev)
+    h = a.hint if a.hint is not None else bench_config.HINT[a.config]
+    for _ in range(a.iters):
+        if cfg["T"] == 1:
+            spdp.split_eval(tours[0].contiguous(), dist, d, inst["Q"], S=cfg["S"], window_hint=h)
+        else:
+            spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h)
+torch.cuda.synchronize()
+print("done")

@@ -1,0 +1,66 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+The oracle cannot evaluate every output of C3/C4 in seconds, so those are
+checked on sampled outputs the oracle computes one by one (plus the fused SAA
+partial against a separate reduction of the per-scenario costs); C2 is checked
+completely (all 10^6 costs and the SAA estimate).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+import bench_config  # noqa: E402  (repo root, same launch configuration as bench.py)
+
+
+@pytest.fixture(scope="module")
+def spdp():
+    import paper_2511_18022_b200 as m
+    return m
+
+
+def _sample_cols(model, idx):
+    cols = [oracle.gen_demands(model, int(s), 1) for s in idx]
+    return np.concatenate(cols, axis=1)
+
+
+def test_c2_full_all_costs_and_saa(spdp):
+    cfg = synth.config_instance("C2")
+    inst, S = cfg["inst"], cfg["S"]
+    d = spdp.gen_demands(cfg["model"], 0, S)
+    tour, dist = torch.from_numpy(inst["tour"]).cuda(), torch.from_numpy(inst["dist"]).cuda()
+    cost, part = spdp.split_eval(tour, dist, d, inst["Q"], S=S, window_hint=bench_config.HINT["C2"])
+    dem = oracle.gen_demands(cfg["model"], 0, S)
+    assert np.array_equal(d.cpu().numpy().view(np.uint16)[:, :S], dem)
+    want = oracle.split(inst["tour"], inst["dist"], dem, inst["Q"])
+    got = cost.cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, want)
+    w = oracle.saa(want)
+    est = spdp.saa_mean(part)
+    assert est["m"] == S and est["mean"] == w["mean"]
+    assert abs(est["var"] - w["var"]) <= 1e-12 * w["var"]
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_sampled(spdp, name):
+    cfg = synth.config_instance(name)
+    inst, S, T = cfg["inst"], cfg["S"], cfg["T"]
+    d = spdp.gen_demands(cfg["model"], 0, S)
+    tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).cuda()
+    dist = torch.from_numpy(inst["dist"]).cuda()
+    cost, part = spdp.split_eval_batch(tours, dist, d, inst["Q"], S=S, window_hint=bench_config.HINT[name])
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([rng.integers(0, S, size=150), [0, 1, S - 2, S - 1]]))
+    dem = _sample_cols(cfg["model"], idx)
+    got = cost.cpu().numpy()
+    for t in sorted(set([0, T - 1] + list(rng.integers(0, T, size=3)))):
+        want = oracle.split(cfg["tours"][t], inst["dist"], dem, inst["Q"])
+        assert np.array_equal(got[t, idx].astype(np.int64), want), "tour %d" % t
+    # the fused SAA partial equals an independent reduction of the device's per-scenario costs
+    for t in (0, T - 1):
+        ref = spdp.saa_reduce(cost[t].contiguous())
+        assert torch.equal(ref.cpu(), part[t].cpu())

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by element.
+
+Bar: bit-exact for the generated demands, masks, prefixes and
+every per-scenario cost (integers); SAA sums exact, mean identical.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def spdp():
+    import paper_2511_18022_b200 as m
+    return m
+
+
+def to_dev(a, dtype=None):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint16:
+        a = a.view(np.int16)
+    t = torch.from_numpy(a)
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def dev_u16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def oracle_cost_as_i32(c):
+    c = np.asarray(c)
+    return np.where(c == oracle.INF, 2**31 - 1, c).astype(np.int64)
+
+
+# ------------------------------------------------------------------ a1 generator
+@pytest.mark.parametrize("kind", [synth.FIXED, synth.UNIFORM, synth.CORRELATED])
+def test_gen_demands_bit_exact(spdp, kind):
+    inst = synth.make_instance(100, seed=101)
+    model = synth.demand_model(inst["nominal"], inst["Q"], kind=kind, seed=0x5EED0001)
+    S = 50_003
+    d = spdp.gen_demands(model, 0, S)
+    want = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
+    assert np.array_equal(dev_u16(d)[:, :S], want[:, :S])
+    # shard invariance: a rank's slice equals the same columns of the single run
+    b, e = 12_345, 40_000
+    shard = spdp.gen_demands(model, b, e - b)
+    assert np.array_equal(dev_u16(shard)[:, :e - b], want[:, b:e])
+
+
+# ------------------------------------------------------------------ a3 / a4
+def test_prefix_and_mask(spdp):
+    inst = synth.make_instance(60, seed=5, r=3.0)
+    model = synth.demand_model(inst["nominal"], inst["Q"] + 40, seed=17)  # some q > Q -> INFEASIBLE masks
+    S = 3001
+    dem = oracle.gen_demands(model, 0, S)
+    tour = to_dev(inst["tour"])
+    D = to_dev(dem)
+    P = spdp.demand_prefix(tour, D).cpu().numpy().astype(np.int64)
+    assert np.array_equal(P, oracle.demand_prefix(inst["tour"], dem))
+    M = spdp.split_mask(tour, D, inst["Q"]).cpu().numpy()
+    assert np.array_equal(M, oracle.mask(inst["tour"], dem, inst["Q"]))
+
+
+# ------------------------------------------------------------------ a5 / a6 single tour
+def _check_split(spdp, inst, dem, S, hints=(0, 8, 16, 32, 64), Q=None):
+    Q = inst["Q"] if Q is None else Q
+    want = oracle_cost_as_i32(oracle.split(inst["tour"], inst["dist"], dem, Q, S=S))
+    want_saa = oracle.saa(oracle.split(inst["tour"], inst["dist"], dem, Q, S=S))
+    tour, dist, D = to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem)
+    for h in hints:
+        cost, part = spdp.split_eval(tour, dist, D, Q, S=S, window_hint=h, validate=(h == 0))
+        got = cost.cpu().numpy().astype(np.int64)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, "hint %d: %d mismatches, first s=%d got %d want %d" % (
+            h, bad.size, bad[0], got[bad[0]], want[bad[0]])
+        p = part.cpu().numpy()
+        assert p[0] == want_saa["m"] and p[1] == want_saa["infeasible"]
+        assert p[2] == want_saa["sum"] and (int(p[4]) << 32) + int(p[3]) == want_saa["sumsq"]
+        if want_saa["m"] > 0:
+            est = spdp.saa_mean(part)
+            assert est["mean"] == want_saa["mean"]
+            assert est["var"] == pytest.approx(want_saa["var"], rel=1e-12, abs=1e-12)
+    return want
+
+
+def test_split_config1_brute_force(spdp):
+    cfg = synth.config_instance("C1")
+    inst = cfg["inst"]
+    dem = oracle.gen_demands(cfg["model"], 0, 100, ld=104)
+    want = _check_split(spdp, inst, dem, 100)
+    import pyref
+    for s in range(100):
+        q_tour = [int(dem[c - 1, s]) for c in inst["tour"]]
+        bf, _ = pyref.brute_force_split(inst["tour"].tolist(), q_tour, inst["dist"].tolist(), inst["Q"])
+        assert want[s] == bf
+
+
+@pytest.mark.parametrize("name,S", [("C2", 20_011), ("C3", 3_001), ("C4", 1_203)])
+def test_split_configs_multi_tile_ragged(spdp, name, S):
+    cfg = synth.config_instance(name)
+    dem = oracle.gen_demands(cfg["model"], 0, S, ld=spdp.padded_ld(S))
+    _check_split(spdp, cfg["inst"], dem, S)
+
+
+def test_split_edge_cases(spdp):
+    rng = np.random.default_rng(0)
+    # n = 1; zero demands (window = whole tour -> general kernel); q == Q; q > Q (infeasible);
+    # Q larger than every load.
+    for n in (1, 2, 7, 33, 300):
+        inst = synth.make_instance(n, seed=n, r=3.0)
+        Q = inst["Q"]
+        S = 777
+        rows = rng.integers(0, Q + 1, size=(S, n))
+        rows[0] = 0
+        rows[1] = Q
+        rows[2, rng.integers(0, n)] = Q + 1
+        rows[3:40] = rng.integers(0, 2, size=(37, n))
+        dem = synth.explicit_demands(rows.tolist())
+        _check_split(spdp, inst, dem, S, hints=(0, 8, 64))
+        _check_split(spdp, inst, dem, S, hints=(16,), Q=2**31 - 1)
+
+
+def test_split_all_infeasible_partial(spdp):
+    inst = synth.make_instance(5, seed=1)
+    dem = synth.explicit_demands([[inst["Q"] + 1] * 5] * 9)
+    cost, part = spdp.split_eval(to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem), inst["Q"], S=9)
+    assert (cost.cpu().numpy() == spdp.INFEASIBLE).all()
+    assert part.cpu().numpy()[1] == 9
+    with pytest.raises(spdp.SpdpError):
+        spdp.saa_mean(part)
+
+
+# ------------------------------------------------------------------ a8 batched tours
+def test_split_batch_tours(spdp):
+    inst = synth.make_instance(150, seed=9, r=6.0)
+    tours = synth.perturb_tours(inst["tour"], 37, 3)
+    model = synth.demand_model(inst["nominal"], inst["Q"], seed=5)
+    S = 2_500
+    dem = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
+    want = oracle.split_tours(tours, inst["dist"], dem, inst["Q"], S=S)
+    for h in (0, 16, 32):
+        cost, part = spdp.split_eval_batch(to_dev(tours), to_dev(inst["dist"]), to_dev(dem), inst["Q"], S=S,
+                                           window_hint=h)
+        assert np.array_equal(cost.cpu().numpy().astype(np.int64), oracle_cost_as_i32(want))
+        p = part.cpu().numpy()
+        for t in range(tours.shape[0]):
+            w = oracle.saa(want[t])
+            assert p[t, 0] == w["m"] and p[t, 2] == w["sum"] and (int(p[t, 4]) << 32) + int(p[t, 3]) == w["sumsq"]
+
+
+# ------------------------------------------------------------------ validation / errors
+def test_validation_errors(spdp):
+    inst = synth.make_instance(10, seed=2)
+    dem = to_dev(synth.explicit_demands([[1] * 10] * 8))
+    bad_tour = inst["tour"].copy()
+    bad_tour[0] = bad_tour[1]
+    with pytest.raises(spdp.SpdpError) as e:
+        spdp.split_eval(to_dev(bad_tour), to_dev(inst["dist"]), dem, inst["Q"], validate=True)
+    assert e.value.status == spdp.SPDP_E_DATA
+    with pytest.raises(spdp.SpdpError) as e:
+        spdp.split_eval(to_dev(inst["tour"]), to_dev(inst["dist"]), dem, 0)
+    assert e.value.status == spdp.SPDP_E_USAGE
+    neg = inst["dist"].copy()
+    neg[0, inst["tour"][0]] = -1
+    with pytest.raises(spdp.SpdpError):
+        spdp.split_eval(to_dev(inst["tour"]), to_dev(neg), dem, inst["Q"], validate=True)
+
+
+# ------------------------------------------------------------------ e2e host path
+def test_host_entry_matches_device(spdp):
+    cfg = synth.config_instance("C2")
+    inst = cfg["inst"]
+    S = 10_007
+    dem = oracle.gen_demands(cfg["model"], 0, S, ld=S + 5)  # ragged host ld
+    want = oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], S=S)
+    cost_h = np.zeros(S, dtype=np.int32)
+    est = spdp.split_eval_host(inst["tour"], inst["dist"], dem, inst["Q"], S=S, cost_h=cost_h, window_hint=16)
+    assert np.array_equal(cost_h.astype(np.int64), oracle_cost_as_i32(want))
+    assert est["mean"] == oracle.saa(want)["mean"]
+
+
+# ------------------------------------------------------------------ a9 / a10 IRP
+def test_irp_parity(spdp):
+    cfg = synth.irp_config(S=301)
+    irp = cfg["irp"]
+    H, M = irp["H"], irp["M"]
+    dem = oracle.gen_demands(cfg["model"], 0, 301, ld=304)
+    want = oracle.irp(H, M, irp["visit"], irp["cust"], dem, S=301)
+    cost, part = spdp.irp_dp(irp["visit"], irp["cust"], to_dev(dem), H, M, S=301)
+    assert np.array_equal(cost.cpu().numpy(), want)
+    assert part.cpu().numpy()[2] == int(want.sum())
+
+
+def test_irp_random_small(spdp):
+    rng = np.random.default_rng(4)
+    for trial in range(12):
+        H, M = int(rng.integers(1, 9)), int(rng.integers(1, 4))
+        visit = rng.integers(0, 2, size=(M, H)).astype(np.uint8)
+        cust = []
+        for _ in range(M):
+            U = int(rng.integers(0, 200 if trial % 2 else 40))
+            X = int(rng.integers(0, U + 5))
+            cust.append([U, X, int(rng.integers(0, U + 1)), int(rng.integers(0, 4)), int(rng.integers(0, 30)),
+                         int(rng.integers(0, 4))])
+        cust = np.array(cust, dtype=np.int32)
+        S = 67
+        dem = rng.integers(0, 60, size=(H * M, 72)).astype(np.uint16)
+        want = oracle.irp(H, M, visit, cust, dem, S=S)
+        cost, _ = spdp.irp_dp(visit, cust, to_dev(dem), H, M, S=S)
+        assert np.array_equal(cost.cpu().numpy(), want), "trial %d" % trial
