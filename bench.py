@@ -240,6 +240,8 @@ def main():
     ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for e in ev_s + ev_e:  # torch creates the CUDA event lazily, on its first record
+        e.record(stream)
     props = torch.cuda.get_device_properties(dev)
     try:
         smi_id = "%08X:%02X:%02X.0" % (props.pci_domain_id, props.pci_bus_id, props.pci_device_id)

@@ -110,10 +110,13 @@ def _check(rc: int, where: str):
 
 def set_profile_events(start=None, stop=None):
     """Record torch.cuda.Event pair (start, stop) around the dominant kernel of the next calls
-    on this thread (the sweep / IRP kernel); call with no arguments to clear."""
+    on this thread (the sweep / IRP kernel); call with no arguments to clear.  The events must
+    already exist (torch creates them lazily: record them once first)."""
     if start is None or stop is None:
         _lib.spdp_set_profile_events(None, None)
     else:
+        if not start.cuda_event or not stop.cuda_event:
+            raise ValueError("set_profile_events: events not created yet (record them once first)")
         _lib.spdp_set_profile_events(ctypes.c_void_p(start.cuda_event), ctypes.c_void_p(stop.cuda_event))
 
 

@@ -19,6 +19,8 @@
 // cooperates on one scenario's window with a shuffle min.
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -26,8 +28,15 @@ namespace spdp {
 
 // ---------------------------------------------------------------- workspace
 struct WsLayout {
-    size_t hdr, tickets, g0, tabs, bpart, ovf, total;
+    size_t hdr, tickets, g0, tabs, tabsf, tinfo, bpart, ovf, total;
     int64_t nblocks;
+};
+
+// Per-tour info for the fp32 sweep: g0f = (g(0) + OFF) / 2^24 (float bits),
+// off = OFF = D[n] (makes every g(p) + OFF >= 0), ok = every value the fp32
+// sweep forms is an integer (times 2^-24) below 2^24, hence exact.
+struct TourInfo {
+    int32_t g0f_bits, off, ok, pad;
 };
 
 constexpr int kSweepThreads = 256;
@@ -41,6 +50,8 @@ inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
     L.tickets = off; off = align_up(off + sizeof(unsigned) * (size_t)T, 256);
     L.g0 = off; off = align_up(off + sizeof(int32_t) * (size_t)T, 256);
     L.tabs = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
+    L.tabsf = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
+    L.tinfo = off; off = align_up(off + sizeof(TourInfo) * (size_t)T, 256);
     L.bpart = off; off = align_up(off + sizeof(spdp_saa_partial) * (size_t)T * (size_t)L.nblocks, 256);
     L.ovf = off; off = align_up(off + sizeof(unsigned long long) * (size_t)T * (size_t)S, 256);
     L.total = off;
@@ -57,11 +68,14 @@ enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
 __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restrict__ tours, int n,
                                                          const int32_t* __restrict__ dist,
                                                          int2* __restrict__ tabs, int32_t* __restrict__ g0,
+                                                         int2* __restrict__ tabsf, TourInfo* __restrict__ tinfo,
                                                          unsigned* __restrict__ hdr, unsigned* __restrict__ tickets,
                                                          int validate) {
     extern __shared__ unsigned char smem_raw[];
     long long* wsum = reinterpret_cast<long long*>(smem_raw);              // 32 warp sums
-    unsigned* seen = reinterpret_cast<unsigned*>(smem_raw + 32 * sizeof(long long));  // bitmap
+    long long* dn = wsum + 32;                                             // D[n]
+    int* cmx = reinterpret_cast<int*>(dn + 1);                             // block max of the used costs
+    unsigned* seen = reinterpret_cast<unsigned*>(smem_raw + 34 * sizeof(long long));  // bitmap
     const int t = blockIdx.x;
     const int32_t* tour = tours + (int64_t)t * n;
     int2* tab = tabs + (int64_t)t * (n + kTabPad);
@@ -70,7 +84,10 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     const int lane = tid & 31, wid = tid >> 5;
 
     if (t == 0 && tid == 0) hdr[HDR_OVF_COUNT] = 0u;
-    if (tid == 0) tickets[t] = 0u;
+    if (tid == 0) {
+        tickets[t] = 0u;
+        *cmx = 0;
+    }
     if (validate) {
         for (int i = tid; i < (n + 32) / 32; i += nt) seen[i] = 0u;
         __syncthreads();
@@ -123,6 +140,8 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     }
     __syncthreads();
     long long D = wsum[wid] + incl - local;  // D at position lo+1 (1-based): sum of arcs before lo
+    if (lo <= n - 1 && n - 1 < hi) *dn = D + local;  // D[n] = all arcs
+    atomicMax(cmx, cmax);
     for (int i = lo; i < hi; ++i) {
         const int a = node(i);
         const int ca0 = dist[(int64_t)a * N1];
@@ -140,82 +159,253 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     }
     for (int i = n + tid; i < n + kTabPad; i += nt) tab[i] = make_int2(0, 0);
     if (tid == 0) g0[t] = dist[node(0)];
+    __syncthreads();
+    // fp32 tables: cg / 2^24 (exact: |cg| <= 2 cmax), g0f = (g0 + OFF) / 2^24
+    {
+        const long long OFF = *dn, cm = *cmx;
+        int2* tabf = tabsf + (int64_t)t * (n + kTabPad);
+        for (int i = tid; i < n + kTabPad; i += nt) {
+            const int2 e = tab[i];
+            tabf[i] = make_int2(e.x, __float_as_int((float)e.y * 0x1p-24f));
+        }
+        if (tid == 0) {
+            TourInfo ti;
+            ti.g0f_bits = __float_as_int((float)(dist[node(0)] + OFF) * 0x1p-24f);
+            ti.off = (int)(OFF < INT_MAX ? OFF : INT_MAX);
+            // g + OFF <= (2n + 1) cmax + OFF and f(n) + OFF <= 2 n cmax + OFF: all below 2^24
+            ti.ok = ((2LL * n + 2) * cm + OFF < (1LL << 24)) ? 1 : 0;
+            ti.pad = 0;
+            tinfo[t] = ti;
+        }
+    }
     // range: |g|, |f| <= 3 n cmax (SURVEY §7 hard part 10)
     if ((long long)cmax * (3LL * n + 1) >= (long long)INT_MAX) bad |= ST_RANGE;
     if (bad) atomicOr(&hdr[HDR_STATUS], bad);
 }
 
 // ---------------------------------------------------------------- a5: the sweep
-// One scenario per thread.  The candidate ring holds, for the last W split
-// points p (slot p mod W): G = g(p) and Y = P'(p) + Q, where P'(p) = 1 + sum of
-// the first p tour-order demands.  p is in the Eq. (3) window of layer i iff
-// P'(i) - P'(p) <= Q  <=>  Y >= P'(i).  Because q >= 0 the
-// window is a contiguous suffix (DESIGN R5), so the candidate loop walks from
-// the newest slot backwards and leaves as soon as no lane of the warp has a
-// feasible candidate left.  The layer loop is unrolled by W so every ring
-// index is a compile-time register name.  A scenario whose window would
-// exceed the ring (the slot being evicted is still feasible) is appended to
-// the overflow list and finished by split_general_kernel.
-template <int W, int PD>
-__global__ void __launch_bounds__(kSweepThreads, (W <= 16 ? 2 : 1))
-    split_sweep_kernel(const int2* __restrict__ tabs, const int32_t* __restrict__ g0s, int n,
-                       const uint16_t* __restrict__ demand, int64_t ld, int64_t S, uint32_t Q,
-                       int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ bpart,
-                       spdp_saa_partial* __restrict__ partial, unsigned* __restrict__ tickets,
-                       unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ ovf_count) {
-    static_assert(W % PD == 0, "PD must divide W");
-    extern __shared__ int2 stab[];  // n + kTabPad entries
+// One scenario per thread, 256 scenarios per CTA.  The candidate ring holds, for
+// the last W split points p (slot p mod W): G = g(p) and Y = P'(p) + Q, where
+// P'(p) = 1 + sum of the first p tour-order demands.  p is in the Eq. (3)
+// window of layer i iff P'(i) - P'(p) <= Q  <=>  Y >= P'(i).
+// Because q >= 0 the window is a contiguous suffix (DESIGN R5), so the
+// candidate loop walks from the newest slot backwards and leaves as soon as no
+// lane of the warp has a feasible candidate left.  The layer loop is unrolled
+// by W so every ring index is a compile-time register name.  A scenario whose
+// window would exceed the ring (the slot being evicted is still feasible) is
+// appended to the overflow list and finished by split_general_kernel.
+//
+// Demand stream: the CTA's tile [n rows (tour order) x 256 scenarios] is staged
+// through shared memory in chunks of W rows by bulk-async copies (the TMA
+// engine, one 512-byte copy per row, gathered by the tour) into an NS-deep ring
+// of stages guarded by mbarriers, so NS-1 chunks are always in flight while
+// the CTA computes on the current one.
+template <int W>
+struct SweepCfg {
+    static constexpr int NS = (W <= 8) ? 6 : (W <= 16 ? 4 : (W <= 32 ? 3 : 2));  // stages
+    static constexpr int kStageElems = W * kSweepThreads;                        // u16 per stage
+    static constexpr size_t kStageBytes = sizeof(uint16_t) * kStageElems;
+    static constexpr int kHdr = 128;  // NS mbarriers (8 B) + NS stage-consumption counters (4 B)
+    static size_t smem_bytes(int n) {
+        return kHdr + NS * kStageBytes + sizeof(int2) * (size_t)(n + kTabPad);
+    }
+};
+
+// Value / load types of the two sweep variants.  int: exact int32 with a
+// predicated min per candidate (ISETP + VIMNMX on the ALU pipe).  fp32:
+// integer-valued floats scaled by 2^-24 (exact, TourInfo::ok), each candidate
+// masked branch-free on the FMA pipe -- s = sat(P'(i) - Y), c = sat(G + s) is G
+// when feasible and 1.0 (above every G < 1) when not -- and folded with a
+// 3-input min (FMNMX3), so the ALU pipe carries half an op per candidate.
+template <bool F32>
+struct SweepT {
+    using V = int;
+    using L = uint32_t;
+};
+template <>
+struct SweepT<true> {
+    using V = float;
+    using L = float;
+};
+
+template <int W, int VE, bool F32>
+__global__ void __launch_bounds__(kSweepThreads, (W <= 16 ? 4 : 1))
+    split_sweep_kernel(const int2* __restrict__ tabs, const int32_t* __restrict__ g0s,
+                       const TourInfo* __restrict__ tinfo, int n, const uint16_t* __restrict__ demand,
+                       int64_t ld, int64_t S, uint32_t Q, int32_t* __restrict__ cost,
+                       spdp_saa_partial* __restrict__ bpart, spdp_saa_partial* __restrict__ partial,
+                       unsigned* __restrict__ tickets, unsigned long long* __restrict__ ovf_list,
+                       unsigned* __restrict__ ovf_count) {
+    using Cfg = SweepCfg<W>;
+    using V = typename SweepT<F32>::V;
+    using LT = typename SweepT<F32>::L;
+    constexpr int NS = Cfg::NS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);                             // NS mbarriers
+    unsigned* done = reinterpret_cast<unsigned*>(smem_raw + 64);                       // NS counters
+    uint16_t* dbuf = reinterpret_cast<uint16_t*>(smem_raw + Cfg::kHdr);                // NS x W x 256
+    int2* stab = reinterpret_cast<int2*>(smem_raw + Cfg::kHdr + NS * Cfg::kStageBytes);  // n + kTabPad
     __shared__ Part red[kSweepThreads / 32];
     __shared__ bool am_last;
+
     const int t = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t s0 = (int64_t)blockIdx.x * kSweepThreads;
+    const int cols = (int)((S - s0) < kSweepThreads ? (S - s0) : kSweepThreads);
+    const uint32_t row_bytes = (uint32_t)(((cols + 7) & ~7) * sizeof(uint16_t));
+    const int nchunks = (n + W - 1) / W;
     {
         const int2* tab = tabs + (int64_t)t * (n + kTabPad);
-        for (int i = threadIdx.x; i < n + kTabPad; i += blockDim.x) stab[i] = tab[i];
+        for (int i = tid; i < n + kTabPad; i += kSweepThreads) stab[i] = tab[i];
+    }
+    if (tid == 0) {
+        for (int k = 0; k < NS; ++k) {
+            mbar_init(&bar[k], 1);
+            done[k] = 0u;
+        }
+        fence_mbar_init();
     }
     __syncthreads();
-    const int64_t s_raw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = s_raw < S;
-    const int64_t s = live ? s_raw : S - 1;  // tail lanes replay a real scenario
-    const uint16_t* col = demand + s;
+    const uint64_t pol = policy_evict_first();
+    // producer: one warp refills stage (c % NS) with chunk c (rows c*W .. c*W+W-1)
+    auto issue = [&](int c) {
+        const int stage = c % NS;
+        const int r0 = c * W;
+        const int rows = (n - r0) < W ? (n - r0) : W;
+        if (lane == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&bar[stage], row_bytes * (uint32_t)rows);
+        }
+        __syncwarp();
+        for (int r = lane; r < rows; r += 32)
+            bulk_g2s(dbuf + (size_t)stage * Cfg::kStageElems + r * kSweepThreads,
+                     demand + (int64_t)stab[r0 + r].x * ld + s0, row_bytes, &bar[stage], pol);
+    };
+    if (wid == 0)
+        for (int c = 0; c < NS && c < nchunks; ++c) issue(c);
 
-    uint32_t qb[PD];
-#pragma unroll
-    for (int k = 0; k < PD; ++k) qb[k] = ld_stream_u16(col + (int64_t)stab[k].x * ld);
+    const bool live = tid < cols;
+    const int col = live ? tid : cols - 1;  // tail lanes replay a real scenario
+    const int64_t s = s0 + col;
 
-    int G[W];
-    uint32_t Y[W];
+    V G[W];
+    LT Y[W];
+    V gprev;
+    LT P, Qv;
+    bool f32_ok = true;
+    if constexpr (F32) {
+        const TourInfo ti = tinfo[t];
+        f32_ok = ti.ok != 0;
+        gprev = __int_as_float(ti.g0f_bits);
+        P = 0.0f;
+        Qv = (float)Q;
 #pragma unroll
-    for (int k = 0; k < W; ++k) {
-        G[k] = INT_MAX;
-        Y[k] = 0u;  // never feasible: P' >= 1
+        for (int k = 0; k < W; ++k) {
+            G[k] = 0.0f;
+            Y[k] = -1.0f;  // never feasible: P' >= 0
+        }
+    } else {
+        gprev = g0s[t];
+        P = 1u;
+        Qv = Q;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            G[k] = INT_MAX;
+            Y[k] = 0u;  // never feasible: P' >= 1
+        }
     }
-    int gprev = g0s[t];
-    uint32_t P = 1u;
-    bool bad = false, ovf = false;
+    uint32_t qmax = 0u;   // bad  <=> some q > Q  (Eq. (2) set empty, DESIGN R4)
+    V ovfacc = (V)-1;     // ovf  <=> some evicted slot still feasible: max(Y - P'(i)) >= 0
 
-    for (int i0 = 0; i0 < n; i0 += W) {
+    // One layer (computes f(L+1)); j = L mod W is a compile-time constant.
+    auto layer = [&](const uint16_t* buf, const int j, const int L) {
+        const uint32_t qi = buf[j * kSweepThreads];
+        qmax = max(qmax, qi);
+        LT Pn;
+        if constexpr (F32) {
+            Pn = P + __uint2float_rn(qi);
+            ovfacc = fmaxf(ovfacc, Y[j] - Pn);
+        } else {
+            Pn = P + qi;
+            ovfacc = max(ovfacc, (int)(Y[j] - Pn));
+        }
+        G[j] = gprev;
+        Y[j] = P + Qv;
+        V best = gprev;  // p = L
+        if constexpr (F32) {
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
-            const int L = i0 + j;  // computes f(L+1)
-            if (L >= n) break;
-            const uint32_t q = qb[j % PD];
-            qb[j % PD] = ld_stream_u16(col + (int64_t)stab[L + PD].x * ld);
-            const uint32_t Pn = P + q;
-            bad |= (q > Q);
-            ovf |= (Y[j] >= Pn);  // evicted p = L - W still in window(L+1)
-            G[j] = gprev;
-            Y[j] = P + Q;
-            int best = gprev;     // p = L
+            for (int k0 = 1; k0 < W; k0 += VE) {
+                if (!__any_sync(kFull, Y[(j - k0 + W) % W] >= Pn)) break;
+                float c[VE];
+#pragma unroll
+                for (int u = 0; u < VE; ++u) {
+                    const int k = k0 + u;
+                    const int sl = (j - k + W) % W;
+                    c[u] = (k < W) ? __saturatef(G[sl] + __saturatef(Pn - Y[sl])) : 1.0f;
+                }
+#pragma unroll
+                for (int u = 0; u + 1 < VE; u += 2) best = fminf(best, fminf(c[u], c[u + 1]));
+                if (VE & 1) best = fminf(best, c[VE - 1]);
+            }
+            gprev = best + __int_as_float(stab[L].y);
+        } else {
+            V best1 = best;  // second accumulator: two independent min chains
 #pragma unroll
             for (int k = 1; k < W; ++k) {
                 const int sl = (j - k + W) % W;
                 const bool f = Y[sl] >= Pn;
-                if ((k & 1) && !__any_sync(kFull, f)) break;
-                if (f) best = min(best, G[sl]);
+                if ((k % VE) == 1 % VE && !__any_sync(kFull, f)) break;
+                if (f) {
+                    if (k & 1) best1 = min(best1, G[sl]);
+                    else best = min(best, G[sl]);
+                }
             }
-            gprev = best + stab[L].y;
-            P = Pn;
+            gprev = min(best, best1) + stab[L].y;
         }
+        P = Pn;
+    };
+
+    // The final chunk is padded to W layers with demand q_pad = min(Q, 65535) and cg = 0:
+    // a demand of Q collapses every window to the newest slot, so the padded layers
+    // never flag an overflow and never disturb the ring slot that holds f(n).
+    const int rem = n % W;
+    const uint32_t qpad = Q < 65535u ? Q : 65535u;
+    constexpr int NW = kSweepThreads / 32;
+    for (int c = 0; c < nchunks; ++c) {
+        const int stage = c % NS;
+        mbar_wait(&bar[stage], (uint32_t)((c / NS) & 1));
+        uint16_t* bufw = dbuf + (size_t)stage * Cfg::kStageElems + col;
+        if (rem != 0 && c == nchunks - 1)
+            for (int j = rem; j < W; ++j) bufw[j * kSweepThreads] = (uint16_t)qpad;
+        const uint16_t* buf = bufw;
+        const int i0 = c * W;
+#pragma unroll
+        for (int j = 0; j < W; ++j) layer(buf, j, i0 + j);
+        // release the stage: the last warp to finish it refills it (no CTA-wide barrier,
+        // so warps with narrow windows run ahead of warps with wide ones)
+        __syncwarp();
+        unsigned last = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            last = (atomicAdd(&done[stage], 1u) == NW - 1);
+            if (last) done[stage] = 0u;
+        }
+        last = __shfl_sync(kFull, last, 0);
+        if (last && c + NS < nchunks) issue(c + NS);
+    }
+    // f(n): the slot of position n holds it (pushed by the first padded layer), or gprev if n % W == 0
+    if (rem != 0) {
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+            if (k == rem) gprev = G[k];
+    }
+    const bool bad = qmax > Q;
+    const bool ovf = (ovfacc >= (V)0) || !f32_ok;
+    int fval;
+    if constexpr (F32) {
+        fval = (int)(gprev * 0x1p24f) - tinfo[t].off;
+    } else {
+        fval = gprev;
     }
 
     const bool deferred = live && ovf && !bad;
@@ -223,13 +413,13 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 16 ? 2 : 1))
         const unsigned long long key = ((unsigned long long)t << 40) | (unsigned long long)s;
         ovf_list[atomicAdd(ovf_count, 1u)] = key;
     }
-    if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : gprev;
+    if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
     if (partial == nullptr) return;
 
     Part p{0, 0, 0, 0, 0};
-    if (live && !deferred) part_add_cost(p, gprev, !bad);
+    if (live && !deferred) part_add_cost(p, fval, !bad);
     Part r = block_sum(p, red);
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         part_store(&bpart[(int64_t)t * gridDim.x + blockIdx.x], r);
         __threadfence();
         am_last = (atomicAdd(&tickets[t], 1u) == gridDim.x - 1);
@@ -239,7 +429,7 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 16 ? 2 : 1))
     __threadfence();
     Part acc{0, 0, 0, 0, 0};
     const spdp_saa_partial* bp = bpart + (int64_t)t * gridDim.x;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    for (int b = tid; b < (int)gridDim.x; b += kSweepThreads) {
         acc.n_feas += __ldcg(&bp[b].n_feas);
         acc.n_infeas += __ldcg(&bp[b].n_infeas);
         acc.sum += __ldcg(&bp[b].sum);
@@ -248,7 +438,7 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 16 ? 2 : 1))
     }
     __syncthreads();
     Part tot = block_sum(acc, red);
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         part_store(&partial[t], tot);
         tickets[t] = 0u;
     }
@@ -403,25 +593,79 @@ __global__ void __launch_bounds__(256) saa_reduce_kernel(const int32_t* __restri
 }
 
 // ---------------------------------------------------------------- host dispatch
-template <int W>
-static spdp_status launch_sweep(dim3 grid, size_t smem, cudaStream_t st, const int2* tabs, const int32_t* g0, int n,
-                                const uint16_t* demand, int64_t ld, int64_t S, uint32_t Q, int32_t* cost,
-                                spdp_saa_partial* bpart, spdp_saa_partial* partial, unsigned* tickets,
-                                unsigned long long* ovf_list, unsigned* ovf_count) {
-    constexpr int PD = W < 16 ? W : 16;
-    auto kern = split_sweep_kernel<W, PD>;
+struct SweepArgs {
+    const int2* tabs;
+    const int2* tabsf;
+    const int32_t* g0;
+    const TourInfo* tinfo;
+    int n;
+    const uint16_t* demand;
+    int64_t ld, S;
+    uint32_t Q;
+    int32_t* cost;
+    spdp_saa_partial* bpart;
+    spdp_saa_partial* partial;
+    unsigned* tickets;
+    unsigned long long* ovf;
+    unsigned* ovf_count;
+};
+
+template <int W, int VE, bool F32>
+static spdp_status launch_sweep_t(dim3 grid, cudaStream_t st, const SweepArgs& a) {
+    auto kern = split_sweep_kernel<W, VE, F32>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e == cudaSuccess)  // all of the unified L1/smem as shared memory: occupancy is smem-bound
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_sweep)");
         attr_set = true;
     }
     prof_begin(st);
-    kern<<<grid, kSweepThreads, smem, st>>>(tabs, g0, n, demand, ld, S, Q, cost, bpart, partial, tickets, ovf_list,
-                                            ovf_count);
+    kern<<<grid, kSweepThreads, SweepCfg<W>::smem_bytes(a.n), st>>>(F32 ? a.tabsf : a.tabs, a.g0, a.tinfo, a.n, a.demand,
+                                                                    a.ld, a.S, a.Q, a.cost, a.bpart, a.partial,
+                                                                    a.tickets, a.ovf, a.ovf_count);
     spdp_status rc = last_launch("split_sweep_kernel");
     prof_end(st);
     return rc;
+}
+
+// Tuning knobs (environment, read once): SPDP_SWEEP=auto|int|f32 selects the
+// candidate arithmetic; SPDP_VOTE_EVERY selects the warp-vote stride.
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+static int sweep_mode() {  // 0 auto, 1 int, 2 f32
+    static int m = [] {
+        const char* e = getenv("SPDP_SWEEP");
+        if (!e) return 0;
+        if (!strcmp(e, "int")) return 1;
+        if (!strcmp(e, "f32")) return 2;
+        return 0;
+    }();
+    return m;
+}
+
+static spdp_status launch_sweep(int W, bool f32, dim3 grid, cudaStream_t st, const SweepArgs& a) {
+    static const int ve = env_int("SPDP_VOTE_EVERY", 4);
+    if (f32) {
+        switch (W) {
+            case 8: return ve == 2 ? launch_sweep_t<8, 2, true>(grid, st, a) : launch_sweep_t<8, 4, true>(grid, st, a);
+            case 16:
+                return ve == 2 ? launch_sweep_t<16, 2, true>(grid, st, a)
+                               : (ve == 8 ? launch_sweep_t<16, 8, true>(grid, st, a) : launch_sweep_t<16, 4, true>(grid, st, a));
+            default:
+                return ve == 8 ? launch_sweep_t<32, 8, true>(grid, st, a) : launch_sweep_t<32, 4, true>(grid, st, a);
+        }
+    }
+    switch (W) {
+        case 8: return ve == 2 ? launch_sweep_t<8, 2, false>(grid, st, a) : launch_sweep_t<8, 4, false>(grid, st, a);
+        case 16: return ve == 2 ? launch_sweep_t<16, 2, false>(grid, st, a) : launch_sweep_t<16, 4, false>(grid, st, a);
+        case 32: return ve == 2 ? launch_sweep_t<32, 2, false>(grid, st, a) : launch_sweep_t<32, 4, false>(grid, st, a);
+        default: return launch_sweep_t<64, 4, false>(grid, st, a);
+    }
 }
 
 static int pick_w(int hint) {
@@ -454,6 +698,8 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     unsigned* tickets = reinterpret_cast<unsigned*>(w + L.tickets);
     int32_t* g0 = reinterpret_cast<int32_t*>(w + L.g0);
     int2* tabs = reinterpret_cast<int2*>(w + L.tabs);
+    int2* tabsf = reinterpret_cast<int2*>(w + L.tabsf);
+    TourInfo* tinfo = reinterpret_cast<TourInfo*>(w + L.tinfo);
     spdp_saa_partial* bpart = reinterpret_cast<spdp_saa_partial*>(w + L.bpart);
     unsigned long long* ovf = reinterpret_cast<unsigned long long*>(w + L.ovf);
     // Q above the largest possible load behaves as "everything fits"; clamp so P' + Q fits uint32.
@@ -466,8 +712,8 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     }
     {
         const int threads = 1024;
-        const size_t smem = 32 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
-        tour_prep_kernel<<<T, threads, smem, st>>>(tours, n, dist, tabs, g0, hdr, tickets, validate ? 1 : 0);
+        const size_t smem = 34 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
+        tour_prep_kernel<<<T, threads, smem, st>>>(tours, n, dist, tabs, g0, tabsf, tinfo, hdr, tickets, validate ? 1 : 0);
         if ((rc = last_launch("tour_prep_kernel"))) return rc;
     }
     int W = pick_w(window_hint);
@@ -489,14 +735,15 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         if (window_hint == 0) W = pick_w((int)(h[HDR_SAMPLE_W] + h[HDR_SAMPLE_W] / 4 + 1));
     }
     const dim3 grid((unsigned)L.nblocks, (unsigned)T);
-    const size_t smem = sizeof(int2) * (size_t)(n + kTabPad);
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
-    switch (W) {
-        case 8: rc = launch_sweep<8>(grid, smem, st, tabs, g0, n, demand, ld, S, Qe, cost, bpart, partial, tickets, ovf, ovf_count); break;
-        case 16: rc = launch_sweep<16>(grid, smem, st, tabs, g0, n, demand, ld, S, Qe, cost, bpart, partial, tickets, ovf, ovf_count); break;
-        case 32: rc = launch_sweep<32>(grid, smem, st, tabs, g0, n, demand, ld, S, Qe, cost, bpart, partial, tickets, ovf, ovf_count); break;
-        default: rc = launch_sweep<64>(grid, smem, st, tabs, g0, n, demand, ld, S, Qe, cost, bpart, partial, tickets, ovf, ovf_count); break;
-    }
+    const SweepArgs args{tabs, tabsf, g0, tinfo, n, demand, ld, S, Qe, cost, bpart, partial, tickets, ovf, ovf_count};
+    // fp32 sweep when every load value it forms (P' <= n min(Q, 65535) for feasible scenarios,
+    // Y = P' + Q) is an exact float; the per-tour cost range is checked on the device (TourInfo::ok)
+    const int64_t qeff = Qe < 65535u ? (int64_t)Qe : 65535;
+    const bool f32_loads_exact = ((int64_t)n + 64) * qeff + (int64_t)Qe + 1 < (1LL << 24);  // + padded layers
+    const int mode = sweep_mode();
+    const bool use_f32 = W <= 32 && (mode == 2 || (mode == 0 && f32_loads_exact)) && (mode != 2 || f32_loads_exact);
+    rc = launch_sweep(W, use_f32, grid, st, args);
     if (rc) return rc;
     {
         // overflow list: warps per CTA limited by the per-warp smem (g and prefix: 8 (n+1) bytes)
