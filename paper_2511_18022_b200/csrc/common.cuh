@@ -83,6 +83,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// ---- cp.async (LDGSTS): per-thread 16-byte global -> shared copies, L2-only (.cg) ----
+// (no L2 cache-policy operand: ptxas 12.9 can place the policy descriptor in a misaligned
+// uniform register pair for LDGSTS, which traps as an illegal instruction)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Warp + block reduction of the SAA partial fields.
 struct Part {
     long long n_feas, n_infeas, sum, sq_lo, sq_hi;

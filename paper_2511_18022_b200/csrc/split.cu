@@ -27,11 +27,6 @@
 namespace spdp {
 
 // ---------------------------------------------------------------- workspace
-struct WsLayout {
-    size_t hdr, tickets, g0, tabs, tabsf, tinfo, bpart, ovf, total;
-    int64_t nblocks;
-};
-
 // Per-tour info for the fp32 sweep: g0f = (g(0) + OFF) / 2^24 (float bits),
 // off = OFF = D[n] (makes every g(p) + OFF >= 0), ok = every value the fp32
 // sweep forms is an integer (times 2^-24) below 2^24, hence exact.
@@ -39,37 +34,46 @@ struct TourInfo {
     int32_t g0f_bits, off, ok, pad;
 };
 
-constexpr int kSweepThreads = 256;
-constexpr int kTabPad = 64;  // padding rows so the prefetch never reads past the table
+constexpr int kTabPad = 64;       // padding rows after each tour table
+constexpr int kSlots = 32;  // SAA partial slots per tour (spread the sweep's atomics)
+
+// Cg planes: per tour [2][cg_stride(n)] int32 (plane 0 int Cg, plane 1 fp32 Cg / 2^24 bits), zero padded;
+// the stride keeps every chunk's W-entry slice 16-byte aligned for the bulk copies.
+__host__ __device__ inline int cg_stride(int n) { return (n + kTabPad + 7) & ~7; }
+
+struct WsLayout {
+    size_t hdr, g0, tinfo, tabs, tabsf, cgs, slots, ovf, total;
+};
 
 inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
     WsLayout L;
     size_t off = 0;
-    L.nblocks = ceil_div(S, kSweepThreads);
     L.hdr = off; off += 256;
-    L.tickets = off; off = align_up(off + sizeof(unsigned) * (size_t)T, 256);
     L.g0 = off; off = align_up(off + sizeof(int32_t) * (size_t)T, 256);
+    L.tinfo = off; off = align_up(off + sizeof(TourInfo) * (size_t)T, 256);
     L.tabs = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
     L.tabsf = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
-    L.tinfo = off; off = align_up(off + sizeof(TourInfo) * (size_t)T, 256);
-    L.bpart = off; off = align_up(off + sizeof(spdp_saa_partial) * (size_t)T * (size_t)L.nblocks, 256);
+    L.cgs = off; off = align_up(off + sizeof(int32_t) * 2 * (size_t)T * (size_t)cg_stride(n), 256);
+    L.slots = off; off = align_up(off + sizeof(spdp_saa_partial) * (size_t)T * (size_t)kSlots, 256);
     L.ovf = off; off = align_up(off + sizeof(unsigned long long) * (size_t)T * (size_t)S, 256);
     L.total = off;
     return L;
 }
 
 // header words
-enum { HDR_OVF_COUNT = 0, HDR_STATUS = 1, HDR_SAMPLE_W = 2 };
+enum { HDR_OVF_COUNT = 0, HDR_STATUS = 1, HDR_SAMPLE_W = 2, HDR_TILE = 3 };
 enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
 
 // ---------------------------------------------------------------- a2: tour prep
 // One CTA per tour.  tab[i] = {row of customer s_{i+1}, Cg[i]} (0-based layer i
 // computes f(i+1)); tab[n-1].y = B[n].  g0[t] = c_{0,s_1}.  D is a block scan.
+// Also zeroes the tour's SAA partial and the overflow counter.
 __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restrict__ tours, int n,
                                                          const int32_t* __restrict__ dist,
                                                          int2* __restrict__ tabs, int32_t* __restrict__ g0,
                                                          int2* __restrict__ tabsf, TourInfo* __restrict__ tinfo,
-                                                         unsigned* __restrict__ hdr, unsigned* __restrict__ tickets,
+                                                         int32_t* __restrict__ cgs, spdp_saa_partial* __restrict__ slots,
+                                                         unsigned* __restrict__ hdr, spdp_saa_partial* __restrict__ partial,
                                                          int validate) {
     extern __shared__ unsigned char smem_raw[];
     long long* wsum = reinterpret_cast<long long*>(smem_raw);              // 32 warp sums
@@ -83,10 +87,15 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, wid = tid >> 5;
 
-    if (t == 0 && tid == 0) hdr[HDR_OVF_COUNT] = 0u;
+    if (t == 0 && tid == 0) {
+        hdr[HDR_OVF_COUNT] = 0u;
+        hdr[HDR_TILE] = 0u;
+    }
+    if (slots)
+        for (int i = tid; i < kSlots; i += nt) slots[(int64_t)t * kSlots + i] = spdp_saa_partial{0, 0, 0, 0, 0, 0};
     if (tid == 0) {
-        tickets[t] = 0u;
         *cmx = 0;
+        if (partial) partial[t] = spdp_saa_partial{0, 0, 0, 0, 0, 0};  // the finish kernel accumulates
     }
     if (validate) {
         for (int i = tid; i < (n + 32) / 32; i += nt) seen[i] = 0u;
@@ -164,9 +173,14 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     {
         const long long OFF = *dn, cm = *cmx;
         int2* tabf = tabsf + (int64_t)t * (n + kTabPad);
-        for (int i = tid; i < n + kTabPad; i += nt) {
-            const int2 e = tab[i];
-            tabf[i] = make_int2(e.x, __float_as_int((float)e.y * 0x1p-24f));
+        const int cs = cg_stride(n);
+        int32_t* cgi = cgs + (int64_t)t * 2 * cs;  // plane 0: int Cg, plane 1: fp32 Cg / 2^24
+        for (int i = tid; i < cs; i += nt) {
+            const int2 e = (i < n + kTabPad) ? tab[i] : make_int2(0, 0);
+            const int fb = __float_as_int((float)e.y * 0x1p-24f);
+            if (i < n + kTabPad) tabf[i] = make_int2(e.x, fb);
+            cgi[i] = e.y;
+            cgi[cs + i] = fb;
         }
         if (tid == 0) {
             TourInfo ti;
@@ -184,39 +198,50 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
 }
 
 // ---------------------------------------------------------------- a5: the sweep
-// One scenario per thread, 256 scenarios per CTA.  The candidate ring holds, for
-// the last W split points p (slot p mod W): G = g(p) and Y = P'(p) + Q, where
-// P'(p) = 1 + sum of the first p tour-order demands.  p is in the Eq. (3)
-// window of layer i iff P'(i) - P'(p) <= Q  <=>  Y >= P'(i).
-// Because q >= 0 the window is a contiguous suffix (DESIGN R5), so the
-// candidate loop walks from the newest slot backwards and leaves as soon as no
-// lane of the warp has a feasible candidate left.  The layer loop is unrolled
-// by W so every ring index is a compile-time register name.  A scenario whose
-// window would exceed the ring (the slot being evicted is still feasible) is
-// appended to the overflow list and finished by split_general_kernel.
+// One scenario per thread.  The candidate ring holds, for the last W split
+// points p (slot p mod W): G = g(p) and Y = P'(p) + Q, where P'(p) = 1 + sum of
+// the first p tour-order demands.  p is in the Eq. (3) window of layer i iff
+// P'(i) - P'(p) <= Q  <=>  Y >= P'(i).  Because q >= 0 the
+// window is a contiguous suffix (DESIGN R5), so the candidate loop walks from
+// the newest slot backwards and leaves as soon as no lane of the warp has a
+// feasible candidate left.  The layer loop is unrolled by W so every ring
+// index is a compile-time register name.  A scenario whose window would
+// exceed the ring (the slot being evicted is still feasible) is appended to
+// the overflow list and finished by split_finish_kernel.
 //
-// Demand stream: the CTA's tile [n rows (tour order) x 256 scenarios] is staged
-// through shared memory in chunks of W rows by bulk-async copies (the TMA
-// engine, one 512-byte copy per row, gathered by the tour) into an NS-deep ring
-// of stages guarded by mbarriers, so NS-1 chunks are always in flight while
-// the CTA computes on the current one.
+// Work decomposition: a single wave of persistent CTAs whose warps are fully
+// independent.  Every warp takes 32-scenario tiles (one scenario per lane; tile
+// id = tour * tiles_per_tour + scenario block) from a global atomic counter,
+// and streams its own tiles through a private NS-deep ring of shared-memory
+// stages; a stage holds one chunk = W demand rows (64 B per row, gathered by
+// the tour) plus the chunk's W Cg values, copied with cp.async (LDGSTS, 16 B
+// per lane) in commit groups, so a warp only ever waits for its own data and
+// runs at its own pace (windows, hence work, differ from warp to warp).  The
+// stream runs across tile boundaries; a per-warp queue in shared memory hands
+// the tile ids from the copy side to the compute side.  SAA partials are
+// flushed per tile with a warp reduction and atomics into kSlots slots per tour.
+//
+// Value types: int = exact int32 with a predicated min per candidate (ISETP +
+// VIMNMX, ALU pipe); fp32 = integer values scaled by 2^-24 (exact, see
+// TourInfo::ok), each candidate masked branch-free on the FMA pipe --
+// s = sat(P'(i) - Y), c = sat(G + s) is G when feasible and 1.0 (above every
+// G < 1) when not -- and folded with 3-input mins (FMNMX3).
+constexpr int kSweepWarps = 8;
+constexpr int kSweepThreads = 32 * kSweepWarps;
+constexpr int kTile = 32;   // scenarios per warp tile
+constexpr int kVote = 4;    // candidates per group; groups after the first are guarded by a warp vote
+constexpr int kQueue = 16;  // tile-id queue entries per warp (>= tiles the copies can run ahead + 1)
+
 template <int W>
 struct SweepCfg {
-    static constexpr int NS = (W <= 8) ? 6 : (W <= 16 ? 4 : (W <= 32 ? 3 : 2));  // stages
-    static constexpr int kStageElems = W * kSweepThreads;                        // u16 per stage
-    static constexpr size_t kStageBytes = sizeof(uint16_t) * kStageElems;
-    static constexpr int kHdr = 128;  // NS mbarriers (8 B) + NS stage-consumption counters (4 B)
-    static size_t smem_bytes(int n) {
-        return kHdr + NS * kStageBytes + sizeof(int2) * (size_t)(n + kTabPad);
-    }
+    static constexpr int NS = (W <= 8) ? 12 : (W <= 16 ? 7 : (W <= 24 ? 6 : (W <= 32 ? 4 : 3)));  // stages
+    static constexpr int kRowsBytes = W * kTile * (int)sizeof(uint16_t);   // W x 64 B
+    static constexpr int kStageBytes = kRowsBytes + W * (int)sizeof(int32_t);  // rows + Cg slice (16 B multiple)
+    static constexpr int kWarpBytes = kQueue * 8 + NS * kStageBytes;
+    static constexpr size_t kSmem = (size_t)kSweepWarps * kWarpBytes;
+    static_assert((W * 4) % 16 == 0, "W must be a multiple of 4");
 };
 
-// Value / load types of the two sweep variants.  int: exact int32 with a
-// predicated min per candidate (ISETP + VIMNMX on the ALU pipe).  fp32:
-// integer-valued floats scaled by 2^-24 (exact, TourInfo::ok), each candidate
-// masked branch-free on the FMA pipe -- s = sat(P'(i) - Y), c = sat(G + s) is G
-// when feasible and 1.0 (above every G < 1) when not -- and folded with a
-// 3-input min (FMNMX3), so the ALU pipe carries half an op per candidate.
 template <bool F32>
 struct SweepT {
     using V = int;
@@ -228,239 +253,237 @@ struct SweepT<true> {
     using L = float;
 };
 
-template <int W, int VE, bool F32>
-__global__ void __launch_bounds__(kSweepThreads, (W <= 16 ? 4 : 1))
-    split_sweep_kernel(const int2* __restrict__ tabs, const int32_t* __restrict__ g0s,
-                       const TourInfo* __restrict__ tinfo, int n, const uint16_t* __restrict__ demand,
-                       int64_t ld, int64_t S, uint32_t Q, int32_t* __restrict__ cost,
-                       spdp_saa_partial* __restrict__ bpart, spdp_saa_partial* __restrict__ partial,
-                       unsigned* __restrict__ tickets, unsigned long long* __restrict__ ovf_list,
-                       unsigned* __restrict__ ovf_count) {
+template <int W, bool F32>
+__global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1)))
+    split_sweep_kernel(const int2* __restrict__ tabs, const int32_t* __restrict__ cgs,
+                       const int32_t* __restrict__ g0s, const TourInfo* __restrict__ tinfo, int n, int T,
+                       const uint16_t* __restrict__ demand, int64_t ld, int64_t S, uint32_t Q,
+                       int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
+                       unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
     using Cfg = SweepCfg<W>;
     using V = typename SweepT<F32>::V;
     using LT = typename SweepT<F32>::L;
     constexpr int NS = Cfg::NS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);                             // NS mbarriers
-    unsigned* done = reinterpret_cast<unsigned*>(smem_raw + 64);                       // NS counters
-    uint16_t* dbuf = reinterpret_cast<uint16_t*>(smem_raw + Cfg::kHdr);                // NS x W x 256
-    int2* stab = reinterpret_cast<int2*>(smem_raw + Cfg::kHdr + NS * Cfg::kStageBytes);  // n + kTabPad
-    __shared__ Part red[kSweepThreads / 32];
-    __shared__ bool am_last;
-
-    const int t = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int64_t s0 = (int64_t)blockIdx.x * kSweepThreads;
-    const int cols = (int)((S - s0) < kSweepThreads ? (S - s0) : kSweepThreads);
-    const uint32_t row_bytes = (uint32_t)(((cols + 7) & ~7) * sizeof(uint16_t));
+    unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
+    int64_t* tq = reinterpret_cast<int64_t*>(wbase);  // this warp's tile queue
+    unsigned char* stage_base = wbase + kQueue * 8;
+    const int64_t ntile_s = (S + kTile - 1) / kTile;
+    const int64_t ntiles = ntile_s * T;
     const int nchunks = (n + W - 1) / W;
-    {
-        const int2* tab = tabs + (int64_t)t * (n + kTabPad);
-        for (int i = tid; i < n + kTabPad; i += kSweepThreads) stab[i] = tab[i];
-    }
-    if (tid == 0) {
-        for (int k = 0; k < NS; ++k) {
-            mbar_init(&bar[k], 1);
-            done[k] = 0u;
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const uint64_t pol = policy_evict_first();
-    // producer: one warp refills stage (c % NS) with chunk c (rows c*W .. c*W+W-1)
-    auto issue = [&](int c) {
-        const int stage = c % NS;
-        const int r0 = c * W;
-        const int rows = (n - r0) < W ? (n - r0) : W;
-        if (lane == 0) {
-            fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&bar[stage], row_bytes * (uint32_t)rows);
-        }
-        __syncwarp();
-        for (int r = lane; r < rows; r += 32)
-            bulk_g2s(dbuf + (size_t)stage * Cfg::kStageElems + r * kSweepThreads,
-                     demand + (int64_t)stab[r0 + r].x * ld + s0, row_bytes, &bar[stage], pol);
-    };
-    if (wid == 0)
-        for (int c = 0; c < NS && c < nchunks; ++c) issue(c);
-
-    const bool live = tid < cols;
-    const int col = live ? tid : cols - 1;  // tail lanes replay a real scenario
-    const int64_t s = s0 + col;
-
-    V G[W];
-    LT Y[W];
-    V gprev;
-    LT P, Qv;
-    bool f32_ok = true;
-    if constexpr (F32) {
-        const TourInfo ti = tinfo[t];
-        f32_ok = ti.ok != 0;
-        gprev = __int_as_float(ti.g0f_bits);
-        P = 0.0f;
-        Qv = (float)Q;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            G[k] = 0.0f;
-            Y[k] = -1.0f;  // never feasible: P' >= 0
-        }
-    } else {
-        gprev = g0s[t];
-        P = 1u;
-        Qv = Q;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            G[k] = INT_MAX;
-            Y[k] = 0u;  // never feasible: P' >= 1
-        }
-    }
-    uint32_t qmax = 0u;   // bad  <=> some q > Q  (Eq. (2) set empty, DESIGN R4)
-    V ovfacc = (V)-1;     // ovf  <=> some evicted slot still feasible: max(Y - P'(i)) >= 0
-
-    // One layer (computes f(L+1)); j = L mod W is a compile-time constant.
-    auto layer = [&](const uint16_t* buf, const int j, const int L) {
-        const uint32_t qi = buf[j * kSweepThreads];
-        qmax = max(qmax, qi);
-        LT Pn;
-        if constexpr (F32) {
-            Pn = P + __uint2float_rn(qi);
-            ovfacc = fmaxf(ovfacc, Y[j] - Pn);
-        } else {
-            Pn = P + qi;
-            ovfacc = max(ovfacc, (int)(Y[j] - Pn));
-        }
-        G[j] = gprev;
-        Y[j] = P + Qv;
-        V best = gprev;  // p = L
-        if constexpr (F32) {
-#pragma unroll
-            for (int k0 = 1; k0 < W; k0 += VE) {
-                if (!__any_sync(kFull, Y[(j - k0 + W) % W] >= Pn)) break;
-                float c[VE];
-#pragma unroll
-                for (int u = 0; u < VE; ++u) {
-                    const int k = k0 + u;
-                    const int sl = (j - k + W) % W;
-                    c[u] = (k < W) ? __saturatef(G[sl] + __saturatef(Pn - Y[sl])) : 1.0f;
-                }
-#pragma unroll
-                for (int u = 0; u + 1 < VE; u += 2) best = fminf(best, fminf(c[u], c[u + 1]));
-                if (VE & 1) best = fminf(best, c[VE - 1]);
-            }
-            gprev = best + __int_as_float(stab[L].y);
-        } else {
-            V best1 = best;  // second accumulator: two independent min chains
-#pragma unroll
-            for (int k = 1; k < W; ++k) {
-                const int sl = (j - k + W) % W;
-                const bool f = Y[sl] >= Pn;
-                if ((k % VE) == 1 % VE && !__any_sync(kFull, f)) break;
-                if (f) {
-                    if (k & 1) best1 = min(best1, G[sl]);
-                    else best = min(best, G[sl]);
-                }
-            }
-            gprev = min(best, best1) + stab[L].y;
-        }
-        P = Pn;
-    };
-
-    // The final chunk is padded to W layers with demand q_pad = min(Q, 65535) and cg = 0:
-    // a demand of Q collapses every window to the newest slot, so the padded layers
-    // never flag an overflow and never disturb the ring slot that holds f(n).
     const int rem = n % W;
+    const int cgs_stride = cg_stride(n);
     const uint32_t qpad = Q < 65535u ? Q : 65535u;
-    constexpr int NW = kSweepThreads / 32;
-    for (int c = 0; c < nchunks; ++c) {
-        const int stage = c % NS;
-        mbar_wait(&bar[stage], (uint32_t)((c / NS) & 1));
-        uint16_t* bufw = dbuf + (size_t)stage * Cfg::kStageElems + col;
-        if (rem != 0 && c == nchunks - 1)
-            for (int j = rem; j < W; ++j) bufw[j * kSweepThreads] = (uint16_t)qpad;
-        const uint16_t* buf = bufw;
-        const int i0 = c * W;
-#pragma unroll
-        for (int j = 0; j < W; ++j) layer(buf, j, i0 + j);
-        // release the stage: the last warp to finish it refills it (no CTA-wide barrier,
-        // so warps with narrow windows run ahead of warps with wide ones)
-        __syncwarp();
-        unsigned last = 0;
-        if (lane == 0) {
-            __threadfence_block();
-            last = (atomicAdd(&done[stage], 1u) == NW - 1);
-            if (last) done[stage] = 0u;
+    unsigned* tile_ctr = hdr + HDR_TILE;
+    unsigned* ovf_count = hdr + HDR_OVF_COUNT;
+
+    // ---- copy side: chunk k of this warp's stream = chunk k % nchunks of local tile k / nchunks
+    int64_t p_tile = -1;
+    auto issue = [&](unsigned k) {  // always commits one group (possibly empty) to keep the count
+        const int c = (int)(k % nchunks);
+        if (c == 0) {
+            unsigned id = 0;
+            if (lane == 0) id = atomicAdd(tile_ctr, 1u);
+            id = __shfl_sync(kFull, id, 0);
+            p_tile = (int64_t)id < ntiles ? (int64_t)id : -1;
+            if (lane == 0) tq[(k / nchunks) % kQueue] = p_tile;
         }
-        last = __shfl_sync(kFull, last, 0);
-        if (last && c + NS < nchunks) issue(c + NS);
-    }
-    // f(n): the slot of position n holds it (pushed by the first padded layer), or gprev if n % W == 0
-    if (rem != 0) {
+        if (p_tile >= 0) {
+            unsigned char* sb = stage_base + (size_t)(k % NS) * Cfg::kStageBytes;
+            const int t = (int)(p_tile / ntile_s);
+            const int64_t s0 = (p_tile % ntile_s) * kTile;
+            const int r0 = c * W;
+            const int rows = (n - r0) < W ? (n - r0) : W;
+            const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
+            const int segs = ((cols + 7) & ~7) / 8;  // 16-byte segments per row (within ld)
+            const int2* __restrict__ tab = tabs + (int64_t)t * (n + kTabPad);
+            for (int e = lane; e < rows * 4; e += 32) {
+                const int r = e >> 2, sg = e & 3;
+                if (sg < segs)
+                    cp_async16(sb + r * (kTile * 2) + sg * 16,
+                               demand + (int64_t)__ldg(&tab[r0 + r].x) * ld + s0 + sg * 8);
+            }
+            if (lane < W / 4)
+                cp_async16(sb + Cfg::kRowsBytes + lane * 16,
+                           cgs + (int64_t)t * 2 * cgs_stride + (F32 ? cgs_stride : 0) + r0 + lane * 4);
+        }
+        cp_async_commit();
+    };
+    for (int k = 0; k < NS; ++k) issue((unsigned)k);
+
+    unsigned c_k = 0;  // compute-side chunk sequence number
+    for (unsigned u = 0;; ++u) {
+        cp_async_wait<NS - 1>();  // the tile's first chunk (the oldest outstanding group) has landed
+        __syncwarp();
+        const int64_t tile = tq[u % kQueue];
+        if (tile < 0) break;
+        const int t = (int)(tile / ntile_s);
+        const int64_t s0 = (tile % ntile_s) * kTile;
+        const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
+        const bool live = lane < cols;
+        const int col = live ? lane : cols - 1;  // tail lanes replay a real scenario
+        int2 toff = make_int2(0, 1);
+        if constexpr (F32) toff = make_int2(tinfo[t].off, tinfo[t].ok);
+
+        V G[W];
+        LT Y[W];
+        V gprev;
+        LT P, Qv;
+        if constexpr (F32) {
+            gprev = __int_as_float(tinfo[t].g0f_bits);
+            P = 0.0f;
+            Qv = (float)Q;
 #pragma unroll
-        for (int k = 0; k < W; ++k)
-            if (k == rem) gprev = G[k];
-    }
-    const bool bad = qmax > Q;
-    const bool ovf = (ovfacc >= (V)0) || !f32_ok;
-    int fval;
-    if constexpr (F32) {
-        fval = (int)(gprev * 0x1p24f) - tinfo[t].off;
-    } else {
-        fval = gprev;
-    }
+            for (int k = 0; k < W; ++k) {
+                G[k] = 0.0f;
+                Y[k] = -1.0f;  // never feasible: P' >= 0
+            }
+        } else {
+            gprev = g0s[t];
+            P = 1u;
+            Qv = Q;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                G[k] = INT_MAX;
+                Y[k] = 0u;  // never feasible: P' >= 1
+            }
+        }
+        uint32_t qmax = 0u;  // bad <=> some q > Q (Eq. (2) set empty, DESIGN R4)
+        V ovfacc = (V)-1;    // ovf <=> some evicted slot still feasible: max(Y - P'(i)) >= 0
 
-    const bool deferred = live && ovf && !bad;
-    if (deferred) {
-        const unsigned long long key = ((unsigned long long)t << 40) | (unsigned long long)s;
-        ovf_list[atomicAdd(ovf_count, 1u)] = key;
-    }
-    if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
-    if (partial == nullptr) return;
+        // one layer (computes f(L+1)); j = L mod W is a compile-time constant
+        auto layer = [&](const uint16_t* buf, const int32_t* cgc, const int j) {
+            const int cgi = cgc[j];
+            const uint32_t qi = buf[j * kTile];
+            qmax = max(qmax, qi);
+            LT Pn;
+            if constexpr (F32) {
+                Pn = P + __uint2float_rn(qi);
+                ovfacc = fmaxf(ovfacc, Y[j] - Pn);
+            } else {
+                Pn = P + qi;
+                ovfacc = max(ovfacc, (int)(Y[j] - Pn));
+            }
+            G[j] = gprev;
+            Y[j] = P + Qv;
+            V best = gprev, best1 = gprev;  // p = L; two independent min chains
+#pragma unroll
+            for (int k0 = 1; k0 < W; k0 += kVote) {
+                if (k0 > 1 && !__any_sync(kFull, Y[(j - k0 + W) % W] >= Pn)) break;
+#pragma unroll
+                for (int v = 0; v < kVote; ++v) {
+                    const int k = k0 + v;
+                    if (k < W) {
+                        const int sl = (j - k + W) % W;
+                        if constexpr (F32) {
+                            const float cnd = __saturatef(G[sl] + __saturatef(Pn - Y[sl]));
+                            if (v & 1) best1 = fminf(best1, cnd);
+                            else best = fminf(best, cnd);
+                        } else {
+                            if (Y[sl] >= Pn) {
+                                if (v & 1) best1 = min(best1, G[sl]);
+                                else best = min(best, G[sl]);
+                            }
+                        }
+                    }
+                }
+            }
+            if constexpr (F32) gprev = fminf(best, best1) + __int_as_float(cgi);
+            else gprev = min(best, best1) + cgi;
+            P = Pn;
+        };
 
-    Part p{0, 0, 0, 0, 0};
-    if (live && !deferred) part_add_cost(p, fval, !bad);
-    Part r = block_sum(p, red);
-    if (tid == 0) {
-        part_store(&bpart[(int64_t)t * gridDim.x + blockIdx.x], r);
-        __threadfence();
-        am_last = (atomicAdd(&tickets[t], 1u) == gridDim.x - 1);
+        for (int c = 0; c < nchunks; ++c) {
+            if (c > 0) {
+                cp_async_wait<NS - 1>();
+                __syncwarp();
+            }
+            unsigned char* sb = stage_base + (size_t)(c_k % NS) * Cfg::kStageBytes;
+            uint16_t* bufw = reinterpret_cast<uint16_t*>(sb) + col;
+            const int32_t* cgc = reinterpret_cast<const int32_t*>(sb + Cfg::kRowsBytes);
+            // the final chunk is padded to W layers with q_pad = min(Q, 65535) and Cg = 0: a demand
+            // of Q collapses every window to the newest slot, so the padded layers never flag an
+            // overflow and never disturb the ring slot that holds f(n)
+            if (rem != 0 && c == nchunks - 1) {
+                for (int j = rem; j < W; ++j) bufw[j * kTile] = (uint16_t)qpad;
+                __syncwarp();
+            }
+#pragma unroll
+            for (int j = 0; j < W; ++j) layer(bufw, cgc, j);
+            __syncwarp();  // every lane is done with this stage
+            issue(c_k + NS);
+            ++c_k;
+        }
+        // f(n): the slot of position n holds it (pushed by the first padded layer), or gprev if n % W == 0
+        if (rem != 0) {
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                if (k == rem) gprev = G[k];
+        }
+        const bool bad = qmax > Q;
+        const bool ovf = (ovfacc >= (V)0) || toff.y == 0;
+        int fval;
+        if constexpr (F32) fval = (int)(gprev * 0x1p24f) - toff.x;
+        else fval = gprev;
+        const int64_t s = s0 + col;
+        const bool deferred = live && ovf && !bad;
+        if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
+        if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
+        if (slots) {  // per-tile flush of the SAA partial
+            Part p{0, 0, 0, 0, 0};
+            if (live && !deferred) part_add_cost(p, fval, !bad);
+            p = warp_sum(p);
+            if (lane == 0) {
+                spdp_saa_partial* d = &slots[(int64_t)t * kSlots + ((blockIdx.x * kSweepWarps + wid) % kSlots)];
+                atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)p.n_feas);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)p.n_infeas);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)p.sum);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)p.sq_lo);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)p.sq_hi);
+            }
+        }
     }
-    __syncthreads();
-    if (!am_last) return;
-    __threadfence();
-    Part acc{0, 0, 0, 0, 0};
-    const spdp_saa_partial* bp = bpart + (int64_t)t * gridDim.x;
-    for (int b = tid; b < (int)gridDim.x; b += kSweepThreads) {
-        acc.n_feas += __ldcg(&bp[b].n_feas);
-        acc.n_infeas += __ldcg(&bp[b].n_infeas);
-        acc.sum += __ldcg(&bp[b].sum);
-        acc.sq_lo += __ldcg(&bp[b].sumsq_lo);
-        acc.sq_hi += __ldcg(&bp[b].sumsq_hi);
-    }
-    __syncthreads();
-    Part tot = block_sum(acc, red);
-    if (tid == 0) {
-        part_store(&partial[t], tot);
-        tickets[t] = 0u;
-    }
+    cp_async_wait<0>();
 }
 
-// ---------------------------------------------------------------- general kernel
-// Transition-level parallelism: one warp per scenario, the
-// lanes split the candidates p in [mask(i), i-1] and combine them with a
-// shuffle min; mask(i) advances monotonically (two-pointer on the prefix).
-// Handles any window width; used for the overflow list of the sweep.
-__device__ __forceinline__ int warp_min(int v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
-    return v;
-}
-
-__global__ void __launch_bounds__(256) split_general_kernel(
-    const int2* __restrict__ tabs, const int32_t* __restrict__ g0s, int n, const uint16_t* __restrict__ demand,
-    int64_t ld, int64_t S, uint32_t Q, int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ partial,
+// ---------------------------------------------------------------- finish kernel
+// (1) SAA partial of each tour: sum of its CTAs' slots, added atomically (the
+//     partials are zeroed by tour_prep_kernel);
+// (2) the overflow list, with transition-level parallelism:
+//     one warp per scenario, the lanes split the candidates p in
+//     [mask(i), i-1] and combine them with REDUX.MIN; mask(i) advances
+//     monotonically with a ballot.  Any window width.
+__global__ void __launch_bounds__(256) split_finish_kernel(
+    const spdp_saa_partial* __restrict__ slots, int kslots, int T, const int2* __restrict__ tabs,
+    const int32_t* __restrict__ g0s, int n, const uint16_t* __restrict__ demand, int64_t ld, int64_t S, uint32_t Q,
+    int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ partial,
     const unsigned long long* __restrict__ ovf_list, const unsigned* __restrict__ ovf_count) {
     extern __shared__ unsigned char smem_raw[];
+    __shared__ Part red[8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (partial) {
+        for (int t = blockIdx.x; t < T; t += gridDim.x) {
+            Part a{0, 0, 0, 0, 0};
+            for (int b = threadIdx.x; b < kslots; b += blockDim.x) {
+                const spdp_saa_partial& e = slots[(int64_t)t * kslots + b];
+                a.n_feas += e.n_feas;
+                a.n_infeas += e.n_infeas;
+                a.sum += e.sum;
+                a.sq_lo += e.sumsq_lo;
+                a.sq_hi += e.sumsq_hi;
+            }
+            Part r = block_sum(a, red);
+            if (threadIdx.x == 0) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].n_feas), (unsigned long long)r.n_feas);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].n_infeas), (unsigned long long)r.n_infeas);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sum), (unsigned long long)r.sum);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_lo), (unsigned long long)r.sq_lo);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_hi), (unsigned long long)r.sq_hi);
+            }
+            __syncthreads();
+        }
+    }
     int* g = reinterpret_cast<int*>(smem_raw) + (size_t)wid * 2 * (n + 1);
     uint32_t* pre = reinterpret_cast<uint32_t*>(g + (n + 1));
     const unsigned count = *ovf_count;
@@ -469,15 +492,15 @@ __global__ void __launch_bounds__(256) split_general_kernel(
         const int t = (int)(key >> 40);
         const int64_t s = (int64_t)(key & ((1ull << 40) - 1));
         const int2* tab = tabs + (int64_t)t * (n + kTabPad);
-        // tour-order prefix P'(i) = 1 + sum_{k<=i} q, i = 0..n
-        uint32_t carry = 1u;
-        if (lane == 0) pre[0] = 1u;
+        // tour-order prefix P(i) = sum_{k<=i} q, i = 0..n: all loads in flight, then a warp scan
+        uint32_t carry = 0u;
+        if (lane == 0) pre[0] = 0u;
         for (int base = 0; base < n; base += 32) {
             const int i = base + lane;
             uint32_t v = (i < n) ? (uint32_t)demand[(int64_t)tab[i].x * ld + s] : 0u;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                uint32_t u = __shfl_up_sync(kFull, v, o);
+                const uint32_t u = __shfl_up_sync(kFull, v, o);
                 if (lane >= o) v += u;
             }
             if (i < n) pre[i + 1] = carry + v;
@@ -485,14 +508,23 @@ __global__ void __launch_bounds__(256) split_general_kernel(
         }
         if (lane == 0) g[0] = g0s[t];
         __syncwarp();
-        int m = 0;
+        int m = 0;  // mask(L+1), monotone in L
         for (int L = 0; L < n; ++L) {
             const uint32_t Pn = pre[L + 1];
-            while (Pn - pre[m] > Q) ++m;  // uniform across the warp (smem broadcast)
+            const int cg = tab[L].y;
+            for (;;) {  // first p >= m with P(L+1) - P(p) <= Q (p = L always qualifies: q <= Q)
+                const int p = m + lane;
+                const unsigned b = __ballot_sync(kFull, p <= L && Pn - pre[p] <= Q);
+                if (b) {
+                    m += __ffs(b) - 1;
+                    break;
+                }
+                m += 32;
+            }
             int best = INT_MAX;
             for (int p = m + lane; p <= L; p += 32) best = min(best, g[p]);
-            best = warp_min(best);
-            if (lane == 0) g[L + 1] = best + tab[L].y;
+            best = __reduce_min_sync(kFull, best);
+            if (lane == 0) g[L + 1] = best + cg;
             __syncwarp();
         }
         const int f = g[n];
@@ -595,48 +627,55 @@ __global__ void __launch_bounds__(256) saa_reduce_kernel(const int32_t* __restri
 // ---------------------------------------------------------------- host dispatch
 struct SweepArgs {
     const int2* tabs;
-    const int2* tabsf;
+    const int32_t* cgs;
     const int32_t* g0;
     const TourInfo* tinfo;
-    int n;
+    int n, T;
     const uint16_t* demand;
     int64_t ld, S;
     uint32_t Q;
     int32_t* cost;
-    spdp_saa_partial* bpart;
-    spdp_saa_partial* partial;
-    unsigned* tickets;
+    spdp_saa_partial* slots;
     unsigned long long* ovf;
-    unsigned* ovf_count;
+    unsigned* hdr;
 };
 
-template <int W, int VE, bool F32>
-static spdp_status launch_sweep_t(dim3 grid, cudaStream_t st, const SweepArgs& a) {
-    auto kern = split_sweep_kernel<W, VE, F32>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e == cudaSuccess)  // all of the unified L1/smem as shared memory: occupancy is smem-bound
+static int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+// Launches the sweep: one wave of persistent CTAs (occupancy x SMs).
+template <int W, bool F32>
+static spdp_status launch_sweep_t(cudaStream_t st, const SweepArgs& a) {
+    auto kern = split_sweep_kernel<W, F32>;
+    static int blocks_per_sm = 0;
+    if (blocks_per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e == cudaSuccess)  // all of the unified L1/smem as shared memory
             e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_sweep)");
-        attr_set = true;
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kSweepThreads, SweepCfg<W>::kSmem);
+        if (e != cudaSuccess) return cuda_check(e, "split_sweep setup");
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
+    const int64_t ntiles = ((a.S + kTile - 1) / kTile) * a.T;
+    int64_t grid = (int64_t)blocks_per_sm * num_sms();
+    const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
+    if (grid > need) grid = need;
     prof_begin(st);
-    kern<<<grid, kSweepThreads, SweepCfg<W>::smem_bytes(a.n), st>>>(F32 ? a.tabsf : a.tabs, a.g0, a.tinfo, a.n, a.demand,
-                                                                    a.ld, a.S, a.Q, a.cost, a.bpart, a.partial,
-                                                                    a.tickets, a.ovf, a.ovf_count);
+    kern<<<(unsigned)grid, kSweepThreads, SweepCfg<W>::kSmem, st>>>(a.tabs, a.cgs, a.g0, a.tinfo, a.n, a.T, a.demand,
+                                                                    a.ld, a.S, a.Q, a.cost, a.slots, a.ovf, a.hdr);
     spdp_status rc = last_launch("split_sweep_kernel");
     prof_end(st);
     return rc;
 }
 
-// Tuning knobs (environment, read once): SPDP_SWEEP=auto|int|f32 selects the
-// candidate arithmetic; SPDP_VOTE_EVERY selects the warp-vote stride.
-static int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
-
+// Tuning knob (environment, read once): SPDP_SWEEP=auto|int|f32 selects the candidate arithmetic.
 static int sweep_mode() {  // 0 auto, 1 int, 2 f32
     static int m = [] {
         const char* e = getenv("SPDP_SWEEP");
@@ -648,30 +687,31 @@ static int sweep_mode() {  // 0 auto, 1 int, 2 f32
     return m;
 }
 
-static spdp_status launch_sweep(int W, bool f32, dim3 grid, cudaStream_t st, const SweepArgs& a) {
-    static const int ve = env_int("SPDP_VOTE_EVERY", 4);
+static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArgs& a) {
     if (f32) {
         switch (W) {
-            case 8: return ve == 2 ? launch_sweep_t<8, 2, true>(grid, st, a) : launch_sweep_t<8, 4, true>(grid, st, a);
-            case 16:
-                return ve == 2 ? launch_sweep_t<16, 2, true>(grid, st, a)
-                               : (ve == 8 ? launch_sweep_t<16, 8, true>(grid, st, a) : launch_sweep_t<16, 4, true>(grid, st, a));
-            default:
-                return ve == 8 ? launch_sweep_t<32, 8, true>(grid, st, a) : launch_sweep_t<32, 4, true>(grid, st, a);
+            case 8: return launch_sweep_t<8, true>(st, a);
+            case 16: return launch_sweep_t<16, true>(st, a);
+            case 20: return launch_sweep_t<20, true>(st, a);
+            case 24: return launch_sweep_t<24, true>(st, a);
+            default: return launch_sweep_t<32, true>(st, a);
         }
     }
     switch (W) {
-        case 8: return ve == 2 ? launch_sweep_t<8, 2, false>(grid, st, a) : launch_sweep_t<8, 4, false>(grid, st, a);
-        case 16: return ve == 2 ? launch_sweep_t<16, 2, false>(grid, st, a) : launch_sweep_t<16, 4, false>(grid, st, a);
-        case 32: return ve == 2 ? launch_sweep_t<32, 2, false>(grid, st, a) : launch_sweep_t<32, 4, false>(grid, st, a);
-        default: return launch_sweep_t<64, 4, false>(grid, st, a);
+        case 8: return launch_sweep_t<8, false>(st, a);
+        case 16: return launch_sweep_t<16, false>(st, a);
+        case 20: return launch_sweep_t<20, false>(st, a);
+        case 24: return launch_sweep_t<24, false>(st, a);
+        case 32: return launch_sweep_t<32, false>(st, a);
+        default: return launch_sweep_t<64, false>(st, a);
     }
 }
 
+// Ring width W: the smallest instantiated width that holds the expected maximum window.
 static int pick_w(int hint) {
-    if (hint <= 8) return 8;
-    if (hint <= 16) return 16;
-    if (hint <= 32) return 32;
+    static const int widths[] = {8, 16, 20, 24, 32, 64};
+    for (int w : widths)
+        if (hint <= w) return w;
     return 64;
 }
 
@@ -692,15 +732,13 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     if (window_hint < 0) return fail(SPDP_E_USAGE, "%s: window_hint < 0", fn);
     const WsLayout L = ws_layout(n, S, T);
     if (ws_bytes < L.total) return fail(SPDP_E_USAGE, "%s: workspace %zu < required %zu", fn, ws_bytes, L.total);
-    if (L.nblocks > 0x7fffffffLL) return fail(SPDP_E_RESOURCE, "%s: grid too large", fn);
     char* w = static_cast<char*>(ws);
     unsigned* hdr = reinterpret_cast<unsigned*>(w + L.hdr);
-    unsigned* tickets = reinterpret_cast<unsigned*>(w + L.tickets);
     int32_t* g0 = reinterpret_cast<int32_t*>(w + L.g0);
+    TourInfo* tinfo = reinterpret_cast<TourInfo*>(w + L.tinfo);
     int2* tabs = reinterpret_cast<int2*>(w + L.tabs);
     int2* tabsf = reinterpret_cast<int2*>(w + L.tabsf);
-    TourInfo* tinfo = reinterpret_cast<TourInfo*>(w + L.tinfo);
-    spdp_saa_partial* bpart = reinterpret_cast<spdp_saa_partial*>(w + L.bpart);
+    spdp_saa_partial* slots = reinterpret_cast<spdp_saa_partial*>(w + L.slots);
     unsigned long long* ovf = reinterpret_cast<unsigned long long*>(w + L.ovf);
     // Q above the largest possible load behaves as "everything fits"; clamp so P' + Q fits uint32.
     const uint32_t Qe = (uint32_t)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
@@ -711,9 +749,11 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         if (rc) return rc;
     }
     {
-        const int threads = 1024;
+        const int threads = n >= 2048 ? 1024 : 256;
         const size_t smem = 34 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
-        tour_prep_kernel<<<T, threads, smem, st>>>(tours, n, dist, tabs, g0, tabsf, tinfo, hdr, tickets, validate ? 1 : 0);
+        tour_prep_kernel<<<T, threads, smem, st>>>(tours, n, dist, tabs, g0, tabsf, tinfo,
+                                                   reinterpret_cast<int32_t*>(w + L.cgs), partial ? slots : nullptr, hdr,
+                                                   partial, validate ? 1 : 0);
         if ((rc = last_launch("tour_prep_kernel"))) return rc;
     }
     int W = pick_w(window_hint);
@@ -734,31 +774,31 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         }
         if (window_hint == 0) W = pick_w((int)(h[HDR_SAMPLE_W] + h[HDR_SAMPLE_W] / 4 + 1));
     }
-    const dim3 grid((unsigned)L.nblocks, (unsigned)T);
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
-    const SweepArgs args{tabs, tabsf, g0, tinfo, n, demand, ld, S, Qe, cost, bpart, partial, tickets, ovf, ovf_count};
-    // fp32 sweep when every load value it forms (P' <= n min(Q, 65535) for feasible scenarios,
-    // Y = P' + Q) is an exact float; the per-tour cost range is checked on the device (TourInfo::ok)
+    const SweepArgs args{tabs, reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
+                         cost, partial ? slots : nullptr, ovf, hdr};
+    // fp32 sweep when every load value it forms (P' <= (n + W) min(Q, 65535) for feasible scenarios
+    // including the padded layers, Y = P' + Q) is an exact float; the per-tour cost range is checked on
+    // the device (TourInfo::ok: lanes of a tour that fails it are finished by the int finish kernel)
     const int64_t qeff = Qe < 65535u ? (int64_t)Qe : 65535;
-    const bool f32_loads_exact = ((int64_t)n + 64) * qeff + (int64_t)Qe + 1 < (1LL << 24);  // + padded layers
+    const bool f32_loads_exact = ((int64_t)n + 64) * qeff + (int64_t)Qe + 1 < (1LL << 24);
     const int mode = sweep_mode();
-    const bool use_f32 = W <= 32 && (mode == 2 || (mode == 0 && f32_loads_exact)) && (mode != 2 || f32_loads_exact);
-    rc = launch_sweep(W, use_f32, grid, st, args);
-    if (rc) return rc;
+    const bool use_f32 = W <= 32 && f32_loads_exact && mode != 1;
+    if ((rc = launch_sweep(W, use_f32, st, args))) return rc;
     {
-        // overflow list: warps per CTA limited by the per-warp smem (g and prefix: 8 (n+1) bytes)
+        // finish: per-tour SAA partials + the overflow list (warps per CTA limited by 8 (n+1) bytes of smem each)
         const size_t per_warp = 2 * sizeof(int) * (size_t)(n + 1);
         int warps = (int)((160 * 1024) / per_warp);
         warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
         static bool attr_set = false;
         if (!attr_set) {
-            cudaError_t e = cudaFuncSetAttribute(split_general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_general)");
+            cudaError_t e = cudaFuncSetAttribute(split_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_finish)");
             attr_set = true;
         }
-        split_general_kernel<<<296, warps * 32, per_warp * warps, st>>>(tabs, g0, n, demand, ld, S, Qe, cost, partial,
-                                                                         ovf, ovf_count);
-        if ((rc = last_launch("split_general_kernel"))) return rc;
+        split_finish_kernel<<<2 * num_sms(), warps * 32, per_warp * warps, st>>>(
+            partial ? slots : nullptr, kSlots, T, tabs, g0, n, demand, ld, S, Qe, cost, partial, ovf, ovf_count);
+        if ((rc = last_launch("split_finish_kernel"))) return rc;
     }
     return SPDP_OK;
 }
