@@ -148,6 +148,68 @@ __global__ void __launch_bounds__(128) irp_kernel(const uint8_t* __restrict__ vi
     }
 }
 
+// Lane-per-scenario variant (used when every customer has X == 0 or X >= U, so the
+// delivery band of step A is the prefix [0, y]).  A warp owns 32 scenarios (one per
+// lane) and loops over customers and periods; the inventory states of each lane live
+// in shared memory ([U+1][32], lane-contiguous, conflict-free).  Step A and step B
+// are fused into ONE in-place pass over y = 0..U:
+//     run  = min(run, V[y] - c y)                 prefix-min of the band (X >= U)
+//     W    = run + c y                             (= V[y] when the period is not visited)
+//     m0   = min(m0, W - b y)        if y <= d     V'[0] = m0 + b d
+//     V[y - d] = W + h (y - d)       if y - d >= 1 (index y - d was already read)
+// States above `top` are unreachable (+inf) and are never read.  Values stay below
+// 2^29 (host check) and the sentinel is 2^30, so sums never overflow and no special
+// casing of +inf is needed: every result is clamped with one min at the end.
+__global__ void __launch_bounds__(256) irp_lane_kernel(const uint8_t* __restrict__ visit,
+                                                       const IrpCust* __restrict__ cust, int H, int M, int Umax,
+                                                       const uint16_t* __restrict__ demand, int64_t ld, int64_t S,
+                                                       long long* __restrict__ cost) {
+    extern __shared__ int32_t vsm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int32_t* V = vsm + (size_t)wid * (Umax + 1) * 32 + lane;  // V[y] at V[y * 32]
+    const int64_t ntile = (S + 31) / 32;
+    for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntile; tile += (int64_t)gridDim.x * nw) {
+        const int64_t s0 = tile * 32;
+        const bool live = s0 + lane < S;
+        const int64_t s = live ? s0 + lane : S - 1;
+        long long total = 0;
+        for (int m = 0; m < M; ++m) {
+            const IrpCust p = cust[m];
+            const int U = p.U;
+            for (int y = 0; y <= U; ++y) V[y * 32] = kIrpInf;
+            V[p.I0 * 32] = 0;
+            int top = U;  // states above top are +inf
+            int d = demand[(int64_t)m * ld + s];
+            for (int t = 0; t < H; ++t) {
+                const int dn = (t + 1 < H) ? demand[((int64_t)(t + 1) * M + m) * ld + s] : 0;  // prefetch
+                const bool deliver = visit[(int64_t)m * H + t] != 0 && p.X > 0;
+                const int ylim = deliver ? U : top;
+                int run = kIrpInf, m0 = kIrpInf;
+                for (int y = 0; y <= ylim; ++y) {
+                    const int v = (y <= top) ? V[y * 32] : kIrpInf;
+                    int w;
+                    if (deliver) {
+                        run = min(run, v - p.c * y);
+                        w = run + p.c * y;
+                    } else {
+                        w = v;
+                    }
+                    if (y <= d) m0 = min(m0, w - p.b * y);
+                    const int J = y - d;
+                    if (J >= 1) V[J * 32] = min(w + p.h * J, kIrpInf);
+                }
+                V[0] = min(m0 + p.b * d, kIrpInf);
+                top = max(0, ylim - d);
+                d = dn;
+            }
+            int best = kIrpInf;
+            for (int y = 0; y <= top; ++y) best = min(best, V[y * 32]);
+            total += best;
+        }
+        if (live) cost[s] = total;
+    }
+}
+
 __global__ void __launch_bounds__(256) irp_reduce_kernel(const long long* __restrict__ cost, int64_t S,
                                                          spdp_saa_partial* __restrict__ partial) {
     __shared__ Part red[8];
@@ -221,8 +283,29 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     spdp_status rc;
     if ((rc = cuda_check(cudaMemcpyAsync(dcust, cust_h, sizeof(IrpCust) * M, cudaMemcpyHostToDevice, st), "H2D cust"))) return rc;
     if ((rc = cuda_check(cudaMemcpyAsync(dvisit, visit_h, (size_t)M * H, cudaMemcpyHostToDevice, st), "H2D visit"))) return rc;
-    if ((rc = cuda_check(cudaMemsetAsync(cost, 0, sizeof(int64_t) * (size_t)S, st), "memset cost"))) return rc;
     long long* c = reinterpret_cast<long long*>(cost);
+    bool prefix_band = true;  // every customer's delivery band is [0, y] (or empty)
+    for (int m = 0; m < M; ++m) prefix_band &= (cust_h[m].X == 0 || cust_h[m].X >= cust_h[m].U);
+    const size_t lane_smem_warp = sizeof(int32_t) * 32 * (size_t)(Umax + 1);
+    if (prefix_band && lane_smem_warp <= 96 * 1024) {
+        int warps = (int)((192 * 1024) / lane_smem_warp);
+        warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaError_t e = cudaFuncSetAttribute(irp_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(irp_lane_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(irp_lane)");
+            attr_set = true;
+        }
+        const int64_t ntile = (S + 31) / 32;
+        int64_t blocks = (ntile + warps - 1) / warps;
+        prof_begin(st);
+        irp_lane_kernel<<<(unsigned)blocks, warps * 32, lane_smem_warp * warps, st>>>(dvisit, dcust, H, M, Umax, demand,
+                                                                                     ld, S, c);
+        rc = last_launch("irp_lane_kernel");
+        prof_end(st);
+    } else {
+    if ((rc = cuda_check(cudaMemsetAsync(cost, 0, sizeof(int64_t) * (size_t)S, st), "memset cost"))) return rc;
     const int need = Umax + 1;
     if (need <= 32) rc = launch_irp<1>(dvisit, dcust, H, M, demand, ld, S, c, st);
     else if (need <= 64) rc = launch_irp<2>(dvisit, dcust, H, M, demand, ld, S, c, st);
@@ -230,6 +313,7 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     else if (need <= 256) rc = launch_irp<8>(dvisit, dcust, H, M, demand, ld, S, c, st);
     else if (need <= 512) rc = launch_irp<16>(dvisit, dcust, H, M, demand, ld, S, c, st);
     else rc = launch_irp<32>(dvisit, dcust, H, M, demand, ld, S, c, st);
+    }
     if (rc) return rc;
     if (partial) {
         if ((rc = cuda_check(cudaMemsetAsync(partial, 0, sizeof(spdp_saa_partial), st), "memset partial"))) return rc;
