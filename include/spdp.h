@@ -70,6 +70,11 @@ typedef enum {
 /* flags */
 #define SPDP_F_VALIDATE 1u          /* check tour permutation, dist >= 0 and the int32 range
                                        bound on the device; synchronizes; E_DATA on failure */
+/* sweep algorithm (spdp_split_eval / _batch); all give bit-identical results.
+ * Default (none set): register-ring Eq. (3) sweep for windows <= 32, deque otherwise. */
+#define SPDP_F_SWEEP_INT   2u       /* register ring, exact int32, predicated min per candidate */
+#define SPDP_F_SWEEP_F32   4u       /* register ring, exact integer-valued fp32, FMA-pipe masking */
+#define SPDP_F_SWEEP_DEQUE 8u       /* monotone-deque sliding-window minimum, O(1) amortised */
 
 /* Summable SAA partial.  Every field is an int64 that adds
  * elementwise, so partials of disjoint scenario sets combine by a plain SUM

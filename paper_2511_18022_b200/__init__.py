@@ -31,6 +31,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 SPDP_OK, SPDP_E_USAGE, SPDP_E_DATA, SPDP_E_RESOURCE, SPDP_E_CUDA = 0, 2, 3, 4, 5
 INFEASIBLE = 2**31 - 1
 F_VALIDATE = 1
+F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8}  # sweep algorithm flags (spdp.h)
 MAX_N = 16384
 
 SYMBOLS = (
@@ -221,8 +222,10 @@ def split_mask(tour, demand, Q: int, S: int | None = None):
 
 # ------------------------------------------------------------------ a2 + a5 + a6
 def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool = True,
-               want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None, partial=None):
-    """Per-scenario split costs (int32 [S], INFEASIBLE sentinel) and the SAA partial (int64 [6])."""
+               want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None, partial=None,
+               algo: str | None = None):
+    """Per-scenario split costs (int32 [S], INFEASIBLE sentinel) and the SAA partial (int64 [6]).
+    algo: None/"auto", "int", "f32" or "deque" (identical results; see spdp.h)."""
     torch = _torch()
     n, ld = demand.shape
     S = ld if S is None else S
@@ -236,14 +239,14 @@ def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool
     _check(_lib.spdp_split_eval(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld, S,
                                 int(Q), _dev_ptr(cost, "cost") if want_cost else None,
                                 _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
-                                ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_VALIDATE if validate else 0,
+                                ctypes.c_void_p(ws.data_ptr()), ws.numel(), (F_VALIDATE if validate else 0) | F_SWEEP[algo],
                                 _stream(dev)), "spdp_split_eval")
     return cost, partial
 
 
 def split_eval_batch(tours, dist, demand, Q: int, S: int | None = None, want_cost: bool = True,
                      want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None,
-                     partial=None):
+                     partial=None, algo: str | None = None):
     """T tours [T][n] over one demand set: costs int32 [T][S] and partials int64 [T][6]."""
     torch = _torch()
     n, ld = demand.shape
@@ -259,8 +262,9 @@ def split_eval_batch(tours, dist, demand, Q: int, S: int | None = None, want_cos
                                       _dev_ptr(demand, "demand"), ld, S, int(Q),
                                       _dev_ptr(cost, "cost") if want_cost else None,
                                       _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
-                                      ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_VALIDATE if validate else 0,
-                                      _stream(dev)), "spdp_split_eval_batch")
+                                      ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                      (F_VALIDATE if validate else 0) | F_SWEEP[algo], _stream(dev)),
+           "spdp_split_eval_batch")
     return cost, partial
 
 

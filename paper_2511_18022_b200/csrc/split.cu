@@ -972,9 +972,12 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     // the device (TourInfo::ok: lanes of a tour that fails it are finished by the int finish kernel)
     const int64_t qeff = Qe < 65535u ? (int64_t)Qe : 65535;
     const bool f32_loads_exact = ((int64_t)n + 64) * qeff + (int64_t)Qe + 1 < (1LL << 24);
-    const int mode = sweep_mode();
+    int mode = sweep_mode();
+    if (flags & SPDP_F_SWEEP_INT) mode = 1;
+    if (flags & SPDP_F_SWEEP_F32) mode = 2;
+    if (flags & SPDP_F_SWEEP_DEQUE) mode = 3;
     // default int: measured marginally faster on the headline config; SPDP_SWEEP=f32 opts in
-    const bool use_f32 = W <= 32 && f32_loads_exact && mode == 2;
+    const bool use_f32 = W <= 32 && f32_loads_exact && mode == 2;  // (f32 not exact here: int ring)
     // windows wider than the largest cheap register ring: the O(1)-amortised deque sweep
     // (measured 4.8x faster than the W=64 ring at n=1000, slower at small windows)
     if (mode == 3 || (mode == 0 && W > 32)) rc = launch_deque(st, args);

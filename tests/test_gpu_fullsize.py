@@ -33,16 +33,17 @@ def test_c2_full_all_costs_and_saa(spdp):
     inst, S = cfg["inst"], cfg["S"]
     d = spdp.gen_demands(cfg["model"], 0, S)
     tour, dist = torch.from_numpy(inst["tour"]).cuda(), torch.from_numpy(inst["dist"]).cuda()
-    cost, part = spdp.split_eval(tour, dist, d, inst["Q"], S=S, window_hint=bench_config.HINT["C2"])
     dem = oracle.gen_demands(cfg["model"], 0, S)
     assert np.array_equal(d.cpu().numpy().view(np.uint16)[:, :S], dem)
     want = oracle.split(inst["tour"], inst["dist"], dem, inst["Q"])
-    got = cost.cpu().numpy().astype(np.int64)
-    assert np.array_equal(got, want)
     w = oracle.saa(want)
-    est = spdp.saa_mean(part)
-    assert est["m"] == S and est["mean"] == w["mean"]
-    assert abs(est["var"] - w["var"]) <= 1e-12 * w["var"]
+    for algo in (None, "f32", "deque"):  # None = the launch configuration bench.py times
+        cost, part = spdp.split_eval(tour, dist, d, inst["Q"], S=S, window_hint=bench_config.HINT["C2"], algo=algo)
+        got = cost.cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, want), algo
+        est = spdp.saa_mean(part)
+        assert est["m"] == S and est["mean"] == w["mean"]
+        assert abs(est["var"] - w["var"]) <= 1e-12 * w["var"]
 
 
 @pytest.mark.parametrize("name", ["C3", "C4"])

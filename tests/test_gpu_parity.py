@@ -69,17 +69,21 @@ def test_prefix_and_mask(spdp):
 
 
 # ------------------------------------------------------------------ a5 / a6 single tour
-def _check_split(spdp, inst, dem, S, hints=(0, 8, 16, 32, 64), Q=None):
+ALGOS = (None, "int", "f32", "deque")
+
+
+def _check_split(spdp, inst, dem, S, hints=(0, 8, 16, 32, 64), Q=None, algos=ALGOS):
     Q = inst["Q"] if Q is None else Q
     want = oracle_cost_as_i32(oracle.split(inst["tour"], inst["dist"], dem, Q, S=S))
     want_saa = oracle.saa(oracle.split(inst["tour"], inst["dist"], dem, Q, S=S))
     tour, dist, D = to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem)
     for h in hints:
-        cost, part = spdp.split_eval(tour, dist, D, Q, S=S, window_hint=h, validate=(h == 0))
+      for algo in algos:
+        cost, part = spdp.split_eval(tour, dist, D, Q, S=S, window_hint=h, validate=(h == 0), algo=algo)
         got = cost.cpu().numpy().astype(np.int64)
         bad = np.nonzero(got != want)[0]
-        assert bad.size == 0, "hint %d: %d mismatches, first s=%d got %d want %d" % (
-            h, bad.size, bad[0], got[bad[0]], want[bad[0]])
+        assert bad.size == 0, "hint %d algo %s: %d mismatches, first s=%d got %d want %d" % (
+            h, algo, bad.size, bad[0], got[bad[0]], want[bad[0]])
         p = part.cpu().numpy()
         assert p[0] == want_saa["m"] and p[1] == want_saa["infeasible"]
         assert p[2] == want_saa["sum"] and (int(p[4]) << 32) + int(p[3]) == want_saa["sumsq"]
@@ -145,9 +149,9 @@ def test_split_batch_tours(spdp):
     S = 2_500
     dem = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
     want = oracle.split_tours(tours, inst["dist"], dem, inst["Q"], S=S)
-    for h in (0, 16, 32):
+    for h, algo in ((0, None), (16, "int"), (32, "f32"), (16, "deque"), (8, None)):
         cost, part = spdp.split_eval_batch(to_dev(tours), to_dev(inst["dist"]), to_dev(dem), inst["Q"], S=S,
-                                           window_hint=h)
+                                           window_hint=h, algo=algo)
         assert np.array_equal(cost.cpu().numpy().astype(np.int64), oracle_cost_as_i32(want))
         p = part.cpu().numpy()
         for t in range(tours.shape[0]):
