@@ -42,7 +42,7 @@ constexpr int kSlots = 32;  // SAA partial slots per tour (spread the sweep's at
 __host__ __device__ inline int cg_stride(int n) { return (n + kTabPad + 7) & ~7; }
 
 struct WsLayout {
-    size_t hdr, g0, tinfo, tabs, tabsf, cgs, slots, ovf, total;
+    size_t hdr, g0, tinfo, tabs, rowp, cgs, slots, ovf, total;
 };
 
 inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
@@ -52,7 +52,7 @@ inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
     L.g0 = off; off = align_up(off + sizeof(int32_t) * (size_t)T, 256);
     L.tinfo = off; off = align_up(off + sizeof(TourInfo) * (size_t)T, 256);
     L.tabs = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
-    L.tabsf = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
+    L.rowp = off; off = align_up(off + sizeof(uint64_t) * (size_t)T * (size_t)(n + kTabPad), 256);
     L.cgs = off; off = align_up(off + sizeof(int32_t) * 2 * (size_t)T * (size_t)cg_stride(n), 256);
     L.slots = off; off = align_up(off + sizeof(spdp_saa_partial) * (size_t)T * (size_t)kSlots, 256);
     L.ovf = off; off = align_up(off + sizeof(unsigned long long) * (size_t)T * (size_t)S, 256);
@@ -71,7 +71,8 @@ enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
 __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restrict__ tours, int n,
                                                          const int32_t* __restrict__ dist,
                                                          int2* __restrict__ tabs, int32_t* __restrict__ g0,
-                                                         int2* __restrict__ tabsf, TourInfo* __restrict__ tinfo,
+                                                         const uint16_t* __restrict__ demand, int64_t ld,
+                                                         const uint16_t** __restrict__ rowps, TourInfo* __restrict__ tinfo,
                                                          int32_t* __restrict__ cgs, spdp_saa_partial* __restrict__ slots,
                                                          unsigned* __restrict__ hdr, spdp_saa_partial* __restrict__ partial,
                                                          int validate) {
@@ -169,16 +170,16 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     for (int i = n + tid; i < n + kTabPad; i += nt) tab[i] = make_int2(0, 0);
     if (tid == 0) g0[t] = dist[node(0)];
     __syncthreads();
-    // fp32 tables: cg / 2^24 (exact: |cg| <= 2 cmax), g0f = (g0 + OFF) / 2^24
+    // fp32 tables: cg / 2^24 (exact: |cg| <= 2 cmax), g0f = (g0 + OFF) / 2^24; demand row pointers
     {
         const long long OFF = *dn, cm = *cmx;
-        int2* tabf = tabsf + (int64_t)t * (n + kTabPad);
+        const uint16_t** rowp = rowps + (int64_t)t * (n + kTabPad);
         const int cs = cg_stride(n);
         int32_t* cgi = cgs + (int64_t)t * 2 * cs;  // plane 0: int Cg, plane 1: fp32 Cg / 2^24
         for (int i = tid; i < cs; i += nt) {
             const int2 e = (i < n + kTabPad) ? tab[i] : make_int2(0, 0);
             const int fb = __float_as_int((float)e.y * 0x1p-24f);
-            if (i < n + kTabPad) tabf[i] = make_int2(e.x, fb);
+            if (i < n + kTabPad) rowp[i] = demand + (int64_t)e.x * ld;  // pad rows: row 0
             cgi[i] = e.y;
             cgi[cs + i] = fb;
         }
@@ -253,6 +254,52 @@ struct SweepT<true> {
     using L = float;
 };
 
+// Copy side of a sweep warp: chunk k of the warp's stream is chunk k % nchunks of
+// its (k / nchunks)-th tile; the tile id comes from the global atomic counter
+// when the first chunk of a tile is issued and is handed to the compute side
+// through the warp's queue tq.  Every issue() commits exactly one cp.async
+// group (possibly empty) so the compute side can wait by count.
+template <int W, int NS, int kRowsBytes, int kStageBytes>
+struct WarpStream {
+    unsigned char* stage_base;
+    int64_t* tq;
+    const int2* tabs;
+    const int32_t* cg_plane;  // plane base (int or fp32 Cg) of tour 0
+    const uint16_t* demand;
+    int64_t ld, S, ntile_s, ntiles;
+    int n, nchunks, cgs_stride, lane;
+    unsigned* tile_ctr;
+    int64_t p_tile;
+
+    __device__ __forceinline__ void issue(unsigned k) {
+        const int c = (int)(k % nchunks);
+        if (c == 0) {
+            unsigned id = 0;
+            if (lane == 0) id = atomicAdd(tile_ctr, 1u);
+            id = __shfl_sync(kFull, id, 0);
+            p_tile = (int64_t)id < ntiles ? (int64_t)id : -1;
+            if (lane == 0) tq[(k / nchunks) % kQueue] = p_tile;
+        }
+        if (p_tile >= 0) {
+            unsigned char* sb = stage_base + (size_t)(k % NS) * kStageBytes;
+            const int t = (int)(p_tile / ntile_s);
+            const int64_t s0 = (p_tile % ntile_s) * kTile;
+            const int r0 = c * W;
+            const int rows = (n - r0) < W ? (n - r0) : W;
+            const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
+            const int segs = ((cols + 7) & ~7) / 8;  // 16-byte segments per row (within ld)
+            const int2* __restrict__ tab = tabs + (int64_t)t * (n + kTabPad);
+            for (int e = lane; e < rows * 4; e += 32) {
+                const int r = e >> 2, sg = e & 3;
+                if (sg < segs)
+                    cp_async16(sb + r * (kTile * 2) + sg * 16, demand + (int64_t)__ldg(&tab[r0 + r].x) * ld + s0 + sg * 8);
+            }
+            if (lane < W / 4) cp_async16(sb + kRowsBytes + lane * 16, cg_plane + (int64_t)t * 2 * cgs_stride + r0 + lane * 4);
+        }
+        cp_async_commit();
+    }
+};
+
 template <int W, bool F32>
 __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1)))
     split_sweep_kernel(const int2* __restrict__ tabs, const int32_t* __restrict__ cgs,
@@ -275,41 +322,12 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1
     const int rem = n % W;
     const int cgs_stride = cg_stride(n);
     const uint32_t qpad = Q < 65535u ? Q : 65535u;
-    unsigned* tile_ctr = hdr + HDR_TILE;
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
 
-    // ---- copy side: chunk k of this warp's stream = chunk k % nchunks of local tile k / nchunks
-    int64_t p_tile = -1;
-    auto issue = [&](unsigned k) {  // always commits one group (possibly empty) to keep the count
-        const int c = (int)(k % nchunks);
-        if (c == 0) {
-            unsigned id = 0;
-            if (lane == 0) id = atomicAdd(tile_ctr, 1u);
-            id = __shfl_sync(kFull, id, 0);
-            p_tile = (int64_t)id < ntiles ? (int64_t)id : -1;
-            if (lane == 0) tq[(k / nchunks) % kQueue] = p_tile;
-        }
-        if (p_tile >= 0) {
-            unsigned char* sb = stage_base + (size_t)(k % NS) * Cfg::kStageBytes;
-            const int t = (int)(p_tile / ntile_s);
-            const int64_t s0 = (p_tile % ntile_s) * kTile;
-            const int r0 = c * W;
-            const int rows = (n - r0) < W ? (n - r0) : W;
-            const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
-            const int segs = ((cols + 7) & ~7) / 8;  // 16-byte segments per row (within ld)
-            const int2* __restrict__ tab = tabs + (int64_t)t * (n + kTabPad);
-            for (int e = lane; e < rows * 4; e += 32) {
-                const int r = e >> 2, sg = e & 3;
-                if (sg < segs)
-                    cp_async16(sb + r * (kTile * 2) + sg * 16,
-                               demand + (int64_t)__ldg(&tab[r0 + r].x) * ld + s0 + sg * 8);
-            }
-            if (lane < W / 4)
-                cp_async16(sb + Cfg::kRowsBytes + lane * 16,
-                           cgs + (int64_t)t * 2 * cgs_stride + (F32 ? cgs_stride : 0) + r0 + lane * 4);
-        }
-        cp_async_commit();
-    };
+    WarpStream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> ws{stage_base, tq, tabs, cgs + (F32 ? cgs_stride : 0), demand,
+                                                            ld, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane,
+                                                            hdr + HDR_TILE, -1};
+    auto issue = [&](unsigned k) { ws.issue(k); };
     for (int k = 0; k < NS; ++k) issue((unsigned)k);
 
     unsigned c_k = 0;  // compute-side chunk sequence number
@@ -444,6 +462,315 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1
             }
         }
     }
+    cp_async_wait<0>();
+}
+
+// Per-tile epilogue shared by the sweeps: defer overflow lanes to the finish
+// kernel, write the per-scenario costs, flush the tile's SAA partial.
+__device__ __forceinline__ void sweep_tile_epilogue(bool live, bool bad, bool ovf, int fval, int t, int64_t s, int64_t S,
+                                                    int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
+                                                    unsigned long long* __restrict__ ovf_list, unsigned* ovf_count,
+                                                    int slot, int lane) {
+    const bool deferred = live && ovf && !bad;
+    if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
+    if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
+    if (slots) {
+        Part p{0, 0, 0, 0, 0};
+        if (live && !deferred) part_add_cost(p, fval, !bad);
+        p = warp_sum(p);
+        if (lane == 0) {
+            spdp_saa_partial* d = &slots[(int64_t)t * kSlots + slot];
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)p.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)p.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)p.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)p.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)p.sq_hi);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- a5: packed-fp32 sweep
+// The same Eq. (3) ring sweep, with the candidate work shaped for the FMA pipe
+// and the packed fp32x2 unit of sm_100 (FADD2):
+//  * loads: P (tour-order prefix) is kept as the bit pattern of the float
+//    2^23 + P, so P += q is one integer add and the bits ARE the exact float
+//    (no conversion); the ring stores Y = 2^23 + P(p) + Q the same way.
+//  * values: G = (g + OFF) 2^-24 in [0, 1), exact (TourInfo::ok).
+//  * candidate p of age a: s = sat(P(i) - Y) is 0 when p is in the window
+//     and 1 when not (FADD.SAT, exact: integers below 2^24);
+//    two candidates are completed by one FADD2, c = G + s (>= 1 > every
+//    feasible G when masked), and folded by 3-input mins (FMNMX3).
+//  * the ring is float2 pairs {slot 2m, slot 2m+1}; positions 2m, 2m+1 are
+//    adjacent, so at every layer the ages pair up as (1,2),(3,4),.. (odd
+//    layer) or 1,(2,3),(4,5),.. (even layer) -- both compile-time.
+//  * candidate groups: U0 pairs unconditionally, then UG pairs per warp vote
+//    (any lane whose window still reaches the group's youngest age).
+//  * overflow: only tested where the scan reaches the oldest ring age (rare);
+//    a lane whose window reaches it is deferred to the finish kernel.
+//  * a new tile does not clear the ring: P restarts Q + 1 above the previous
+//    tile's last load, which puts every old slot outside every window (the
+//    ring is cleared only when P would leave the exact range).
+//  * the copy side advances incremental cursors (no divisions per chunk) and
+//    the SAA partial is accumulated per lane across tiles, reduced once per
+//    warp (and on a change of tour).
+// Minimum of N floats as a balanced tree of 3-input mins (FMNMX3): depth log3(N).
+template <int N>
+__device__ __forceinline__ float min_tree(const float* v) {
+    if constexpr (N == 1) return v[0];
+    else if constexpr (N == 2) return fminf(v[0], v[1]);
+    else if constexpr (N == 3) return fminf(fminf(v[0], v[1]), v[2]);
+    else {
+        constexpr int A = (N + 2) / 3, B = (N - A + 1) / 2, C = N - A - B;
+        return fminf(fminf(min_tree<A>(v), min_tree<B>(v + A)), min_tree<C>(v + A + B));
+    }
+}
+
+template <int W, int NS, int kRowsBytes, int kStageBytes>
+struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel parameters)
+    int c;          // next chunk of the current copy tile (== nchunks: fetch a new tile)
+    int stage;      // next stage to fill
+    unsigned qw;    // queue write index
+    int ct;         // tour of the copy tile (-1: no more tiles)
+    uint32_t s0;    // first scenario of the copy tile
+    int segs;       // 16-byte segments per row in the copy tile (4 unless ragged)
+
+    // One chunk: lane r < rows copies demand row r0 + r of the tile (4 x 16 B from its row
+    // pointer, built by tour_prep_kernel), lanes < W/4 copy the chunk's Cg slice.
+    __device__ __forceinline__ void issue(unsigned char* stage_base, int2* tq, const uint16_t* const* __restrict__ rowp,
+                                          const int32_t* __restrict__ cgf, int64_t S, uint32_t ntile_s,
+                                          uint32_t ntiles, int n, int nchunks, int cgs_stride, int lane,
+                                          unsigned* tile_ctr) {
+        if (c == nchunks) {
+            unsigned id = 0;
+            if (lane == 0) id = atomicAdd(tile_ctr, 1u);
+            id = __shfl_sync(kFull, id, 0);
+            int2 e = make_int2(-1, 0);
+            ct = -1;
+            if (id < ntiles) {
+                const uint32_t t = id / ntile_s, b = id - t * ntile_s;
+                e = make_int2((int)t, (int)b);
+                ct = (int)t;
+                s0 = b * (uint32_t)kTile;
+                const int64_t left = S - (int64_t)s0;
+                segs = left >= kTile ? 4 : (int)((left + 7) >> 3);
+            }
+            if (lane == 0) tq[qw & (kQueue - 1)] = e;
+            ++qw;
+            c = 0;
+        }
+        if (ct >= 0) {
+            unsigned char* sb = stage_base + stage * kStageBytes;
+            const int r0 = c * W;
+            const int rows = (n - r0) < W ? (n - r0) : W;
+            if (lane < rows) {
+                const uint16_t* src = rowp[(int64_t)ct * (n + kTabPad) + r0 + lane] + s0;
+                unsigned char* dst = sb + lane * (kTile * 2);
+                if (segs == 4) {
+                    cp_async16(dst, src);
+                    cp_async16(dst + 16, src + 8);
+                    cp_async16(dst + 32, src + 16);
+                    cp_async16(dst + 48, src + 24);
+                } else {
+                    for (int k = 0; k < segs; ++k) cp_async16(dst + 16 * k, src + 8 * k);
+                }
+            }
+            if (lane < W / 4) cp_async16(sb + kRowsBytes + lane * 16, cgf + (int64_t)ct * 2 * cgs_stride + r0 + lane * 4);
+        }
+        cp_async_commit();
+        ++c;
+        stage = (stage + 1 == NS) ? 0 : stage + 1;
+    }
+};
+
+template <int W, int U0, int UG>
+__global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
+    split_sweep_f2_kernel(const uint16_t* const* __restrict__ rowp, const int32_t* __restrict__ cgs,
+                          const TourInfo* __restrict__ tinfo, int n, int T, int64_t S, uint32_t Q, uint32_t p_limit,
+                          int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
+                          unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
+    using Cfg = SweepCfg<W>;
+    constexpr int NS = Cfg::NS;
+    constexpr int H = W / 2;  // float2 ring pairs
+    static_assert(W % 4 == 0 && U0 >= 1 && UG >= 1 && kQueue >= NS + 2, "bad sweep config");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
+    int2* tq = reinterpret_cast<int2*>(wbase);
+    unsigned char* stage_base = wbase + kQueue * 8;
+    const uint32_t ntile_s = (uint32_t)((S + kTile - 1) / kTile);
+    const int nchunks = (n + W - 1) / W;
+    const int rem = n % W;
+    const uint32_t qpad = Q < 65535u ? Q : 65535u;
+    constexpr uint32_t kMagic = 0x4B000000u;  // bits of 2^23
+    const int slot = (blockIdx.x * kSweepWarps + wid) % kSlots;
+    unsigned* ovf_count = hdr + HDR_OVF_COUNT;
+
+    const uint32_t ntiles = ntile_s * (uint32_t)T;
+    const int cgs_stride = cg_stride(n);
+    F2Stream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0u, 4};
+    auto issue = [&]() {
+        cs.issue(stage_base, tq, rowp, cgs + cgs_stride, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane, hdr + HDR_TILE);
+    };
+    for (int k = 0; k < NS; ++k) issue();
+
+    float2 G2[H];
+    uint32_t Yb[W];
+#pragma unroll
+    for (int k = 0; k < H; ++k) G2[k] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = 0; k < W; ++k) Yb[k] = 0u;  // float 0 < 2^23 <= P: never in a window
+    uint32_t Pb = kMagic;
+
+    // per-lane SAA accumulator of tour acc_t, kept in shared memory (after the warp's stages)
+    struct LanePart {
+        int nf, ni;
+        long long sum, sqlo, sqhi;
+    };
+    __shared__ LanePart accs[kSweepThreads];
+    LanePart* accp = &accs[tid];
+    *accp = LanePart{0, 0, 0, 0, 0};
+    int acc_t = -1;
+    auto flush = [&]() {
+        const LanePart a = *accp;
+        const Part p = warp_sum(Part{a.nf, a.ni, a.sum, a.sqlo, a.sqhi});
+        *accp = LanePart{0, 0, 0, 0, 0};
+        if (lane == 0 && acc_t >= 0) {
+            spdp_saa_partial* d = &slots[(int64_t)acc_t * kSlots + slot];
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)p.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)p.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)p.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)p.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)p.sq_hi);
+        }
+    };
+
+    int cstage = 0;
+    for (unsigned u = 0;; ++u) {
+        cp_async_wait<NS - 1>();
+        __syncwarp();
+        const int2 tile = tq[u & (kQueue - 1)];
+        if (tile.x < 0) break;
+        const int t = tile.x;
+        const int64_t s0 = (int64_t)tile.y * kTile;
+        const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
+        const bool live = lane < cols;
+        const int col = live ? lane : cols - 1;
+        const TourInfo ti = tinfo[t];
+        if (slots && t != acc_t) {
+            flush();
+            acc_t = t;
+        }
+        // restart P above every old slot's Y (or clear the ring when P nears the exact range's end)
+        if (__any_sync(kFull, Pb - kMagic > p_limit)) {
+#pragma unroll
+            for (int k = 0; k < W; ++k) Yb[k] = 0u;
+            Pb = kMagic;
+        } else {
+            Pb += Q + 1u;
+        }
+        float gprev = __int_as_float(ti.g0f_bits);
+        uint32_t qmax = 0u;
+        bool ovf = false;
+
+        for (int c = 0; c < nchunks; ++c) {
+            if (c > 0) {
+                cp_async_wait<NS - 1>();
+                __syncwarp();
+            }
+            unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
+            uint16_t* bufw = reinterpret_cast<uint16_t*>(sb) + col;
+            const float* cgc = reinterpret_cast<const float*>(sb + Cfg::kRowsBytes);
+            if (rem != 0 && c == nchunks - 1) {  // pad the final chunk (see split_sweep_kernel)
+                for (int j = rem; j < W; ++j) bufw[j * kTile] = (uint16_t)qpad;
+                __syncwarp();
+            }
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const float cg = cgc[j];
+                const uint32_t qi = bufw[j * kTile];
+                qmax = max(qmax, qi);
+                const uint32_t Pnb = Pb + qi;
+                const float Pn = __uint_as_float(Pnb);
+                if (j & 1) G2[j >> 1].y = gprev;
+                else G2[j >> 1].x = gprev;
+                Yb[j] = Pb + Q;
+                // Candidates of age >= 2 first: they depend only on P and on g values of earlier
+                // layers, so the DP chain through the layers is just  g = min(old, g_prev) + Cg.
+                // pair unit v: even layer -> ages (2v+2, 2v+3); odd layer -> age 2 alone (v = 0),
+                // ages (2v+1, 2v+2) (v >= 1).  A pair's younger slot is odd, its older slot
+                // (the float2's .x) is the one below.
+                auto unit = [&](const int v, float& lo, float& hi) {
+                    if ((j & 1) && v == 0) {
+                        const int xs = (j - 1 + W) % W;
+                        lo = hi = G2[xs >> 1].x + __saturatef(Pn - __uint_as_float(Yb[xs]));
+                        return;
+                    }
+                    const int ys = (j & 1) ? ((j - 2 * v + 2 * W) % W) : ((j - 2 * v - 1 + 2 * W) % W);
+                    const int xs = ys - 1;
+                    const float2 sp = make_float2(__saturatef(Pn - __uint_as_float(Yb[xs])),
+                                                  __saturatef(Pn - __uint_as_float(Yb[ys])));
+                    const float2 cnd = __fadd2_rn(G2[xs >> 1], sp);
+                    lo = cnd.x;
+                    hi = cnd.y;
+                };
+                const int nunits = (j & 1) ? H : H - 1;
+                const int os = (j & 1) ? ((j + 1) % W) : ((j + 2) % W);  // oldest scanned slot
+                float cv[2 * U0];
+#pragma unroll
+                for (int v = 0; v < U0; ++v) {
+                    if (v < nunits) unit(v, cv[2 * v], cv[2 * v + 1]);
+                    else cv[2 * v] = cv[2 * v + 1] = 2.0f;
+                }
+                float a = min_tree<2 * U0>(cv);
+                if (U0 >= nunits) ovf |= Yb[os] >= Pnb;
+#pragma unroll
+                for (int v0 = U0; v0 < H; v0 += UG) {
+                    if (v0 >= nunits) break;
+                    const int ys = (j & 1) ? ((j - 2 * v0 + 2 * W) % W) : ((j - 2 * v0 - 1 + 2 * W) % W);
+                    if (!__builtin_expect(__any_sync(kFull, Yb[ys] >= Pnb), 0)) break;
+#pragma unroll
+                    for (int v = v0; v < v0 + UG; ++v)
+                        if (v < nunits) {
+                            float lo, hi;
+                            unit(v, lo, hi);
+                            a = fminf(a, fminf(lo, hi));
+                        }
+                    if (v0 + UG >= nunits) ovf |= Yb[os] >= Pnb;  // the scan reached the oldest ring age
+                }
+                // age 1 (p = i - 1) is always in the window when q <= Q (q > Q: qmax, DESIGN R4)
+                gprev = fminf(a, gprev) + cg;
+                Pb = Pnb;
+            }
+            __syncwarp();
+            issue();
+            cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
+        }
+        if (rem != 0) {  // f(n) sits in the slot of position n (pushed by the first padded layer)
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                if (k == rem) gprev = (k & 1) ? G2[k >> 1].y : G2[k >> 1].x;
+        }
+        const bool bad = qmax > Q;
+        const int fval = (int)(gprev * 0x1p24f) - ti.off;
+        const bool deferred = live && (ovf || ti.ok == 0) && !bad;
+        const int64_t s = s0 + col;
+        if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
+        if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
+        if (live && !deferred) {
+            LanePart a = *accp;
+            if (bad) {
+                a.ni += 1;
+            } else {
+                const unsigned long long sq = (unsigned long long)fval * (unsigned long long)fval;
+                a.nf += 1;
+                a.sum += fval;
+                a.sqlo += (long long)(sq & 0xffffffffull);
+                a.sqhi += (long long)(sq >> 32);
+            }
+            *accp = a;
+        }
+    }
+    if (slots) flush();
     cp_async_wait<0>();
 }
 
@@ -651,8 +978,9 @@ __global__ void __launch_bounds__(256) split_finish_kernel(
             __syncthreads();
         }
     }
-    int* g = reinterpret_cast<int*>(smem_raw) + (size_t)wid * 2 * (n + 1);
+    int* g = reinterpret_cast<int*>(smem_raw) + (size_t)wid * 3 * (n + 1);
     uint32_t* pre = reinterpret_cast<uint32_t*>(g + (n + 1));
+    int* cgl = g + 2 * (n + 1);  // Cg per layer (staged once: no global load on the serial chain)
     const unsigned count = *ovf_count;
     for (unsigned idx = blockIdx.x * nw + wid; idx < count; idx += gridDim.x * nw) {
         const unsigned long long key = ovf_list[idx];
@@ -664,7 +992,12 @@ __global__ void __launch_bounds__(256) split_finish_kernel(
         if (lane == 0) pre[0] = 0u;
         for (int base = 0; base < n; base += 32) {
             const int i = base + lane;
-            uint32_t v = (i < n) ? (uint32_t)demand[(int64_t)tab[i].x * ld + s] : 0u;
+            uint32_t v = 0u;
+            if (i < n) {
+                const int2 e = tab[i];
+                v = demand[(int64_t)e.x * ld + s];
+                cgl[i] = e.y;
+            }
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t u = __shfl_up_sync(kFull, v, o);
@@ -678,7 +1011,7 @@ __global__ void __launch_bounds__(256) split_finish_kernel(
         int m = 0;  // mask(L+1), monotone in L
         for (int L = 0; L < n; ++L) {
             const uint32_t Pn = pre[L + 1];
-            const int cg = tab[L].y;
+            const int cg = cgl[L];
             for (;;) {  // first p >= m with P(L+1) - P(p) <= Q (p = L always qualifies: q <= Q)
                 const int p = m + lane;
                 const unsigned b = __ballot_sync(kFull, p <= L && Pn - pre[p] <= Q);
@@ -793,6 +1126,7 @@ __global__ void __launch_bounds__(256) saa_reduce_kernel(const int32_t* __restri
 
 // ---------------------------------------------------------------- host dispatch
 struct SweepArgs {
+    const uint16_t* const* rowp;
     const int2* tabs;
     const int32_t* cgs;
     const int32_t* g0;
@@ -877,14 +1211,65 @@ static spdp_status launch_deque(cudaStream_t st, const SweepArgs& a) {
     return rc;
 }
 
+template <int W, int U0, int UG>
+static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
+    auto kern = split_sweep_f2_kernel<W, U0, UG>;
+    static int blocks_per_sm = 0;
+    if (blocks_per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SweepCfg<W>::kSmem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kSweepThreads, SweepCfg<W>::kSmem);
+        if (e != cudaSuccess) return cuda_check(e, "split_sweep_f2 setup");
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const int64_t ntiles = ((a.S + kTile - 1) / kTile) * a.T;
+    int64_t grid = (int64_t)blocks_per_sm * num_sms();
+    const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
+    if (grid > need) grid = need;
+    prof_begin(st);
+    // P restarts Q + 1 above the previous tile's loads; one tile adds at most (n + W) q_pad + Q + 1
+    const int64_t qpad = a.Q < 65535u ? a.Q : 65535;
+    const int64_t lim = (1LL << 23) - 1 - ((int64_t)a.n + W) * qpad - 2 * (int64_t)a.Q - 2;
+    if (lim < 0) return fail(SPDP_E_RESOURCE, "split_sweep_f2: loads exceed the exact fp32 range");
+    kern<<<(unsigned)grid, kSweepThreads, SweepCfg<W>::kSmem, st>>>(a.rowp, a.cgs, a.tinfo, a.n, a.T, a.S, a.Q,
+                                                                    (uint32_t)lim, a.cost, a.slots, a.ovf, a.hdr);
+    spdp_status rc = last_launch("split_sweep_f2_kernel");
+    prof_end(st);
+    return rc;
+}
+
+// Tuning knob (environment, read once): SPDP_F2=<U0><UG> picks the candidate grouping of the
+// W=20 packed-fp32 sweep (pairs scanned unconditionally, pairs per warp vote); default 31.
+static int f2_cfg() {
+    static int m = [] {
+        const char* e = getenv("SPDP_F2");
+        return e ? atoi(e) : 0;
+    }();
+    return m;
+}
+
 static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArgs& a) {
     if (f32) {
         switch (W) {
-            case 8: return launch_sweep_t<8, true>(st, a);
-            case 16: return launch_sweep_t<16, true>(st, a);
-            case 20: return launch_sweep_t<20, true>(st, a);
-            case 24: return launch_sweep_t<24, true>(st, a);
-            default: return launch_sweep_t<32, true>(st, a);
+            case 8: return launch_sweep_f2_t<8, 2, 1>(st, a);
+            case 16:
+                switch (f2_cfg()) {
+                    case 21: return launch_sweep_f2_t<16, 2, 1>(st, a);
+                    case 32: return launch_sweep_f2_t<16, 3, 2>(st, a);
+                    case 41: return launch_sweep_f2_t<16, 4, 1>(st, a);
+                    default: return launch_sweep_f2_t<16, 3, 1>(st, a);
+                }
+            case 20:
+                switch (f2_cfg()) {
+                    case 21: return launch_sweep_f2_t<20, 2, 1>(st, a);
+                    case 32: return launch_sweep_f2_t<20, 3, 2>(st, a);
+                    case 41: return launch_sweep_f2_t<20, 4, 1>(st, a);
+                    case 42: return launch_sweep_f2_t<20, 4, 2>(st, a);
+                    default: return launch_sweep_f2_t<20, 3, 1>(st, a);
+                }
+            case 24: return launch_sweep_f2_t<24, 3, 1>(st, a);
+            default: return launch_sweep_f2_t<32, 4, 2>(st, a);
         }
     }
     switch (W) {
@@ -927,7 +1312,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     int32_t* g0 = reinterpret_cast<int32_t*>(w + L.g0);
     TourInfo* tinfo = reinterpret_cast<TourInfo*>(w + L.tinfo);
     int2* tabs = reinterpret_cast<int2*>(w + L.tabs);
-    int2* tabsf = reinterpret_cast<int2*>(w + L.tabsf);
+    const uint16_t** rowp = reinterpret_cast<const uint16_t**>(w + L.rowp);
     spdp_saa_partial* slots = reinterpret_cast<spdp_saa_partial*>(w + L.slots);
     unsigned long long* ovf = reinterpret_cast<unsigned long long*>(w + L.ovf);
     // Q above the largest possible load behaves as "everything fits"; clamp so P' + Q fits uint32.
@@ -941,7 +1326,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     {
         const int threads = n >= 2048 ? 1024 : 256;
         const size_t smem = 34 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
-        tour_prep_kernel<<<T, threads, smem, st>>>(tours, n, dist, tabs, g0, tabsf, tinfo,
+        tour_prep_kernel<<<T, threads, smem, st>>>(tours, n, dist, tabs, g0, demand, ld, rowp, tinfo,
                                                    reinterpret_cast<int32_t*>(w + L.cgs), partial ? slots : nullptr, hdr,
                                                    partial, validate ? 1 : 0);
         if ((rc = last_launch("tour_prep_kernel"))) return rc;
@@ -965,19 +1350,20 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         if (window_hint == 0) W = pick_w((int)(h[HDR_SAMPLE_W] + h[HDR_SAMPLE_W] / 4 + 1));
     }
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
-    const SweepArgs args{tabs, reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
+    const SweepArgs args{rowp, tabs, reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
                          cost, partial ? slots : nullptr, ovf, hdr};
     // fp32 sweep when every load value it forms (P' <= (n + W) min(Q, 65535) for feasible scenarios
     // including the padded layers, Y = P' + Q) is an exact float; the per-tour cost range is checked on
     // the device (TourInfo::ok: lanes of a tour that fails it are finished by the int finish kernel)
+    // (the packed-fp32 sweep keeps loads as 2^23 + P + Q, exact below 2^24)
     const int64_t qeff = Qe < 65535u ? (int64_t)Qe : 65535;
-    const bool f32_loads_exact = ((int64_t)n + 64) * qeff + (int64_t)Qe + 1 < (1LL << 24);
+    const bool f32_loads_exact = ((int64_t)n + 64) * qeff + 2 * (int64_t)Qe + 2 < (1LL << 23);
     int mode = sweep_mode();
     if (flags & SPDP_F_SWEEP_INT) mode = 1;
     if (flags & SPDP_F_SWEEP_F32) mode = 2;
     if (flags & SPDP_F_SWEEP_DEQUE) mode = 3;
-    // default int: measured marginally faster on the headline config; SPDP_SWEEP=f32 opts in
-    const bool use_f32 = W <= 32 && f32_loads_exact && mode == 2;  // (f32 not exact here: int ring)
+    // default for windows <= 32: the packed-fp32 ring when its loads are exact, else the int ring
+    const bool use_f32 = W <= 32 && f32_loads_exact && S < (1LL << 31) && (mode == 2 || mode == 0);
     // windows wider than the largest cheap register ring: the O(1)-amortised deque sweep
     // (measured 4.8x faster than the W=64 ring at n=1000, slower at small windows)
     if (mode == 3 || (mode == 0 && W > 32)) rc = launch_deque(st, args);
@@ -985,7 +1371,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     if (rc) return rc;
     {
         // finish: per-tour SAA partials + the overflow list (warps per CTA limited by 8 (n+1) bytes of smem each)
-        const size_t per_warp = 2 * sizeof(int) * (size_t)(n + 1);
+        const size_t per_warp = 3 * sizeof(int) * (size_t)(n + 1);
         int warps = (int)((160 * 1024) / per_warp);
         warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
         static bool attr_set = false;

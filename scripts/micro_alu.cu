@@ -146,6 +146,64 @@ __global__ void k_ffma(int* out, int seed) {
     if (s == 12345.f) out[0] = (int)s;
 }
 
+// (8) packed candidate idiom of split_sweep_f2_kernel: s = sat(P - Y) x2 (FADD.SAT), c = G + s (FADD2),
+//     best = min3(best, c.x, c.y) (FMNMX3)
+__global__ void k_f2(int* out, int seed) {
+    float best[CH / 2], Y[CH];
+    float2 G[CH / 2];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) Y[c] = (float)(seed * c + threadIdx.x);
+#pragma unroll
+    for (int c = 0; c < CH / 2; ++c) { best[c] = 1.0f; G[c] = make_float2(c * 1e-3f, c * 2e-3f); }
+    float P = (float)seed;
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH / 2; ++c) {
+            const float2 s = make_float2(__saturatef(P - Y[2 * c]), __saturatef(P - Y[2 * c + 1]));
+            const float2 v = __fadd2_rn(G[c], s);
+            best[c] = fminf(best[c], fminf(v.x, v.y));
+        }
+        P += 1.0f;
+    }
+    float s = 0;
+#pragma unroll
+    for (int c = 0; c < CH / 2; ++c) s += best[c];
+    if (s == 12345.f) out[0] = (int)s;
+}
+
+// (9) FADD2 alone (2 adds per instruction)
+__global__ void k_fadd2(int* out, int seed) {
+    float2 a[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) a[c] = make_float2((float)(seed + c), (float)(seed - c));
+    const float2 b = make_float2(0.5f, 0.25f);
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) a[c] = __fadd2_rn(a[c], b);
+    }
+    float s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += a[c].x + a[c].y;
+    if (s == 12345.f) out[0] = (int)s;
+}
+
+// (10) FADD.SAT alone (register operands)
+__global__ void k_fsat1(int* out, int seed) {
+    float a[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) a[c] = (float)(seed + c) * 1e-3f;
+    float b = (float)seed * 1e-4f;
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) a[c] = __saturatef(a[c] - b);
+        b = b * 0.5f;
+    }
+    float s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s += a[c];
+    if (s == 12345.f) out[0] = (int)s;
+}
+
 template <typename K>
 static double run(K kern, const char* name, double cand_per_iter_per_thread, int* d) {
     int blocks = 148 * 8, threads = 256;
@@ -177,6 +235,9 @@ int main() {
     run(k_fmaxmin, "ffma + fmnmx + fmnmx3/2 (float max mask)", CH, d);
     run(k_imaxmin, "viaddmax + vimnmx3/2 (int max mask)", CH, d);
     run(k_ffma, "ffma (fma pipe)", CH, d);
+    run(k_f2, "fadd.sat x2 + fadd2 + fmnmx3 (packed, per cand)", CH, d);
+    run(k_fadd2, "fadd2 (per instruction)", CH, d);
+    run(k_fsat1, "fadd.sat (per instruction)", CH, d);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
     return 0;
