@@ -132,6 +132,13 @@ SPDP_API const char* spdp_last_error(void);
  * stream.  Both are cudaEvent_t.  Pass NULL, NULL to clear.  Thread-local. */
 SPDP_API void spdp_set_profile_events(void* start_event, void* stop_event);
 
+/* Name of the sweep kernel (a5/a8 variant and its ring width) that the last
+ * spdp_split_eval / spdp_split_eval_batch call on this thread enqueued, e.g.
+ * "split_sweep_f2_kernel<20,3,2>"; "" before the first call.  Thread-local,
+ * owned by the library, valid until the next call on this thread.  For
+ * reports (bench.py's roofline line); never needed for correctness. */
+SPDP_API const char* spdp_last_kernel(void);
+
 /* Workspace bytes needed by spdp_split_eval / spdp_split_eval_batch for T tours
  * of n customers over S scenarios (T = 1 for spdp_split_eval). */
 SPDP_API size_t spdp_workspace_bytes(int32_t n, int64_t S, int32_t T);

@@ -38,7 +38,7 @@ SYMBOLS = (
     "spdp_version", "spdp_last_error", "spdp_workspace_bytes", "spdp_gen_demands", "spdp_demand_prefix",
     "spdp_split_mask", "spdp_split_eval", "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean",
     "spdp_host_workspace_bytes", "spdp_split_eval_host", "spdp_irp_workspace_bytes", "spdp_irp_dp",
-    "spdp_set_profile_events",
+    "spdp_set_profile_events", "spdp_last_kernel",
 )
 
 
@@ -73,6 +73,7 @@ def _sig():
     L.spdp_set_profile_events.argtypes = [P, P]
     L.spdp_set_profile_events.restype = None
     L.spdp_last_error.restype = ctypes.c_char_p
+    L.spdp_last_kernel.restype = ctypes.c_char_p
     L.spdp_workspace_bytes.argtypes = [i32, i64, i32]
     L.spdp_workspace_bytes.restype = sz
     L.spdp_host_workspace_bytes.argtypes = [i32, i64]
@@ -119,6 +120,11 @@ def set_profile_events(start=None, stop=None):
         if not start.cuda_event or not stop.cuda_event:
             raise ValueError("set_profile_events: events not created yet (record them once first)")
         _lib.spdp_set_profile_events(ctypes.c_void_p(start.cuda_event), ctypes.c_void_p(stop.cuda_event))
+
+
+def last_kernel() -> str:
+    """Name of the sweep kernel the last split call on this thread enqueued (spdp_last_kernel)."""
+    return _lib.spdp_last_kernel().decode()
 
 
 def version() -> int:

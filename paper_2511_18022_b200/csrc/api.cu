@@ -32,6 +32,15 @@ spdp_status cuda_check(cudaError_t e, const char* what) {
 
 spdp_status last_launch(const char* what) { return cuda_check(cudaGetLastError(), what); }
 
+static thread_local char g_kernel[128] = "";
+
+void set_last_kernel(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_kernel, sizeof(g_kernel), fmt, ap);
+    va_end(ap);
+}
+
 static thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
 
 void prof_begin(cudaStream_t st) {
@@ -54,6 +63,8 @@ extern "C" void spdp_set_profile_events(void* start_event, void* stop_event) {
 }
 
 extern "C" const char* spdp_last_error(void) { return g_err; }
+
+extern "C" const char* spdp_last_kernel(void) { return g_kernel; }
 
 // a6 finalize.  Exact integer moments, one rounding
 // per reported statistic: mean = sum / m, var = (m sumsq - sum^2) / (m (m-1)).

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/spdp.h"
 
 namespace spdp {
@@ -21,6 +23,8 @@ spdp_status last_launch(const char* what);
 // spdp_set_profile_events hook: record around the dominant kernel if set.
 void prof_begin(cudaStream_t st);
 void prof_end(cudaStream_t st);
+// spdp_last_kernel(): record the name of the sweep kernel just enqueued.
+void set_last_kernel(const char* fmt, ...);
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -31,6 +35,29 @@ __device__ __forceinline__ uint32_t ld_stream_u16(const uint16_t* p) {
     unsigned short v;
     asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
     return (uint32_t)v;
+}
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// A kernel launched with launch_pdl() may start while its stream predecessor is
+// still running; pdl_wait() blocks until the predecessor grid has completed and
+// its memory is visible, pdl_trigger() lets the successor start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // ---- bulk-async copy (TMA engine, cp.async.bulk) + mbarrier helpers -------

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     long long* dn = wsum + 32;                                             // D[n]
     int* cmx = reinterpret_cast<int*>(dn + 1);                             // block max of the used costs
     unsigned* seen = reinterpret_cast<unsigned*>(smem_raw + 34 * sizeof(long long));  // bitmap
+    pdl_trigger();  // the sweep's CTAs may launch now (they wait for this grid's completion)
     const int t = blockIdx.x;
     const int32_t* tour = tours + (int64_t)t * n;
     int2* tab = tabs + (int64_t)t * (n + kTabPad);
@@ -152,6 +153,11 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     long long D = wsum[wid] + incl - local;  // D at position lo+1 (1-based): sum of arcs before lo
     if (lo <= n - 1 && n - 1 < hi) *dn = D + local;  // D[n] = all arcs
     atomicMax(cmx, cmax);
+    // every table entry of this thread's positions in one pass (dist re-reads hit L1):
+    // tab[i] = {row, Cg}, the int / fp32 Cg planes and the demand row pointer
+    const int cs = cg_stride(n);
+    int32_t* cgi = cgs + (int64_t)t * 2 * cs;  // plane 0: int Cg, plane 1: fp32 Cg / 2^24 (exact when ok)
+    const uint16_t** rowp = rowps + (int64_t)t * (n + kTabPad);
     for (int i = lo; i < hi; ++i) {
         const int a = node(i);
         const int ca0 = dist[(int64_t)a * N1];
@@ -166,32 +172,33 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
             e.y = (int)(D + ca0);       // B[n] = D[n] + c_{s_n,0}
         }
         tab[i] = e;
+        cgi[i] = e.y;
+        cgi[cs + i] = __float_as_int((float)e.y * 0x1p-24f);
+        rowp[i] = demand + (int64_t)e.x * ld;
     }
-    for (int i = n + tid; i < n + kTabPad; i += nt) tab[i] = make_int2(0, 0);
+    for (int i = n + tid; i < cs; i += nt) {  // padding (rows: row 0; Cg: 0)
+        if (i < n + kTabPad) {
+            tab[i] = make_int2(0, 0);
+            rowp[i] = demand;
+        }
+        cgi[i] = 0;
+        cgi[cs + i] = 0;
+    }
+    for (int i = cs + tid; i < n + kTabPad; i += nt) {
+        tab[i] = make_int2(0, 0);
+        rowp[i] = demand;
+    }
     if (tid == 0) g0[t] = dist[node(0)];
     __syncthreads();
-    // fp32 tables: cg / 2^24 (exact: |cg| <= 2 cmax), g0f = (g0 + OFF) / 2^24; demand row pointers
-    {
+    if (tid == 0) {  // g0f = (g0 + OFF) / 2^24
         const long long OFF = *dn, cm = *cmx;
-        const uint16_t** rowp = rowps + (int64_t)t * (n + kTabPad);
-        const int cs = cg_stride(n);
-        int32_t* cgi = cgs + (int64_t)t * 2 * cs;  // plane 0: int Cg, plane 1: fp32 Cg / 2^24
-        for (int i = tid; i < cs; i += nt) {
-            const int2 e = (i < n + kTabPad) ? tab[i] : make_int2(0, 0);
-            const int fb = __float_as_int((float)e.y * 0x1p-24f);
-            if (i < n + kTabPad) rowp[i] = demand + (int64_t)e.x * ld;  // pad rows: row 0
-            cgi[i] = e.y;
-            cgi[cs + i] = fb;
-        }
-        if (tid == 0) {
-            TourInfo ti;
-            ti.g0f_bits = __float_as_int((float)(dist[node(0)] + OFF) * 0x1p-24f);
-            ti.off = (int)(OFF < INT_MAX ? OFF : INT_MAX);
-            // g + OFF <= (2n + 1) cmax + OFF and f(n) + OFF <= 2 n cmax + OFF: all below 2^24
-            ti.ok = ((2LL * n + 2) * cm + OFF < (1LL << 24)) ? 1 : 0;
-            ti.pad = 0;
-            tinfo[t] = ti;
-        }
+        TourInfo ti;
+        ti.g0f_bits = __float_as_int((float)(dist[node(0)] + OFF) * 0x1p-24f);
+        ti.off = (int)(OFF < INT_MAX ? OFF : INT_MAX);
+        // g + OFF <= (2n + 1) cmax + OFF and f(n) + OFF <= 2 n cmax + OFF: all below 2^24
+        ti.ok = ((2LL * n + 2) * cm + OFF < (1LL << 24)) ? 1 : 0;
+        ti.pad = 0;
+        tinfo[t] = ti;
     }
     // range: |g|, |f| <= 3 n cmax (SURVEY §7 hard part 10)
     if ((long long)cmax * (3LL * n + 1) >= (long long)INT_MAX) bad |= ST_RANGE;
@@ -311,6 +318,7 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1
     using V = typename SweepT<F32>::V;
     using LT = typename SweepT<F32>::L;
     constexpr int NS = Cfg::NS;
+    pdl_wait();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
@@ -591,6 +599,7 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
     using Cfg = SweepCfg<W>;
     constexpr int NS = Cfg::NS;
     constexpr int H = W / 2;  // float2 ring pairs
+    pdl_wait();  // tables, counters and partial slots come from tour_prep_kernel
     static_assert(W % 4 == 0 && U0 >= 1 && UG >= 1 && kQueue >= NS + 2, "bad sweep config");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -696,9 +705,9 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
                 Yb[j] = Pb + Q;
                 // Candidates of age >= 2 first: they depend only on P and on g values of earlier
                 // layers, so the DP chain through the layers is just  g = min(old, g_prev) + Cg.
-                // pair unit v: even layer -> ages (2v+2, 2v+3); odd layer -> age 2 alone (v = 0),
-                // ages (2v+1, 2v+2) (v >= 1).  A pair's younger slot is odd, its older slot
-                // (the float2's .x) is the one below.
+                // pair unit v: even layer -> ages (2v+2, 2v+3), the last one (ages W, 1) wrapping
+                // around the ring; odd layer -> age 2 alone (v = 0), ages (2v+1, 2v+2) (v >= 1).
+                // A pair's odd slot is the float2's .y, the even slot below it the .x.
                 auto unit = [&](const int v, float& lo, float& hi) {
                     if ((j & 1) && v == 0) {
                         const int xs = (j - 1 + W) % W;
@@ -713,8 +722,8 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
                     lo = cnd.x;
                     hi = cnd.y;
                 };
-                const int nunits = (j & 1) ? H : H - 1;
-                const int os = (j & 1) ? ((j + 1) % W) : ((j + 2) % W);  // oldest scanned slot
+                const int nunits = H;
+                const int os = (j + 1) % W;  // oldest ring slot (age W)
                 float cv[2 * U0];
 #pragma unroll
                 for (int v = 0; v < U0; ++v) {
@@ -806,6 +815,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
                        unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
     using Cfg = DequeCfg;
     constexpr int NS = kDqNS, R = kDqRows, D = kDqD;
+    pdl_wait();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
@@ -952,10 +962,11 @@ __global__ void __launch_bounds__(256) split_finish_kernel(
     const spdp_saa_partial* __restrict__ slots, int kslots, int T, const int2* __restrict__ tabs,
     const int32_t* __restrict__ g0s, int n, const uint16_t* __restrict__ demand, int64_t ld, int64_t S, uint32_t Q,
     int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ partial,
-    const unsigned long long* __restrict__ ovf_list, const unsigned* __restrict__ ovf_count) {
+    const unsigned long long* __restrict__ ovf_list, const unsigned* __restrict__ ovf_count, int thread_path) {
     extern __shared__ unsigned char smem_raw[];
     __shared__ Part red[8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    pdl_wait();  // slots and the overflow list come from the sweep
     if (partial) {
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
             Part a{0, 0, 0, 0, 0};
@@ -978,10 +989,55 @@ __global__ void __launch_bounds__(256) split_finish_kernel(
             __syncthreads();
         }
     }
+    const unsigned count = *ovf_count;
+    if (thread_path) {
+        // one thread per overflow scenario (lowest latency: the DP chain is one min + one add per
+        // layer, the window loads are independent of it); per-thread arrays interleaved [i][thread]
+        const int B = blockDim.x, tid = threadIdx.x;
+        uint32_t* Ps = reinterpret_cast<uint32_t*>(smem_raw);
+        int* Gs = reinterpret_cast<int*>(Ps + (size_t)(n + 1) * B);
+        int* Cs = Gs + (size_t)(n + 1) * B;
+        for (unsigned idx = (unsigned)tid * gridDim.x + blockIdx.x; idx < count; idx += gridDim.x * (unsigned)B) {
+            const unsigned long long key = ovf_list[idx];
+            const int t = (int)(key >> 40);
+            const int64_t s = (int64_t)(key & ((1ull << 40) - 1));
+            const int2* tab = tabs + (int64_t)t * (n + kTabPad);
+            uint32_t acc = 0u;
+            Ps[tid] = 0u;
+#pragma unroll 8
+            for (int i = 0; i < n; ++i) {
+                const int2 e = __ldg(&tab[i]);
+                acc += demand[(int64_t)e.x * ld + s];
+                Ps[(size_t)(i + 1) * B + tid] = acc;
+                Cs[(size_t)i * B + tid] = e.y;
+            }
+            int gp = g0s[t];
+            Gs[tid] = gp;
+            int m = 0;
+            for (int L = 0; L < n; ++L) {  // g(L+1) = min_{p in [mask(L+1), L]} g(p) + Cg[L]
+                const uint32_t Pn = Ps[(size_t)(L + 1) * B + tid];
+                while (Pn - Ps[(size_t)m * B + tid] > Q) ++m;  // m <= L: every q <= Q here
+                int best = gp;
+#pragma unroll 4
+                for (int p = m; p < L; ++p) best = min(best, Gs[(size_t)p * B + tid]);
+                gp = best + Cs[(size_t)L * B + tid];
+                Gs[(size_t)(L + 1) * B + tid] = gp;
+            }
+            const int f = gp;
+            if (cost) cost[(int64_t)t * S + s] = f;
+            if (partial) {
+                const unsigned long long sq = (unsigned long long)f * (unsigned long long)f;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].n_feas), 1ull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sum), (unsigned long long)f);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_lo), sq & 0xffffffffull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_hi), sq >> 32);
+            }
+        }
+        return;
+    }
     int* g = reinterpret_cast<int*>(smem_raw) + (size_t)wid * 3 * (n + 1);
     uint32_t* pre = reinterpret_cast<uint32_t*>(g + (n + 1));
     int* cgl = g + 2 * (n + 1);  // Cg per layer (staged once: no global load on the serial chain)
-    const unsigned count = *ovf_count;
     for (unsigned idx = blockIdx.x * nw + wid; idx < count; idx += gridDim.x * nw) {
         const unsigned long long key = ovf_list[idx];
         const int t = (int)(key >> 40);
@@ -1169,9 +1225,11 @@ static spdp_status launch_sweep_t(cudaStream_t st, const SweepArgs& a) {
     const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
     if (grid > need) grid = need;
     prof_begin(st);
-    kern<<<(unsigned)grid, kSweepThreads, SweepCfg<W>::kSmem, st>>>(a.tabs, a.cgs, a.g0, a.tinfo, a.n, a.T, a.demand,
-                                                                    a.ld, a.S, a.Q, a.cost, a.slots, a.ovf, a.hdr);
-    spdp_status rc = last_launch("split_sweep_kernel");
+    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kSweepThreads), SweepCfg<W>::kSmem, st, a.tabs,
+                                           a.cgs, a.g0, a.tinfo, a.n, a.T, a.demand, a.ld, a.S, a.Q, a.cost, a.slots,
+                                           a.ovf, a.hdr),
+                                "split_sweep_kernel");
+    set_last_kernel("split_sweep_kernel<%d,%s>", W, F32 ? "f32" : "int");
     prof_end(st);
     return rc;
 }
@@ -1204,9 +1262,11 @@ static spdp_status launch_deque(cudaStream_t st, const SweepArgs& a) {
     const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
     if (grid > need) grid = need;
     prof_begin(st);
-    split_deque_kernel<<<(unsigned)grid, kSweepThreads, DequeCfg::kSmem, st>>>(a.tabs, a.cgs, a.g0, a.n, a.T, a.demand, a.ld,
-                                                                               a.S, a.Q, a.cost, a.slots, a.ovf, a.hdr);
-    spdp_status rc = last_launch("split_deque_kernel");
+    spdp_status rc = cuda_check(launch_pdl(split_deque_kernel, dim3((unsigned)grid), dim3(kSweepThreads), DequeCfg::kSmem, st,
+                                           a.tabs, a.cgs, a.g0, a.n, a.T, a.demand, a.ld, a.S, a.Q, a.cost, a.slots,
+                                           a.ovf, a.hdr),
+                                "split_deque_kernel");
+    set_last_kernel("split_deque_kernel<%d>", kDqD);
     prof_end(st);
     return rc;
 }
@@ -1232,15 +1292,17 @@ static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
     const int64_t qpad = a.Q < 65535u ? a.Q : 65535;
     const int64_t lim = (1LL << 23) - 1 - ((int64_t)a.n + W) * qpad - 2 * (int64_t)a.Q - 2;
     if (lim < 0) return fail(SPDP_E_RESOURCE, "split_sweep_f2: loads exceed the exact fp32 range");
-    kern<<<(unsigned)grid, kSweepThreads, SweepCfg<W>::kSmem, st>>>(a.rowp, a.cgs, a.tinfo, a.n, a.T, a.S, a.Q,
-                                                                    (uint32_t)lim, a.cost, a.slots, a.ovf, a.hdr);
-    spdp_status rc = last_launch("split_sweep_f2_kernel");
+    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kSweepThreads), SweepCfg<W>::kSmem, st, a.rowp,
+                                           a.cgs, a.tinfo, a.n, a.T, a.S, a.Q, (uint32_t)lim, a.cost, a.slots, a.ovf,
+                                           a.hdr),
+                                "split_sweep_f2_kernel");
+    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d>", W, U0, UG);
     prof_end(st);
     return rc;
 }
 
 // Tuning knob (environment, read once): SPDP_F2=<U0><UG> picks the candidate grouping of the
-// W=20 packed-fp32 sweep (pairs scanned unconditionally, pairs per warp vote); default 31.
+// W=16/20 packed-fp32 sweeps (pairs scanned unconditionally, pairs per warp vote); defaults 31 / 32.
 static int f2_cfg() {
     static int m = [] {
         const char* e = getenv("SPDP_F2");
@@ -1263,10 +1325,10 @@ static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArg
             case 20:
                 switch (f2_cfg()) {
                     case 21: return launch_sweep_f2_t<20, 2, 1>(st, a);
-                    case 32: return launch_sweep_f2_t<20, 3, 2>(st, a);
+                    case 31: return launch_sweep_f2_t<20, 3, 1>(st, a);
                     case 41: return launch_sweep_f2_t<20, 4, 1>(st, a);
                     case 42: return launch_sweep_f2_t<20, 4, 2>(st, a);
-                    default: return launch_sweep_f2_t<20, 3, 1>(st, a);
+                    default: return launch_sweep_f2_t<20, 3, 2>(st, a);
                 }
             case 24: return launch_sweep_f2_t<24, 3, 1>(st, a);
             default: return launch_sweep_f2_t<32, 4, 2>(st, a);
@@ -1371,18 +1433,27 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     if (rc) return rc;
     {
         // finish: per-tour SAA partials + the overflow list (warps per CTA limited by 8 (n+1) bytes of smem each)
+        // overflow scenarios: one thread each (smem 12 (n+1) B per thread) while a CTA still holds
+        // a full warp of them, else one warp each (the warp-cooperative transition-parallel DP)
+        const size_t per_thread = 3 * sizeof(int) * (size_t)(n + 1);
+        const int tp_threads = (int)(((200 * 1024) / per_thread) / 32 * 32);
+        const bool thread_path = tp_threads >= 32;
         const size_t per_warp = 3 * sizeof(int) * (size_t)(n + 1);
-        int warps = (int)((160 * 1024) / per_warp);
+        int warps = thread_path ? (tp_threads > 256 ? 8 : tp_threads / 32) : (int)((160 * 1024) / per_warp);
         warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
+        const size_t fin_smem = thread_path ? per_thread * 32 * warps : per_warp * warps;
         static bool attr_set = false;
         if (!attr_set) {
             cudaError_t e = cudaFuncSetAttribute(split_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_finish)");
             attr_set = true;
         }
-        split_finish_kernel<<<2 * num_sms(), warps * 32, per_warp * warps, st>>>(
-            partial ? slots : nullptr, kSlots, T, tabs, g0, n, demand, ld, S, Qe, cost, partial, ovf, ovf_count);
-        if ((rc = last_launch("split_finish_kernel"))) return rc;
+        rc = cuda_check(launch_pdl(split_finish_kernel, dim3(2 * num_sms()), dim3(warps * 32), fin_smem, st,
+                                   partial ? slots : nullptr, (int)kSlots, T, (const int2*)tabs, (const int32_t*)g0, n,
+                                   demand, ld, S, Qe, cost, partial, (const unsigned long long*)ovf,
+                                   (const unsigned*)ovf_count, thread_path ? 1 : 0),
+                        "split_finish_kernel");
+        if (rc) return rc;
     }
     return SPDP_OK;
 }
