@@ -243,6 +243,7 @@ constexpr int kQueue = 16;  // tile-id queue entries per warp (>= tiles the copi
 template <int W>
 struct SweepCfg {
     static constexpr int NS = (W <= 8) ? 12 : (W <= 16 ? 7 : (W <= 24 ? 6 : (W <= 32 ? 4 : 3)));  // stages
+    static constexpr int kMinBlocks = (W <= 24 ? 3 : 2);  // CTAs per SM the register budget targets
     static constexpr int kRowsBytes = W * kTile * (int)sizeof(uint16_t);   // W x 64 B
     static constexpr int kStageBytes = kRowsBytes + W * (int)sizeof(int32_t);  // rows + Cg slice (16 B multiple)
     static constexpr int kWarpBytes = kQueue * 8 + NS * kStageBytes;
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1
         cp_async_wait<NS - 1>();  // the tile's first chunk (the oldest outstanding group) has landed
         __syncwarp();
         const int64_t tile = tq[u % kQueue];
-        if (tile < 0) break;
+        if (__all_sync(kFull, tile < 0)) break;  // warp-uniform (see split_sweep_f2_kernel)
         const int t = (int)(tile / ntile_s);
         const int64_t s0 = (tile % ntile_s) * kTile;
         const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
@@ -547,7 +548,7 @@ struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel para
     __device__ __forceinline__ void issue(unsigned char* stage_base, int2* tq, const uint16_t* const* __restrict__ rowp,
                                           const int32_t* __restrict__ cgf, int64_t S, uint32_t ntile_s,
                                           uint32_t ntiles, int n, int nchunks, int cgs_stride, int lane,
-                                          unsigned* tile_ctr) {
+                                          unsigned* tile_ctr, uint32_t qpad2) {
         if (c == nchunks) {
             unsigned id = 0;
             if (lane == 0) id = atomicAdd(tile_ctr, 1u);
@@ -581,6 +582,10 @@ struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel para
                 } else {
                     for (int k = 0; k < segs; ++k) cp_async16(dst + 16 * k, src + 8 * k);
                 }
+            } else if (lane < W) {  // final chunk: rows n.. hold q_pad = min(Q, 65535) (see split_sweep_kernel)
+                uint4* dst = reinterpret_cast<uint4*>(sb + lane * (kTile * 2));
+#pragma unroll
+                for (int k = 0; k < 4; ++k) dst[k] = make_uint4(qpad2, qpad2, qpad2, qpad2);
             }
             if (lane < W / 4) cp_async16(sb + kRowsBytes + lane * 16, cgf + (int64_t)ct * 2 * cgs_stride + r0 + lane * 4);
         }
@@ -590,13 +595,22 @@ struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel para
     }
 };
 
-template <int W, int U0, int UG>
-__global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
+// F2Cfg: SweepCfg with the stage count / CTAs per SM of a packed-fp32 variant (MB = 0: defaults).
+template <int W, int MB>
+struct F2Cfg : SweepCfg<W> {
+    static constexpr int NS = MB >= 4 ? 4 : SweepCfg<W>::NS;
+    static constexpr int kMinBlocks = MB > 0 ? MB : SweepCfg<W>::kMinBlocks;
+    static constexpr int kWarpBytes = kQueue * 8 + NS * SweepCfg<W>::kStageBytes;
+    static constexpr size_t kSmem = (size_t)kSweepWarps * kWarpBytes;
+};
+
+template <int W, int U0, int UG, int MB>
+__global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
     split_sweep_f2_kernel(const uint16_t* const* __restrict__ rowp, const int32_t* __restrict__ cgs,
                           const TourInfo* __restrict__ tinfo, int n, int T, int64_t S, uint32_t Q, uint32_t p_limit,
                           int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
                           unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
-    using Cfg = SweepCfg<W>;
+    using Cfg = F2Cfg<W, MB>;
     constexpr int NS = Cfg::NS;
     constexpr int H = W / 2;  // float2 ring pairs
     pdl_wait();  // tables, counters and partial slots come from tour_prep_kernel
@@ -618,7 +632,8 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
     const int cgs_stride = cg_stride(n);
     F2Stream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0u, 4};
     auto issue = [&]() {
-        cs.issue(stage_base, tq, rowp, cgs + cgs_stride, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane, hdr + HDR_TILE);
+        cs.issue(stage_base, tq, rowp, cgs + cgs_stride, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane, hdr + HDR_TILE,
+                 qpad * 0x10001u);
     };
     for (int k = 0; k < NS; ++k) issue();
 
@@ -654,11 +669,13 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
     };
 
     int cstage = 0;
+    cp_async_wait<NS - 1>();  // the first tile's first chunk (later ones: end of the chunk loop)
+    __syncwarp();
     for (unsigned u = 0;; ++u) {
-        cp_async_wait<NS - 1>();
-        __syncwarp();
         const int2 tile = tq[u & (kQueue - 1)];
-        if (tile.x < 0) break;
+        // (a vote, not a plain branch: the value is warp-uniform, and the compiler must know it,
+        // or every warp-synchronous instruction below pays a divergence check, BRA.DIV)
+        if (__all_sync(kFull, tile.x < 0)) break;
         const int t = tile.x;
         const int64_t s0 = (int64_t)tile.y * kTile;
         const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
@@ -681,18 +698,12 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
         uint32_t qmax = 0u;
         bool ovf = false;
 
+        // (the chunk loop has no lane- or data-dependent branch: the copy side pads the final
+        // chunk, and every wait is unconditional -- so its warp votes need no divergence checks)
         for (int c = 0; c < nchunks; ++c) {
-            if (c > 0) {
-                cp_async_wait<NS - 1>();
-                __syncwarp();
-            }
             unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
-            uint16_t* bufw = reinterpret_cast<uint16_t*>(sb) + col;
+            const uint16_t* bufw = reinterpret_cast<const uint16_t*>(sb) + col;
             const float* cgc = reinterpret_cast<const float*>(sb + Cfg::kRowsBytes);
-            if (rem != 0 && c == nchunks - 1) {  // pad the final chunk (see split_sweep_kernel)
-                for (int j = rem; j < W; ++j) bufw[j * kTile] = (uint16_t)qpad;
-                __syncwarp();
-            }
 #pragma unroll
             for (int j = 0; j < W; ++j) {
                 const float cg = cgc[j];
@@ -753,6 +764,8 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : 2))
             __syncwarp();
             issue();
             cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
+            cp_async_wait<NS - 1>();  // the next chunk (or the next tile's first chunk) has landed
+            __syncwarp();
         }
         if (rem != 0) {  // f(n) sits in the slot of position n (pushed by the first padded layer)
 #pragma unroll
@@ -865,7 +878,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
         cp_async_wait<NS - 1>();
         __syncwarp();
         const int64_t tile = tq[u % kQueue];
-        if (tile < 0) break;
+        if (__all_sync(kFull, tile < 0)) break;  // warp-uniform (see split_sweep_f2_kernel)
         const int t = (int)(tile / ntile_s);
         const int64_t s0 = (tile % ntile_s) * kTile;
         const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
@@ -1271,15 +1284,16 @@ static spdp_status launch_deque(cudaStream_t st, const SweepArgs& a) {
     return rc;
 }
 
-template <int W, int U0, int UG>
+template <int W, int U0, int UG, int MB = 0>
 static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
-    auto kern = split_sweep_f2_kernel<W, U0, UG>;
+    using Cfg = F2Cfg<W, MB>;
+    auto kern = split_sweep_f2_kernel<W, U0, UG, MB>;
     static int blocks_per_sm = 0;
     if (blocks_per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SweepCfg<W>::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kSweepThreads, SweepCfg<W>::kSmem);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kSweepThreads, Cfg::kSmem);
         if (e != cudaSuccess) return cuda_check(e, "split_sweep_f2 setup");
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
@@ -1292,11 +1306,11 @@ static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
     const int64_t qpad = a.Q < 65535u ? a.Q : 65535;
     const int64_t lim = (1LL << 23) - 1 - ((int64_t)a.n + W) * qpad - 2 * (int64_t)a.Q - 2;
     if (lim < 0) return fail(SPDP_E_RESOURCE, "split_sweep_f2: loads exceed the exact fp32 range");
-    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kSweepThreads), SweepCfg<W>::kSmem, st, a.rowp,
+    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kSweepThreads), Cfg::kSmem, st, a.rowp,
                                            a.cgs, a.tinfo, a.n, a.T, a.S, a.Q, (uint32_t)lim, a.cost, a.slots, a.ovf,
                                            a.hdr),
                                 "split_sweep_f2_kernel");
-    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d>", W, U0, UG);
+    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d,%d>", W, U0, UG, Cfg::kMinBlocks);
     prof_end(st);
     return rc;
 }
@@ -1320,6 +1334,8 @@ static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArg
                     case 21: return launch_sweep_f2_t<16, 2, 1>(st, a);
                     case 32: return launch_sweep_f2_t<16, 3, 2>(st, a);
                     case 41: return launch_sweep_f2_t<16, 4, 1>(st, a);
+                    case 314: return launch_sweep_f2_t<16, 3, 1, 4>(st, a);
+                    case 324: return launch_sweep_f2_t<16, 3, 2, 4>(st, a);
                     default: return launch_sweep_f2_t<16, 3, 1>(st, a);
                 }
             case 20:
