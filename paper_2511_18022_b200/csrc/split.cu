@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
         const bool live = lane < cols;
         const int col = live ? lane : cols - 1;
         const TourInfo ti = tinfo[t];
-        if (slots && t != acc_t) {
+        if (__any_sync(kFull, slots && t != acc_t)) {  // (a vote: the flush's shuffles stay convergent)
             flush();
             acc_t = t;
         }
@@ -699,8 +699,9 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
         bool ovf = false;
 
         // (the chunk loop has no lane- or data-dependent branch: the copy side pads the final
-        // chunk, and every wait is unconditional -- so its warp votes need no divergence checks)
-        for (int c = 0; c < nchunks; ++c) {
+        // chunk, every wait is unconditional and the back edge is a warp vote -- so the compiler
+        // can prove the warp converged and the layer votes need no divergence checks, BRA.DIV)
+        for (int c = 0;;) {
             unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
             const uint16_t* bufw = reinterpret_cast<const uint16_t*>(sb) + col;
             const float* cgc = reinterpret_cast<const float*>(sb + Cfg::kRowsBytes);
@@ -766,6 +767,7 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
             cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
             cp_async_wait<NS - 1>();  // the next chunk (or the next tile's first chunk) has landed
             __syncwarp();
+            if (__all_sync(kFull, ++c >= nchunks)) break;
         }
         if (rem != 0) {  // f(n) sits in the slot of position n (pushed by the first padded layer)
 #pragma unroll
@@ -1316,7 +1318,7 @@ static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
 }
 
 // Tuning knob (environment, read once): SPDP_F2=<U0><UG> picks the candidate grouping of the
-// W=16/20 packed-fp32 sweeps (pairs scanned unconditionally, pairs per warp vote); defaults 31 / 32.
+// W=16/20 packed-fp32 sweeps (pairs scanned unconditionally, pairs per warp vote); default 31.
 static int f2_cfg() {
     static int m = [] {
         const char* e = getenv("SPDP_F2");
@@ -1341,10 +1343,11 @@ static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArg
             case 20:
                 switch (f2_cfg()) {
                     case 21: return launch_sweep_f2_t<20, 2, 1>(st, a);
-                    case 31: return launch_sweep_f2_t<20, 3, 1>(st, a);
+                    case 32: return launch_sweep_f2_t<20, 3, 2>(st, a);
                     case 41: return launch_sweep_f2_t<20, 4, 1>(st, a);
                     case 42: return launch_sweep_f2_t<20, 4, 2>(st, a);
-                    default: return launch_sweep_f2_t<20, 3, 2>(st, a);
+                    case 324: return launch_sweep_f2_t<20, 3, 2, 4>(st, a);
+                    default: return launch_sweep_f2_t<20, 3, 1>(st, a);
                 }
             case 24: return launch_sweep_f2_t<24, 3, 1>(st, a);
             default: return launch_sweep_f2_t<32, 4, 2>(st, a);
