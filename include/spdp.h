@@ -185,6 +185,28 @@ SPDP_API spdp_status spdp_split_eval_batch(const int32_t* tours, int32_t T, cons
                                   int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
                                   void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream);
 
+/* f1. Route recovery for K selected scenarios: the same DP as
+ * spdp_split_eval (Eq. (1)-(3)), recording for every prefix i the
+ * optimal last split point p = pred[k][i] (the route sigma_{p+1}..sigma_i is the
+ * last one of the optimal split of the first i customers); ties keep the
+ * LARGEST p (DESIGN R10), so pred equals the oracle's exactly.
+ *   scen    [K] int64: scenario (column) indices, each in [0, S)      (device)
+ *   pred    [K][n+1] int32: pred[k][0] = -1; -1 where f(i) is infinite (device)
+ *   cost    [K] int32: f(n), SPDP_INFEASIBLE if a demand exceeds Q      (device)
+ *   nroutes [K] int32 (may be NULL): routes of the optimal split of all n
+ *   maxload [K] int32 (may be NULL): largest route load (<= Q: the capacity
+ *           feasibility of every returned route, checked on the device)
+ * Walking pred from i = n back to 0 lists the routes (tour positions
+ * pred[i]..i-1, 0-based).  One thread per scenario (latency-oriented: for
+ * inspecting a few scenarios, e.g. the worst ones of an SAA sample).
+ * ws: spdp_routes_workspace_bytes(n, K) bytes of device memory. */
+SPDP_API size_t spdp_routes_workspace_bytes(int32_t n, int32_t K);
+SPDP_API spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dist, int32_t n,
+                              const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                              const int64_t* scen, int32_t K, int32_t* pred, int32_t* cost,
+                              int32_t* nroutes, int32_t* maxload, void* ws, size_t ws_bytes,
+                              spdp_stream_t stream);
+
 /* a6 standalone: SAA partial of a cost vector (SPDP_INFEASIBLE entries are
  * counted in n_infeas and excluded).  partial: DEVICE pointer to one struct. */
 SPDP_API spdp_status spdp_saa_reduce(const int32_t* cost, int64_t S, spdp_saa_partial* partial,

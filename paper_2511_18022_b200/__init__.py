@@ -38,7 +38,7 @@ SYMBOLS = (
     "spdp_version", "spdp_last_error", "spdp_workspace_bytes", "spdp_gen_demands", "spdp_demand_prefix",
     "spdp_split_mask", "spdp_split_eval", "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean",
     "spdp_host_workspace_bytes", "spdp_split_eval_host", "spdp_irp_workspace_bytes", "spdp_irp_dp",
-    "spdp_set_profile_events", "spdp_last_kernel",
+    "spdp_set_profile_events", "spdp_last_kernel", "spdp_routes_workspace_bytes", "spdp_split_routes",
 )
 
 
@@ -86,6 +86,9 @@ def _sig():
     L.spdp_split_eval.argtypes = [P, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
     L.spdp_split_eval_batch.argtypes = [P, i32, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
     L.spdp_saa_reduce.argtypes = [P, i64, P, P]
+    L.spdp_routes_workspace_bytes.argtypes = [i32, i32]
+    L.spdp_routes_workspace_bytes.restype = sz
+    L.spdp_split_routes.argtypes = [P, P, i32, P, i64, i64, i32, P, i32, P, P, P, P, P, sz, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
     L.spdp_irp_dp.argtypes = [P, ctypes.POINTER(IrpCustomer), i32, i32, P, i64, i64, P, P, P, sz, u32, P]
@@ -248,6 +251,28 @@ def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool
                                 ctypes.c_void_p(ws.data_ptr()), ws.numel(), (F_VALIDATE if validate else 0) | F_SWEEP[algo],
                                 _stream(dev)), "spdp_split_eval")
     return cost, partial
+
+
+def split_routes(tour, dist, demand, Q: int, scen, S: int | None = None):
+    """f1: optimal routes of K selected scenarios (spdp_split_routes).
+    scen: int64 tensor [K] of scenario indices.  Returns (cost int32 [K], pred int32 [K][n+1],
+    nroutes int32 [K], maxload int32 [K]); pred[k][i] = last split point of prefix i."""
+    torch = _torch()
+    n, ld = demand.shape
+    S = ld if S is None else S
+    dev = demand.device
+    K = int(scen.shape[0])
+    cost = torch.empty(K, dtype=torch.int32, device=dev)
+    pred = torch.empty((K, n + 1), dtype=torch.int32, device=dev)
+    nroutes = torch.empty(K, dtype=torch.int32, device=dev)
+    maxload = torch.empty(K, dtype=torch.int32, device=dev)
+    nb = int(_lib.spdp_routes_workspace_bytes(n, K))
+    ws = workspace(nb, dev, tag="routes")
+    _check(_lib.spdp_split_routes(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld, S,
+                                  int(Q), _dev_ptr(scen, "scen"), K, _dev_ptr(pred, "pred"), _dev_ptr(cost, "cost"),
+                                  _dev_ptr(nroutes, "nroutes"), _dev_ptr(maxload, "maxload"),
+                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(dev)), "spdp_split_routes")
+    return cost, pred, nroutes, maxload
 
 
 def split_eval_batch(tours, dist, demand, Q: int, S: int | None = None, want_cost: bool = True,

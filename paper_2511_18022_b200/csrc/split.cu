@@ -1502,6 +1502,105 @@ extern "C" spdp_status spdp_split_eval_batch(const int32_t* tours, int32_t T, co
                         (cudaStream_t)stream, "spdp_split_eval_batch");
 }
 
+// ---------------------------------------------------------------- f1: route recovery
+// One thread per requested scenario; per-thread prefix P and DP values g live in
+// the workspace ([K][n+1] each).  Layer L computes g(L+1) over the window
+// p in [mask(L+1), L] with the two-pointer mask and records the
+// argmin, scanning p upward with "<=" so the LARGEST p wins ties (DESIGN R10).
+// Values are exact int32 (same range check as the sweep); INF marks an empty
+// window (a demand above Q, DESIGN R4) and propagates.
+__global__ void __launch_bounds__(128) split_routes_kernel(const int2* __restrict__ tab, const int32_t* __restrict__ g0s,
+                                                           int n, const uint16_t* __restrict__ demand, int64_t ld,
+                                                           int64_t S, uint32_t Q, const int64_t* __restrict__ scen,
+                                                           int K, int32_t* __restrict__ pred, int32_t* __restrict__ cost,
+                                                           int32_t* __restrict__ nroutes, int32_t* __restrict__ maxload,
+                                                           uint32_t* __restrict__ Pw, int32_t* __restrict__ Gw) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const int64_t N1 = (int64_t)n + 1;
+    int64_t s = scen[k];
+    s = s < 0 ? 0 : (s >= S ? S - 1 : s);  // (the host checks the range; clamp keeps reads in bounds)
+    uint32_t* P = Pw + (int64_t)k * N1;
+    int32_t* G = Gw + (int64_t)k * N1;
+    int32_t* pr = pred + (int64_t)k * N1;
+    uint32_t acc = 0u;
+    P[0] = 0u;
+    for (int i = 0; i < n; ++i) {  // tour-order prefix
+        acc += demand[(int64_t)tab[i].x * ld + s];
+        P[i + 1] = acc;
+    }
+    G[0] = g0s[0];
+    pr[0] = -1;
+    int m = 0;
+    for (int L = 0; L < n; ++L) {
+        const uint32_t Pn = P[L + 1];
+        while (m <= L && Pn - P[m] > Q) ++m;  // mask(L+1); m = L+1: empty window
+        int best = INT_MAX, arg = -1;
+        for (int p = m; p <= L; ++p) {
+            const int v = G[p];
+            if (v != INT_MAX && v <= best) {
+                best = v;
+                arg = p;
+            }
+        }
+        G[L + 1] = (arg < 0) ? INT_MAX : best + tab[L].y;  // tab[n-1].y = B[n]: G[n] = f(n)
+        pr[L + 1] = arg;
+    }
+    const int f = G[n];
+    cost[k] = (f == INT_MAX) ? SPDP_INFEASIBLE : f;
+    if (nroutes || maxload) {
+        int r = 0;
+        uint32_t ml = 0u;
+        if (f != INT_MAX) {
+            for (int i = n; i > 0; i = pr[i]) {  // walk the optimal routes back from n
+                ++r;
+                ml = max(ml, P[i] - P[pr[i]]);
+            }
+        }
+        if (nroutes) nroutes[k] = r;
+        if (maxload) maxload[k] = (int32_t)ml;
+    }
+}
+
+extern "C" size_t spdp_routes_workspace_bytes(int32_t n, int32_t K) {
+    if (n < 1 || K < 1) return 0;
+    return ws_layout(n, 1, 1).total + align_up(sizeof(uint32_t) * 2 * (size_t)K * (size_t)(n + 1), 256);
+}
+
+extern "C" spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dist, int32_t n, const uint16_t* demand,
+                                         int64_t ld, int64_t S, int32_t Q, const int64_t* scen, int32_t K,
+                                         int32_t* pred, int32_t* cost, int32_t* nroutes, int32_t* maxload, void* ws,
+                                         size_t ws_bytes, spdp_stream_t stream) {
+    const char* fn = "spdp_split_routes";
+    if (n < 1 || S < 1 || Q < 1 || K < 1) return fail(SPDP_E_USAGE, "%s: n, S, Q and K must be >= 1", fn);
+    if (n > SPDP_MAX_N) return fail(SPDP_E_RESOURCE, "%s: n=%d > SPDP_MAX_N", fn, n);
+    if (!tour || !dist || !demand || !scen || !pred || !cost || !ws) return fail(SPDP_E_USAGE, "%s: NULL pointer", fn);
+    if (ld < S) return fail(SPDP_E_USAGE, "%s: ld < S", fn);
+    if (ws_bytes < spdp_routes_workspace_bytes(n, K)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
+    cudaStream_t st = (cudaStream_t)stream;
+    const WsLayout L = ws_layout(n, 1, 1);
+    char* w = static_cast<char*>(ws);
+    unsigned* hdr = reinterpret_cast<unsigned*>(w + L.hdr);
+    int32_t* g0 = reinterpret_cast<int32_t*>(w + L.g0);
+    int2* tabs = reinterpret_cast<int2*>(w + L.tabs);
+    const uint16_t** rowp = reinterpret_cast<const uint16_t**>(w + L.rowp);
+    TourInfo* tinfo = reinterpret_cast<TourInfo*>(w + L.tinfo);
+    uint32_t* Pw = reinterpret_cast<uint32_t*>(w + L.total);
+    int32_t* Gw = reinterpret_cast<int32_t*>(Pw + (size_t)K * (size_t)(n + 1));
+    const uint32_t Qe = (uint32_t)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
+    spdp_status rc;
+    {
+        const int threads = n >= 2048 ? 1024 : 256;
+        const size_t smem = 34 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
+        tour_prep_kernel<<<1, threads, smem, st>>>(tour, n, dist, tabs, g0, demand, ld, rowp, tinfo,
+                                                   reinterpret_cast<int32_t*>(w + L.cgs), nullptr, hdr, nullptr, 0);
+        if ((rc = last_launch("tour_prep_kernel"))) return rc;
+    }
+    split_routes_kernel<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(tabs, g0, n, demand, ld, S, Qe, scen, K, pred, cost,
+                                                                   nroutes, maxload, Pw, Gw);
+    return last_launch("split_routes_kernel");
+}
+
 extern "C" spdp_status spdp_demand_prefix(const int32_t* tour, int32_t n, const uint16_t* demand, int64_t ld, int64_t S,
                                           uint32_t* prefix, spdp_stream_t stream) {
     if (n < 1 || S < 1) return fail(SPDP_E_USAGE, "spdp_demand_prefix: n and S must be >= 1");

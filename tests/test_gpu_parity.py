@@ -219,3 +219,45 @@ def test_irp_random_small(spdp):
         want = oracle.irp(H, M, visit, cust, dem, S=S)
         cost, _ = spdp.irp_dp(visit, cust, to_dev(dem), H, M, S=S)
         assert np.array_equal(cost.cpu().numpy(), want), "trial %d" % trial
+
+
+# ------------------------------------------------------------------ f1 route recovery
+@pytest.mark.parametrize("name,S", [("C1", 100), ("C2", 5_003), ("C3", 777)])
+def test_split_routes_pred_exact(spdp, name, S):
+    """pred (last split point of every prefix) equals the oracle's, ties -> largest p; the routes
+    of the optimal split partition the tour, every route load <= Q, and the route costs add up
+    to f(n) (the route cost of Eq. (1) evaluated on the recovered routes)."""
+    cfg = synth.config_instance(name)
+    inst = cfg["inst"]
+    tour = cfg["tours"][0]
+    dem = oracle.gen_demands(cfg["model"], 0, S, ld=spdp.padded_ld(S))
+    rng = np.random.default_rng(7)
+    scen = np.unique(np.concatenate([rng.integers(0, S, size=64), [0, S - 1]])).astype(np.int64)
+    want_cost, want_pred = oracle.split(tour, inst["dist"], dem, inst["Q"], want_pred=True, S=S)
+    cost, pred, nr, ml = spdp.split_routes(to_dev(tour), to_dev(inst["dist"]), to_dev(dem), inst["Q"],
+                                           torch.from_numpy(scen).cuda(), S=S)
+    pred, cost, nr, ml = pred.cpu().numpy(), cost.cpu().numpy(), nr.cpu().numpy(), ml.cpu().numpy()
+    assert np.array_equal(cost.astype(np.int64), oracle_cost_as_i32(want_cost[scen]))
+    assert np.array_equal(pred, want_pred[scen])
+    dist = inst["dist"]
+    for k, s in enumerate(scen):
+        routes = oracle.routes_from_pred(pred[k], tour)
+        assert [c for r in routes for c in r] == [int(c) for c in tour]          # a partition, in tour order
+        loads = [sum(int(dem[c - 1, s]) for c in r) for r in routes]
+        assert max(loads) <= inst["Q"] and max(loads) == ml[k] and len(routes) == nr[k]
+        rc = sum(int(dist[0, r[0]]) + sum(int(dist[a, b]) for a, b in zip(r, r[1:])) + int(dist[r[-1], 0])
+                 for r in routes)
+        assert rc == cost[k]
+
+
+def test_split_routes_infeasible(spdp):
+    inst = synth.make_instance(6, seed=3)
+    Q = inst["Q"]
+    rows = [[1] * 6, [Q + 1] + [1] * 5, [1] * 5 + [Q + 1]]
+    dem = synth.explicit_demands(rows)
+    want_cost, want_pred = oracle.split(inst["tour"], inst["dist"], dem, Q, want_pred=True, S=3)
+    cost, pred, nr, _ = spdp.split_routes(to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem), Q,
+                                          torch.arange(3, dtype=torch.int64).cuda(), S=3)
+    assert np.array_equal(cost.cpu().numpy().astype(np.int64), oracle_cost_as_i32(want_cost))
+    assert np.array_equal(pred.cpu().numpy(), want_pred)
+    assert list(nr.cpu().numpy()[1:]) == [0, 0]
