@@ -604,7 +604,7 @@ struct F2Cfg : SweepCfg<W> {
     static constexpr size_t kSmem = (size_t)kSweepWarps * kWarpBytes;
 };
 
-template <int W, int U0, int UG, int MB>
+template <int W, int U0, int UG, int MB, int NG>
 __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
     split_sweep_f2_kernel(const uint16_t* const* __restrict__ rowp, const int32_t* __restrict__ cgs,
                           const TourInfo* __restrict__ tinfo, int n, int T, int64_t S, uint32_t Q, uint32_t p_limit,
@@ -705,10 +705,12 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
             unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
             const uint16_t* bufw = reinterpret_cast<const uint16_t*>(sb) + col;
             const float* cgc = reinterpret_cast<const float*>(sb + Cfg::kRowsBytes);
+            uint32_t qnext = bufw[0];
 #pragma unroll
             for (int j = 0; j < W; ++j) {
                 const float cg = cgc[j];
-                const uint32_t qi = bufw[j * kTile];
+                const uint32_t qi = qnext;  // loaded one layer ahead
+                if (j + 1 < W) qnext = bufw[(j + 1) * kTile];
                 qmax = max(qmax, qi);
                 const uint32_t Pnb = Pb + qi;
                 const float Pn = __uint_as_float(Pnb);
@@ -744,19 +746,22 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
                 }
                 float a = min_tree<2 * U0>(cv);
                 if (U0 >= nunits) ovf |= Yb[os] >= Pnb;
+                // NG voted groups of UG pairs, then (if still needed) the rest in one straight run
 #pragma unroll
-                for (int v0 = U0; v0 < H; v0 += UG) {
+                for (int gi = 0; gi <= NG; ++gi) {
+                    const int v0 = U0 + gi * UG;
+                    const int v1 = gi < NG ? v0 + UG : H;
                     if (v0 >= nunits) break;
                     const int ys = (j & 1) ? ((j - 2 * v0 + 2 * W) % W) : ((j - 2 * v0 - 1 + 2 * W) % W);
                     if (!__builtin_expect(__any_sync(kFull, Yb[ys] >= Pnb), 0)) break;
 #pragma unroll
-                    for (int v = v0; v < v0 + UG; ++v)
+                    for (int v = v0; v < v1; ++v)
                         if (v < nunits) {
                             float lo, hi;
                             unit(v, lo, hi);
                             a = fminf(a, fminf(lo, hi));
                         }
-                    if (v0 + UG >= nunits) ovf |= Yb[os] >= Pnb;  // the scan reached the oldest ring age
+                    if (v1 >= nunits) ovf |= Yb[os] >= Pnb;  // the scan reached the oldest ring age
                 }
                 // age 1 (p = i - 1) is always in the window when q <= Q (q > Q: qmax, DESIGN R4)
                 gprev = fminf(a, gprev) + cg;
@@ -1286,10 +1291,10 @@ static spdp_status launch_deque(cudaStream_t st, const SweepArgs& a) {
     return rc;
 }
 
-template <int W, int U0, int UG, int MB = 0>
+template <int W, int U0, int UG, int MB = 0, int NG = W>
 static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
     using Cfg = F2Cfg<W, MB>;
-    auto kern = split_sweep_f2_kernel<W, U0, UG, MB>;
+    auto kern = split_sweep_f2_kernel<W, U0, UG, MB, NG>;
     static int blocks_per_sm = 0;
     if (blocks_per_sm == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
@@ -1312,7 +1317,7 @@ static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
                                            a.cgs, a.tinfo, a.n, a.T, a.S, a.Q, (uint32_t)lim, a.cost, a.slots, a.ovf,
                                            a.hdr),
                                 "split_sweep_f2_kernel");
-    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d,%d>", W, U0, UG, Cfg::kMinBlocks);
+    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d,%d,%d>", W, U0, UG, Cfg::kMinBlocks, NG);
     prof_end(st);
     return rc;
 }
