@@ -18,6 +18,8 @@
 // layers.  A warp takes a tile of 32 scenarios of one customer: the tile's
 // demands [H][32] are staged in shared memory with coalesced loads.
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -210,6 +212,86 @@ __global__ void __launch_bounds__(256) irp_lane_kernel(const uint8_t* __restrict
     }
 }
 
+// Lane-per-scenario variant with a LAZY demand shift (same results as irp_lane_kernel).
+// Step B of a period moves the whole value function by d and adds h J; instead of
+// rewriting the array, V is kept as
+//     V[J] = A[(J + off) mod B] + alpha J + K        (B = U + 1, per lane)
+// and a period without delivery costs O(d) (the V'[0] term) instead of O(U):
+//     V'[J] = V[J + d] + h J  ==>  off += d,  K += alpha d,  alpha += h,
+//     V'[0] = b d + min_{y <= min(d, top)} (V[y] - b y)   written at A[off'] - K'.
+// A period WITH delivery (band [0, y], X >= U) recomputes W[y] = c y + min_{I <= y}
+// (V[I] - c I) over y = 0..U in place and resets alpha = K = 0.  States above `top`
+// are +inf and never read.  Sentinels: an entry whose value is >= 2^29 (no real
+// value is: host check) is unreachable; reads add alpha J + K >= 0 to a stored
+// value <= 2^30, so nothing overflows int32 and an unreachable entry stays >= 2^29.
+__global__ void __launch_bounds__(128) irp_lazy_kernel(const uint8_t* __restrict__ visit,
+                                                       const IrpCust* __restrict__ cust, int H, int M, int Umax,
+                                                       const uint16_t* __restrict__ demand, int64_t ld, int64_t S,
+                                                       long long* __restrict__ cost) {
+    extern __shared__ int32_t vsm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int32_t* A = vsm + (size_t)wid * (Umax + 1) * 32 + lane;  // A[x] at A[x * 32]
+    constexpr int32_t kReal = 1 << 29;                        // values >= kReal are unreachable
+    const int64_t ntile = (S + 31) / 32;
+    for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntile; tile += (int64_t)gridDim.x * nw) {
+        const int64_t s0 = tile * 32;
+        const bool live = s0 + lane < S;
+        const int64_t s = live ? s0 + lane : S - 1;
+        long long total = 0;
+        for (int m = 0; m < M; ++m) {
+            const IrpCust p = cust[m];
+            const int U = p.U, B = U + 1;
+            for (int y = 0; y <= U; ++y) A[y * 32] = (y == p.I0) ? 0 : kIrpInf;
+            int off = 0, top = U;
+            int32_t alpha = 0, K = 0;
+            int d = demand[(int64_t)m * ld + s];
+            for (int t = 0; t < H; ++t) {
+                const int dn = (t + 1 < H) ? demand[((int64_t)(t + 1) * M + m) * ld + s] : 0;  // prefetch
+                if (visit[(int64_t)m * H + t] != 0 && p.X > 0) {
+                    // delivery: W[y] = c y + min_{I <= y} (V[I] - c I), y = 0..U, in place (warp-uniform branch)
+                    int32_t run = kIrpInf;
+                    int x = off;
+                    for (int y = 0; y <= U; ++y) {
+                        const int32_t v = (y <= top) ? A[x * 32] + alpha * y + K : kIrpInf;
+                        run = min(run, v - p.c * y);
+                        const int32_t w = run + p.c * y;
+                        A[x * 32] = w >= kReal ? kIrpInf : w;
+                        x = (x + 1 == B) ? 0 : x + 1;
+                    }
+                    alpha = 0;
+                    K = 0;
+                    top = U;
+                }
+                // demand d: V'[0] = b d + min_{y <= min(d, top)} (V[y] - b y); V'[J] = V[J + d] + h J
+                int32_t m0 = kIrpInf;
+                const int ylim = d < top ? d : top;
+                int x = off;
+                for (int y = 0; y <= ylim; ++y) {
+                    m0 = min(m0, A[x * 32] + (alpha - p.b) * y + K);
+                    x = (x + 1 == B) ? 0 : x + 1;
+                }
+                const int dd = d < B ? d : B;  // (a shift by >= B leaves only J = 0; K is then relative)
+                K += alpha * dd;
+                alpha += p.h;
+                off += dd;
+                if (off >= B) off -= B;
+                top = top > d ? top - d : 0;
+                const int32_t v0 = (m0 >= kReal) ? kIrpInf : m0 + p.b * d;
+                A[off * 32] = (v0 >= kReal) ? kIrpInf : v0 - K;
+                d = dn;
+            }
+            int32_t best = kIrpInf;
+            int x = off;
+            for (int y = 0; y <= top; ++y) {
+                best = min(best, A[x * 32] + alpha * y + K);
+                x = (x + 1 == B) ? 0 : x + 1;
+            }
+            total += best;
+        }
+        if (live) cost[s] = total;
+    }
+}
+
 __global__ void __launch_bounds__(256) irp_reduce_kernel(const long long* __restrict__ cost, int64_t S,
                                                          spdp_saa_partial* __restrict__ partial) {
     __shared__ Part red[8];
@@ -287,7 +369,28 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     bool prefix_band = true;  // every customer's delivery band is [0, y] (or empty)
     for (int m = 0; m < M; ++m) prefix_band &= (cust_h[m].X == 0 || cust_h[m].X >= cust_h[m].U);
     const size_t lane_smem_warp = sizeof(int32_t) * 32 * (size_t)(Umax + 1);
-    if (prefix_band && lane_smem_warp <= 96 * 1024) {
+    static const int irp_mode = [] {  // tuning knob: SPDP_IRP=lane selects the eager-shift kernel
+        const char* e = getenv("SPDP_IRP");
+        return (e && !strcmp(e, "lane")) ? 1 : 0;
+    }();
+    if (prefix_band && lane_smem_warp <= 48 * 1024 && irp_mode == 0) {
+        // lazy-shift lane kernel: 4 warps per CTA, several CTAs per SM
+        const int warps = 4;
+        static bool attr_lazy = false;
+        if (!attr_lazy) {
+            cudaError_t e = cudaFuncSetAttribute(irp_lazy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(irp_lazy_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(irp_lazy)");
+            attr_lazy = true;
+        }
+        const int64_t ntile = (S + 31) / 32;
+        const int64_t blocks = (ntile + warps - 1) / warps;
+        prof_begin(st);
+        irp_lazy_kernel<<<(unsigned)blocks, warps * 32, lane_smem_warp * warps, st>>>(dvisit, dcust, H, M, Umax, demand,
+                                                                                     ld, S, c);
+        rc = last_launch("irp_lazy_kernel");
+        prof_end(st);
+    } else if (prefix_band && lane_smem_warp <= 96 * 1024) {
         int warps = (int)((192 * 1024) / lane_smem_warp);
         warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
         static bool attr_set = false;

@@ -261,3 +261,25 @@ def test_split_routes_infeasible(spdp):
     assert np.array_equal(cost.cpu().numpy().astype(np.int64), oracle_cost_as_i32(want_cost))
     assert np.array_equal(pred.cpu().numpy(), want_pred)
     assert list(nr.cpu().numpy()[1:]) == [0, 0]
+
+
+def test_irp_lazy_shift_prefix_band(spdp):
+    """The lazy-shift lane kernel (every customer has X == 0 or X >= U): random parameters,
+    demands above U (shift past the whole state space), long horizons without delivery."""
+    rng = np.random.default_rng(11)
+    for trial in range(10):
+        H, M = int(rng.integers(1, 40)), int(rng.integers(1, 4))
+        visit = (rng.random((M, H)) < rng.random()).astype(np.uint8)
+        cust = []
+        for _ in range(M):
+            U = int(rng.integers(0, 128))
+            X = 0 if rng.random() < 0.15 else int(rng.integers(U, U + 50))
+            cust.append([U, X, int(rng.integers(0, U + 1)), int(rng.integers(0, 5)), int(rng.integers(0, 40)),
+                         int(rng.integers(0, 5))])
+        cust = np.array(cust, dtype=np.int32)
+        S = 333
+        dem = rng.integers(0, 2 * 128 if trial % 3 == 0 else 40, size=(H * M, 336)).astype(np.uint16)
+        want = oracle.irp(H, M, visit, cust, dem, S=S)
+        cost, part = spdp.irp_dp(visit, cust, to_dev(dem), H, M, S=S)
+        assert np.array_equal(cost.cpu().numpy(), want), "trial %d" % trial
+        assert part.cpu().numpy()[2] == int(want.sum())
