@@ -598,7 +598,8 @@ struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel para
 // F2Cfg: SweepCfg with the stage count / CTAs per SM of a packed-fp32 variant (MB = 0: defaults).
 template <int W, int MB>
 struct F2Cfg : SweepCfg<W> {
-    static constexpr int NS = MB >= 4 ? 4 : SweepCfg<W>::NS;
+    // (W = 24: 4 stages keep 3 CTAs per SM within the shared memory)
+    static constexpr int NS = (MB >= 4 || W == 24) ? 4 : SweepCfg<W>::NS;
     static constexpr int kMinBlocks = MB > 0 ? MB : SweepCfg<W>::kMinBlocks;
     static constexpr int kWarpBytes = kQueue * 8 + NS * SweepCfg<W>::kStageBytes;
     static constexpr size_t kSmem = (size_t)kSweepWarps * kWarpBytes;
@@ -974,18 +975,84 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
 // ---------------------------------------------------------------- finish kernel
 // (1) SAA partial of each tour: sum of its CTAs' slots, added atomically (the
 //     partials are zeroed by tour_prep_kernel);
-// (2) the overflow list, with transition-level parallelism:
-//     one warp per scenario, the lanes split the candidates p in
-//     [mask(i), i-1] and combine them with REDUX.MIN; mask(i) advances
-//     monotonically with a ballot.  Any window width.
-__global__ void __launch_bounds__(256) split_finish_kernel(
+// (2) the overflow list (scenarios whose window outgrew the sweep's ring): one
+//     THREAD per scenario with a kOvfW-entry register ring (the exact-int32 Eq. (3)
+//     scan of split_sweep_kernel, each thread exiting its own candidate loop at its
+//     window's edge; demands gathered from global memory kOvfPf layers ahead), so a
+//     few thousand overflow scenarios run fully in parallel with no scratch memory;
+// (3) scenarios whose window outgrows even that ring: one warp per scenario with
+//     transition-level parallelism -- the lanes split the
+//     candidates p in [mask(i), i-1] and combine them with REDUX.MIN, mask(i)
+//     advances monotonically with a ballot; any window width.
+constexpr int kOvfW = 32;   // register ring of the overflow threads (its code is unrolled W x W: keep it small)
+constexpr int kOvfPf = 8;   // demand prefetch distance (layers)
+
+// Exact int32 Eq. (3) scan of one scenario with a W-entry register ring; false if
+// some window reached past the ring (the result is then not valid).
+template <int W>
+__device__ __forceinline__ bool ring_split_one(const int2* __restrict__ tab, int g0, int n,
+                                               const uint16_t* __restrict__ demand, int64_t ld, int64_t s, uint32_t Q,
+                                               int& f) {
+    static_assert(W % kOvfPf == 0, "prefetch distance must divide the ring");
+    int G[W];
+    uint32_t Y[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        G[k] = INT_MAX;
+        Y[k] = 0u;  // P' >= 1: never in a window
+    }
+    uint32_t qb[kOvfPf];  // demands and Cg of the next kOvfPf layers (static slots: layer L uses slot L % kOvfPf)
+    int cb[kOvfPf];
+#pragma unroll
+    for (int k = 0; k < kOvfPf; ++k) {
+        const int2 e = (k < n) ? __ldg(&tab[k]) : make_int2(0, 0);
+        qb[k] = (k < n) ? demand[(int64_t)e.x * ld + s] : 0u;
+        cb[k] = e.y;
+    }
+    int gprev = g0;
+    uint32_t P = 1u;  // P'(i) = 1 + prefix
+    bool ovf = false;
+    for (int L0 = 0; L0 < n; L0 += W) {
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const int L = L0 + j;
+            if (L < n) {
+                const uint32_t q = qb[j % kOvfPf];
+                const int cg = cb[j % kOvfPf];
+                const int La = L + kOvfPf;
+                if (La < n) {
+                    const int2 e = __ldg(&tab[La]);
+                    qb[j % kOvfPf] = demand[(int64_t)e.x * ld + s];
+                    cb[j % kOvfPf] = e.y;
+                }
+                const uint32_t Pn = P + q;
+                ovf |= Y[j] >= Pn;  // the slot being overwritten is still in the window
+                G[j] = gprev;
+                Y[j] = P + Q;
+                int best = gprev;
+#pragma unroll
+                for (int k = 1; k < W; ++k) {
+                    const int sl = (j - k + W) % W;
+                    if (Y[sl] < Pn) break;  // the window is a contiguous suffix (DESIGN R5)
+                    best = min(best, G[sl]);
+                }
+                gprev = best + cg;
+                P = Pn;
+            }
+        }
+    }
+    f = gprev;
+    return !ovf;
+}
+
+__global__ void __launch_bounds__(128) split_finish_kernel(
     const spdp_saa_partial* __restrict__ slots, int kslots, int T, const int2* __restrict__ tabs,
     const int32_t* __restrict__ g0s, int n, const uint16_t* __restrict__ demand, int64_t ld, int64_t S, uint32_t Q,
     int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ partial,
-    const unsigned long long* __restrict__ ovf_list, const unsigned* __restrict__ ovf_count, int thread_path) {
+    const unsigned long long* __restrict__ ovf_list, const unsigned* __restrict__ ovf_count) {
     extern __shared__ unsigned char smem_raw[];
-    __shared__ Part red[8];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ Part red[4];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     pdl_wait();  // slots and the overflow list come from the sweep
     if (partial) {
         for (int t = blockIdx.x; t < T; t += gridDim.x) {
@@ -1010,111 +1077,84 @@ __global__ void __launch_bounds__(256) split_finish_kernel(
         }
     }
     const unsigned count = *ovf_count;
-    if (thread_path) {
-        // one thread per overflow scenario (lowest latency: the DP chain is one min + one add per
-        // layer, the window loads are independent of it); per-thread arrays interleaved [i][thread]
-        const int B = blockDim.x, tid = threadIdx.x;
-        uint32_t* Ps = reinterpret_cast<uint32_t*>(smem_raw);
-        int* Gs = reinterpret_cast<int*>(Ps + (size_t)(n + 1) * B);
-        int* Cs = Gs + (size_t)(n + 1) * B;
-        for (unsigned idx = (unsigned)tid * gridDim.x + blockIdx.x; idx < count; idx += gridDim.x * (unsigned)B) {
-            const unsigned long long key = ovf_list[idx];
-            const int t = (int)(key >> 40);
-            const int64_t s = (int64_t)(key & ((1ull << 40) - 1));
-            const int2* tab = tabs + (int64_t)t * (n + kTabPad);
-            uint32_t acc = 0u;
-            Ps[tid] = 0u;
-#pragma unroll 8
-            for (int i = 0; i < n; ++i) {
-                const int2 e = __ldg(&tab[i]);
-                acc += demand[(int64_t)e.x * ld + s];
-                Ps[(size_t)(i + 1) * B + tid] = acc;
-                Cs[(size_t)i * B + tid] = e.y;
-            }
-            int gp = g0s[t];
-            Gs[tid] = gp;
-            int m = 0;
-            for (int L = 0; L < n; ++L) {  // g(L+1) = min_{p in [mask(L+1), L]} g(p) + Cg[L]
-                const uint32_t Pn = Ps[(size_t)(L + 1) * B + tid];
-                while (Pn - Ps[(size_t)m * B + tid] > Q) ++m;  // m <= L: every q <= Q here
-                int best = gp;
-#pragma unroll 4
-                for (int p = m; p < L; ++p) best = min(best, Gs[(size_t)p * B + tid]);
-                gp = best + Cs[(size_t)L * B + tid];
-                Gs[(size_t)(L + 1) * B + tid] = gp;
-            }
-            const int f = gp;
-            if (cost) cost[(int64_t)t * S + s] = f;
-            if (partial) {
-                const unsigned long long sq = (unsigned long long)f * (unsigned long long)f;
-                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].n_feas), 1ull);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sum), (unsigned long long)f);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_lo), sq & 0xffffffffull);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_hi), sq >> 32);
-            }
+    auto emit = [&](int t, int64_t s, int f) {
+        if (cost) cost[(int64_t)t * S + s] = f;
+        if (partial) {
+            const unsigned long long sq = (unsigned long long)f * (unsigned long long)f;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].n_feas), 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sum), (unsigned long long)f);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_lo), sq & 0xffffffffull);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_hi), sq >> 32);
         }
-        return;
-    }
-    int* g = reinterpret_cast<int*>(smem_raw) + (size_t)wid * 3 * (n + 1);
+    };
+    int* g = reinterpret_cast<int*>(smem_raw) + (size_t)wid * 3 * (n + 1);  // warp scratch of (3)
     uint32_t* pre = reinterpret_cast<uint32_t*>(g + (n + 1));
-    int* cgl = g + 2 * (n + 1);  // Cg per layer (staged once: no global load on the serial chain)
-    for (unsigned idx = blockIdx.x * nw + wid; idx < count; idx += gridDim.x * nw) {
-        const unsigned long long key = ovf_list[idx];
-        const int t = (int)(key >> 40);
-        const int64_t s = (int64_t)(key & ((1ull << 40) - 1));
-        const int2* tab = tabs + (int64_t)t * (n + kTabPad);
-        // tour-order prefix P(i) = sum_{k<=i} q, i = 0..n: all loads in flight, then a warp scan
-        uint32_t carry = 0u;
-        if (lane == 0) pre[0] = 0u;
-        for (int base = 0; base < n; base += 32) {
-            const int i = base + lane;
-            uint32_t v = 0u;
-            if (i < n) {
-                const int2 e = tab[i];
-                v = demand[(int64_t)e.x * ld + s];
-                cgl[i] = e.y;
-            }
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t u = __shfl_up_sync(kFull, v, o);
-                if (lane >= o) v += u;
-            }
-            if (i < n) pre[i + 1] = carry + v;
-            carry += __shfl_sync(kFull, v, 31);
+    int* cgl = g + 2 * (n + 1);
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < count; base += stride) {
+        // (2) one overflow scenario per lane
+        const unsigned idx = base + lane;
+        int t = 0, f = 0;
+        int64_t s = 0;
+        bool todo = false;
+        if (idx < count) {
+            const unsigned long long key = ovf_list[idx];
+            t = (int)(key >> 40);
+            s = (int64_t)(key & ((1ull << 40) - 1));
+            const bool ok = ring_split_one<kOvfW>(tabs + (int64_t)t * (n + kTabPad), g0s[t], n, demand, ld, s, Q, f);
+            if (ok) emit(t, s, f);
+            todo = !ok;
         }
-        if (lane == 0) g[0] = g0s[t];
-        __syncwarp();
-        int m = 0;  // mask(L+1), monotone in L
-        for (int L = 0; L < n; ++L) {
-            const uint32_t Pn = pre[L + 1];
-            const int cg = cgl[L];
-            for (;;) {  // first p >= m with P(L+1) - P(p) <= Q (p = L always qualifies: q <= Q)
-                const int p = m + lane;
-                const unsigned b = __ballot_sync(kFull, p <= L && Pn - pre[p] <= Q);
-                if (b) {
-                    m += __ffs(b) - 1;
-                    break;
+        // (3) the lanes whose window outgrew the ring, one at a time, by the whole warp
+        unsigned pending = __ballot_sync(kFull, todo);
+        while (pending) {
+            const int src = __ffs(pending) - 1;
+            pending &= pending - 1;
+            const int tt = __shfl_sync(kFull, t, src);
+            const int64_t ss = __shfl_sync(kFull, s, src);
+            const int2* tab = tabs + (int64_t)tt * (n + kTabPad);
+            // tour-order prefix P(i) = sum_{k<=i} q, i = 0..n: all loads in flight, then a warp scan
+            uint32_t carry = 0u;
+            if (lane == 0) pre[0] = 0u;
+            for (int b = 0; b < n; b += 32) {
+                const int i = b + lane;
+                uint32_t v = 0u;
+                if (i < n) {
+                    const int2 e = tab[i];
+                    v = demand[(int64_t)e.x * ld + ss];
+                    cgl[i] = e.y;
                 }
-                m += 32;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t u = __shfl_up_sync(kFull, v, o);
+                    if (lane >= o) v += u;
+                }
+                if (i < n) pre[i + 1] = carry + v;
+                carry += __shfl_sync(kFull, v, 31);
             }
-            int best = INT_MAX;
-            for (int p = m + lane; p <= L; p += 32) best = min(best, g[p]);
-            best = __reduce_min_sync(kFull, best);
-            if (lane == 0) g[L + 1] = best + cg;
+            if (lane == 0) g[0] = g0s[tt];
+            __syncwarp();
+            int m = 0;  // mask(L+1), monotone in L
+            for (int L = 0; L < n; ++L) {
+                const uint32_t Pn = pre[L + 1];
+                for (;;) {  // first p >= m with P(L+1) - P(p) <= Q (p = L always qualifies: q <= Q)
+                    const int p = m + lane;
+                    const unsigned bb = __ballot_sync(kFull, p <= L && Pn - pre[p] <= Q);
+                    if (bb) {
+                        m += __ffs(bb) - 1;
+                        break;
+                    }
+                    m += 32;
+                }
+                int best = INT_MAX;
+                for (int p = m + lane; p <= L; p += 32) best = min(best, g[p]);
+                best = __reduce_min_sync(kFull, best);
+                if (lane == 0) g[L + 1] = best + cgl[L];
+                __syncwarp();
+            }
+            if (lane == 0) emit(tt, ss, g[n]);
             __syncwarp();
         }
-        const int f = g[n];
-        if (lane == 0) {
-            if (cost) cost[(int64_t)t * S + s] = f;
-            if (partial) {
-                const unsigned long long sq = (unsigned long long)f * (unsigned long long)f;
-                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].n_feas), 1ull);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sum), (unsigned long long)f);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_lo), sq & 0xffffffffull);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_hi), sq >> 32);
-            }
-        }
-        __syncwarp();
     }
 }
 
@@ -1457,25 +1497,20 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     if (rc) return rc;
     {
         // finish: per-tour SAA partials + the overflow list (warps per CTA limited by 8 (n+1) bytes of smem each)
-        // overflow scenarios: one thread each (smem 12 (n+1) B per thread) while a CTA still holds
-        // a full warp of them, else one warp each (the warp-cooperative transition-parallel DP)
-        const size_t per_thread = 3 * sizeof(int) * (size_t)(n + 1);
-        const int tp_threads = (int)(((200 * 1024) / per_thread) / 32 * 32);
-        const bool thread_path = tp_threads >= 32;
+        // finish: the SAA partials + the overflow list (one thread per scenario; 4 warps per CTA,
+        // each with 12 (n+1) B of shared scratch for the rare windows wider than kOvfW)
         const size_t per_warp = 3 * sizeof(int) * (size_t)(n + 1);
-        int warps = thread_path ? (tp_threads > 256 ? 8 : tp_threads / 32) : (int)((160 * 1024) / per_warp);
-        warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
-        const size_t fin_smem = thread_path ? per_thread * 32 * warps : per_warp * warps;
+        const int warps = per_warp * 4 <= 192 * 1024 ? 4 : 1;
         static bool attr_set = false;
         if (!attr_set) {
             cudaError_t e = cudaFuncSetAttribute(split_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_finish)");
             attr_set = true;
         }
-        rc = cuda_check(launch_pdl(split_finish_kernel, dim3(2 * num_sms()), dim3(warps * 32), fin_smem, st,
+        rc = cuda_check(launch_pdl(split_finish_kernel, dim3(4 * num_sms()), dim3(warps * 32), per_warp * warps, st,
                                    partial ? slots : nullptr, (int)kSlots, T, (const int2*)tabs, (const int32_t*)g0, n,
                                    demand, ld, S, Qe, cost, partial, (const unsigned long long*)ovf,
-                                   (const unsigned*)ovf_count, thread_path ? 1 : 0),
+                                   (const unsigned*)ovf_count),
                         "split_finish_kernel");
         if (rc) return rc;
     }
