@@ -400,6 +400,19 @@ def measure_rows(spdp, torch, dev, pk):
             "ms": ms, "evals_per_s": cfg["T"] * cfg["S"] / (ms / 1e3), "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
             "candidates_est": cand, "alu_frac_est": cand / (ms / 1e3) / alu_peak}
         del d
+    # f1: route recovery (spdp_split_routes) for 4096 scenarios of C2 (one thread per scenario)
+    cfg2 = synth.config_instance("C2")
+    inst2 = cfg2["inst"]
+    d = spdp.gen_demands(cfg2["model"], 0, cfg2["S"], device=dev)
+    tour2, dist2 = torch.from_numpy(inst2["tour"]).to(dev), torch.from_numpy(inst2["dist"]).to(dev)
+    K = 4096
+    scen = torch.arange(0, cfg2["S"], cfg2["S"] // K, dtype=torch.int64, device=dev)[:K].contiguous()
+    fn = lambda: spdp.split_routes(tour2, dist2, d, inst2["Q"], scen, S=cfg2["S"])
+    ms = _time_events(fn, torch, dev, iters=5)
+    _, _, _, ml = spdp.split_routes(tour2, dist2, d, inst2["Q"], scen, S=cfg2["S"])
+    rows["f1_routes_C2"] = {"ms": ms, "scenarios": K, "scenarios_per_s": K / (ms / 1e3),
+                            "max_route_load_le_Q": bool((ml <= inst2["Q"]).all().item())}
+    del d
     # a9/a10: IRP (C5)
     c5 = synth.irp_config()
     irp = c5["irp"]
