@@ -55,8 +55,9 @@ def _L():
         lib.oracle_split_batch.argtypes = [i32, P, P, i32, P, i64, i64, i32, P, P, P, ctypes.c_int]
         lib.oracle_split_batch_tours.argtypes = [i32, i32, P, P, i32, P, i64, i64, P, ctypes.c_int]
         lib.oracle_saa.argtypes = [P, i64, P, P]
+        lib.oracle_split_penalized.argtypes = [i32, P, P, i32, i64, P, i64, i64, P, P, ctypes.c_int]
         lib.oracle_irp.argtypes = [i32, i32, P, P, P, i64, i64, P, ctypes.c_int]
-        for name in ("oracle_gen_demands", "oracle_split_batch", "oracle_split_batch_tours",
+        for name in ("oracle_gen_demands", "oracle_split_batch", "oracle_split_batch_tours", "oracle_split_penalized",
                      "oracle_saa", "oracle_irp", "oracle_num_threads"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -153,6 +154,25 @@ def split(tour, dist, demand, Q, method: str = "scan", want_pred: bool = False,
     if want_windows:
         out.append(wsum)
     return out[0] if len(out) == 1 else tuple(out)
+
+
+def split_penalized(tour, dist, demand, Q, lam: int, want_pred: bool = False, S: int | None = None,
+                    threads: int = 0):
+    """f2 penalized split (DESIGN R22): every p admissible, lam * max(0, load - Q) added.
+    int64 [S] costs (and [S][n+1] predecessors, ties -> largest p)."""
+    tour = np.ascontiguousarray(tour, dtype=np.int32)
+    dist = np.ascontiguousarray(dist, dtype=np.int32)
+    demand = np.ascontiguousarray(demand, dtype=np.uint16)
+    n = tour.shape[0]
+    ld = demand.shape[1]
+    S = ld if S is None else S
+    cost = np.zeros(S, dtype=np.int64)
+    pred = np.zeros((S, n + 1), dtype=np.int32) if want_pred else None
+    rc = _L().oracle_split_penalized(n, _p(tour), _p(dist), int(Q), int(lam), _p(demand), ld, int(S), _p(cost),
+                                     _p(pred) if pred is not None else None, int(threads))
+    if rc:
+        raise ValueError("oracle_split_penalized rc=%d" % rc)
+    return (cost, pred) if want_pred else cost
 
 
 def split_tours(tours, dist, demand, Q, S: int | None = None, threads: int = 0) -> np.ndarray:

@@ -322,6 +322,60 @@ int oracle_split_batch_tours(int32_t n, int32_t T, const int32_t* tours, const i
 }
 
 /* ------------------------------------------------------------------------ */
+/* f2. Penalized split, DESIGN R22 (the paper names a      */
+/* "penalized cost" only; SPEC:206 widens the window to every p    */
+/* and adds lambda * max(0, load - Q), SPEC:252 keeps single-customer routes  */
+/* admissible):                                                              */
+/*   f(0) = 0,                                                               */
+/*   f(i) = min_{0<=p<=i-1} f(p) + c_{0,s_{p+1}} + sum_{k=p+1}^{i-1}          */
+/*          c_{s_k,s_{k+1}} + c_{s_i,0} + lambda * max(0, sum_{k=p+1}^{i} q - Q) */
+/* Literal O(n^2) descending scan (load and chain accumulated right-to-left). */
+/* Ties keep the largest p.  Every scenario is feasible.                     */
+/* ------------------------------------------------------------------------ */
+int oracle_split_penalized(int32_t n, const int32_t* tour, const int32_t* dist, int32_t Q, int64_t lambda,
+                           const uint16_t* demand, int64_t ld, int64_t S, int64_t* cost, int32_t* pred,
+                           int threads)
+{
+    if (n < 1 || S < 0 || Q < 1 || ld < S || lambda < 0) return 2;
+    const int64_t N1 = (int64_t)n + 1;
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel
+#endif
+    {
+        int64_t* q = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+        int64_t* f = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+        for (int64_t s = 0; s < S; ++s) {
+            for (int32_t k = 1; k <= n; ++k) q[k - 1] = demand[(int64_t)(tour[k - 1] - 1) * ld + s];
+            int32_t* pr = pred ? pred + s * N1 : NULL;
+            f[0] = 0;
+            for (int32_t i = 1; i <= n; ++i) {
+                int64_t best = ORACLE_INF, load = 0, chain = 0;
+                int32_t arg = -1;
+                for (int32_t p = i - 1; p >= 0; --p) {
+                    load += q[p];                                   /* q_{sigma_{p+1}} */
+                    if (p + 1 <= i - 1) chain += dist[(int64_t)tour[p] * N1 + tour[p + 1]];
+                    const int64_t over = load - Q > 0 ? load - Q : 0;
+                    int64_t cand = f[p] + dist[0 * N1 + tour[p]] + chain + dist[(int64_t)tour[i - 1] * N1 + 0]
+                                   + lambda * over;
+                    if (cand < best) { best = cand; arg = p; }
+                }
+                f[i] = best;
+                if (pr) pr[i] = arg;
+            }
+            if (pr) pr[0] = -1;
+            cost[s] = f[n];
+        }
+        free(q);
+        free(f);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* a6. SAA estimate (PAPER:48, 264 (P_m)).                      */
 /* Over feasible scenarios (cost != ORACLE_INF):                              */
 /*   m = #feasible, mean = (1/m) sum c,                                      */

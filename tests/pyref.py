@@ -5,6 +5,7 @@ agreement is evidence, not a retyped formula:
 
 * brute_force_split   -- enumerate all 2^(n-1) contiguous partitions of the tour
                          (SPEC:230-238), cost of each route computed from scratch.
+* brute_force_penalized -- the same enumeration with lam * max(0, load - Q) per route.
 * deque_split         -- O(n) sliding-window-minimum split on the separable form
                          f(i) = B[i] + min_{p in [mask(i), i-1]} (f(p) + A[p])
                          with a monotone deque (Vidal-style linear split).
@@ -40,6 +41,25 @@ def route_cost(route, dist):
     for a, b in zip(route, route[1:]):
         c += dist[a][b]
     return c + dist[route[-1]][0]
+
+
+def brute_force_penalized(tour, q_tour, dist, Q, lam):
+    """Penalized split by enumeration: min over all contiguous partitions of
+    sum(route cost + lam * max(0, route load - Q)) (DESIGN R22)."""
+    n = len(tour)
+    best = None
+    for cuts in itertools.product((0, 1), repeat=n - 1):
+        routes, start = [], 0
+        for k, cut in enumerate(cuts):
+            if cut:
+                routes.append(list(range(start, k + 1)))
+                start = k + 1
+        routes.append(list(range(start, n)))
+        cost = sum(route_cost([tour[k] for k in r], dist) + lam * max(0, sum(q_tour[k] for k in r) - Q)
+                   for r in routes)
+        if best is None or cost < best:
+            best = cost
+    return best
 
 
 def brute_force_split(tour, q_tour, dist, Q):
