@@ -400,6 +400,19 @@ def measure_rows(spdp, torch, dev, pk):
             "ms": ms, "evals_per_s": cfg["T"] * cfg["S"] / (ms / 1e3), "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
             "candidates_est": cand, "alu_frac_est": cand / (ms / 1e3) / alu_peak}
         del d
+    # f2: penalized split at C2 (lambda = 10 cost units per unit of overload, Q of C2)
+    cfg2 = synth.config_instance("C2")
+    inst2 = cfg2["inst"]
+    d = spdp.gen_demands(cfg2["model"], 0, cfg2["S"], device=dev)
+    tour2, dist2 = torch.from_numpy(inst2["tour"]).to(dev), torch.from_numpy(inst2["dist"]).to(dev)
+    costp = torch.empty(cfg2["S"], dtype=torch.int32, device=dev)
+    partp = torch.zeros(6, dtype=torch.int64, device=dev)
+    fn = lambda: spdp.split_eval_penalized(tour2, dist2, d, inst2["Q"], 10, S=cfg2["S"], cost=costp, partial=partp,
+                                           window_hint=bench_config.HINT["C2"])
+    ms = _time_events(fn, torch, dev, iters=5)
+    rows["f2_penalized_C2"] = {"ms": ms, "lambda": 10, "evals_per_s": cfg2["S"] / (ms / 1e3),
+                               "kernel": spdp.last_kernel()}
+    del d
     # f1: route recovery (spdp_split_routes) for 4096 scenarios of C2 (one thread per scenario)
     cfg2 = synth.config_instance("C2")
     inst2 = cfg2["inst"]

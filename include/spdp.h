@@ -185,6 +185,22 @@ SPDP_API spdp_status spdp_split_eval_batch(const int32_t* tours, int32_t T, cons
                                   int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
                                   void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream);
 
+/* f2. Penalized split (DESIGN R22): the split of spdp_split_eval
+ * with EVERY p admissible and a linear overload penalty (the paper
+ * reports "penalized cost" only, without defining it):
+ *   f(i) = min_{0 <= p <= i-1} f(p) + t(p,i) + lambda * max(0, sum_{k=p+1}^{i} q - Q)
+ * lambda >= 0 (cost units per unit of overload).  Every scenario is feasible
+ * (partial->n_infeas = 0).  lambda = 0 is the split without capacity; a lambda
+ * above every route-cost difference gives the strict split whenever that is
+ * feasible.  Same workspace (spdp_workspace_bytes(n, S, 1)), layout and window_hint
+ * semantics as spdp_split_eval; int32 results (scenarios whose lambda * load
+ * reaches 2^29 are finished in int64 by a slower per-scenario kernel). */
+SPDP_API spdp_status spdp_split_eval_penalized(const int32_t* tour, const int32_t* dist, int32_t n,
+                                      const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                                      int32_t lambda, int32_t* cost, spdp_saa_partial* partial,
+                                      int32_t window_hint, void* ws, size_t ws_bytes, uint32_t flags,
+                                      spdp_stream_t stream);
+
 /* f1. Route recovery for K selected scenarios: the same DP as
  * spdp_split_eval (Eq. (1)-(3)), recording for every prefix i the
  * optimal last split point p = pred[k][i] (the route sigma_{p+1}..sigma_i is the

@@ -39,6 +39,7 @@ SYMBOLS = (
     "spdp_split_mask", "spdp_split_eval", "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean",
     "spdp_host_workspace_bytes", "spdp_split_eval_host", "spdp_irp_workspace_bytes", "spdp_irp_dp",
     "spdp_set_profile_events", "spdp_last_kernel", "spdp_routes_workspace_bytes", "spdp_split_routes",
+    "spdp_split_eval_penalized",
 )
 
 
@@ -86,6 +87,7 @@ def _sig():
     L.spdp_split_eval.argtypes = [P, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
     L.spdp_split_eval_batch.argtypes = [P, i32, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
     L.spdp_saa_reduce.argtypes = [P, i64, P, P]
+    L.spdp_split_eval_penalized.argtypes = [P, P, i32, P, i64, i64, i32, i32, P, P, i32, P, sz, u32, P]
     L.spdp_routes_workspace_bytes.argtypes = [i32, i32]
     L.spdp_routes_workspace_bytes.restype = sz
     L.spdp_split_routes.argtypes = [P, P, i32, P, i64, i64, i32, P, i32, P, P, P, P, P, sz, P]
@@ -250,6 +252,27 @@ def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool
                                 _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
                                 ctypes.c_void_p(ws.data_ptr()), ws.numel(), (F_VALIDATE if validate else 0) | F_SWEEP[algo],
                                 _stream(dev)), "spdp_split_eval")
+    return cost, partial
+
+
+def split_eval_penalized(tour, dist, demand, Q: int, lam: int, S: int | None = None, want_cost: bool = True,
+                         want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None,
+                         partial=None):
+    """f2: penalized split costs (int32 [S]) and the SAA partial (spdp_split_eval_penalized)."""
+    torch = _torch()
+    n, ld = demand.shape
+    S = ld if S is None else S
+    dev = demand.device
+    if want_cost and cost is None:
+        cost = torch.empty(S, dtype=torch.int32, device=dev)
+    if want_partial and partial is None:
+        partial = torch.zeros(6, dtype=torch.int64, device=dev)
+    ws = workspace(workspace_bytes(n, S, 1), dev)
+    _check(_lib.spdp_split_eval_penalized(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"),
+                                          ld, S, int(Q), int(lam), _dev_ptr(cost, "cost") if want_cost else None,
+                                          _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
+                                          ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_VALIDATE if validate else 0,
+                                          _stream(dev)), "spdp_split_eval_penalized")
     return cost, partial
 
 

@@ -972,6 +972,208 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------- f2: penalized sweep
+// Penalized split (DESIGN R22): every p is a candidate,
+//   g(i) = Cg[i] + min_p  g(p) + lambda * max(0, P'(i) - Y(p)),   Y(p) = P'(p) + Q,
+// i.e. routes may exceed Q at lambda per unit of overload.  Ring entries store G = g(p)
+// and Z = g(p) - lambda Y(p), so a candidate is ONE add-max (VIADDMNMX):
+//   c = max(lambda P'(i) + Z, G)      (= G inside the capacity window, penalised outside).
+// The ring holds the last W split points; an older point is folded, when it leaves the
+// ring, into H = min Z (its candidate is then H + lambda P'(i)) -- exact as long as it has
+// already left the capacity window, which the eviction checks (else the lane is deferred
+// to the finish kernel, like every lane whose lambda P' could leave the int32 range).
+// No warp votes: every ring entry is a candidate at every layer.
+template <int W>
+__global__ void __launch_bounds__(kSweepThreads, 3)
+    split_penalized_kernel(const uint16_t* const* __restrict__ rowp, const int32_t* __restrict__ cgs,
+                           const int32_t* __restrict__ g0s, int n, int T, int64_t S, uint32_t Q, int32_t lam,
+                           int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
+                           unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
+    using Cfg = F2Cfg<W, 0>;
+    constexpr int NS = Cfg::NS;
+    constexpr int32_t kBig = 1 << 30;
+    pdl_wait();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
+    int2* tq = reinterpret_cast<int2*>(wbase);
+    unsigned char* stage_base = wbase + kQueue * 8;
+    const uint32_t ntile_s = (uint32_t)((S + kTile - 1) / kTile);
+    const uint32_t ntiles = ntile_s * (uint32_t)T;
+    const int nchunks = (n + W - 1) / W;
+    const int rem = n % W;
+    const int cgs_stride = cg_stride(n);
+    const int slot = (blockIdx.x * kSweepWarps + wid) % kSlots;
+    unsigned* ovf_count = hdr + HDR_OVF_COUNT;
+
+    F2Stream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0u, 4};
+    auto issue = [&]() {
+        // (final-chunk padding: demand min(Q + 1, 65535) and Cg 0, so a padded layer pushes every
+        // older point out of the capacity window -- no false deferral -- after f(n) was pushed)
+        cs.issue(stage_base, tq, rowp, cgs, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane, hdr + HDR_TILE,
+                 (Q < 65535u ? Q + 1u : 65535u) * 0x10001u);
+    };
+    for (int k = 0; k < NS; ++k) issue();
+
+    struct LanePart {
+        int nf, ni;
+        long long sum, sqlo, sqhi;
+    };
+    __shared__ LanePart accs[kSweepThreads];
+    LanePart* accp = &accs[tid];
+    *accp = LanePart{0, 0, 0, 0, 0};
+    int acc_t = -1;
+    auto flush = [&]() {
+        const LanePart a = *accp;
+        const Part p = warp_sum(Part{a.nf, a.ni, a.sum, a.sqlo, a.sqhi});
+        *accp = LanePart{0, 0, 0, 0, 0};
+        if (lane == 0 && acc_t >= 0) {
+            spdp_saa_partial* d = &slots[(int64_t)acc_t * kSlots + slot];
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)p.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)p.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)p.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)p.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)p.sq_hi);
+        }
+    };
+
+    int cstage = 0;
+    cp_async_wait<NS - 1>();
+    __syncwarp();
+    for (unsigned u = 0;; ++u) {
+        const int2 tile = tq[u & (kQueue - 1)];
+        if (__all_sync(kFull, tile.x < 0)) break;
+        const int t = tile.x;
+        const int64_t s0 = (int64_t)tile.y * kTile;
+        const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
+        const bool live = lane < cols;
+        const int col = live ? lane : cols - 1;
+        if (__any_sync(kFull, slots && t != acc_t)) {
+            flush();
+            acc_t = t;
+        }
+        int G[W], Z[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            G[k] = kBig;  // empty slot: never the minimum (real values < 2^29), Z = G - lambda * 0
+            Z[k] = kBig;
+        }
+        int32_t H = kBig;  // min Z over the points that left the ring
+        int gprev = g0s[t];
+        uint32_t P = 1u;   // P'(i) = 1 + prefix
+        bool ovf = false;
+        for (int c = 0;;) {
+            const unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
+            const uint16_t* buf = reinterpret_cast<const uint16_t*>(sb) + col;
+            const int32_t* cgc = reinterpret_cast<const int32_t*>(sb + Cfg::kRowsBytes);
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const uint32_t q = buf[j * kTile];
+                const uint32_t Pn = P + q;
+                const int32_t lp = lam * (int32_t)Pn;
+                // evict slot j (the point W layers back) into H; if it is still inside the capacity
+                // window (lambda P' + Z < G, lambda > 0) its penalty-free cost would be lost: defer
+                ovf |= lp + Z[j] < G[j];
+                H = min(H, Z[j]);
+                G[j] = gprev;
+                Z[j] = gprev - lam * (int32_t)(P + Q);
+                int best = H + lp;
+#pragma unroll
+                for (int k = 0; k < W; ++k) best = min(best, __viaddmax_s32(lp, Z[k], G[k]));
+                gprev = best + cgc[j];
+                P = Pn;
+            }
+            __syncwarp();
+            issue();
+            cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
+            cp_async_wait<NS - 1>();
+            __syncwarp();
+            if (__all_sync(kFull, ++c >= nchunks)) break;
+        }
+        if (rem != 0) {  // f(n): the slot of position n (pushed by the first padded layer)
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                if (k == rem) gprev = G[k];
+        }
+        // lambda P' grew monotonically: its final value bounds every intermediate one
+        ovf |= (int64_t)lam * (int64_t)(P + Q) >= (int64_t)(1 << 29);
+        const bool deferred = live && ovf;
+        const int64_t s = s0 + col;
+        if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
+        if (cost && live && !deferred) cost[(int64_t)t * S + s] = gprev;
+        if (live && !deferred) {
+            LanePart a = *accp;
+            const unsigned long long sq = (unsigned long long)gprev * (unsigned long long)gprev;
+            a.nf += 1;
+            a.sum += gprev;
+            a.sqlo += (long long)(sq & 0xffffffffull);
+            a.sqhi += (long long)(sq >> 32);
+            *accp = a;
+        }
+    }
+    if (slots) flush();
+    cp_async_wait<0>();
+}
+
+// Deferred penalized scenarios: one warp each, every p in [0, L] a candidate (lanes over p,
+// REDUX-free int64 shuffle min), int64 values; per-warp scratch of 3 (n+1) words.
+__global__ void __launch_bounds__(128) split_penalized_finish_kernel(
+    const int2* __restrict__ tabs, const int32_t* __restrict__ g0s, int n, const uint16_t* __restrict__ demand,
+    int64_t ld, int64_t S, uint32_t Q, int64_t lam, int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ partial,
+    const unsigned long long* __restrict__ ovf_list, const unsigned* __restrict__ ovf_count) {
+    extern __shared__ unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    pdl_wait();
+    long long* g = reinterpret_cast<long long*>(smem_raw) + (size_t)wid * 2 * (n + 1);
+    long long* pre = g + (n + 1);
+    const unsigned count = *ovf_count;
+    for (unsigned idx = blockIdx.x * nw + wid; idx < count; idx += gridDim.x * nw) {
+        const unsigned long long key = ovf_list[idx];
+        const int t = (int)(key >> 40);
+        const int64_t s = (int64_t)(key & ((1ull << 40) - 1));
+        const int2* tab = tabs + (int64_t)t * (n + kTabPad);
+        long long carry = 0;
+        if (lane == 0) pre[0] = 0;
+        for (int b = 0; b < n; b += 32) {
+            const int i = b + lane;
+            long long v = (i < n) ? (long long)demand[(int64_t)tab[i].x * ld + s] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long w = __shfl_up_sync(kFull, v, o);
+                if (lane >= o) v += w;
+            }
+            if (i < n) pre[i + 1] = carry + v;
+            carry += __shfl_sync(kFull, v, 31);
+        }
+        if (lane == 0) g[0] = g0s[t];
+        __syncwarp();
+        for (int L = 0; L < n; ++L) {
+            const long long Pn = pre[L + 1];
+            long long best = LLONG_MAX;
+            for (int p = lane; p <= L; p += 32) {
+                const long long over = Pn - pre[p] - (long long)Q;
+                best = min(best, g[p] + (over > 0 ? lam * over : 0));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(kFull, best, o));
+            if (lane == 0) g[L + 1] = best + tab[L].y;
+            __syncwarp();
+        }
+        const long long f = g[n];
+        if (lane == 0) {
+            if (cost) cost[(int64_t)t * S + s] = f < INT_MAX ? (int32_t)f : INT_MAX - 1;
+            if (partial) {
+                const unsigned long long sq = (unsigned long long)f * (unsigned long long)f;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].n_feas), 1ull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sum), (unsigned long long)f);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_lo), sq & 0xffffffffull);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&partial[t].sumsq_hi), sq >> 32);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ---------------------------------------------------------------- finish kernel
 // (1) SAA partial of each tour: sum of its CTAs' slots, added atomically (the
 //     partials are zeroed by tour_prep_kernel);
@@ -1076,7 +1278,7 @@ __global__ void __launch_bounds__(128) split_finish_kernel(
             __syncthreads();
         }
     }
-    const unsigned count = *ovf_count;
+    const unsigned count = ovf_count ? *ovf_count : 0u;
     auto emit = [&](int t, int64_t s, int f) {
         if (cost) cost[(int64_t)t * S + s] = f;
         if (partial) {
@@ -1416,10 +1618,36 @@ static int pick_w(int hint) {
     return 64;
 }
 
+template <int W>
+static spdp_status launch_penalized_t(cudaStream_t st, const SweepArgs& a, int32_t lam) {
+    using Cfg = F2Cfg<W, 0>;
+    auto kern = split_penalized_kernel<W>;
+    static int blocks_per_sm = 0;
+    if (blocks_per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kSweepThreads, Cfg::kSmem);
+        if (e != cudaSuccess) return cuda_check(e, "split_penalized setup");
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const int64_t ntiles = ((a.S + kTile - 1) / kTile) * a.T;
+    int64_t grid = (int64_t)blocks_per_sm * num_sms();
+    const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
+    if (grid > need) grid = need;
+    prof_begin(st);
+    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kSweepThreads), Cfg::kSmem, st, a.rowp, a.cgs,
+                                           a.g0, a.n, a.T, a.S, a.Q, lam, a.cost, a.slots, a.ovf, a.hdr),
+                                "split_penalized_kernel");
+    set_last_kernel("split_penalized_kernel<%d>", W);
+    prof_end(st);
+    return rc;
+}
+
 static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,
                                 const uint16_t* demand, int64_t ld, int64_t S, int32_t Q, int32_t* cost,
                                 spdp_saa_partial* partial, int32_t window_hint, void* ws, size_t ws_bytes,
-                                uint32_t flags, cudaStream_t st, const char* fn) {
+                                uint32_t flags, cudaStream_t st, const char* fn, int32_t lam = -1) {
     if (n < 1) return fail(SPDP_E_USAGE, "%s: n=%d < 1", fn, n);
     if (n > SPDP_MAX_N) return fail(SPDP_E_RESOURCE, "%s: n=%d > SPDP_MAX_N=%d", fn, n, SPDP_MAX_N);
     if (T < 1) return fail(SPDP_E_USAGE, "%s: T=%d < 1", fn, T);
@@ -1492,6 +1720,34 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     const bool use_f32 = W <= 32 && f32_loads_exact && S < (1LL << 31) && (mode == 2 || mode == 0);
     // windows wider than the largest cheap register ring: the O(1)-amortised deque sweep
     // (measured 4.8x faster than the W=64 ring at n=1000, slower at small windows)
+    if (lam >= 0) {  // f2 penalized split (DESIGN R22)
+        if (S >= (1LL << 31)) return fail(SPDP_E_RESOURCE, "%s: S >= 2^31", fn);
+        rc = W <= 16 ? launch_penalized_t<16>(st, args, lam) : launch_penalized_t<24>(st, args, lam);
+        if (rc) return rc;
+        const size_t per_warp = 2 * sizeof(long long) * (size_t)(n + 1);
+        const int warps = per_warp * 4 <= 192 * 1024 ? 4 : 1;
+        static bool attr_pen = false;
+        if (!attr_pen) {
+            cudaError_t e = cudaFuncSetAttribute(split_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(split_penalized_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(penalized finish)");
+            attr_pen = true;
+        }
+        // SAA slots -> partial (no strict overflow list), then the deferred penalized scenarios
+        rc = cuda_check(launch_pdl(split_finish_kernel, dim3(num_sms()), dim3(128), (size_t)0, st,
+                                   partial ? slots : nullptr, (int)kSlots, T, (const int2*)tabs, (const int32_t*)g0, n,
+                                   demand, ld, S, Qe, cost, partial, (const unsigned long long*)ovf,
+                                   (const unsigned*)nullptr),
+                        "split_finish_kernel");
+        if (rc) return rc;
+        rc = cuda_check(launch_pdl(split_penalized_finish_kernel, dim3(2 * num_sms()), dim3(warps * 32), per_warp * warps,
+                                   st, (const int2*)tabs, (const int32_t*)g0, n, demand, ld, S, (uint32_t)Q,
+                                   (int64_t)lam, cost, partial, (const unsigned long long*)ovf,
+                                   (const unsigned*)(hdr + HDR_OVF_COUNT)),
+                        "split_penalized_finish_kernel");
+        return rc;
+    }
     if (mode == 3 || (mode == 0 && W > 32)) rc = launch_deque(st, args);
     else rc = launch_sweep(W, use_f32, st, args);
     if (rc) return rc;
@@ -1532,6 +1788,16 @@ extern "C" spdp_status spdp_split_eval(const int32_t* tour, const int32_t* dist,
                                        spdp_stream_t stream) {
     return split_common(tour, 1, dist, n, demand, ld, S, Q, cost, partial, window_hint, ws, ws_bytes, flags,
                         (cudaStream_t)stream, "spdp_split_eval");
+}
+
+extern "C" spdp_status spdp_split_eval_penalized(const int32_t* tour, const int32_t* dist, int32_t n,
+                                                 const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                                                 int32_t lambda, int32_t* cost, spdp_saa_partial* partial,
+                                                 int32_t window_hint, void* ws, size_t ws_bytes, uint32_t flags,
+                                                 spdp_stream_t stream) {
+    if (lambda < 0) return fail(SPDP_E_USAGE, "spdp_split_eval_penalized: lambda=%d < 0", lambda);
+    return split_common(tour, 1, dist, n, demand, ld, S, Q, cost, partial, window_hint, ws, ws_bytes, flags,
+                        (cudaStream_t)stream, "spdp_split_eval_penalized", lambda);
 }
 
 extern "C" spdp_status spdp_split_eval_batch(const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,

@@ -283,3 +283,45 @@ def test_irp_lazy_shift_prefix_band(spdp):
         cost, part = spdp.irp_dp(visit, cust, to_dev(dem), H, M, S=S)
         assert np.array_equal(cost.cpu().numpy(), want), "trial %d" % trial
         assert part.cpu().numpy()[2] == int(want.sum())
+
+
+# ------------------------------------------------------------------ f2 penalized split
+@pytest.mark.parametrize("name,S,lam", [("C1", 100, 5), ("C2", 20_011, 10), ("C2", 3_001, 0), ("C3", 2_003, 50),
+                                        ("C2", 2_003, 10 ** 6)])
+def test_split_penalized_parity(spdp, name, S, lam):
+    cfg = synth.config_instance(name)
+    inst = cfg["inst"]
+    tour = cfg["tours"][0]
+    Q = inst["Q"] - inst["Q"] // 4  # tighter than the demand model's clamp: overloaded routes are common
+    dem = oracle.gen_demands(cfg["model"], 0, S, ld=spdp.padded_ld(S))
+    want = oracle.split_penalized(tour, inst["dist"], dem, Q, lam, S=S)
+    for h in (0, 16, 24):
+        cost, part = spdp.split_eval_penalized(to_dev(tour), to_dev(inst["dist"]), to_dev(dem), Q, lam, S=S,
+                                               window_hint=h)
+        got = cost.cpu().numpy().astype(np.int64)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, "hint %d: %d mismatches, first s=%d got %d want %d" % (
+            h, bad.size, bad[0], got[bad[0]], want[bad[0]])
+        p = part.cpu().numpy()
+        w = oracle.saa(want)
+        assert p[0] == S and p[1] == 0 and p[2] == w["sum"] and (int(p[4]) << 32) + int(p[3]) == w["sumsq"]
+
+
+def test_split_penalized_edge_cases(spdp):
+    """Demands above Q (overloaded single customers), zero demands (window = whole tour:
+    deferred lanes), lambda large enough to push lanes to the int64 path."""
+    rng = np.random.default_rng(3)
+    for n in (1, 5, 40, 150):
+        inst = synth.make_instance(n, seed=40 + n, r=3.0)
+        Q = inst["Q"]
+        rows = rng.integers(0, Q + 1, size=(300, n))
+        rows[0] = 0
+        rows[1] = Q + 5
+        rows[2:40] = rng.integers(0, 3, size=(38, n))
+        rows[40:60] = rng.integers(Q // 2, 2 * Q, size=(20, n))
+        dem = synth.explicit_demands(rows.tolist())
+        for lam in (0, 7, 3000):
+            want = oracle.split_penalized(inst["tour"], inst["dist"], dem, Q, lam, S=300)
+            cost, _ = spdp.split_eval_penalized(to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem), Q, lam, S=300,
+                                                window_hint=16)
+            assert np.array_equal(cost.cpu().numpy().astype(np.int64), want), (n, lam)
