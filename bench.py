@@ -222,7 +222,8 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        spdp.split_eval(tour, dist, demand, Q, S=S_loc, window_hint=hint, cost=cost, partial=partial)
+        spdp.split_eval(tour, dist, demand, Q, S=S_loc, window_hint=hint, cost=cost, partial=partial,
+                        mean_window=bench_config.MEAN[args.config])
         if world > 1:
             pdist.allreduce_partials(partial)
 
@@ -388,7 +389,7 @@ def measure_rows(spdp, torch, dev, pk):
         part = torch.zeros((cfg["T"], 6), dtype=torch.int64, device=dev)
         h = bench_config.HINT[name]
         fn = lambda: spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, partial=part,
-                                           window_hint=h)
+                                           window_hint=h, mean_window=bench_config.MEAN[name])
         ms = _time_events(fn, torch, dev, iters=3)
         m = spdp.split_mask(tours[0].contiguous(), d, inst["Q"], S=cfg["S"])
         idx = torch.arange(1, cfg["n"] + 1, device=dev, dtype=torch.int64).unsqueeze(1)

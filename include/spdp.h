@@ -75,6 +75,11 @@ typedef enum {
 #define SPDP_F_SWEEP_INT   2u       /* register ring, exact int32, predicated min per candidate */
 #define SPDP_F_SWEEP_F32   4u       /* register ring, exact integer-valued fp32, FMA-pipe masking */
 #define SPDP_F_SWEEP_DEQUE 8u       /* monotone-deque sliding-window minimum, O(1) amortised */
+/* bits 8..15 of flags: the expected MEAN window width i - mask(i) (0 = unknown; with
+ * window_hint = 0 it is sampled).  A tuning hint like window_hint: it picks how many
+ * candidates the sweep evaluates before its first warp vote, never the result. */
+#define SPDP_F_MEAN_WINDOW_SHIFT 8
+#define SPDP_F_MEAN_WINDOW(w) ((uint32_t)((w) < 255 ? (w) : 255) << SPDP_F_MEAN_WINDOW_SHIFT)
 
 /* Summable SAA partial.  Every field is an int64 that adds
  * elementwise, so partials of disjoint scenario sets combine by a plain SUM

@@ -166,6 +166,11 @@ def _stream(device):
 _WS = {}
 
 
+def _mean_flag(mean_window: int) -> int:
+    """flags bits 8..15: expected mean window (spdp.h SPDP_F_MEAN_WINDOW)."""
+    return (min(max(int(mean_window), 0), 255)) << 8
+
+
 def workspace(nbytes: int, device, tag: str = "split"):
     """Cached per-device scratch buffer (torch uint8), grown on demand."""
     torch = _torch()
@@ -234,7 +239,7 @@ def split_mask(tour, demand, Q: int, S: int | None = None):
 # ------------------------------------------------------------------ a2 + a5 + a6
 def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool = True,
                want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None, partial=None,
-               algo: str | None = None):
+               algo: str | None = None, mean_window: int = 0):
     """Per-scenario split costs (int32 [S], INFEASIBLE sentinel) and the SAA partial (int64 [6]).
     algo: None/"auto", "int", "f32" or "deque" (identical results; see spdp.h)."""
     torch = _torch()
@@ -250,7 +255,8 @@ def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool
     _check(_lib.spdp_split_eval(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld, S,
                                 int(Q), _dev_ptr(cost, "cost") if want_cost else None,
                                 _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
-                                ctypes.c_void_p(ws.data_ptr()), ws.numel(), (F_VALIDATE if validate else 0) | F_SWEEP[algo],
+                                ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                (F_VALIDATE if validate else 0) | F_SWEEP[algo] | _mean_flag(mean_window),
                                 _stream(dev)), "spdp_split_eval")
     return cost, partial
 
@@ -300,7 +306,7 @@ def split_routes(tour, dist, demand, Q: int, scen, S: int | None = None):
 
 def split_eval_batch(tours, dist, demand, Q: int, S: int | None = None, want_cost: bool = True,
                      want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None,
-                     partial=None, algo: str | None = None):
+                     partial=None, algo: str | None = None, mean_window: int = 0):
     """T tours [T][n] over one demand set: costs int32 [T][S] and partials int64 [T][6]."""
     torch = _torch()
     n, ld = demand.shape
@@ -317,7 +323,7 @@ def split_eval_batch(tours, dist, demand, Q: int, S: int | None = None, want_cos
                                       _dev_ptr(cost, "cost") if want_cost else None,
                                       _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(),
-                                      (F_VALIDATE if validate else 0) | F_SWEEP[algo], _stream(dev)),
+                                      (F_VALIDATE if validate else 0) | F_SWEEP[algo] | _mean_flag(mean_window), _stream(dev)),
            "spdp_split_eval_batch")
     return cost, partial
 

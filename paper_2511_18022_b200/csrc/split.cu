@@ -61,7 +61,7 @@ inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
 }
 
 // header words
-enum { HDR_OVF_COUNT = 0, HDR_STATUS = 1, HDR_SAMPLE_W = 2, HDR_TILE = 3 };
+enum { HDR_OVF_COUNT = 0, HDR_STATUS = 1, HDR_SAMPLE_W = 2, HDR_TILE = 3, HDR_SAMPLE_SUM = 4 /* u64 */, HDR_SAMPLE_CNT = 6 };
 enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
 
 // ---------------------------------------------------------------- a2: tour prep
@@ -1368,6 +1368,7 @@ __global__ void sample_window_kernel(const int2* __restrict__ tab, int n, const 
     // two-pointer on the tour-order prefix, re-reading the left demand
     uint32_t P = 0, Pm = 0;
     int m = 0, wmax = 1;
+    unsigned long long wsum = 0;
     for (int i = 1; i <= n; ++i) {
         const uint32_t q = demand[(int64_t)tab[i - 1].x * ld + s];
         if (q > Q) return;  // infeasible scenario: not representative
@@ -1377,8 +1378,11 @@ __global__ void sample_window_kernel(const int2* __restrict__ tab, int n, const 
             ++m;
         }
         wmax = max(wmax, i - m);
+        wsum += (unsigned long long)(i - m);
     }
     atomicMax(&hdr[HDR_SAMPLE_W], (unsigned)wmax);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&hdr[HDR_SAMPLE_SUM]), wsum);
+    atomicAdd(&hdr[HDR_SAMPLE_CNT], 1u);
 }
 
 // ---------------------------------------------------------------- a3 / a4 standalone
@@ -1574,11 +1578,15 @@ static int f2_cfg() {
     return m;
 }
 
-static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArgs& a) {
+static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArgs& a, int mean_w) {
     if (f32) {
+        // unconditional candidate pairs U0 ~ 0.8 x the mean window (measured: C2, mean 3.75 -> 3;
+        // C3, mean 7.7 -> 6); an SPDP_F2 setting overrides
+        const bool wide = mean_w >= 6 && f2_cfg() == 0;
         switch (W) {
             case 8: return launch_sweep_f2_t<8, 2, 1>(st, a);
             case 16:
+                if (wide) return launch_sweep_f2_t<16, 5, 1>(st, a);
                 switch (f2_cfg()) {
                     case 21: return launch_sweep_f2_t<16, 2, 1>(st, a);
                     case 32: return launch_sweep_f2_t<16, 3, 2>(st, a);
@@ -1588,16 +1596,20 @@ static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArg
                     default: return launch_sweep_f2_t<16, 3, 1>(st, a);
                 }
             case 20:
+                if (wide) return launch_sweep_f2_t<20, 6, 2>(st, a);
                 switch (f2_cfg()) {
                     case 21: return launch_sweep_f2_t<20, 2, 1>(st, a);
                     case 32: return launch_sweep_f2_t<20, 3, 2>(st, a);
                     case 41: return launch_sweep_f2_t<20, 4, 1>(st, a);
                     case 42: return launch_sweep_f2_t<20, 4, 2>(st, a);
                     case 324: return launch_sweep_f2_t<20, 3, 2, 4>(st, a);
+                    case 51: return launch_sweep_f2_t<20, 5, 1>(st, a);
+                    case 52: return launch_sweep_f2_t<20, 5, 2>(st, a);
+                    case 62: return launch_sweep_f2_t<20, 6, 2>(st, a);
                     default: return launch_sweep_f2_t<20, 3, 1>(st, a);
                 }
-            case 24: return launch_sweep_f2_t<24, 3, 1>(st, a);
-            default: return launch_sweep_f2_t<32, 4, 2>(st, a);
+            case 24: return wide ? launch_sweep_f2_t<24, 6, 2>(st, a) : launch_sweep_f2_t<24, 3, 1>(st, a);
+            default: return wide ? launch_sweep_f2_t<32, 8, 2>(st, a) : launch_sweep_f2_t<32, 4, 2>(st, a);
         }
     }
     switch (W) {
@@ -1686,13 +1698,14 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         if ((rc = last_launch("tour_prep_kernel"))) return rc;
     }
     int W = pick_w(window_hint);
+    int mean_w = (int)((flags >> SPDP_F_MEAN_WINDOW_SHIFT) & 0xffu);  // expected mean window (0: unknown)
     if (validate || window_hint == 0) {
         if (window_hint == 0) {
             const int64_t Ss = S < 4096 ? S : 4096;
             sample_window_kernel<<<(unsigned)ceil_div(Ss, 256), 256, 0, st>>>(tabs, n, demand, ld, Ss, Qe, hdr);
             if ((rc = last_launch("sample_window_kernel"))) return rc;
         }
-        unsigned h[4];
+        unsigned h[8];
         if ((rc = cuda_check(cudaMemcpyAsync(h, hdr, sizeof(h), cudaMemcpyDeviceToHost, st), "memcpy(hdr)"))) return rc;
         if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
         if (validate && h[HDR_STATUS]) {
@@ -1701,7 +1714,12 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
                         (b & ST_NEG_DIST) ? " negative cost" : "",
                         (b & ST_RANGE) ? " 3*n*max(dist) exceeds the int32 range" : "");
         }
-        if (window_hint == 0) W = pick_w((int)(h[HDR_SAMPLE_W] + h[HDR_SAMPLE_W] / 4 + 1));
+        if (window_hint == 0) {
+            W = pick_w((int)(h[HDR_SAMPLE_W] + h[HDR_SAMPLE_W] / 4 + 1));
+            const unsigned long long wsum = (unsigned long long)h[HDR_SAMPLE_SUM] | ((unsigned long long)h[HDR_SAMPLE_SUM + 1] << 32);
+            if (h[HDR_SAMPLE_CNT] > 0 && mean_w == 0)
+                mean_w = (int)((wsum + (unsigned long long)h[HDR_SAMPLE_CNT] * n / 2) / ((unsigned long long)h[HDR_SAMPLE_CNT] * n));
+        }
     }
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
     const SweepArgs args{rowp, tabs, reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
@@ -1749,7 +1767,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         return rc;
     }
     if (mode == 3 || (mode == 0 && W > 32)) rc = launch_deque(st, args);
-    else rc = launch_sweep(W, use_f32, st, args);
+    else rc = launch_sweep(W, use_f32, st, args, mean_w);
     if (rc) return rc;
     {
         // finish: per-tour SAA partials + the overflow list (warps per CTA limited by 8 (n+1) bytes of smem each)

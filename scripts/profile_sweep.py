@@ -35,8 +35,10 @@ else:
     h = a.hint if a.hint is not None else bench_config.HINT[a.config]
     for _ in range(a.iters):
         if cfg["T"] == 1:
-            spdp.split_eval(tours[0].contiguous(), dist, d, inst["Q"], S=cfg["S"], window_hint=h)
+            spdp.split_eval(tours[0].contiguous(), dist, d, inst["Q"], S=cfg["S"], window_hint=h,
+                            mean_window=bench_config.MEAN[a.config])
         else:
-            spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h)
+            spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h,
+                                  mean_window=bench_config.MEAN[a.config])
 torch.cuda.synchronize()
 print("done")

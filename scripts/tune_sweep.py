@@ -8,6 +8,7 @@ sys.path.insert(0, ROOT)
 import numpy as np
 import torch
 
+import bench_config
 import paper_2511_18022_b200 as spdp
 import synth
 
@@ -29,7 +30,8 @@ for name in configs:
             if it >= 3:
                 spdp.set_profile_events(*evs[it - 3])
                 tot[it - 3][0].record()
-            spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], window_hint=h, want_cost=cfg["T"] == 1)
+            spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], window_hint=h, want_cost=cfg["T"] == 1,
+                                  mean_window=int(os.environ.get("SPDP_MEANW", bench_config.MEAN[name])))
             if it >= 3:
                 tot[it - 3][1].record()
         spdp.set_profile_events()

@@ -53,7 +53,8 @@ def test_full_size_sampled(spdp, name):
     d = spdp.gen_demands(cfg["model"], 0, S)
     tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).cuda()
     dist = torch.from_numpy(inst["dist"]).cuda()
-    cost, part = spdp.split_eval_batch(tours, dist, d, inst["Q"], S=S, window_hint=bench_config.HINT[name])
+    cost, part = spdp.split_eval_batch(tours, dist, d, inst["Q"], S=S, window_hint=bench_config.HINT[name],
+                                       mean_window=bench_config.MEAN[name])
     rng = np.random.default_rng(0)
     idx = np.unique(np.concatenate([rng.integers(0, S, size=150), [0, 1, S - 2, S - 1]]))
     dem = _sample_cols(cfg["model"], idx)
