@@ -215,15 +215,21 @@ def main():
     hint = args.window_hint if args.window_hint is not None else bench_config.HINT[args.config]
 
     demand = spdp.gen_demands(cfg["model"], s_begin, S_loc, device=dev)
+    T = cfg["T"]
     tour = torch.from_numpy(inst["tour"]).to(dev)
+    tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
     dist = torch.from_numpy(inst["dist"]).to(dev)
-    cost = torch.empty(S_loc, dtype=torch.int32, device=dev)
-    partial = torch.zeros(6, dtype=torch.int64, device=dev)
+    cost = torch.empty((T, S_loc) if T > 1 else S_loc, dtype=torch.int32, device=dev)
+    partial = torch.zeros((T, 6) if T > 1 else 6, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        spdp.split_eval(tour, dist, demand, Q, S=S_loc, window_hint=hint, cost=cost, partial=partial,
-                        mean_window=bench_config.MEAN[args.config])
+        if T > 1:  # batched tours (a8): T candidate tours over the same scenarios
+            spdp.split_eval_batch(tours, dist, demand, Q, S=S_loc, window_hint=hint, cost=cost, partial=partial,
+                                  mean_window=bench_config.MEAN[args.config])
+        else:
+            spdp.split_eval(tour, dist, demand, Q, S=S_loc, window_hint=hint, cost=cost, partial=partial,
+                            mean_window=bench_config.MEAN[args.config])
         if world > 1:
             pdist.allreduce_partials(partial)
 
@@ -234,7 +240,7 @@ def main():
     # algorithmic work: Eq. (3) candidates sum_i (i - mask(i)) from the standalone mask kernel (untimed)
     m = spdp.split_mask(tour, demand, Q, S=S_loc)
     idx = torch.arange(1, n + 1, device=dev, dtype=torch.int64).unsqueeze(1)
-    cand = int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item())
+    cand = int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item()) * T  # (T > 1: tour 0's count x T, estimate)
     del m
     torch.cuda.synchronize(dev)
 
@@ -284,10 +290,10 @@ def main():
     if world > 1:
         ms_step = pdist.max_over_ranks(ms_step, device=dev)
         sweep_ms = pdist.max_over_ranks(sweep_ms, device=dev)
-    value = S_glob * 1.0 / (ms_step / 1e3)
+    value = S_glob * T * 1.0 / (ms_step / 1e3)
 
     pk = peaks()
-    bytes_alg = n * S_loc * 2 + S_loc * 4  # demand stream (u16, read once) + per-scenario costs (i32)
+    bytes_alg = n * S_loc * 2 + T * S_loc * 4  # demand stream (u16, read once) + per-scenario costs (i32)
     hbm_achieved = bytes_alg / (sweep_ms / 1e3) / 1e9
     alu_peak = N_SM * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6  # candidates/s
     alu_achieved = cand / (sweep_ms / 1e3)
@@ -309,10 +315,14 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": "%s: X-n101-shaped CVRPSD, n=%d, Q=%d, %d correlated-demand scenarios per GPU "
-                                   "(cv=0.3, rho=0.5), 1 giant tour" % (args.config, n, Q, S_loc),
-                       "n": n, "S_per_gpu": S_loc, "S_global": S_glob, "T": 1, "window_hint": hint,
-                       "l2": "inputs larger than L2 (demand %.0f MB/GPU > 126 MB)" % (n * S_loc * 2 / 1e6),
+            "config": {"workload": "%s: X-n%d-shaped CVRPSD, n=%d, Q=%d, %d correlated-demand scenarios per GPU "
+                                   "(cv=0.3, rho=0.5), %d giant tour%s" % (args.config, n + 1, n, Q, S_loc, T,
+                                                                        "s" if T > 1 else ""),
+                       "n": n, "S_per_gpu": S_loc, "S_global": S_glob, "T": T, "window_hint": hint,
+                       "mean_window_hint": bench_config.MEAN[args.config],
+                       "l2": ("inputs larger than L2 (demand %.0f MB/GPU > 126 MB)" if n * S_loc * 2 > 126e6 else
+                              "demand %.0f MB/GPU fits L2 (126 MB): steps after the first read it from L2")
+                             % (n * S_loc * 2 / 1e6),
                        "parallelism": "scenario-sharded dp%d, 1 int64 all-reduce/step" % world},
             "roofline": roof, "clocks": clocks, "gpu_launches": 3 * args.steps}
 
@@ -337,7 +347,8 @@ def main():
         line["e2e"] = {"value": S_glob / te, "unit": UNIT,
                        "h2d_bytes_per_step": int(dem_h.numel() * 2 + tour_h.nbytes + dist_h.nbytes),
                        "d2h_bytes_per_step": int(S_loc * 4 + 48), "ms_per_step": te * 1e3,
-                       "api": "spdp_split_eval_host (pinned host demand, costs + SAA estimate back)",
+                       "api": "spdp_split_eval_host (pinned host demand, costs + SAA estimate back)"
+                              + (", tour 0 of the %d" % T if T > 1 else ""),
                        "saa_mean": est["mean"]}
 
     # ------------------------------------------------------------------ per-row measurements (rank 0, N=1)
@@ -346,7 +357,10 @@ def main():
 
     # ------------------------------------------------------------------ oracle cpu_baseline (rank 0, N=1)
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(cfg, cost, S_loc, spdp, partial)
+        line["cpu_baseline"] = cpu_baseline(cfg, cost[0] if T > 1 else cost, S_loc, spdp,
+                                            partial[0] if T > 1 else partial)
+        if T > 1:
+            line["cpu_baseline"]["sample"] += " (tour 0 of the %d)" % T
 
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -379,6 +393,20 @@ def measure_rows(spdp, torch, dev, pk):
     rows["a1_gen_C2"] = {"ms": ms, "demands_per_s": cfg2["n"] * cfg2["S"] / (ms / 1e3),
                          "write_GBps": cfg2["n"] * cfg2["S"] * 2 / (ms / 1e3) / 1e9}
     del out
+    # a5 S-sweep at C2 (analogue of the paper's runtime-vs-scenarios figure): the first S columns
+    d = spdp.gen_demands(cfg2["model"], 0, cfg2["S"], device=dev)
+    inst2 = cfg2["inst"]
+    tour2, dist2 = torch.from_numpy(inst2["tour"]).to(dev), torch.from_numpy(inst2["dist"]).to(dev)
+    sweep = {}
+    for S_ in (10_000, 100_000, 1_000_000):
+        c_ = torch.empty(S_, dtype=torch.int32, device=dev)
+        p_ = torch.zeros(6, dtype=torch.int64, device=dev)
+        fn = lambda: spdp.split_eval(tour2, dist2, d, inst2["Q"], S=S_, window_hint=bench_config.HINT["C2"],
+                                     mean_window=bench_config.MEAN["C2"], cost=c_, partial=p_)
+        ms = _time_events(fn, torch, dev, iters=20)
+        sweep[str(S_)] = {"ms": ms, "evals_per_s": S_ / (ms / 1e3)}
+    rows["a5_C2_S_sweep"] = sweep
+    del d
     # a8: batched tours (C3) and a5 at n=1000 (C4, 1 GPU)
     for name in ("C3", "C4"):
         cfg = synth.config_instance(name)
