@@ -140,7 +140,7 @@ def run_reference(args):
     cfg = synth.config_instance(args.config)
     inst = cfg["inst"]
     S_full = cfg["S"]
-    threads = oracle.num_threads()
+    threads = max(oracle.num_threads(), os.cpu_count() or 1)  # all host cores (torchrun sets OMP_NUM_THREADS=1)
     # size the per-step sample for ~1 s of oracle work (bounded; whole run stays within minutes)
     S_probe = 20_000
     dem = oracle.gen_demands(cfg["model"], 0, S_probe, threads=threads)
@@ -198,10 +198,18 @@ def main():
     world, rank, local = dist_env()
     if world != args.gpus:
         args.gpus = world if world > 1 else args.gpus
+    # (SPDP_BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo -- a functional check of the N > 1
+    # path on a one-GPU box; its timings mean nothing)
+    share = os.environ.get("SPDP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+        if share:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
 
     cfg = synth.config_instance(args.config)
     inst, n, Q = cfg["inst"], cfg["n"], cfg["Q"]
@@ -492,7 +500,7 @@ def measure_rows(spdp, torch, dev, pk):
 def cpu_baseline(cfg, cost_dev, S, spdp, partial_dev):
     import oracle
     inst = cfg["inst"]
-    threads = oracle.num_threads()
+    threads = max(oracle.num_threads(), os.cpu_count() or 1)  # all host cores (torchrun sets OMP_NUM_THREADS=1)
     dem = oracle.gen_demands(cfg["model"], 0, S, threads=threads)
     t0 = time.perf_counter()
     want = oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], threads=threads)
