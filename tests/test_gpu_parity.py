@@ -325,3 +325,18 @@ def test_split_penalized_edge_cases(spdp):
             cost, _ = spdp.split_eval_penalized(to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem), Q, lam, S=300,
                                                 window_hint=16)
             assert np.array_equal(cost.cpu().numpy().astype(np.int64), want), (n, lam)
+
+
+def test_split_f2_large_loads_ring_reset(spdp):
+    """Large Q and demands: the packed-fp32 sweep's tile-to-tile prefix restart runs into its exact
+    range every few tiles and must clear the ring (p_limit path); costs stay bit-exact."""
+    inst = synth.make_instance(60, seed=77, Q=20_000)
+    rng = np.random.default_rng(8)
+    S = 1_200_003  # ~10 tiles per warp: several restarts and resets per warp
+    dem = np.zeros((60, spdp.padded_ld(S)), dtype=np.uint16)
+    dem[:, :S] = rng.integers(0, 20_001, size=(60, S), dtype=np.uint16)
+    want = oracle_cost_as_i32(oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], S=S))
+    for algo, h in ((None, 20), ("f32", 16), ("int", 20)):
+        cost, _ = spdp.split_eval(to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem), inst["Q"], S=S,
+                                  window_hint=h, algo=algo)
+        assert np.array_equal(cost.cpu().numpy().astype(np.int64), want), algo
