@@ -540,7 +540,7 @@ struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel para
     int stage;      // next stage to fill
     unsigned qw;    // queue write index
     int ct;         // tour of the copy tile (-1: no more tiles)
-    uint32_t s0;    // first scenario of the copy tile
+    int64_t s0;     // first scenario of the copy tile
     int segs;       // 16-byte segments per row in the copy tile (4 unless ragged)
 
     // One chunk: lane r < rows copies demand row r0 + r of the tile (4 x 16 B from its row
@@ -559,8 +559,8 @@ struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel para
                 const uint32_t t = id / ntile_s, b = id - t * ntile_s;
                 e = make_int2((int)t, (int)b);
                 ct = (int)t;
-                s0 = b * (uint32_t)kTile;
-                const int64_t left = S - (int64_t)s0;
+                s0 = (int64_t)b * kTile;
+                const int64_t left = S - s0;
                 segs = left >= kTile ? 4 : (int)((left + 7) >> 3);
             }
             if (lane == 0) tq[qw & (kQueue - 1)] = e;
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
 
     const uint32_t ntiles = ntile_s * (uint32_t)T;
     const int cgs_stride = cg_stride(n);
-    F2Stream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0u, 4};
+    F2Stream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0, 4};
     auto issue = [&]() {
         cs.issue(stage_base, tq, rowp, cgs + cgs_stride, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane, hdr + HDR_TILE,
                  qpad * 0x10001u);
@@ -830,9 +830,9 @@ struct DequeCfg {
 };
 
 __global__ void __launch_bounds__(kSweepThreads, 3)
-    split_deque_kernel(const int2* __restrict__ tabs, const int32_t* __restrict__ cgs,
-                       const int32_t* __restrict__ g0s, int n, int T, const uint16_t* __restrict__ demand, int64_t ld,
-                       int64_t S, uint32_t Q, int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
+    split_deque_kernel(const uint16_t* const* __restrict__ rowp, const int32_t* __restrict__ cgs,
+                       const int32_t* __restrict__ g0s, int n, int T, int64_t S, uint32_t Q,
+                       int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
                        unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
     using Cfg = DequeCfg;
     constexpr int NS = kDqNS, R = kDqRows, D = kDqD;
@@ -840,55 +840,31 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
-    int64_t* tq = reinterpret_cast<int64_t*>(wbase);
+    int2* tq = reinterpret_cast<int2*>(wbase);
     unsigned char* stage_base = wbase + kQueue * 8;
     int2* dq = reinterpret_cast<int2*>(stage_base + NS * Cfg::kStageBytes) + lane;  // [D][32] {g, Y}
-    const int64_t ntile_s = (S + kTile - 1) / kTile;
-    const int64_t ntiles = ntile_s * T;
+    const uint32_t ntile_s = (uint32_t)((S + kTile - 1) / kTile);
+    const uint32_t ntiles = ntile_s * (uint32_t)T;
     const int nchunks = (n + R - 1) / R;
     const int cgs_stride = cg_stride(n);
-    unsigned* tile_ctr = hdr + HDR_TILE;
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
 
-    int64_t p_tile = -1;
-    auto issue = [&](unsigned k) {
-        const int c = (int)(k % nchunks);
-        if (c == 0) {
-            unsigned id = 0;
-            if (lane == 0) id = atomicAdd(tile_ctr, 1u);
-            id = __shfl_sync(kFull, id, 0);
-            p_tile = (int64_t)id < ntiles ? (int64_t)id : -1;
-            if (lane == 0) tq[(k / nchunks) % kQueue] = p_tile;
-        }
-        if (p_tile >= 0) {
-            unsigned char* sb = stage_base + (size_t)(k % NS) * Cfg::kStageBytes;
-            const int t = (int)(p_tile / ntile_s);
-            const int64_t s0 = (p_tile % ntile_s) * kTile;
-            const int r0 = c * R;
-            const int rows = (n - r0) < R ? (n - r0) : R;
-            const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
-            const int segs = ((cols + 7) & ~7) / 8;
-            const int2* __restrict__ tab = tabs + (int64_t)t * (n + kTabPad);
-            for (int e = lane; e < rows * 4; e += 32) {
-                const int r = e >> 2, sg = e & 3;
-                if (sg < segs)
-                    cp_async16(sb + r * (kTile * 2) + sg * 16,
-                               demand + (int64_t)__ldg(&tab[r0 + r].x) * ld + s0 + sg * 8);
-            }
-            if (lane < R / 4) cp_async16(sb + Cfg::kRowsBytes + lane * 16, cgs + (int64_t)t * 2 * cgs_stride + r0 + lane * 4);
-        }
-        cp_async_commit();
+    // copy side: the row-pointer stream of the packed-fp32 sweep (int Cg plane; the padded rows
+    // of the final chunk are never read: the layer loop stops at n)
+    F2Stream<R, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0, 4};
+    auto issue = [&]() {
+        cs.issue(stage_base, tq, rowp, cgs, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane, hdr + HDR_TILE, 0u);
     };
-    for (int k = 0; k < NS; ++k) issue((unsigned)k);
+    for (int k = 0; k < NS; ++k) issue();
 
-    unsigned c_k = 0;
+    int cstage = 0;
+    cp_async_wait<NS - 1>();
+    __syncwarp();
     for (unsigned u = 0;; ++u) {
-        cp_async_wait<NS - 1>();
-        __syncwarp();
-        const int64_t tile = tq[u % kQueue];
-        if (__all_sync(kFull, tile < 0)) break;  // warp-uniform (see split_sweep_f2_kernel)
-        const int t = (int)(tile / ntile_s);
-        const int64_t s0 = (tile % ntile_s) * kTile;
+        const int2 tile = tq[u & (kQueue - 1)];
+        if (__all_sync(kFull, tile.x < 0)) break;  // warp-uniform (see split_sweep_f2_kernel)
+        const int t = tile.x;
+        const int64_t s0 = (int64_t)tile.y * kTile;
         const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
         const bool live = lane < cols;
         const int col = live ? lane : cols - 1;
@@ -901,12 +877,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
         int fg = 0, bg = INT_MIN;  // cached front g and back g
         uint32_t fy = 0u;          // cached front Y
 
-        for (int c = 0; c < nchunks; ++c) {
-            if (c > 0) {
-                cp_async_wait<NS - 1>();
-                __syncwarp();
-            }
-            unsigned char* sb = stage_base + (size_t)(c_k % NS) * Cfg::kStageBytes;
+        for (int c = 0;;) {
+            const unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
             const uint16_t* buf = reinterpret_cast<const uint16_t*>(sb) + col;
             const int32_t* cgc = reinterpret_cast<const int32_t*>(sb + Cfg::kRowsBytes);
             const int rows = (n - c * R) < R ? (n - c * R) : R;
@@ -947,8 +919,11 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
                 P = Pn;
             }
             __syncwarp();
-            issue(c_k + NS);
-            ++c_k;
+            issue();
+            cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
+            cp_async_wait<NS - 1>();
+            __syncwarp();
+            if (__all_sync(kFull, ++c >= nchunks)) break;
         }
         const bool bad = qmax > Q;
         const int64_t s = s0 + col;
@@ -1006,7 +981,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
     const int slot = (blockIdx.x * kSweepWarps + wid) % kSlots;
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
 
-    F2Stream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0u, 4};
+    F2Stream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0, 4};
     auto issue = [&]() {
         // (final-chunk padding: demand min(Q + 1, 65535) and Cg 0, so a padded layer pushes every
         // older point out of the capacity window -- no false deferral -- after f(n) was pushed)
@@ -1529,8 +1504,7 @@ static spdp_status launch_deque(cudaStream_t st, const SweepArgs& a) {
     if (grid > need) grid = need;
     prof_begin(st);
     spdp_status rc = cuda_check(launch_pdl(split_deque_kernel, dim3((unsigned)grid), dim3(kSweepThreads), DequeCfg::kSmem, st,
-                                           a.tabs, a.cgs, a.g0, a.n, a.T, a.demand, a.ld, a.S, a.Q, a.cost, a.slots,
-                                           a.ovf, a.hdr),
+                                           a.rowp, a.cgs, a.g0, a.n, a.T, a.S, a.Q, a.cost, a.slots, a.ovf, a.hdr),
                                 "split_deque_kernel");
     set_last_kernel("split_deque_kernel<%d>", kDqD);
     prof_end(st);
