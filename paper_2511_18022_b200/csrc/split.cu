@@ -251,252 +251,6 @@ struct SweepCfg {
     static_assert((W * 4) % 16 == 0, "W must be a multiple of 4");
 };
 
-template <bool F32>
-struct SweepT {
-    using V = int;
-    using L = uint32_t;
-};
-template <>
-struct SweepT<true> {
-    using V = float;
-    using L = float;
-};
-
-// Copy side of a sweep warp: chunk k of the warp's stream is chunk k % nchunks of
-// its (k / nchunks)-th tile; the tile id comes from the global atomic counter
-// when the first chunk of a tile is issued and is handed to the compute side
-// through the warp's queue tq.  Every issue() commits exactly one cp.async
-// group (possibly empty) so the compute side can wait by count.
-template <int W, int NS, int kRowsBytes, int kStageBytes>
-struct WarpStream {
-    unsigned char* stage_base;
-    int64_t* tq;
-    const int2* tabs;
-    const int32_t* cg_plane;  // plane base (int or fp32 Cg) of tour 0
-    const uint16_t* demand;
-    int64_t ld, S, ntile_s, ntiles;
-    int n, nchunks, cgs_stride, lane;
-    unsigned* tile_ctr;
-    int64_t p_tile;
-
-    __device__ __forceinline__ void issue(unsigned k) {
-        const int c = (int)(k % nchunks);
-        if (c == 0) {
-            unsigned id = 0;
-            if (lane == 0) id = atomicAdd(tile_ctr, 1u);
-            id = __shfl_sync(kFull, id, 0);
-            p_tile = (int64_t)id < ntiles ? (int64_t)id : -1;
-            if (lane == 0) tq[(k / nchunks) % kQueue] = p_tile;
-        }
-        if (p_tile >= 0) {
-            unsigned char* sb = stage_base + (size_t)(k % NS) * kStageBytes;
-            const int t = (int)(p_tile / ntile_s);
-            const int64_t s0 = (p_tile % ntile_s) * kTile;
-            const int r0 = c * W;
-            const int rows = (n - r0) < W ? (n - r0) : W;
-            const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
-            const int segs = ((cols + 7) & ~7) / 8;  // 16-byte segments per row (within ld)
-            const int2* __restrict__ tab = tabs + (int64_t)t * (n + kTabPad);
-            for (int e = lane; e < rows * 4; e += 32) {
-                const int r = e >> 2, sg = e & 3;
-                if (sg < segs)
-                    cp_async16(sb + r * (kTile * 2) + sg * 16, demand + (int64_t)__ldg(&tab[r0 + r].x) * ld + s0 + sg * 8);
-            }
-            if (lane < W / 4) cp_async16(sb + kRowsBytes + lane * 16, cg_plane + (int64_t)t * 2 * cgs_stride + r0 + lane * 4);
-        }
-        cp_async_commit();
-    }
-};
-
-template <int W, bool F32>
-__global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1)))
-    split_sweep_kernel(const int2* __restrict__ tabs, const int32_t* __restrict__ cgs,
-                       const int32_t* __restrict__ g0s, const TourInfo* __restrict__ tinfo, int n, int T,
-                       const uint16_t* __restrict__ demand, int64_t ld, int64_t S, uint32_t Q,
-                       int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
-                       unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
-    using Cfg = SweepCfg<W>;
-    using V = typename SweepT<F32>::V;
-    using LT = typename SweepT<F32>::L;
-    constexpr int NS = Cfg::NS;
-    pdl_wait();
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
-    int64_t* tq = reinterpret_cast<int64_t*>(wbase);  // this warp's tile queue
-    unsigned char* stage_base = wbase + kQueue * 8;
-    const int64_t ntile_s = (S + kTile - 1) / kTile;
-    const int64_t ntiles = ntile_s * T;
-    const int nchunks = (n + W - 1) / W;
-    const int rem = n % W;
-    const int cgs_stride = cg_stride(n);
-    const uint32_t qpad = Q < 65535u ? Q : 65535u;
-    unsigned* ovf_count = hdr + HDR_OVF_COUNT;
-
-    WarpStream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> ws{stage_base, tq, tabs, cgs + (F32 ? cgs_stride : 0), demand,
-                                                            ld, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane,
-                                                            hdr + HDR_TILE, -1};
-    auto issue = [&](unsigned k) { ws.issue(k); };
-    for (int k = 0; k < NS; ++k) issue((unsigned)k);
-
-    unsigned c_k = 0;  // compute-side chunk sequence number
-    for (unsigned u = 0;; ++u) {
-        cp_async_wait<NS - 1>();  // the tile's first chunk (the oldest outstanding group) has landed
-        __syncwarp();
-        const int64_t tile = tq[u % kQueue];
-        if (__all_sync(kFull, tile < 0)) break;  // warp-uniform (see split_sweep_f2_kernel)
-        const int t = (int)(tile / ntile_s);
-        const int64_t s0 = (tile % ntile_s) * kTile;
-        const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
-        const bool live = lane < cols;
-        const int col = live ? lane : cols - 1;  // tail lanes replay a real scenario
-        int2 toff = make_int2(0, 1);
-        if constexpr (F32) toff = make_int2(tinfo[t].off, tinfo[t].ok);
-
-        V G[W];
-        LT Y[W];
-        V gprev;
-        LT P, Qv;
-        if constexpr (F32) {
-            gprev = __int_as_float(tinfo[t].g0f_bits);
-            P = 0.0f;
-            Qv = (float)Q;
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                G[k] = 0.0f;
-                Y[k] = -1.0f;  // never feasible: P' >= 0
-            }
-        } else {
-            gprev = g0s[t];
-            P = 1u;
-            Qv = Q;
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                G[k] = INT_MAX;
-                Y[k] = 0u;  // never feasible: P' >= 1
-            }
-        }
-        uint32_t qmax = 0u;  // bad <=> some q > Q (Eq. (2) set empty, DESIGN R4)
-        V ovfacc = (V)-1;    // ovf <=> some evicted slot still feasible: max(Y - P'(i)) >= 0
-
-        // one layer (computes f(L+1)); j = L mod W is a compile-time constant
-        auto layer = [&](const uint16_t* buf, const int32_t* cgc, const int j) {
-            const int cgi = cgc[j];
-            const uint32_t qi = buf[j * kTile];
-            qmax = max(qmax, qi);
-            LT Pn;
-            if constexpr (F32) {
-                Pn = P + __uint2float_rn(qi);
-                ovfacc = fmaxf(ovfacc, Y[j] - Pn);
-            } else {
-                Pn = P + qi;
-                ovfacc = max(ovfacc, (int)(Y[j] - Pn));
-            }
-            G[j] = gprev;
-            Y[j] = P + Qv;
-            V best = gprev, best1 = gprev;  // p = L; two independent min chains
-#pragma unroll
-            for (int k0 = 1; k0 < W; k0 += kVote) {
-                if (k0 > 1 && !__any_sync(kFull, Y[(j - k0 + W) % W] >= Pn)) break;
-#pragma unroll
-                for (int v = 0; v < kVote; ++v) {
-                    const int k = k0 + v;
-                    if (k < W) {
-                        const int sl = (j - k + W) % W;
-                        if constexpr (F32) {
-                            const float cnd = __saturatef(G[sl] + __saturatef(Pn - Y[sl]));
-                            if (v & 1) best1 = fminf(best1, cnd);
-                            else best = fminf(best, cnd);
-                        } else {
-                            if (Y[sl] >= Pn) {
-                                if (v & 1) best1 = min(best1, G[sl]);
-                                else best = min(best, G[sl]);
-                            }
-                        }
-                    }
-                }
-            }
-            if constexpr (F32) gprev = fminf(best, best1) + __int_as_float(cgi);
-            else gprev = min(best, best1) + cgi;
-            P = Pn;
-        };
-
-        for (int c = 0; c < nchunks; ++c) {
-            if (c > 0) {
-                cp_async_wait<NS - 1>();
-                __syncwarp();
-            }
-            unsigned char* sb = stage_base + (size_t)(c_k % NS) * Cfg::kStageBytes;
-            uint16_t* bufw = reinterpret_cast<uint16_t*>(sb) + col;
-            const int32_t* cgc = reinterpret_cast<const int32_t*>(sb + Cfg::kRowsBytes);
-            // the final chunk is padded to W layers with q_pad = min(Q, 65535) and Cg = 0: a demand
-            // of Q collapses every window to the newest slot, so the padded layers never flag an
-            // overflow and never disturb the ring slot that holds f(n)
-            if (rem != 0 && c == nchunks - 1) {
-                for (int j = rem; j < W; ++j) bufw[j * kTile] = (uint16_t)qpad;
-                __syncwarp();
-            }
-#pragma unroll
-            for (int j = 0; j < W; ++j) layer(bufw, cgc, j);
-            __syncwarp();  // every lane is done with this stage
-            issue(c_k + NS);
-            ++c_k;
-        }
-        // f(n): the slot of position n holds it (pushed by the first padded layer), or gprev if n % W == 0
-        if (rem != 0) {
-#pragma unroll
-            for (int k = 0; k < W; ++k)
-                if (k == rem) gprev = G[k];
-        }
-        const bool bad = qmax > Q;
-        const bool ovf = (ovfacc >= (V)0) || toff.y == 0;
-        int fval;
-        if constexpr (F32) fval = (int)(gprev * 0x1p24f) - toff.x;
-        else fval = gprev;
-        const int64_t s = s0 + col;
-        const bool deferred = live && ovf && !bad;
-        if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
-        if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
-        if (slots) {  // per-tile flush of the SAA partial
-            Part p{0, 0, 0, 0, 0};
-            if (live && !deferred) part_add_cost(p, fval, !bad);
-            p = warp_sum(p);
-            if (lane == 0) {
-                spdp_saa_partial* d = &slots[(int64_t)t * kSlots + ((blockIdx.x * kSweepWarps + wid) % kSlots)];
-                atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)p.n_feas);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)p.n_infeas);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)p.sum);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)p.sq_lo);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)p.sq_hi);
-            }
-        }
-    }
-    cp_async_wait<0>();
-}
-
-// Per-tile epilogue shared by the sweeps: defer overflow lanes to the finish
-// kernel, write the per-scenario costs, flush the tile's SAA partial.
-__device__ __forceinline__ void sweep_tile_epilogue(bool live, bool bad, bool ovf, int fval, int t, int64_t s, int64_t S,
-                                                    int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
-                                                    unsigned long long* __restrict__ ovf_list, unsigned* ovf_count,
-                                                    int slot, int lane) {
-    const bool deferred = live && ovf && !bad;
-    if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
-    if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
-    if (slots) {
-        Part p{0, 0, 0, 0, 0};
-        if (live && !deferred) part_add_cost(p, fval, !bad);
-        p = warp_sum(p);
-        if (lane == 0) {
-            spdp_saa_partial* d = &slots[(int64_t)t * kSlots + slot];
-            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)p.n_feas);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)p.n_infeas);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)p.sum);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)p.sq_lo);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)p.sq_hi);
-        }
-    }
-}
 
 // ---------------------------------------------------------------- a5: packed-fp32 sweep
 // The same Eq. (3) ring sweep, with the candidate work shaped for the FMA pipe
@@ -571,23 +325,30 @@ struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel para
             unsigned char* sb = stage_base + stage * kStageBytes;
             const int r0 = c * W;
             const int rows = (n - r0) < W ? (n - r0) : W;
-            if (lane < rows) {
-                const uint16_t* src = rowp[(int64_t)ct * (n + kTabPad) + r0 + lane] + s0;
-                unsigned char* dst = sb + lane * (kTile * 2);
-                if (segs == 4) {
-                    cp_async16(dst, src);
-                    cp_async16(dst + 16, src + 8);
-                    cp_async16(dst + 32, src + 16);
-                    cp_async16(dst + 48, src + 24);
-                } else {
-                    for (int k = 0; k < segs; ++k) cp_async16(dst + 16 * k, src + 8 * k);
-                }
-            } else if (lane < W) {  // final chunk: rows n.. hold q_pad = min(Q, 65535) (see split_sweep_kernel)
-                uint4* dst = reinterpret_cast<uint4*>(sb + lane * (kTile * 2));
 #pragma unroll
-                for (int k = 0; k < 4; ++k) dst[k] = make_uint4(qpad2, qpad2, qpad2, qpad2);
+            for (int rb = 0; rb < W; rb += 32) {  // row r = rb + lane (W > 32: several rows per lane)
+                const int r = rb + lane;
+                if (r < rows) {
+                    const uint16_t* src = rowp[(int64_t)ct * (n + kTabPad) + r0 + r] + s0;
+                    unsigned char* dst = sb + r * (kTile * 2);
+                    if (segs == 4) {
+                        cp_async16(dst, src);
+                        cp_async16(dst + 16, src + 8);
+                        cp_async16(dst + 32, src + 16);
+                        cp_async16(dst + 48, src + 24);
+                    } else {
+                        for (int k = 0; k < segs; ++k) cp_async16(dst + 16 * k, src + 8 * k);
+                    }
+                } else if (r < W) {  // final chunk: rows n.. hold the caller's padding demand
+                    uint4* dst = reinterpret_cast<uint4*>(sb + r * (kTile * 2));
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) dst[k] = make_uint4(qpad2, qpad2, qpad2, qpad2);
+                }
             }
-            if (lane < W / 4) cp_async16(sb + kRowsBytes + lane * 16, cgf + (int64_t)ct * 2 * cgs_stride + r0 + lane * 4);
+#pragma unroll
+            for (int cb = 0; cb < W / 4; cb += 32)
+                if (cb + lane < W / 4)
+                    cp_async16(sb + kRowsBytes + (cb + lane) * 16, cgf + (int64_t)ct * 2 * cgs_stride + r0 + (cb + lane) * 4);
         }
         cp_async_commit();
         ++c;
@@ -794,6 +555,160 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
                 const unsigned long long sq = (unsigned long long)fval * (unsigned long long)fval;
                 a.nf += 1;
                 a.sum += fval;
+                a.sqlo += (long long)(sq & 0xffffffffull);
+                a.sqhi += (long long)(sq >> 32);
+            }
+            *accp = a;
+        }
+    }
+    if (slots) flush();
+    cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------- a5: exact-int32 ring sweep
+// The Eq. (3) ring sweep in exact int32 (used when the packed-fp32 sweep's exactness
+// checks fail, or with SPDP_F_SWEEP_INT).  One scenario per lane, a register ring of the
+// last W split points {G = g(p), Y = P'(p) + Q}, P'(p) = 1 + prefix; candidate p is in
+// the window iff Y >= P'(i), a predicated min per candidate (ISETP +
+// VIMNMX, ALU pipe); the newest kVote candidates unconditionally, then groups of kVote
+// behind a warp vote.  Same copy side / warp-uniform structure as the packed-fp32 sweep.
+template <int W>
+__global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1)))
+    split_sweep_kernel(const uint16_t* const* __restrict__ rowp, const int32_t* __restrict__ cgs,
+                       const int32_t* __restrict__ g0s, int n, int T, int64_t S, uint32_t Q,
+                       int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
+                       unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
+    using Cfg = SweepCfg<W>;
+    constexpr int NS = Cfg::NS;
+    pdl_wait();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
+    int2* tq = reinterpret_cast<int2*>(wbase);
+    unsigned char* stage_base = wbase + kQueue * 8;
+    const uint32_t ntile_s = (uint32_t)((S + kTile - 1) / kTile);
+    const uint32_t ntiles = ntile_s * (uint32_t)T;
+    const int nchunks = (n + W - 1) / W;
+    const int rem = n % W;
+    const int cgs_stride = cg_stride(n);
+    const uint32_t qpad = Q < 65535u ? Q : 65535u;
+    const int slot = (blockIdx.x * kSweepWarps + wid) % kSlots;
+    unsigned* ovf_count = hdr + HDR_OVF_COUNT;
+
+    // (final chunk padded with q_pad = min(Q, 65535), Cg = 0: a demand of Q collapses every
+    // window to the newest slot, so padded layers never flag an overflow nor disturb f(n))
+    F2Stream<W, NS, Cfg::kRowsBytes, Cfg::kStageBytes> cs{nchunks, 0, 0u, -1, 0, 4};
+    auto issue = [&]() {
+        cs.issue(stage_base, tq, rowp, cgs, S, ntile_s, ntiles, n, nchunks, cgs_stride, lane, hdr + HDR_TILE,
+                 qpad * 0x10001u);
+    };
+    for (int k = 0; k < NS; ++k) issue();
+
+    struct LanePart {
+        int nf, ni;
+        long long sum, sqlo, sqhi;
+    };
+    __shared__ LanePart accs[kSweepThreads];
+    LanePart* accp = &accs[tid];
+    *accp = LanePart{0, 0, 0, 0, 0};
+    int acc_t = -1;
+    auto flush = [&]() {
+        const LanePart a = *accp;
+        const Part p = warp_sum(Part{a.nf, a.ni, a.sum, a.sqlo, a.sqhi});
+        *accp = LanePart{0, 0, 0, 0, 0};
+        if (lane == 0 && acc_t >= 0) {
+            spdp_saa_partial* d = &slots[(int64_t)acc_t * kSlots + slot];
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)p.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)p.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)p.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)p.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)p.sq_hi);
+        }
+    };
+
+    int cstage = 0;
+    cp_async_wait<NS - 1>();
+    __syncwarp();
+    for (unsigned u = 0;; ++u) {
+        const int2 tile = tq[u & (kQueue - 1)];
+        if (__all_sync(kFull, tile.x < 0)) break;  // warp-uniform (see split_sweep_f2_kernel)
+        const int t = tile.x;
+        const int64_t s0 = (int64_t)tile.y * kTile;
+        const int cols = (int)((S - s0) < kTile ? (S - s0) : kTile);
+        const bool live = lane < cols;
+        const int col = live ? lane : cols - 1;  // tail lanes replay a real scenario
+        if (__any_sync(kFull, slots && t != acc_t)) {
+            flush();
+            acc_t = t;
+        }
+        int G[W];
+        uint32_t Y[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            G[k] = INT_MAX;
+            Y[k] = 0u;  // never feasible: P' >= 1
+        }
+        int gprev = g0s[t];
+        uint32_t P = 1u;
+        uint32_t qmax = 0u;  // bad <=> some q > Q (Eq. (2) set empty, DESIGN R4)
+        int ovfacc = -1;     // ovf <=> some evicted slot still feasible: max(Y - P'(i)) >= 0
+        for (int c = 0;;) {
+            const unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
+            const uint16_t* buf = reinterpret_cast<const uint16_t*>(sb) + col;
+            const int32_t* cgc = reinterpret_cast<const int32_t*>(sb + Cfg::kRowsBytes);
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const int cgi = cgc[j];
+                const uint32_t qi = buf[j * kTile];
+                qmax = max(qmax, qi);
+                const uint32_t Pn = P + qi;
+                ovfacc = max(ovfacc, (int)(Y[j] - Pn));
+                G[j] = gprev;
+                Y[j] = P + Q;
+                int best = gprev, best1 = gprev;  // p = L; two independent min chains
+#pragma unroll
+                for (int k0 = 1; k0 < W; k0 += kVote) {
+                    if (k0 > 1 && !__any_sync(kFull, Y[(j - k0 + W) % W] >= Pn)) break;
+#pragma unroll
+                    for (int v = 0; v < kVote; ++v) {
+                        const int k = k0 + v;
+                        if (k < W) {
+                            const int sl = (j - k + W) % W;
+                            if (Y[sl] >= Pn) {
+                                if (v & 1) best1 = min(best1, G[sl]);
+                                else best = min(best, G[sl]);
+                            }
+                        }
+                    }
+                }
+                gprev = min(best, best1) + cgi;
+                P = Pn;
+            }
+            __syncwarp();
+            issue();
+            cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
+            cp_async_wait<NS - 1>();
+            __syncwarp();
+            if (__all_sync(kFull, ++c >= nchunks)) break;
+        }
+        if (rem != 0) {  // f(n) sits in the slot of position n (pushed by the first padded layer)
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                if (k == rem) gprev = G[k];
+        }
+        const bool bad = qmax > Q;
+        const bool deferred = live && ovfacc >= 0 && !bad;
+        const int64_t s = s0 + col;
+        if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
+        if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : gprev;
+        if (live && !deferred) {
+            LanePart a = *accp;
+            if (bad) {
+                a.ni += 1;
+            } else {
+                const unsigned long long sq = (unsigned long long)gprev * (unsigned long long)gprev;
+                a.nf += 1;
+                a.sum += gprev;
                 a.sqlo += (long long)(sq & 0xffffffffull);
                 a.sqhi += (long long)(sq >> 32);
             }
@@ -1448,12 +1363,12 @@ static int num_sms() {
 }
 
 // Launches the sweep: one wave of persistent CTAs (occupancy x SMs).
-template <int W, bool F32>
+template <int W>
 static spdp_status launch_sweep_t(cudaStream_t st, const SweepArgs& a) {
-    auto kern = split_sweep_kernel<W, F32>;
+    auto kern = split_sweep_kernel<W>;
     static int blocks_per_sm = 0;
     if (blocks_per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SweepCfg<W>::kSmem);
         if (e == cudaSuccess)  // all of the unified L1/smem as shared memory
             e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e == cudaSuccess)
@@ -1466,11 +1381,10 @@ static spdp_status launch_sweep_t(cudaStream_t st, const SweepArgs& a) {
     const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
     if (grid > need) grid = need;
     prof_begin(st);
-    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kSweepThreads), SweepCfg<W>::kSmem, st, a.tabs,
-                                           a.cgs, a.g0, a.tinfo, a.n, a.T, a.demand, a.ld, a.S, a.Q, a.cost, a.slots,
-                                           a.ovf, a.hdr),
+    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kSweepThreads), SweepCfg<W>::kSmem, st, a.rowp,
+                                           a.cgs, a.g0, a.n, a.T, a.S, a.Q, a.cost, a.slots, a.ovf, a.hdr),
                                 "split_sweep_kernel");
-    set_last_kernel("split_sweep_kernel<%d,%s>", W, F32 ? "f32" : "int");
+    set_last_kernel("split_sweep_kernel<%d,int>", W);
     prof_end(st);
     return rc;
 }
@@ -1587,12 +1501,12 @@ static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArg
         }
     }
     switch (W) {
-        case 8: return launch_sweep_t<8, false>(st, a);
-        case 16: return launch_sweep_t<16, false>(st, a);
-        case 20: return launch_sweep_t<20, false>(st, a);
-        case 24: return launch_sweep_t<24, false>(st, a);
-        case 32: return launch_sweep_t<32, false>(st, a);
-        default: return launch_sweep_t<64, false>(st, a);
+        case 8: return launch_sweep_t<8>(st, a);
+        case 16: return launch_sweep_t<16>(st, a);
+        case 20: return launch_sweep_t<20>(st, a);
+        case 24: return launch_sweep_t<24>(st, a);
+        case 32: return launch_sweep_t<32>(st, a);
+        default: return launch_sweep_t<64>(st, a);
     }
 }
 
