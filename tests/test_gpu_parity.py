@@ -340,3 +340,19 @@ def test_split_f2_large_loads_ring_reset(spdp):
         cost, _ = spdp.split_eval(to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem), inst["Q"], S=S,
                                   window_hint=h, algo=algo)
         assert np.array_equal(cost.cpu().numpy().astype(np.int64), want), algo
+
+
+@pytest.mark.parametrize("hint", [8, 16, 20, 24, 32])
+def test_split_wide_first_group_variants(spdp, hint):
+    """The mean-window hint (spdp.h SPDP_F_MEAN_WINDOW) selects the sweep variants with a wide
+    unconditional candidate group; results are identical for every hint pair."""
+    cfg = synth.config_instance("C3")
+    inst = cfg["inst"]
+    S = 4_099
+    dem = oracle.gen_demands(cfg["model"], 0, S, ld=spdp.padded_ld(S))
+    tours = cfg["tours"][:5]
+    want = oracle.split_tours(tours, inst["dist"], dem, inst["Q"], S=S)
+    for mean in (0, 3, 8, 30):
+        cost, _ = spdp.split_eval_batch(to_dev(tours), to_dev(inst["dist"]), to_dev(dem), inst["Q"], S=S,
+                                        window_hint=hint, mean_window=mean)
+        assert np.array_equal(cost.cpu().numpy().astype(np.int64), oracle_cost_as_i32(want)), (hint, mean)
