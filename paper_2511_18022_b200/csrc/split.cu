@@ -366,7 +366,7 @@ struct F2Cfg : SweepCfg<W> {
     static constexpr size_t kSmem = (size_t)kSweepWarps * kWarpBytes;
 };
 
-template <int W, int U0, int UG, int MB, int NG>
+template <int W, int U0, int UG, int MB, int NG, bool PAIR = false>
 __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
     split_sweep_f2_kernel(const uint16_t* const* __restrict__ rowp, const int32_t* __restrict__ cgs,
                           const TourInfo* __restrict__ tinfo, int n, int T, int64_t S, uint32_t Q, uint32_t p_limit,
@@ -467,67 +467,104 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
             unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
             const uint16_t* bufw = reinterpret_cast<const uint16_t*>(sb) + col;
             const float* cgc = reinterpret_cast<const float*>(sb + Cfg::kRowsBytes);
-            uint32_t qnext = bufw[0];
-#pragma unroll
-            for (int j = 0; j < W; ++j) {
-                const float cg = cgc[j];
-                const uint32_t qi = qnext;  // loaded one layer ahead
-                if (j + 1 < W) qnext = bufw[(j + 1) * kTile];
-                qmax = max(qmax, qi);
-                const uint32_t Pnb = Pb + qi;
-                const float Pn = __uint_as_float(Pnb);
-                if (j & 1) G2[j >> 1].y = gprev;
-                else G2[j >> 1].x = gprev;
-                Yb[j] = Pb + Q;
-                // Candidates of age >= 2 first: they depend only on P and on g values of earlier
-                // layers, so the DP chain through the layers is just  g = min(old, g_prev) + Cg.
-                // pair unit v: even layer -> ages (2v+2, 2v+3), the last one (ages W, 1) wrapping
-                // around the ring; odd layer -> age 2 alone (v = 0), ages (2v+1, 2v+2) (v >= 1).
-                // A pair's odd slot is the float2's .y, the even slot below it the .x.
-                auto unit = [&](const int v, float& lo, float& hi) {
-                    if ((j & 1) && v == 0) {
-                        const int xs = (j - 1 + W) % W;
-                        lo = hi = G2[xs >> 1].x + __saturatef(Pn - __uint_as_float(Yb[xs]));
-                        return;
-                    }
-                    const int ys = (j & 1) ? ((j - 2 * v + 2 * W) % W) : ((j - 2 * v - 1 + 2 * W) % W);
-                    const int xs = ys - 1;
-                    const float2 sp = make_float2(__saturatef(Pn - __uint_as_float(Yb[xs])),
-                                                  __saturatef(Pn - __uint_as_float(Yb[ys])));
-                    const float2 cnd = __fadd2_rn(G2[xs >> 1], sp);
-                    lo = cnd.x;
-                    hi = cnd.y;
-                };
-                const int nunits = H;
-                const int os = (j + 1) % W;  // oldest ring slot (age W)
+            // candidate pair unit v of layer jj (compile-time): even layer -> ages (2v+2, 2v+3), the
+            // last one (ages W, 1) wrapping around the ring; odd layer -> age 2 alone (v = 0), ages
+            // (2v+1, 2v+2) (v >= 1).  A pair's odd slot is the float2's .y, the even slot below it the .x.
+            auto unit = [&](const int jj, const float Pn, const int v, float& lo, float& hi) {
+                if ((jj & 1) && v == 0) {
+                    const int xs = (jj - 1 + W) % W;
+                    lo = hi = G2[xs >> 1].x + __saturatef(Pn - __uint_as_float(Yb[xs]));
+                    return;
+                }
+                const int ys = (jj & 1) ? ((jj - 2 * v + 2 * W) % W) : ((jj - 2 * v - 1 + 2 * W) % W);
+                const int xs = ys - 1;
+                const float2 sp = make_float2(__saturatef(Pn - __uint_as_float(Yb[xs])),
+                                              __saturatef(Pn - __uint_as_float(Yb[ys])));
+                const float2 cnd = __fadd2_rn(G2[xs >> 1], sp);
+                lo = cnd.x;
+                hi = cnd.y;
+            };
+            auto youngest = [&](const int jj, const int v) {  // slot of unit v's youngest age
+                return (jj & 1) ? ((jj - 2 * v + 2 * W) % W) : ((jj - 2 * v - 1 + 2 * W) % W);
+            };
+            // Candidates of age >= 2 first: they depend only on P and on g values of earlier
+            // layers, so the DP chain through the layers is just  g = min(old, g_prev) + Cg.
+            auto first_group = [&](const int jj, const float Pn, const uint32_t Pnb) -> float {
                 float cv[2 * U0];
 #pragma unroll
                 for (int v = 0; v < U0; ++v) {
-                    if (v < nunits) unit(v, cv[2 * v], cv[2 * v + 1]);
+                    if (v < H) unit(jj, Pn, v, cv[2 * v], cv[2 * v + 1]);
                     else cv[2 * v] = cv[2 * v + 1] = 2.0f;
                 }
-                float a = min_tree<2 * U0>(cv);
-                if (U0 >= nunits) ovf |= Yb[os] >= Pnb;
-                // NG voted groups of UG pairs, then (if still needed) the rest in one straight run
+                if (U0 >= H) ovf |= Yb[(jj + 1) % W] >= Pnb;  // oldest ring age (W) reached
+                return min_tree<2 * U0>(cv);
+            };
+            // NG voted groups of UG pairs, then (if still needed) the rest in one straight run
+            auto deep_groups = [&](const int jj, const float Pn, const uint32_t Pnb, float a) -> float {
 #pragma unroll
                 for (int gi = 0; gi <= NG; ++gi) {
                     const int v0 = U0 + gi * UG;
                     const int v1 = gi < NG ? v0 + UG : H;
-                    if (v0 >= nunits) break;
-                    const int ys = (j & 1) ? ((j - 2 * v0 + 2 * W) % W) : ((j - 2 * v0 - 1 + 2 * W) % W);
-                    if (!__builtin_expect(__any_sync(kFull, Yb[ys] >= Pnb), 0)) break;
+                    if (v0 >= H) break;
+                    if (!__any_sync(kFull, Yb[youngest(jj, v0)] >= Pnb)) break;
 #pragma unroll
                     for (int v = v0; v < v1; ++v)
-                        if (v < nunits) {
+                        if (v < H) {
                             float lo, hi;
-                            unit(v, lo, hi);
+                            unit(jj, Pn, v, lo, hi);
                             a = fminf(a, fminf(lo, hi));
                         }
-                    if (v1 >= nunits) ovf |= Yb[os] >= Pnb;  // the scan reached the oldest ring age
+                    if (v1 >= H) ovf |= Yb[(jj + 1) % W] >= Pnb;  // the scan reached the oldest ring age
                 }
-                // age 1 (p = i - 1) is always in the window when q <= Q (q > Q: qmax, DESIGN R4)
-                gprev = fminf(a, gprev) + cg;
-                Pb = Pnb;
+                return a;
+            };
+            uint32_t qnext = bufw[0];
+            if constexpr (PAIR) {
+                // Two layers at a time: every candidate of age >= 2 of BOTH layers is known before
+                // either layer's result, so both first groups run back to back and ONE warp vote
+                // guards the deeper groups of the pair (one skip branch per two layers).
+#pragma unroll
+                for (int j = 0; j < W; j += 2) {
+                    const float cg0 = cgc[j], cg1 = cgc[j + 1];
+                    const uint32_t q0 = qnext;
+                    const uint32_t q1 = bufw[(j + 1) * kTile];
+                    if (j + 2 < W) qnext = bufw[(j + 2) * kTile];
+                    qmax = max(qmax, max(q0, q1));
+                    const uint32_t Pnb0 = Pb + q0, Pnb1 = Pnb0 + q1;
+                    const float Pn0 = __uint_as_float(Pnb0), Pn1 = __uint_as_float(Pnb1);
+                    G2[j >> 1].x = gprev;  // slot j: the point of layer j's age 1
+                    Yb[j] = Pb + Q;
+                    float a0 = first_group(j, Pn0, Pnb0);
+                    float a1 = first_group(j + 1, Pn1, Pnb1);
+                    if (U0 < H && __any_sync(kFull, Yb[youngest(j, U0)] >= Pnb0 || Yb[youngest(j + 1, U0)] >= Pnb1)) {
+                        a0 = deep_groups(j, Pn0, Pnb0, a0);
+                        a1 = deep_groups(j + 1, Pn1, Pnb1, a1);
+                    }
+                    Yb[j + 1] = Pnb0 + Q;  // (after layer j read slot j + 1 as its age W)
+                    // age 1 (p = i - 1) is always in the window when q <= Q (q > Q: qmax, DESIGN R4)
+                    const float g0 = fminf(a0, gprev) + cg0;
+                    G2[j >> 1].y = g0;
+                    gprev = fminf(a1, g0) + cg1;
+                    Pb = Pnb1;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    const float cg = cgc[j];
+                    const uint32_t qi = qnext;  // loaded one layer ahead
+                    if (j + 1 < W) qnext = bufw[(j + 1) * kTile];
+                    qmax = max(qmax, qi);
+                    const uint32_t Pnb = Pb + qi;
+                    const float Pn = __uint_as_float(Pnb);
+                    if (j & 1) G2[j >> 1].y = gprev;
+                    else G2[j >> 1].x = gprev;
+                    Yb[j] = Pb + Q;
+                    float a = first_group(j, Pn, Pnb);
+                    a = deep_groups(j, Pn, Pnb, a);
+                    // age 1 (p = i - 1) is always in the window when q <= Q (q > Q: qmax, DESIGN R4)
+                    gprev = fminf(a, gprev) + cg;
+                    Pb = Pnb;
+                }
             }
             __syncwarp();
             issue();
@@ -1425,10 +1462,10 @@ static spdp_status launch_deque(cudaStream_t st, const SweepArgs& a) {
     return rc;
 }
 
-template <int W, int U0, int UG, int MB = 0, int NG = W>
+template <int W, int U0, int UG, int MB = 0, int NG = W, bool PAIR = false>
 static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
     using Cfg = F2Cfg<W, MB>;
-    auto kern = split_sweep_f2_kernel<W, U0, UG, MB, NG>;
+    auto kern = split_sweep_f2_kernel<W, U0, UG, MB, NG, PAIR>;
     static int blocks_per_sm = 0;
     if (blocks_per_sm == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
@@ -1451,7 +1488,7 @@ static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
                                            a.cgs, a.tinfo, a.n, a.T, a.S, a.Q, (uint32_t)lim, a.cost, a.slots, a.ovf,
                                            a.hdr),
                                 "split_sweep_f2_kernel");
-    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d,%d,%d>", W, U0, UG, Cfg::kMinBlocks, NG);
+    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d,%d,%d%s>", W, U0, UG, Cfg::kMinBlocks, NG, PAIR ? ",pair" : "");
     prof_end(st);
     return rc;
 }
@@ -1484,13 +1521,14 @@ static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArg
                     default: return launch_sweep_f2_t<16, 3, 1>(st, a);
                 }
             case 20:
-                if (wide) return launch_sweep_f2_t<20, 6, 2>(st, a);
+                if (wide) return launch_sweep_f2_t<20, 6, 2, 0, 20, true>(st, a);  // (pairs: -1.4 % at C3)
                 switch (f2_cfg()) {
                     case 21: return launch_sweep_f2_t<20, 2, 1>(st, a);
                     case 32: return launch_sweep_f2_t<20, 3, 2>(st, a);
                     case 41: return launch_sweep_f2_t<20, 4, 1>(st, a);
                     case 42: return launch_sweep_f2_t<20, 4, 2>(st, a);
                     case 324: return launch_sweep_f2_t<20, 3, 2, 4>(st, a);
+                    case 3199: return launch_sweep_f2_t<20, 3, 1, 0, 20, true>(st, a);
                     case 51: return launch_sweep_f2_t<20, 5, 1>(st, a);
                     case 52: return launch_sweep_f2_t<20, 5, 2>(st, a);
                     case 62: return launch_sweep_f2_t<20, 6, 2>(st, a);
