@@ -437,6 +437,24 @@ def measure_rows(spdp, torch, dev, pk):
         sweep[str(S_)] = {"ms": ms, "evals_per_s": S_ / (ms / 1e3)}
     rows["a5_C2_S_sweep"] = sweep
     del d
+    # a5 sensitivity: C2 with r = 16 customers per route (Q 4x, windows ~4x: mean 15,
+    # max 46 -> the monotone-deque sweep)
+    inst16 = synth.make_instance(100, 101, r=16.0)
+    model16 = synth.demand_model(inst16["nominal"], inst16["Q"], seed=0x5EED0001)
+    d = spdp.gen_demands(model16, 0, cfg2["S"], device=dev)
+    tour16, dist16 = torch.from_numpy(inst16["tour"]).to(dev), torch.from_numpy(inst16["dist"]).to(dev)
+    c_ = torch.empty(cfg2["S"], dtype=torch.int32, device=dev)
+    p_ = torch.zeros(6, dtype=torch.int64, device=dev)
+    fn = lambda: spdp.split_eval(tour16, dist16, d, inst16["Q"], S=cfg2["S"], window_hint=64, cost=c_, partial=p_)
+    ms = _time_events(fn, torch, dev, iters=10)
+    m = spdp.split_mask(tour16, d, inst16["Q"], S=cfg2["S"])
+    idx = torch.arange(1, 101, device=dev, dtype=torch.int64).unsqueeze(1)
+    cand16 = int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item())
+    del m
+    rows["a5_C2_r16"] = {"ms": ms, "Q": inst16["Q"], "evals_per_s": cfg2["S"] / (ms / 1e3), "kernel": spdp.last_kernel(),
+                         "candidates": cand16,
+                         "alu_frac": cand16 / (ms / 1e3) / (N_SM * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6)}
+    del d
     # a8: batched tours (C3) and a5 at n=1000 (C4, 1 GPU)
     for name in ("C3", "C4"):
         cfg = synth.config_instance(name)
