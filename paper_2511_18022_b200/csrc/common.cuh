@@ -110,6 +110,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// ---- shared-memory access by 32-bit shared address --------------------------------
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ int2 lds_s32x2(uint32_t a) {
+    int2 v;
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_s32x2(uint32_t a, int x, int y) {
+    asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+
 // ---- cp.async (LDGSTS): per-thread 16-byte global -> shared copies, L2-only (.cg) ----
 // (no L2 cache-policy operand: ptxas 12.9 can place the policy descriptor in a misaligned
 // uniform register pair for LDGSTS, which traps as an illegal instruction)

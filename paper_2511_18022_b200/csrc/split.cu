@@ -794,7 +794,10 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
     unsigned char* wbase = smem_raw + (size_t)wid * Cfg::kWarpBytes;
     int2* tq = reinterpret_cast<int2*>(wbase);
     unsigned char* stage_base = wbase + kQueue * 8;
-    int2* dq = reinterpret_cast<int2*>(stage_base + NS * Cfg::kStageBytes) + lane;  // [D][32] {g, Y}
+    // [D][32] {g, Y} per warp (lane-contiguous rows of 256 B, conflict-free), as a shared address
+    const uint32_t dqa = smem_u32(stage_base + NS * Cfg::kStageBytes) + 8u * (uint32_t)lane;
+    constexpr uint32_t kMask = (uint32_t)(D - 1) * 256u;
+    static_assert((D & (D - 1)) == 0, "D must be a power of two");
     const uint32_t ntile_s = (uint32_t)((S + kTile - 1) / kTile);
     const uint32_t ntiles = ntile_s * (uint32_t)T;
     const int nchunks = (n + R - 1) / R;
@@ -825,50 +828,60 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
         uint32_t P = 1u;
         uint32_t qmax = 0u;
         bool ovf = false;
-        int hd = 0, tl = 0;        // deque = entries [hd, tl) (indices mod D)
-        int fg = 0, bg = INT_MIN;  // cached front g and back g
+        // deque = entries [hd, tl) (mod D), kept as byte offsets (x 256 = one [32] row of int2);
+        // entry e lives at dqa + (e & 0xF00)
+        uint32_t hd8 = 0u, tl8 = 0u;
+        int fg = 0, bg = INT_MIN;  // cached front g and back g (INT_MIN: empty)
         uint32_t fy = 0u;          // cached front Y
+        auto layer = [&](const uint32_t q, const int cg) {
+            qmax = max(qmax, q);
+            const uint32_t Pn = P + q;
+            const uint32_t ynew = P + Q;
+            // push p = L with g(p) = gprev: pop dominated points (g >= gprev) from the back
+            for (;;) {
+                const bool pop = bg >= gprev;
+                if (!__any_sync(kFull, pop)) break;
+                const uint32_t ntl = tl8 - (pop ? 256u : 0u);
+                const int nb = lds_s32(dqa + ((ntl - 256u) & kMask));
+                if (pop) {
+                    tl8 = ntl;
+                    bg = (ntl != hd8) ? nb : INT_MIN;
+                }
+            }
+            ovf |= (tl8 - hd8 == (uint32_t)D * 256u);  // capacity exceeded: the overflow path
+            sts_s32x2(dqa + (tl8 & kMask), gprev, (int)ynew);
+            if (tl8 == hd8) {
+                fg = gprev;
+                fy = ynew;
+            }
+            tl8 += 256u;
+            bg = gprev;
+            // pop split points that left the window (Y < P'(L+1)) from the front
+            for (;;) {
+                const bool pop = tl8 - hd8 > 256u && fy < Pn;
+                if (!__any_sync(kFull, pop)) break;
+                const uint32_t nhd = hd8 + (pop ? 256u : 0u);
+                const int2 e = lds_s32x2(dqa + (nhd & kMask));
+                if (pop) {
+                    hd8 = nhd;
+                    fg = e.x;
+                    fy = (uint32_t)e.y;
+                }
+            }
+            gprev = fg + cg;  // the front is the window minimum
+            P = Pn;
+        };
 
         for (int c = 0;;) {
             const unsigned char* sb = stage_base + cstage * Cfg::kStageBytes;
             const uint16_t* buf = reinterpret_cast<const uint16_t*>(sb) + col;
             const int32_t* cgc = reinterpret_cast<const int32_t*>(sb + Cfg::kRowsBytes);
             const int rows = (n - c * R) < R ? (n - c * R) : R;
-            for (int j = 0; j < rows; ++j) {
-                const uint32_t q = buf[j * kTile];
-                qmax = max(qmax, q);
-                const uint32_t Pn = P + q;
-                const uint32_t ynew = P + Q;
-                // push p = L with g(p) = gprev: pop dominated points (g >= gprev) from the back
-                for (;;) {
-                    const bool pop = tl != hd && bg >= gprev;
-                    if (!__any_sync(kFull, pop)) break;
-                    if (pop) {
-                        --tl;
-                        bg = tl != hd ? dq[((tl - 1) & (D - 1)) * kTile].x : INT_MIN;
-                    }
-                }
-                ovf |= (tl - hd == D);  // capacity exceeded: this scenario goes to the overflow path
-                dq[(tl & (D - 1)) * kTile] = make_int2(gprev, (int)ynew);
-                ++tl;
-                bg = gprev;
-                if (tl - hd == 1) {
-                    fg = gprev;
-                    fy = ynew;
-                }
-                // pop split points that left the window (Y < P'(L+1)) from the front
-                for (;;) {
-                    const bool pop = tl - hd > 1 && fy < Pn;
-                    if (!__any_sync(kFull, pop)) break;
-                    if (pop) {
-                        ++hd;
-                        const int2 e = dq[(hd & (D - 1)) * kTile];
-                        fg = e.x;
-                        fy = (uint32_t)e.y;
-                    }
-                }
-                gprev = fg + cgc[j];
-                P = Pn;
+            if (rows == R) {  // (warp-uniform) full chunk: unrolled, static stage offsets
+#pragma unroll
+                for (int j = 0; j < R; ++j) layer(buf[j * kTile], cgc[j]);
+            } else {
+                for (int j = 0; j < rows; ++j) layer(buf[j * kTile], cgc[j]);
             }
             __syncwarp();
             issue();
