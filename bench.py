@@ -466,7 +466,7 @@ def measure_rows(spdp, torch, dev, pk):
         h = bench_config.HINT[name]
         fn = lambda: spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, partial=part,
                                            window_hint=h, mean_window=bench_config.MEAN[name])
-        ms = _time_events(fn, torch, dev, iters=3)
+        ms = _time_events(fn, torch, dev, iters=6)
         m = spdp.split_mask(tours[0].contiguous(), d, inst["Q"], S=cfg["S"])
         idx = torch.arange(1, cfg["n"] + 1, device=dev, dtype=torch.int64).unsqueeze(1)
         cand0 = int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item())
