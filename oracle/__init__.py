@@ -56,8 +56,11 @@ def _L():
         lib.oracle_split_batch_tours.argtypes = [i32, i32, P, P, i32, P, i64, i64, P, ctypes.c_int]
         lib.oracle_saa.argtypes = [P, i64, P, P]
         lib.oracle_split_penalized.argtypes = [i32, P, P, i32, i64, P, i64, i64, P, P, ctypes.c_int]
+        lib.oracle_split_values.argtypes = [i32, P, P, i32, P, i64, i64, P, P, ctypes.c_int]
+        lib.oracle_split_limits.argtypes = [i32, P, P, i32, i64, i32, P, i64, i64, P, P, P, ctypes.c_int]
         lib.oracle_irp.argtypes = [i32, i32, P, P, P, i64, i64, P, ctypes.c_int]
         for name in ("oracle_gen_demands", "oracle_split_batch", "oracle_split_batch_tours", "oracle_split_penalized",
+                     "oracle_split_values", "oracle_split_limits",
                      "oracle_saa", "oracle_irp", "oracle_num_threads"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -173,6 +176,46 @@ def split_penalized(tour, dist, demand, Q, lam: int, want_pred: bool = False, S:
     if rc:
         raise ValueError("oracle_split_penalized rc=%d" % rc)
     return (cost, pred) if want_pred else cost
+
+
+def split_values(tour, dist, demand, Q, S: int | None = None, threads: int = 0):
+    """f3 (DESIGN R23): prefix / suffix split values, int64 [S][n+1] each (INF = infeasible):
+    fwd[s][i] = Split of sigma_1..sigma_i, bwd[s][i] = Split of sigma_{i+1}..sigma_n."""
+    tour = np.ascontiguousarray(tour, dtype=np.int32)
+    dist = np.ascontiguousarray(dist, dtype=np.int32)
+    demand = np.ascontiguousarray(demand, dtype=np.uint16)
+    n = tour.shape[0]
+    ld = demand.shape[1]
+    S = ld if S is None else S
+    fwd = np.zeros((S, n + 1), dtype=np.int64)
+    bwd = np.zeros((S, n + 1), dtype=np.int64)
+    rc = _L().oracle_split_values(n, _p(tour), _p(dist), int(Q), _p(demand), ld, int(S), _p(fwd), _p(bwd),
+                                  int(threads))
+    if rc:
+        raise ValueError("oracle_split_values rc=%d" % rc)
+    return fwd, bwd
+
+
+def split_limits(tour, dist, demand, Q, Lmax: int = -1, K: int = 0, want_pred: bool = False,
+                 S: int | None = None, threads: int = 0):
+    """f4 (DESIGN R24): split with route duration t(p,i) <= Lmax (Lmax < 0: none) and at most
+    K routes (K <= 0: none).  int64 [S] costs (INF = infeasible), optionally the optimum's
+    predecessors [S][n+1] (-1 off the path) and route counts [S]."""
+    tour = np.ascontiguousarray(tour, dtype=np.int32)
+    dist = np.ascontiguousarray(dist, dtype=np.int32)
+    demand = np.ascontiguousarray(demand, dtype=np.uint16)
+    n = tour.shape[0]
+    ld = demand.shape[1]
+    S = ld if S is None else S
+    cost = np.zeros(S, dtype=np.int64)
+    pred = np.zeros((S, n + 1), dtype=np.int32) if want_pred else None
+    kused = np.zeros(S, dtype=np.int32) if want_pred else None
+    rc = _L().oracle_split_limits(n, _p(tour), _p(dist), int(Q), int(Lmax), int(K), _p(demand), ld, int(S),
+                                  _p(cost), _p(pred) if want_pred else None, _p(kused) if want_pred else None,
+                                  int(threads))
+    if rc:
+        raise ValueError("oracle_split_limits rc=%d" % rc)
+    return (cost, pred, kused) if want_pred else cost
 
 
 def split_tours(tours, dist, demand, Q, S: int | None = None, threads: int = 0) -> np.ndarray:

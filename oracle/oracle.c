@@ -28,6 +28,11 @@
  *                            in the test); PAPER:64-66 Example 1(i) routes; closed forms
  *   oracle_split_scan        == oracle_split_eq1 on random cases; O(n) deque split
  *                            (independent algorithm, in the test) for deterministic demand
+ *   oracle_split_values      brute force over the partitions of every prefix / suffix;
+ *                            b(i) of a tour = f(n-i) of the reversed tour under the
+ *                            transposed costs; f(i) + b(i) >= cost, = at optimal boundaries
+ *   oracle_split_limits      brute force over partitions with <= K routes of duration
+ *                            <= Lmax; no limits = plain split; monotone in K and Lmax
  *   oracle_saa               Python statistics.fmean/variance (exact Fractions) on costs
  *   oracle_irp               brute force over all action sequences (pure Python, in
  *                            the test); two closed forms
@@ -246,10 +251,10 @@ static int64_t split_eq1_one(int32_t n, const int32_t* tour, const int32_t* dist
 /* Ties: strict "<" while p decreases keeps the LARGEST p (DESIGN R10).      */
 /* Also returns sum_i w(i), w(i) = i - mask(i): the Eq. (3) candidate count. */
 /* ------------------------------------------------------------------------ */
-static int64_t split_scan_one(int32_t n, const int32_t* tour, const int32_t* dist, int32_t Q,
+/* (N1 = the row stride of dist: n + 1 for a whole tour, larger for a sub-tour.) */
+static int64_t split_scan_sub(int32_t n, const int32_t* tour, const int32_t* dist, int64_t N1, int32_t Q,
                               const int64_t* q, int64_t* f, int32_t* pred, int64_t* wsum)
 {
-    const int64_t N1 = (int64_t)n + 1;
     int64_t cnt = 0;
     f[0] = 0;
     for (int32_t i = 1; i <= n; ++i) {
@@ -271,6 +276,12 @@ static int64_t split_scan_one(int32_t n, const int32_t* tour, const int32_t* dis
     if (pred) pred[0] = -1;
     if (wsum) *wsum = cnt;
     return f[n];
+}
+
+static int64_t split_scan_one(int32_t n, const int32_t* tour, const int32_t* dist, int32_t Q,
+                              const int64_t* q, int64_t* f, int32_t* pred, int64_t* wsum)
+{
+    return split_scan_sub(n, tour, dist, (int64_t)n + 1, Q, q, f, pred, wsum);
 }
 
 /* Batch driver: scenario s of demand[n][ld] (customer-id rows, DESIGN R1),
@@ -317,6 +328,138 @@ int oracle_split_batch_tours(int32_t n, int32_t T, const int32_t* tours, const i
         int rc = oracle_split_batch(n, tours + (int64_t)t * n, dist, Q, demand, ld, S, 0,
                                     cost + (int64_t)t * S, NULL, NULL, threads);
         if (rc) return rc;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* f3. Prefix and suffix split values of one tour, the   */
+/* state that candidate tours sharing a prefix / suffix with it reuse        */
+/* ("explore many more candidate first-stage tours"; DESIGN    */
+/* R23).  Written as the definitions, not as a recursion over each other:    */
+/*   fwd[i] = Split(sigma_1..sigma_i)      i = 0..n  (fwd[0] = 0)            */
+/*   bwd[i] = Split(sigma_{i+1}..sigma_n)  i = 0..n  (bwd[n] = 0)            */
+/* where Split(.) is Eq. (1) of the sub-tour as a standalone problem         */
+/* (PAPER:98-101): fwd[i] is f(i) of the scan (Eq. (1) restricted to the      */
+/* first i customers is the same recursion), bwd[i] is one more call of the  */
+/* scan on the suffix.  O(n^2 w) per scenario: small cases only.            */
+/* ORACLE_INF where the sub-tour holds a demand above Q (DESIGN R4).          */
+/* fwd, bwd: [S][n+1] (row per scenario).                                     */
+/* ------------------------------------------------------------------------ */
+int oracle_split_values(int32_t n, const int32_t* tour, const int32_t* dist, int32_t Q,
+                        const uint16_t* demand, int64_t ld, int64_t S,
+                        int64_t* fwd, int64_t* bwd, int threads)
+{
+    if (n < 1 || S < 0 || Q < 1 || ld < S) return 2;
+    const int64_t N1 = (int64_t)n + 1;
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel
+#endif
+    {
+        int64_t* q = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+        int64_t* f = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+        for (int64_t s = 0; s < S; ++s) {
+            for (int32_t k = 1; k <= n; ++k) q[k - 1] = demand[(int64_t)(tour[k - 1] - 1) * ld + s];
+            split_scan_one(n, tour, dist, Q, q, f, NULL, NULL);
+            for (int32_t i = 0; i <= n; ++i) fwd[s * N1 + i] = f[i];
+            bwd[s * N1 + n] = 0;
+            for (int32_t i = 0; i < n; ++i)   /* the suffix sigma_{i+1..n}: n - i customers */
+                bwd[s * N1 + i] = split_scan_sub(n - i, tour + i, dist, N1, Q, q + i, f, NULL, NULL);
+        }
+        free(q);
+        free(f);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* f4. Split with a route-duration limit and a fleet     */
+/* limit (DESIGN R24; "route length/duration constraints, if         */
+/* applicable", "three vehicles available"):                         */
+/*   a route (p, i] is admissible iff  sum_{k=p+1}^{i} q <= Q  and           */
+/*   t(p, i) = c_{0,s_{p+1}} + sum_{k=p+1}^{i-1} c_{s_k,s_{k+1}} + c_{s_i,0}  */
+/*   <= Lmax  (route duration = route cost; Lmax < 0: no limit);             */
+/*   F_0(0) = 0, F_0(i>0) = inf,                                             */
+/*   F_k(i) = min_{admissible (p,i]} F_{k-1}(p) + t(p, i)   (k = 1..K)        */
+/*   cost = min_{1 <= k <= K} F_k(n)          (K <= 0: no fleet limit, K = n) */
+/* The Eq. (1) layered DAG with a vehicle-count layer dimension.  Descending */
+/* scan: the load break is exact (R5); the duration test only skips (t need  */
+/* not be monotone in p without the triangle inequality).  Ties: the         */
+/* smallest k, then (strict "<" while p decreases) the largest p.            */
+/* pred (nullable) [S][n+1]: the last split point of the chosen layer's      */
+/* path, k_used (nullable) [S]: the route count of the optimum.              */
+/* ------------------------------------------------------------------------ */
+int oracle_split_limits(int32_t n, const int32_t* tour, const int32_t* dist, int32_t Q,
+                        int64_t Lmax, int32_t K, const uint16_t* demand, int64_t ld, int64_t S,
+                        int64_t* cost, int32_t* pred, int32_t* k_used, int threads)
+{
+    if (n < 1 || S < 0 || Q < 1 || ld < S) return 2;
+    const int64_t N1 = (int64_t)n + 1;
+    const int32_t KK = (K <= 0 || K > n) ? n : K;
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel
+#endif
+    {
+        int64_t* q = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+        int64_t* F = (int64_t*)malloc(sizeof(int64_t) * (size_t)(KK + 1) * (size_t)N1);
+        int32_t* arg = (int32_t*)malloc(sizeof(int32_t) * (size_t)(KK + 1) * (size_t)N1);
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+        for (int64_t s = 0; s < S; ++s) {
+            for (int32_t k = 1; k <= n; ++k) q[k - 1] = demand[(int64_t)(tour[k - 1] - 1) * ld + s];
+            for (int32_t i = 0; i <= n; ++i) { F[i] = ORACLE_INF; arg[i] = -1; }
+            F[0] = 0;
+            for (int32_t k = 1; k <= KK; ++k) {
+                int64_t* Fk = F + (int64_t)k * N1;
+                const int64_t* Fp = F + (int64_t)(k - 1) * N1;
+                Fk[0] = ORACLE_INF;
+                arg[(int64_t)k * N1] = -1;
+                for (int32_t i = 1; i <= n; ++i) {
+                    int64_t best = ORACLE_INF, load = 0, chain = 0;
+                    int32_t a = -1;
+                    for (int32_t p = i - 1; p >= 0; --p) {
+                        load += q[p];                               /* q_{sigma_{p+1}} */
+                        if (load > Q) break;
+                        if (p + 1 <= i - 1) chain += dist[(int64_t)tour[p] * N1 + tour[p + 1]];
+                        const int64_t t = dist[0 * N1 + tour[p]] + chain + dist[(int64_t)tour[i - 1] * N1 + 0];
+                        if (Lmax >= 0 && t > Lmax) continue;
+                        if (Fp[p] == ORACLE_INF) continue;
+                        const int64_t cand = Fp[p] + t;
+                        if (cand < best) { best = cand; a = p; }
+                    }
+                    Fk[i] = best;
+                    arg[(int64_t)k * N1 + i] = a;
+                }
+            }
+            int64_t best = ORACLE_INF;
+            int32_t kb = 0;
+            for (int32_t k = 1; k <= KK; ++k)
+                if (F[(int64_t)k * N1 + n] < best) { best = F[(int64_t)k * N1 + n]; kb = k; }
+            cost[s] = best;
+            if (k_used) k_used[s] = best == ORACLE_INF ? 0 : kb;
+            if (pred) {
+                int32_t* pr = pred + s * N1;
+                for (int32_t i = 0; i <= n; ++i) pr[i] = -1;
+                if (best != ORACLE_INF) {       /* the optimum's path: layer kb at n, kb-1 at its pred, ... */
+                    int32_t i = n, k = kb;
+                    while (i > 0 && k > 0) {
+                        const int32_t p = arg[(int64_t)k * N1 + i];
+                        pr[i] = p;
+                        i = p;
+                        --k;
+                    }
+                }
+            }
+        }
+        free(q);
+        free(F);
+        free(arg);
     }
     return 0;
 }
