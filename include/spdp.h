@@ -228,6 +228,40 @@ SPDP_API spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dist,
                               int32_t* nroutes, int32_t* maxload, void* ws, size_t ws_bytes,
                               spdp_stream_t stream);
 
+/* f3 (DESIGN R23). Prefix and suffix split values of one tour,
+ * the state that candidate tours sharing a prefix / suffix with it reuse
+ * (evaluate many candidate first-stage tours):
+ *   fwd[i*S + j] = Split(sigma_1..sigma_i)      of scenario j, i = 0..n (fwd[0] = 0)
+ *   bwd[i*S + j] = Split(sigma_{i+1}..sigma_n)  of scenario j, i = 0..n (bwd[n] = 0)
+ * (Split = Eq. (1), of the sub-tour as a standalone problem).
+ * int32 [n+1][S] each (DEVICE, caller-owned), SPDP_INFEASIBLE where the prefix /
+ * suffix holds a demand above Q.  fwd[n] = bwd[0] = the spdp_split_eval cost.
+ * One thread per scenario, any window width.  ws: spdp_values_workspace_bytes(n)
+ * bytes of device memory.  Same argument rules as spdp_split_eval. */
+SPDP_API size_t spdp_values_workspace_bytes(int32_t n);
+SPDP_API spdp_status spdp_split_values(const int32_t* tour, const int32_t* dist, int32_t n,
+                              const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                              int32_t* fwd, int32_t* bwd, void* ws, size_t ws_bytes,
+                              spdp_stream_t stream);
+
+/* f3. Neighbourhood evaluation: the split cost of T candidate tours [T][n] that
+ * are permutations of the same customers as `parent`, from the parent's values
+ * (fwd, bwd from spdp_split_values on the SAME demand, dist and Q).  A candidate
+ * equal to the parent on positions 1..a and s0+1..n only re-runs the Eq. (3)
+ * sweep from layer a+1 to the last layer a route starting before s0 can reach,
+ * then takes cost = min_{s0 <= i <= E} f(i) + bwd[i] (every split has a route
+ * boundary there).  Results (cost [T][S] int32, may be NULL; partial [T], may be
+ * NULL, overwritten) are bit-identical to spdp_split_eval_batch on `tours`.
+ * window_hint: as spdp_split_eval (selects the register ring: 16, 24 or 32;
+ * wider windows are finished by the general kernel).  SPDP_F_VALIDATE checks the
+ * candidates (not the parent).  ws: spdp_neighbour_workspace_bytes(n, S, T). */
+SPDP_API size_t spdp_neighbour_workspace_bytes(int32_t n, int64_t S, int32_t T);
+SPDP_API spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int32_t* fwd, const int32_t* bwd,
+                                       const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,
+                                       const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                                       int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
+                                       void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream);
+
 /* a6 standalone: SAA partial of a cost vector (SPDP_INFEASIBLE entries are
  * counted in n_infeas and excluded).  partial: DEVICE pointer to one struct. */
 SPDP_API spdp_status spdp_saa_reduce(const int32_t* cost, int64_t S, spdp_saa_partial* partial,

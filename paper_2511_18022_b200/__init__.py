@@ -39,7 +39,8 @@ SYMBOLS = (
     "spdp_split_mask", "spdp_split_eval", "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean",
     "spdp_host_workspace_bytes", "spdp_split_eval_host", "spdp_irp_workspace_bytes", "spdp_irp_dp",
     "spdp_set_profile_events", "spdp_last_kernel", "spdp_routes_workspace_bytes", "spdp_split_routes",
-    "spdp_split_eval_penalized",
+    "spdp_split_eval_penalized", "spdp_values_workspace_bytes", "spdp_split_values",
+    "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours",
 )
 
 
@@ -91,12 +92,19 @@ def _sig():
     L.spdp_routes_workspace_bytes.argtypes = [i32, i32]
     L.spdp_routes_workspace_bytes.restype = sz
     L.spdp_split_routes.argtypes = [P, P, i32, P, i64, i64, i32, P, i32, P, P, P, P, P, sz, P]
+    L.spdp_values_workspace_bytes.argtypes = [i32]
+    L.spdp_values_workspace_bytes.restype = sz
+    L.spdp_split_values.argtypes = [P, P, i32, P, i64, i64, i32, P, P, P, sz, P]
+    L.spdp_neighbour_workspace_bytes.argtypes = [i32, i64, i32]
+    L.spdp_neighbour_workspace_bytes.restype = sz
+    L.spdp_split_eval_neighbours.argtypes = [P, P, P, P, i32, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
     L.spdp_irp_dp.argtypes = [P, ctypes.POINTER(IrpCustomer), i32, i32, P, i64, i64, P, P, P, sz, u32, P]
     for name in ("spdp_gen_demands", "spdp_demand_prefix", "spdp_split_mask", "spdp_split_eval",
                  "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean", "spdp_split_eval_host",
-                 "spdp_irp_dp"):
+                 "spdp_irp_dp", "spdp_split_values", "spdp_split_eval_neighbours", "spdp_split_eval_penalized",
+                 "spdp_split_routes"):
         getattr(L, name).restype = st
 
 
@@ -325,6 +333,50 @@ def split_eval_batch(tours, dist, demand, Q: int, S: int | None = None, want_cos
                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(),
                                       (F_VALIDATE if validate else 0) | F_SWEEP[algo] | _mean_flag(mean_window), _stream(dev)),
            "spdp_split_eval_batch")
+    return cost, partial
+
+
+def split_values(tour, dist, demand, Q: int, S: int | None = None, fwd=None, bwd=None):
+    """f3: prefix / suffix split values of one tour (spdp_split_values).
+    Returns (fwd, bwd), int32 [n+1][S] each: fwd[i] = Split of the first i customers,
+    bwd[i] = Split of the customers after position i (INFEASIBLE sentinel)."""
+    torch = _torch()
+    n, ld = demand.shape
+    S = ld if S is None else S
+    dev = demand.device
+    if fwd is None:
+        fwd = torch.empty((n + 1, S), dtype=torch.int32, device=dev)
+    if bwd is None:
+        bwd = torch.empty((n + 1, S), dtype=torch.int32, device=dev)
+    ws = workspace(int(_lib.spdp_values_workspace_bytes(n)), dev, tag="values")
+    _check(_lib.spdp_split_values(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld, S,
+                                  int(Q), _dev_ptr(fwd, "fwd"), _dev_ptr(bwd, "bwd"), ctypes.c_void_p(ws.data_ptr()),
+                                  ws.numel(), _stream(dev)), "spdp_split_values")
+    return fwd, bwd
+
+
+def split_eval_neighbours(parent, fwd, bwd, tours, dist, demand, Q: int, S: int | None = None,
+                          want_cost: bool = True, want_partial: bool = True, window_hint: int = 0,
+                          validate: bool = False, cost=None, partial=None):
+    """f3: split costs of T candidate tours [T][n] from the parent's values (spdp_split_eval_neighbours);
+    bit-identical to split_eval_batch(tours, ...).  Returns (cost int32 [T][S], partial int64 [T][6])."""
+    torch = _torch()
+    n, ld = demand.shape
+    T = tours.shape[0]
+    S = ld if S is None else S
+    dev = demand.device
+    if want_cost and cost is None:
+        cost = torch.empty((T, S), dtype=torch.int32, device=dev)
+    if want_partial and partial is None:
+        partial = torch.zeros((T, 6), dtype=torch.int64, device=dev)
+    ws = workspace(int(_lib.spdp_neighbour_workspace_bytes(n, S, T)), dev, tag="nbr")
+    _check(_lib.spdp_split_eval_neighbours(_dev_ptr(parent, "parent"), _dev_ptr(fwd, "fwd"), _dev_ptr(bwd, "bwd"),
+                                           _dev_ptr(tours, "tours"), T, _dev_ptr(dist, "dist"), n,
+                                           _dev_ptr(demand, "demand"), ld, S, int(Q),
+                                           _dev_ptr(cost, "cost") if want_cost else None,
+                                           _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
+                                           ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_VALIDATE if validate else 0,
+                                           _stream(dev)), "spdp_split_eval_neighbours")
     return cost, partial
 
 

@@ -1,0 +1,367 @@
+// nbr.cu -- f3: prefix / suffix split values of a parent tour and
+// the evaluation of candidate tours that share a prefix and a suffix with it
+// (the neighbourhood evaluation behind the paper's "explore many more candidate
+// first-stage tours"; DESIGN R23).
+//
+// Values of one tour sigma (the definitions: Split of every prefix / suffix):
+//   f(i) = Split(sigma_1..sigma_i),  b(i) = Split(sigma_{i+1}..sigma_n).
+// With the separable route cost t(p, i) = A[p] + B[i] (split.cu):
+//   f(i) = B[i] + min_{p in [mask(i), i-1]} f(p) + A[p]            (Eq. (3))
+//   b(i) = A[i] + min_{j in [i+1, maxj(i)]} b(j) + B[j]            (the mirror)
+// with maxj(i) = max{j : sum_{k=i+1}^{j} q <= Q}.
+//
+// A candidate tour that agrees with the parent on positions 1..a and s0+1..n
+// (a < s0, 1-based) has f(p) = f_parent(p) for p <= a and b(i) = b_parent(i) for
+// i >= s0, and every split of it has a route boundary in [s0, E] where E is the
+// last layer a route starting before s0 can reach (the load of positions
+// s0..E+1 exceeds Q, or E = n).  So
+//   cost = min_{i in [s0, E]} f(i) + b_parent(i),
+// where f(i) for i = a+1..E comes from the Eq. (3) sweep restarted at layer a+1
+// on a ring seeded with f_parent(a-W+1..a) -- O(s0 - a + window) layers instead of n.
+#include <climits>
+
+#include "common.cuh"
+#include "split_ws.cuh"
+
+namespace spdp {
+
+// Per-tour position table e[i], i = 0..n:  {row of customer sigma_i (i >= 1), A[i] (i < n),
+// B[i] (i >= 1), 0}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
+// D[1] = 0, D[i] = D[i-1] + c_{s_{i-1},s_i}.
+// info[t] = {a, s0, 0, 0}: a = common prefix length with the parent, s0 = n - common suffix
+// length (a = s0 = n: the tour equals the parent).  One warp per tour.
+__global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict__ tours, const int32_t* __restrict__ parent,
+                                                      int n, const int32_t* __restrict__ dist, int4* __restrict__ etabs,
+                                                      int4* __restrict__ info) {
+    const int t = blockIdx.x, lane = threadIdx.x;
+    const int32_t* tour = tours + (int64_t)t * n;
+    int4* e = etabs + (int64_t)t * (n + 1);
+    const int64_t N1 = (int64_t)n + 1;
+    auto node = [&](int i) -> int {  // customer at 0-based position i, clamped to 1..n
+        const int c = tour[i];
+        return c < 1 ? 1 : (c > n ? n : c);
+    };
+    long long carry = 0;  // D at the chunk's first position
+    for (int b = 0; b < n; b += 32) {
+        const int i = b + lane;  // 0-based position i = 1-based i + 1
+        const int c = i < n ? node(i) : 1;
+        const int arc = (i + 1 < n) ? dist[(int64_t)c * N1 + node(i + 1)] : 0;
+        long long incl = arc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long u = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += u;
+        }
+        const long long D = carry + incl - arc;  // D[i+1]
+        if (i < n) {
+            int4 v;
+            v.x = c - 1;
+            v.y = (i + 1 < n) ? (int)(dist[node(i + 1)] - (D + arc)) : 0;  // A[i+1] = c_{0,s_{i+2}} - D[i+2]
+            v.z = (int)(D + dist[(int64_t)c * N1]);                          // B[i+1]
+            v.w = 0;
+            e[i + 1] = v;
+        }
+        carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) e[0] = make_int4(0, dist[node(0)], 0, 0);  // A[0] = c_{0,s_1}
+    if (parent && info) {
+        int a = n, last = -1;
+        for (int b = 0; b < n; b += 32) {
+            const int i = b + lane;
+            const unsigned mm = __ballot_sync(kFull, i < n && tour[i] != parent[i]);
+            if (mm) {
+                a = b + __ffs(mm) - 1;
+                break;
+            }
+        }
+        for (int b = n - 1; b >= 0 && a < n; b -= 32) {
+            const int i = b - lane;
+            const unsigned mm = __ballot_sync(kFull, i >= 0 && tour[i] != parent[i]);
+            if (mm) {
+                last = b - (__ffs(mm) - 1);
+                break;
+            }
+        }
+        if (lane == 0) info[t] = make_int4(a, a < n ? last + 1 : n, 0, 0);
+    }
+}
+
+// f and b of one tour, one scenario per thread: two-pointer masks (PAPER:120-127 and
+// its mirror), window minima read back from the thread's own rows of fwd / bwd
+// ([n+1][S], coalesced across the warp).  Any window width.  INF = SPDP_INFEASIBLE
+// where the prefix / suffix holds a demand above Q (DESIGN R4).
+__global__ void __launch_bounds__(256) split_values_kernel(const int4* __restrict__ e, int n,
+                                                           const uint16_t* __restrict__ demand, int64_t ld, int64_t S,
+                                                           int Q, int32_t* fwd, int32_t* bwd) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const uint16_t* dcol = demand + s;
+    int32_t* fc = fwd + s;
+    int32_t* bc = bwd + s;
+    auto q_at = [&](int i) -> int { return dcol[(int64_t)__ldg(&e[i].x) * ld]; };  // q of position i >= 1
+    // forward: f(i) = B[i] + min_{p in [m, i-1]} f(p) + A[p], m = mask(i)
+    fc[0] = 0;
+    {
+        int P = 0, Pm = 0, m = 0;
+        bool bad = false;
+        for (int i = 1; i <= n; ++i) {
+            const int4 ei = __ldg(&e[i]);
+            const int q = dcol[(int64_t)ei.x * ld];
+            bad |= q > Q;
+            if (bad) {
+                fc[(int64_t)i * S] = SPDP_INFEASIBLE;
+                continue;
+            }
+            P += q;
+            while (P - Pm > Q) Pm += q_at(++m);  // P(m) = sum_{k<=m} q; stops at m <= i-1 (q <= Q)
+            int best = INT_MAX;
+            for (int p = m; p < i; ++p) best = min(best, fc[(int64_t)p * S] + __ldg(&e[p].y));
+            fc[(int64_t)i * S] = best + ei.z;
+        }
+    }
+    // backward: b(i) = A[i] + min_{j in [i+1, M]} b(j) + B[j], M = maxj(i); R(i) = sum_{k>i} q
+    bc[(int64_t)n * S] = 0;
+    {
+        int R = 0, RM = 0, M = n;
+        bool bad = false;
+        for (int i = n - 1; i >= 0; --i) {
+            const int q = q_at(i + 1);
+            bad |= q > Q;
+            if (bad) {
+                bc[(int64_t)i * S] = SPDP_INFEASIBLE;
+                continue;
+            }
+            R += q;
+            while (R - RM > Q) RM += q_at(M--);  // R(M-1) = R(M) + q(M); stops at M >= i+1
+            int best = INT_MAX;
+            for (int j = i + 1; j <= M; ++j) best = min(best, bc[(int64_t)j * S] + __ldg(&e[j].z));
+            bc[(int64_t)i * S] = best + __ldg(&e[i].y);
+        }
+    }
+}
+
+// The restarted sweep: one scenario per thread, one candidate tour per blockIdx.y.
+// Ring of the last W split points p (slot (p - a - 1) mod W): {G = f(p) + A[p],
+// Y = P(p) + Q} with P relative to P(a) = 0; p is in the window of layer i iff
+// Y >= P(i).  Seeded from the parent's f(a-W+1..a).  Demands and b_parent of the
+// next kNbrPf layers are prefetched into static register slots.  A lane whose
+// window reaches past the ring is appended to the overflow list (finished from
+// scratch by split_finish_kernel on the candidate's own tables).
+constexpr int kNbrThreads = 128;
+constexpr int kNbrPf = 8;
+
+template <int W>
+__global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
+    const int4* __restrict__ etabs, const int4* __restrict__ info, int n, const uint16_t* __restrict__ demand,
+    int64_t ld, int64_t S, int Q, const int32_t* __restrict__ fwd, const int32_t* __restrict__ bwd,
+    int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots, unsigned long long* __restrict__ ovf_list,
+    unsigned* __restrict__ ovf_count) {
+    static_assert(W % kNbrPf == 0, "the prefetch distance must divide the ring");
+    __shared__ Part red[kNbrThreads / 32];
+    const int t = blockIdx.y;
+    const int4 in = info[t];
+    const int a = in.x, s0 = in.y;
+    const int4* e = etabs + (int64_t)t * (n + 1);
+    const int64_t s = (int64_t)blockIdx.x * kNbrThreads + threadIdx.x;
+    const bool live = s < S;
+    const int64_t col = live ? s : S - 1;
+    const int32_t* fcol = fwd + col;
+    const int32_t* bcol = bwd + col;
+    const uint16_t* dcol = demand + col;
+    const int pc = fcol[(int64_t)n * S];  // the parent's cost: same customers, same feasibility (R4)
+    int result = pc;
+    bool ovf = false;
+    if (a < n) {  // (a, s0 are uniform per CTA; every lane enters: the loop votes over the full warp)
+        int G[W], Y[W];
+        {
+            int P = 0;  // P(p) - P(a), walking p down from a
+#pragma unroll
+            for (int k = 1; k <= W; ++k) {
+                const int p = a + 1 - k;
+                if (p >= 0) {
+                    const int4 ep = __ldg(&e[p]);
+                    G[W - k] = fcol[(int64_t)p * S] + ep.y;
+                    Y[W - k] = P + Q;
+                    if (p >= 1) P -= dcol[(int64_t)ep.x * ld];
+                } else {
+                    G[W - k] = INT_MAX;
+                    Y[W - k] = INT_MIN;  // never in a window
+                }
+            }
+        }
+        int qb[kNbrPf], bb[kNbrPf];
+#pragma unroll
+        for (int k = 0; k < kNbrPf; ++k) {
+            const int i = a + 1 + k;
+            qb[k] = 0;
+            bb[k] = 0;
+            if (i <= n) {
+                qb[k] = dcol[(int64_t)__ldg(&e[i].x) * ld];
+                if (i >= s0) bb[k] = bcol[(int64_t)i * S];
+            }
+        }
+        int P = 0, Ps = 0;  // P(i) and P(s0 - 1) (= P(a) when s0 - 1 == a)
+        int total = INT_MAX;
+        bool active = pc != SPDP_INFEASIBLE;  // an infeasible scenario only follows the warp
+        for (int base = a + 1;; base += W) {
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const int i = base + j;
+                if (i > n) break;  // warp-uniform
+                const int4 ei = __ldg(&e[i]);
+                const int q = qb[j % kNbrPf];
+                const int bv = bb[j % kNbrPf];
+                const int ia = i + kNbrPf;
+                if (ia <= n) {
+                    qb[j % kNbrPf] = dcol[(int64_t)__ldg(&e[ia].x) * ld];
+                    if (ia >= s0) bb[j % kNbrPf] = bcol[(int64_t)ia * S];
+                }
+                const int Pn = P + q;
+                // no route starting before s0 reaches layer i: the boundary set [s0, i-1] is complete
+                if (i > s0 && Pn - Ps > Q) active = false;
+                int best = G[(j - 1 + W) % W];  // age 1: always in the window (q <= Q)
+#pragma unroll
+                for (int k0 = 2; k0 <= W; k0 += 4) {
+                    if (!__any_sync(kFull, active && Y[(j - k0 + W) % W] >= Pn)) break;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int k = k0 + v;
+                        if (k <= W) {
+                            const int sl = (j - k + W) % W;
+                            if (Y[sl] >= Pn) best = min(best, G[sl]);
+                        }
+                    }
+                }
+                // age W (slot j) in the window and an older split point exists: past the ring
+                if (active && Y[j] >= Pn && i - W >= 1) ovf = true;
+                if (active && i >= s0) total = min(total, best + ei.z + bv);
+                G[j] = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
+                Y[j] = Pn + Q;
+                if (i == s0 - 1) Ps = Pn;
+                P = Pn;
+            }
+            if (base + W > n || !__any_sync(kFull, active && !ovf)) break;
+        }
+        result = pc == SPDP_INFEASIBLE ? pc : total;
+    }
+    const bool deferred = live && ovf;
+    if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
+    if (cost && live && !deferred) cost[(int64_t)t * S + s] = result;
+    if (slots) {
+        Part p{0, 0, 0, 0, 0};
+        if (live && !deferred) part_add_cost(p, result, result != SPDP_INFEASIBLE);
+        const Part r = block_sum(p, red);
+        if (threadIdx.x == 0) {
+            spdp_saa_partial* d = &slots[(int64_t)t * kSlots + (blockIdx.x % kSlots)];
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)r.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)r.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)r.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)r.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)r.sq_hi);
+        }
+    }
+}
+
+static size_t etab_bytes(int32_t n, int32_t T) { return align_up(sizeof(int4) * (size_t)T * (size_t)(n + 1), 256); }
+
+static spdp_status check_common(const char* fn, int32_t n, int64_t S, int32_t Q, int64_t ld, const void* demand) {
+    if (n < 1) return fail(SPDP_E_USAGE, "%s: n=%d < 1", fn, n);
+    if (n > SPDP_MAX_N) return fail(SPDP_E_RESOURCE, "%s: n=%d > SPDP_MAX_N=%d", fn, n, SPDP_MAX_N);
+    if (S < 1) return fail(SPDP_E_USAGE, "%s: S=%lld < 1", fn, (long long)S);
+    if (S >= (1LL << 40)) return fail(SPDP_E_RESOURCE, "%s: S too large", fn);
+    if (Q < 1) return fail(SPDP_E_USAGE, "%s: Q=%d < 1 (SPEC:34)", fn, Q);
+    if (ld < S || (ld % 8) != 0) return fail(SPDP_E_USAGE, "%s: ld=%lld must be >= S and a multiple of 8", fn, (long long)ld);
+    if (((uintptr_t)demand & 15u) != 0) return fail(SPDP_E_USAGE, "%s: demand must be 16-byte aligned", fn);
+    return SPDP_OK;
+}
+
+}  // namespace spdp
+
+using namespace spdp;
+
+extern "C" size_t spdp_values_workspace_bytes(int32_t n) {
+    if (n < 1) return 0;
+    return etab_bytes(n, 1);
+}
+
+extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dist, int32_t n, const uint16_t* demand,
+                                         int64_t ld, int64_t S, int32_t Q, int32_t* fwd, int32_t* bwd, void* ws,
+                                         size_t ws_bytes, spdp_stream_t stream) {
+    const char* fn = "spdp_split_values";
+    spdp_status rc = check_common(fn, n, S, Q, ld, demand);
+    if (rc) return rc;
+    if (!tour || !dist || !demand || !fwd || !bwd || !ws) return fail(SPDP_E_USAGE, "%s: NULL required pointer", fn);
+    if (ws_bytes < spdp_values_workspace_bytes(n)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
+    cudaStream_t st = (cudaStream_t)stream;
+    int4* e = static_cast<int4*>(ws);
+    nbr_prep_kernel<<<1, 32, 0, st>>>(tour, nullptr, n, dist, e, nullptr);
+    if ((rc = last_launch("nbr_prep_kernel"))) return rc;
+    // Q above the largest possible load behaves as "everything fits"; clamp so sums stay in int32
+    const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
+    prof_begin(st);
+    split_values_kernel<<<(unsigned)ceil_div(S, 256), 256, 0, st>>>(e, n, demand, ld, S, Qe, fwd, bwd);
+    prof_end(st);
+    set_last_kernel("split_values_kernel");
+    return last_launch("split_values_kernel");
+}
+
+extern "C" size_t spdp_neighbour_workspace_bytes(int32_t n, int64_t S, int32_t T) {
+    if (n < 1 || S < 1 || T < 1) return 0;
+    return ws_layout(n, S, T).total + etab_bytes(n, T) + align_up(sizeof(int4) * (size_t)T, 256);
+}
+
+template <int W>
+static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info, int n, const uint16_t* demand,
+                                int64_t ld, int64_t S, int T, int Q, const int32_t* fwd, const int32_t* bwd,
+                                int32_t* cost, spdp_saa_partial* slots, unsigned long long* ovf, unsigned* ovf_count) {
+    prof_begin(st);
+    split_nbr_kernel<W><<<dim3((unsigned)ceil_div(S, kNbrThreads), (unsigned)T), kNbrThreads, 0, st>>>(
+        e, info, n, demand, ld, S, Q, fwd, bwd, cost, slots, ovf, ovf_count);
+    prof_end(st);
+    set_last_kernel("split_nbr_kernel<%d>", W);
+    return last_launch("split_nbr_kernel");
+}
+
+extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int32_t* fwd, const int32_t* bwd,
+                                                  const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,
+                                                  const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                                                  int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
+                                                  void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream) {
+    const char* fn = "spdp_split_eval_neighbours";
+    spdp_status rc = check_common(fn, n, S, Q, ld, demand);
+    if (rc) return rc;
+    if (T < 1) return fail(SPDP_E_USAGE, "%s: T=%d < 1", fn, T);
+    if (T >= 65536) return fail(SPDP_E_RESOURCE, "%s: T=%d >= 65536", fn, T);
+    if (window_hint < 0) return fail(SPDP_E_USAGE, "%s: window_hint < 0", fn);
+    if (!parent || !fwd || !bwd || !tours || !dist || !demand || !ws)
+        return fail(SPDP_E_USAGE, "%s: NULL required pointer", fn);
+    if (ws_bytes < spdp_neighbour_workspace_bytes(n, S, T)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
+    cudaStream_t st = (cudaStream_t)stream;
+    const WsLayout L = ws_layout(n, S, T);
+    char* w = static_cast<char*>(ws);
+    int4* e = reinterpret_cast<int4*>(w + L.total);
+    int4* info = reinterpret_cast<int4*>(w + L.total + etab_bytes(n, T));
+    const bool validate = (flags & SPDP_F_VALIDATE) != 0;
+    unsigned* hdr = reinterpret_cast<unsigned*>(w + L.hdr);
+    if (validate && (rc = cuda_check(cudaMemsetAsync(hdr, 0, 256, st), "cudaMemsetAsync(hdr)"))) return rc;
+    // the candidates' own tables (for the overflow path) + zeroed SAA slots / partials
+    if ((rc = launch_tour_prep(tours, T, n, dist, demand, ld, w, L, partial, partial != nullptr, validate, st))) return rc;
+    if (validate) {
+        unsigned h[2];
+        if ((rc = cuda_check(cudaMemcpyAsync(h, hdr, sizeof(h), cudaMemcpyDeviceToHost, st), "memcpy(hdr)"))) return rc;
+        if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
+        if (h[HDR_STATUS]) return fail(SPDP_E_DATA, "%s: invalid candidate tour or costs (status %u)", fn, h[HDR_STATUS]);
+    }
+    nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parent, n, dist, e, info);
+    if ((rc = last_launch("nbr_prep_kernel"))) return rc;
+    const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
+    spdp_saa_partial* slots = partial ? reinterpret_cast<spdp_saa_partial*>(w + L.slots) : nullptr;
+    unsigned long long* ovf = reinterpret_cast<unsigned long long*>(w + L.ovf);
+    unsigned* ovf_count = hdr + HDR_OVF_COUNT;
+    const int W = window_hint == 0 ? 32 : (window_hint <= 16 ? 16 : (window_hint <= 24 ? 24 : 32));
+    if (W == 16) rc = launch_nbr_t<16>(st, e, info, n, demand, ld, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    else if (W == 24) rc = launch_nbr_t<24>(st, e, info, n, demand, ld, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    else rc = launch_nbr_t<32>(st, e, info, n, demand, ld, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    if (rc) return rc;
+    return launch_finish(w, L, T, n, demand, ld, S, (uint32_t)Qe, cost, partial, false, st);
+}

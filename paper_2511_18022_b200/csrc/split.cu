@@ -23,46 +23,9 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "split_ws.cuh"
 
 namespace spdp {
-
-// ---------------------------------------------------------------- workspace
-// Per-tour info for the fp32 sweep: g0f = (g(0) + OFF) / 2^24 (float bits),
-// off = OFF = D[n] (makes every g(p) + OFF >= 0), ok = every value the fp32
-// sweep forms is an integer (times 2^-24) below 2^24, hence exact.
-struct TourInfo {
-    int32_t g0f_bits, off, ok, pad;
-};
-
-constexpr int kTabPad = 64;       // padding rows after each tour table
-constexpr int kSlots = 32;  // SAA partial slots per tour (spread the sweep's atomics)
-
-// Cg planes: per tour [2][cg_stride(n)] int32 (plane 0 int Cg, plane 1 fp32 Cg / 2^24 bits), zero padded;
-// the stride keeps every chunk's W-entry slice 16-byte aligned for the bulk copies.
-__host__ __device__ inline int cg_stride(int n) { return (n + kTabPad + 7) & ~7; }
-
-struct WsLayout {
-    size_t hdr, g0, tinfo, tabs, rowp, cgs, slots, ovf, total;
-};
-
-inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
-    WsLayout L;
-    size_t off = 0;
-    L.hdr = off; off += 256;
-    L.g0 = off; off = align_up(off + sizeof(int32_t) * (size_t)T, 256);
-    L.tinfo = off; off = align_up(off + sizeof(TourInfo) * (size_t)T, 256);
-    L.tabs = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
-    L.rowp = off; off = align_up(off + sizeof(uint64_t) * (size_t)T * (size_t)(n + kTabPad), 256);
-    L.cgs = off; off = align_up(off + sizeof(int32_t) * 2 * (size_t)T * (size_t)cg_stride(n), 256);
-    L.slots = off; off = align_up(off + sizeof(spdp_saa_partial) * (size_t)T * (size_t)kSlots, 256);
-    L.ovf = off; off = align_up(off + sizeof(unsigned long long) * (size_t)T * (size_t)S, 256);
-    L.total = off;
-    return L;
-}
-
-// header words
-enum { HDR_OVF_COUNT = 0, HDR_STATUS = 1, HDR_SAMPLE_W = 2, HDR_TILE = 3, HDR_SAMPLE_SUM = 4 /* u64 */, HDR_SAMPLE_CNT = 6 };
-enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
 
 // ---------------------------------------------------------------- a2: tour prep
 // One CTA per tour.  tab[i] = {row of customer s_{i+1}, Cg[i]} (0-based layer i
@@ -1628,14 +1591,8 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         rc = cuda_check(cudaMemsetAsync(hdr, 0, 256, st), "cudaMemsetAsync(hdr)");
         if (rc) return rc;
     }
-    {
-        const int threads = n >= 2048 ? 1024 : 256;
-        const size_t smem = 34 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
-        tour_prep_kernel<<<T, threads, smem, st>>>(tours, n, dist, tabs, g0, demand, ld, rowp, tinfo,
-                                                   reinterpret_cast<int32_t*>(w + L.cgs), partial ? slots : nullptr, hdr,
-                                                   partial, validate ? 1 : 0);
-        if ((rc = last_launch("tour_prep_kernel"))) return rc;
-    }
+    if ((rc = launch_tour_prep(tours, T, n, dist, demand, ld, w, L, partial, partial != nullptr, validate, st)))
+        return rc;
     int W = pick_w(window_hint);
     int mean_w = (int)((flags >> SPDP_F_MEAN_WINDOW_SHIFT) & 0xffu);  // expected mean window (0: unknown)
     if (validate || window_hint == 0) {
@@ -1660,7 +1617,6 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
                 mean_w = (int)((wsum + (unsigned long long)h[HDR_SAMPLE_CNT] * n / 2) / ((unsigned long long)h[HDR_SAMPLE_CNT] * n));
         }
     }
-    unsigned* ovf_count = hdr + HDR_OVF_COUNT;
     const SweepArgs args{rowp, tabs, reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
                          cost, partial ? slots : nullptr, ovf, hdr};
     // fp32 sweep when every load value it forms (P' <= (n + W) min(Q, 65535) for feasible scenarios
@@ -1710,26 +1666,49 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     if (mode == 3 || (mode == 0 && (W > 32 || mean_w >= 12))) rc = launch_deque(st, args);
     else rc = launch_sweep(W, use_f32, st, args, mean_w);
     if (rc) return rc;
-    {
-        // finish: per-tour SAA partials + the overflow list (warps per CTA limited by 8 (n+1) bytes of smem each)
-        // finish: the SAA partials + the overflow list (one thread per scenario; 4 warps per CTA,
-        // each with 12 (n+1) B of shared scratch for the rare windows wider than kOvfW)
-        const size_t per_warp = 3 * sizeof(int) * (size_t)(n + 1);
-        const int warps = per_warp * 4 <= 192 * 1024 ? 4 : 1;
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaError_t e = cudaFuncSetAttribute(split_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_finish)");
-            attr_set = true;
-        }
-        rc = cuda_check(launch_pdl(split_finish_kernel, dim3(4 * num_sms()), dim3(warps * 32), per_warp * warps, st,
-                                   partial ? slots : nullptr, (int)kSlots, T, (const int2*)tabs, (const int32_t*)g0, n,
-                                   demand, ld, S, Qe, cost, partial, (const unsigned long long*)ovf,
-                                   (const unsigned*)ovf_count),
-                        "split_finish_kernel");
-        if (rc) return rc;
+    return launch_finish(w, L, T, n, demand, ld, S, Qe, cost, partial, true, st);
+}
+
+spdp_status launch_tour_prep(const int32_t* tours, int32_t T, int32_t n, const int32_t* dist,
+                             const uint16_t* demand, int64_t ld, char* w, const WsLayout& L,
+                             spdp_saa_partial* partial, bool zero_slots, bool validate, cudaStream_t st) {
+    const int threads = n >= 2048 ? 1024 : 256;
+    const size_t smem = 34 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
+    tour_prep_kernel<<<T, threads, smem, st>>>(
+        tours, n, dist, reinterpret_cast<int2*>(w + L.tabs), reinterpret_cast<int32_t*>(w + L.g0), demand, ld,
+        reinterpret_cast<const uint16_t**>(w + L.rowp), reinterpret_cast<TourInfo*>(w + L.tinfo),
+        reinterpret_cast<int32_t*>(w + L.cgs), zero_slots ? reinterpret_cast<spdp_saa_partial*>(w + L.slots) : nullptr,
+        reinterpret_cast<unsigned*>(w + L.hdr), partial, validate ? 1 : 0);
+    return last_launch("tour_prep_kernel");
+}
+
+spdp_status launch_finish(char* w, const WsLayout& L, int32_t T, int32_t n, const uint16_t* demand, int64_t ld,
+                          int64_t S, uint32_t Qe, int32_t* cost, spdp_saa_partial* partial, bool pdl,
+                          cudaStream_t st) {
+    // the SAA partials + the overflow list (one thread per scenario; 4 warps per CTA,
+    // each with 12 (n+1) B of shared scratch for the rare windows wider than kOvfW)
+    const size_t per_warp = 3 * sizeof(int) * (size_t)(n + 1);
+    const int warps = per_warp * 4 <= 192 * 1024 ? 4 : 1;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(split_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_finish)");
+        attr_set = true;
     }
-    return SPDP_OK;
+    const spdp_saa_partial* slots = partial ? reinterpret_cast<const spdp_saa_partial*>(w + L.slots) : nullptr;
+    const int2* tabs = reinterpret_cast<const int2*>(w + L.tabs);
+    const int32_t* g0 = reinterpret_cast<const int32_t*>(w + L.g0);
+    const unsigned long long* ovf = reinterpret_cast<const unsigned long long*>(w + L.ovf);
+    const unsigned* ovf_count = reinterpret_cast<const unsigned*>(w + L.hdr) + HDR_OVF_COUNT;
+    if (pdl)
+        return cuda_check(launch_pdl(split_finish_kernel, dim3(4 * num_sms()), dim3(warps * 32), per_warp * warps, st,
+                                     slots, (int)kSlots, (int)T, tabs, g0, (int)n, demand, ld, S, Qe, cost, partial, ovf,
+                                     ovf_count),
+                          "split_finish_kernel");
+    split_finish_kernel<<<4 * num_sms(), warps * 32, per_warp * warps, st>>>(slots, (int)kSlots, (int)T, tabs, g0, (int)n,
+                                                                             demand, ld, S, Qe, cost, partial, ovf,
+                                                                             ovf_count);
+    return last_launch("split_finish_kernel");
 }
 
 }  // namespace spdp

@@ -1,0 +1,60 @@
+// split_ws.cuh -- the split workspace layout and the host-side launchers of
+// split.cu that other translation units (nbr.cu, limits.cu) reuse.
+#pragma once
+
+#include "common.cuh"
+
+namespace spdp {
+
+// ---------------------------------------------------------------- workspace
+// Per-tour info for the fp32 sweep: g0f = (g(0) + OFF) / 2^24 (float bits),
+// off = OFF = D[n] (makes every g(p) + OFF >= 0), ok = every value the fp32
+// sweep forms is an integer (times 2^-24) below 2^24, hence exact.
+struct TourInfo {
+    int32_t g0f_bits, off, ok, pad;
+};
+
+constexpr int kTabPad = 64;       // padding rows after each tour table
+constexpr int kSlots = 32;  // SAA partial slots per tour (spread the sweep's atomics)
+
+// Cg planes: per tour [2][cg_stride(n)] int32 (plane 0 int Cg, plane 1 fp32 Cg / 2^24 bits), zero padded;
+// the stride keeps every chunk's W-entry slice 16-byte aligned for the bulk copies.
+__host__ __device__ inline int cg_stride(int n) { return (n + kTabPad + 7) & ~7; }
+
+struct WsLayout {
+    size_t hdr, g0, tinfo, tabs, rowp, cgs, slots, ovf, total;
+};
+
+inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
+    WsLayout L;
+    size_t off = 0;
+    L.hdr = off; off += 256;
+    L.g0 = off; off = align_up(off + sizeof(int32_t) * (size_t)T, 256);
+    L.tinfo = off; off = align_up(off + sizeof(TourInfo) * (size_t)T, 256);
+    L.tabs = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
+    L.rowp = off; off = align_up(off + sizeof(uint64_t) * (size_t)T * (size_t)(n + kTabPad), 256);
+    L.cgs = off; off = align_up(off + sizeof(int32_t) * 2 * (size_t)T * (size_t)cg_stride(n), 256);
+    L.slots = off; off = align_up(off + sizeof(spdp_saa_partial) * (size_t)T * (size_t)kSlots, 256);
+    L.ovf = off; off = align_up(off + sizeof(unsigned long long) * (size_t)T * (size_t)S, 256);
+    L.total = off;
+    return L;
+}
+
+// header words
+enum { HDR_OVF_COUNT = 0, HDR_STATUS = 1, HDR_SAMPLE_W = 2, HDR_TILE = 3, HDR_SAMPLE_SUM = 4 /* u64 */, HDR_SAMPLE_CNT = 6 };
+enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
+
+// Host launchers (split.cu).
+// tour_prep_kernel over T tours into the workspace (tables, g0, row pointers, Cg
+// planes; zeroes the SAA slots (if zero_slots), partial[0..T) (if non-NULL) and
+// the overflow counter).
+spdp_status launch_tour_prep(const int32_t* tours, int32_t T, int32_t n, const int32_t* dist,
+                             const uint16_t* demand, int64_t ld, char* ws, const WsLayout& L,
+                             spdp_saa_partial* partial, bool zero_slots, bool validate, cudaStream_t st);
+// split_finish_kernel: SAA slots -> partial, then the overflow list (full
+// recomputation of every listed (tour, scenario) pair from the tour tables).
+spdp_status launch_finish(char* ws, const WsLayout& L, int32_t T, int32_t n, const uint16_t* demand, int64_t ld,
+                          int64_t S, uint32_t Qe, int32_t* cost, spdp_saa_partial* partial, bool pdl,
+                          cudaStream_t st);
+
+}  // namespace spdp
