@@ -477,6 +477,48 @@ def measure_rows(spdp, torch, dev, pk):
             "ms": ms, "evals_per_s": cfg["T"] * cfg["S"] / (ms / 1e3), "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
             "candidates_est": cand, "alu_frac_est": cand / (ms / 1e3) / alu_peak}
         del d
+    # f3: the C3 population evaluated from tour 0's prefix / suffix values (spdp_split_values once,
+    # then spdp_split_eval_neighbours over the 256 candidates): same costs as a8, fewer layers
+    cfg = synth.config_instance("C3")
+    inst = cfg["inst"]
+    d = spdp.gen_demands(cfg["model"], 0, cfg["S"], device=dev)
+    tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
+    parent = tours[0].contiguous()
+    dist = torch.from_numpy(inst["dist"]).to(dev)
+    part = torch.zeros((cfg["T"], 6), dtype=torch.int64, device=dev)
+    fwd = torch.empty((cfg["n"] + 1, cfg["S"]), dtype=torch.int32, device=dev)
+    bwd = torch.empty_like(fwd)
+    h = bench_config.HINT["C3"]
+    ms_v = _time_events(lambda: spdp.split_values(parent, dist, d, inst["Q"], S=cfg["S"], fwd=fwd, bwd=bwd),
+                        torch, dev, iters=6)
+    ms_n = _time_events(lambda: spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, d, inst["Q"], S=cfg["S"],
+                                                           want_cost=False, partial=part, window_hint=h),
+                        torch, dev, iters=6)
+    _, bpart = spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h)
+    equal_c3 = bool(torch.equal(part, bpart))
+    def span(tt):
+        return float(np.mean([0 if (tt[k] == tt[0]).all() else
+                              int(np.nonzero(tt[k] != tt[0])[0][-1] - np.nonzero(tt[k] != tt[0])[0][0] + 1)
+                              for k in range(len(tt))]))
+    # the same 256 x 10^5 evaluation for a granular population (one move of radius <= 10 per candidate)
+    lt = synth.local_move_tours(inst["tour"], cfg["T"], 400)
+    ltours = torch.from_numpy(lt).to(dev)
+    ms_nl = _time_events(lambda: spdp.split_eval_neighbours(parent, fwd, bwd, ltours, dist, d, inst["Q"], S=cfg["S"],
+                                                            want_cost=False, partial=part, window_hint=h),
+                         torch, dev, iters=6)
+    kern = spdp.last_kernel()
+    ms_bl = _time_events(lambda: spdp.split_eval_batch(ltours, dist, d, inst["Q"], S=cfg["S"], want_cost=False,
+                                                       window_hint=h, mean_window=bench_config.MEAN["C3"]),
+                         torch, dev, iters=6)
+    _, lpart = spdp.split_eval_batch(ltours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h)
+    rows["f3_neighbours_C3"] = {
+        "ms": ms_v + ms_n, "values_ms": ms_v, "neighbours_ms": ms_n, "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
+        "evals_per_s": cfg["T"] * cfg["S"] / ((ms_v + ms_n) / 1e3), "mean_changed_span": span(cfg["tours"]),
+        "partials_equal_batch": equal_c3, "kernel": kern,
+        "granular": {"neighbours_ms": ms_nl, "ms": ms_v + ms_nl, "batch_ms": ms_bl, "mean_changed_span": span(lt),
+                     "evals_per_s": cfg["T"] * cfg["S"] / ((ms_v + ms_nl) / 1e3),
+                     "partials_equal_batch": bool(torch.equal(part, lpart))}}
+    del d, fwd, bwd
     # f2: penalized split at C2 (lambda = 10 cost units per unit of overload, Q of C2)
     cfg2 = synth.config_instance("C2")
     inst2 = cfg2["inst"]

@@ -26,13 +26,13 @@
 namespace spdp {
 
 // Per-tour position table e[i], i = 0..n:  {row of customer sigma_i (i >= 1), A[i] (i < n),
-// B[i] (i >= 1), 0}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
+// B[i] (i >= 1), row * ld as a uint32 element offset (used when n ld < 2^32)}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
 // D[1] = 0, D[i] = D[i-1] + c_{s_{i-1},s_i}.
 // info[t] = {a, s0, 0, 0}: a = common prefix length with the parent, s0 = n - common suffix
 // length (a = s0 = n: the tour equals the parent).  One warp per tour.
 __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict__ tours, const int32_t* __restrict__ parent,
-                                                      int n, const int32_t* __restrict__ dist, int4* __restrict__ etabs,
-                                                      int4* __restrict__ info) {
+                                                      int n, const int32_t* __restrict__ dist, int64_t ld,
+                                                      int4* __restrict__ etabs, int4* __restrict__ info) {
     const int t = blockIdx.x, lane = threadIdx.x;
     const int32_t* tour = tours + (int64_t)t * n;
     int4* e = etabs + (int64_t)t * (n + 1);
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict_
             v.x = c - 1;
             v.y = (i + 1 < n) ? (int)(dist[node(i + 1)] - (D + arc)) : 0;  // A[i+1] = c_{0,s_{i+2}} - D[i+2]
             v.z = (int)(D + dist[(int64_t)c * N1]);                          // B[i+1]
-            v.w = 0;
+            v.w = (int)(uint32_t)((uint64_t)(c - 1) * (uint64_t)ld);  // element offset of the row (n ld < 2^32)
             e[i + 1] = v;
         }
         carry += __shfl_sync(kFull, incl, 31);
@@ -140,35 +140,50 @@ __global__ void __launch_bounds__(256) split_values_kernel(const int4* __restric
     }
 }
 
-// The restarted sweep: one scenario per thread, one candidate tour per blockIdx.y.
+// The restarted sweep: one scenario per thread, one candidate tour per blockIdx.x.
 // Ring of the last W split points p (slot (p - a - 1) mod W): {G = f(p) + A[p],
 // Y = P(p) + Q} with P relative to P(a) = 0; p is in the window of layer i iff
-// Y >= P(i).  Seeded from the parent's f(a-W+1..a).  Demands and b_parent of the
-// next kNbrPf layers are prefetched into static register slots.  A lane whose
-// window reaches past the ring is appended to the overflow list (finished from
-// scratch by split_finish_kernel on the candidate's own tables).
+// Y >= P(i).  Seeded from the parent's f(a-W+1..a).  The candidate's position
+// table sits in shared memory (SM) or is read through L1; demands and b_parent of
+// the next kNbrPf layers are prefetched into static register slots (addresses:
+// one 32-bit multiply-add from the table's row offset / the layer index).  Ages
+// 2..kNbrU0+1 are scanned unconditionally, then groups of 4 behind a warp vote.
+// A lane whose window reaches past the ring is appended to the overflow list
+// (finished from scratch by split_finish_kernel on the candidate's own tables).
 constexpr int kNbrThreads = 128;
 constexpr int kNbrPf = 8;
+constexpr int kNbrU0 = 8;
 
-template <int W>
+template <int W, bool SM>
 __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
     const int4* __restrict__ etabs, const int4* __restrict__ info, int n, const uint16_t* __restrict__ demand,
-    int64_t ld, int64_t S, int Q, const int32_t* __restrict__ fwd, const int32_t* __restrict__ bwd,
+    int64_t S, int Q, const int32_t* __restrict__ fwd, const int32_t* __restrict__ bwd,
     int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots, unsigned long long* __restrict__ ovf_list,
     unsigned* __restrict__ ovf_count) {
     static_assert(W % kNbrPf == 0, "the prefetch distance must divide the ring");
+    static_assert(kNbrU0 % 4 == 0 && kNbrU0 < W, "unconditional ages");
     __shared__ Part red[kNbrThreads / 32];
-    const int t = blockIdx.y;
+    extern __shared__ int4 stab[];
+    const int t = blockIdx.x;  // tours fastest: the CTAs resident together share scenario tiles (L2 reuse)
     const int4 in = info[t];
     const int a = in.x, s0 = in.y;
     const int4* e = etabs + (int64_t)t * (n + 1);
-    const int64_t s = (int64_t)blockIdx.x * kNbrThreads + threadIdx.x;
+    if constexpr (SM) {
+        for (int i = threadIdx.x; i <= n; i += kNbrThreads) stab[i] = e[i];
+        __syncthreads();
+    }
+    auto tab = [&](int i) -> int4 {
+        if constexpr (SM) return stab[i];
+        else return __ldg(&e[i]);
+    };
+    const int64_t s = (int64_t)blockIdx.y * kNbrThreads + threadIdx.x;
     const bool live = s < S;
     const int64_t col = live ? s : S - 1;
     const int32_t* fcol = fwd + col;
     const int32_t* bcol = bwd + col;
     const uint16_t* dcol = demand + col;
-    const int pc = fcol[(int64_t)n * S];  // the parent's cost: same customers, same feasibility (R4)
+    const uint32_t Su = (uint32_t)S;  // (n + 1) S < 2^32: row offsets of fwd / bwd in 32 bits
+    const int pc = fcol[(uint32_t)n * Su];  // the parent's cost: same customers, same feasibility (R4)
     int result = pc;
     bool ovf = false;
     if (a < n) {  // (a, s0 are uniform per CTA; every lane enters: the loop votes over the full warp)
@@ -179,10 +194,10 @@ __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
             for (int k = 1; k <= W; ++k) {
                 const int p = a + 1 - k;
                 if (p >= 0) {
-                    const int4 ep = __ldg(&e[p]);
-                    G[W - k] = fcol[(int64_t)p * S] + ep.y;
+                    const int4 ep = tab(p);
+                    G[W - k] = fcol[(uint32_t)p * Su] + ep.y;
                     Y[W - k] = P + Q;
-                    if (p >= 1) P -= dcol[(int64_t)ep.x * ld];
+                    if (p >= 1) P -= dcol[(uint32_t)ep.w];
                 } else {
                     G[W - k] = INT_MAX;
                     Y[W - k] = INT_MIN;  // never in a window
@@ -196,8 +211,8 @@ __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
             qb[k] = 0;
             bb[k] = 0;
             if (i <= n) {
-                qb[k] = dcol[(int64_t)__ldg(&e[i].x) * ld];
-                if (i >= s0) bb[k] = bcol[(int64_t)i * S];
+                qb[k] = dcol[(uint32_t)tab(i).w];
+                if (i >= s0) bb[k] = bcol[(uint32_t)i * Su];
             }
         }
         int P = 0, Ps = 0;  // P(i) and P(s0 - 1) (= P(a) when s0 - 1 == a)
@@ -208,30 +223,43 @@ __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
             for (int j = 0; j < W; ++j) {
                 const int i = base + j;
                 if (i > n) break;  // warp-uniform
-                const int4 ei = __ldg(&e[i]);
+                const int4 ei = tab(i);
                 const int q = qb[j % kNbrPf];
                 const int bv = bb[j % kNbrPf];
                 const int ia = i + kNbrPf;
                 if (ia <= n) {
-                    qb[j % kNbrPf] = dcol[(int64_t)__ldg(&e[ia].x) * ld];
-                    if (ia >= s0) bb[j % kNbrPf] = bcol[(int64_t)ia * S];
+                    qb[j % kNbrPf] = dcol[(uint32_t)tab(ia).w];
+                    if (ia >= s0) bb[j % kNbrPf] = bcol[(uint32_t)ia * Su];
                 }
                 const int Pn = P + q;
                 // no route starting before s0 reaches layer i: the boundary set [s0, i-1] is complete
                 if (i > s0 && Pn - Ps > Q) active = false;
                 int best = G[(j - 1 + W) % W];  // age 1: always in the window (q <= Q)
+                int best1 = INT_MAX;            // second min chain (odd ages)
 #pragma unroll
-                for (int k0 = 2; k0 <= W; k0 += 4) {
+                for (int k = 2; k < 2 + kNbrU0; ++k) {
+                    const int sl = (j - k + W) % W;
+                    if (Y[sl] >= Pn) {
+                        if (k & 1) best1 = min(best1, G[sl]);
+                        else best = min(best, G[sl]);
+                    }
+                }
+#pragma unroll
+                for (int k0 = 2 + kNbrU0; k0 <= W; k0 += 4) {
                     if (!__any_sync(kFull, active && Y[(j - k0 + W) % W] >= Pn)) break;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         const int k = k0 + v;
                         if (k <= W) {
                             const int sl = (j - k + W) % W;
-                            if (Y[sl] >= Pn) best = min(best, G[sl]);
+                            if (Y[sl] >= Pn) {
+                                if (k & 1) best1 = min(best1, G[sl]);
+                                else best = min(best, G[sl]);
+                            }
                         }
                     }
                 }
+                best = min(best, best1);
                 // age W (slot j) in the window and an older split point exists: past the ring
                 if (active && Y[j] >= Pn && i - W >= 1) ovf = true;
                 if (active && i >= s0) total = min(total, best + ei.z + bv);
@@ -252,7 +280,7 @@ __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
         if (live && !deferred) part_add_cost(p, result, result != SPDP_INFEASIBLE);
         const Part r = block_sum(p, red);
         if (threadIdx.x == 0) {
-            spdp_saa_partial* d = &slots[(int64_t)t * kSlots + (blockIdx.x % kSlots)];
+            spdp_saa_partial* d = &slots[(int64_t)t * kSlots + (blockIdx.y % kSlots)];
             atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)r.n_feas);
             atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)r.n_infeas);
             atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)r.sum);
@@ -294,7 +322,7 @@ extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dis
     if (ws_bytes < spdp_values_workspace_bytes(n)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
     cudaStream_t st = (cudaStream_t)stream;
     int4* e = static_cast<int4*>(ws);
-    nbr_prep_kernel<<<1, 32, 0, st>>>(tour, nullptr, n, dist, e, nullptr);
+    nbr_prep_kernel<<<1, 32, 0, st>>>(tour, nullptr, n, dist, ld, e, nullptr);
     if ((rc = last_launch("nbr_prep_kernel"))) return rc;
     // Q above the largest possible load behaves as "everything fits"; clamp so sums stay in int32
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
@@ -310,15 +338,31 @@ extern "C" size_t spdp_neighbour_workspace_bytes(int32_t n, int64_t S, int32_t T
     return ws_layout(n, S, T).total + etab_bytes(n, T) + align_up(sizeof(int4) * (size_t)T, 256);
 }
 
+constexpr int kNbrSmemMaxN = 4095;  // position table in shared memory up to (n + 1) 16 B = 64 KB
+
 template <int W>
 static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info, int n, const uint16_t* demand,
-                                int64_t ld, int64_t S, int T, int Q, const int32_t* fwd, const int32_t* bwd,
+                                int64_t S, int T, int Q, const int32_t* fwd, const int32_t* bwd,
                                 int32_t* cost, spdp_saa_partial* slots, unsigned long long* ovf, unsigned* ovf_count) {
+    const dim3 grid((unsigned)T, (unsigned)ceil_div(S, kNbrThreads));
     prof_begin(st);
-    split_nbr_kernel<W><<<dim3((unsigned)ceil_div(S, kNbrThreads), (unsigned)T), kNbrThreads, 0, st>>>(
-        e, info, n, demand, ld, S, Q, fwd, bwd, cost, slots, ovf, ovf_count);
+    if (n <= kNbrSmemMaxN) {
+        const size_t smem = sizeof(int4) * (size_t)(n + 1);
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t err = cudaFuncSetAttribute(split_nbr_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)(sizeof(int4) * (kNbrSmemMaxN + 1)));
+            if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_nbr_kernel)");
+            attr = true;
+        }
+        split_nbr_kernel<W, true><<<grid, kNbrThreads, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,
+                                                                   ovf_count);
+    } else {
+        split_nbr_kernel<W, false><<<grid, kNbrThreads, 0, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,
+                                                                 ovf_count);
+    }
     prof_end(st);
-    set_last_kernel("split_nbr_kernel<%d>", W);
+    set_last_kernel("split_nbr_kernel<%d,%d>", W, n <= kNbrSmemMaxN ? 1 : 0);
     return last_launch("split_nbr_kernel");
 }
 
@@ -331,11 +375,14 @@ extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const i
     spdp_status rc = check_common(fn, n, S, Q, ld, demand);
     if (rc) return rc;
     if (T < 1) return fail(SPDP_E_USAGE, "%s: T=%d < 1", fn, T);
-    if (T >= 65536) return fail(SPDP_E_RESOURCE, "%s: T=%d >= 65536", fn, T);
+    if (T >= (1 << 23)) return fail(SPDP_E_RESOURCE, "%s: T=%d too large", fn, T);
+    if (ceil_div(S, kNbrThreads) >= 65536) return fail(SPDP_E_RESOURCE, "%s: S=%lld too large (grid)", fn, (long long)S);
     if (window_hint < 0) return fail(SPDP_E_USAGE, "%s: window_hint < 0", fn);
     if (!parent || !fwd || !bwd || !tours || !dist || !demand || !ws)
         return fail(SPDP_E_USAGE, "%s: NULL required pointer", fn);
     if (ws_bytes < spdp_neighbour_workspace_bytes(n, S, T)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
+    if ((uint64_t)n * (uint64_t)ld >= (1ull << 32) || (uint64_t)(n + 1) * (uint64_t)S >= (1ull << 32))
+        return fail(SPDP_E_RESOURCE, "%s: n ld and (n + 1) S must stay below 2^32", fn);
     cudaStream_t st = (cudaStream_t)stream;
     const WsLayout L = ws_layout(n, S, T);
     char* w = static_cast<char*>(ws);
@@ -352,16 +399,16 @@ extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const i
         if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
         if (h[HDR_STATUS]) return fail(SPDP_E_DATA, "%s: invalid candidate tour or costs (status %u)", fn, h[HDR_STATUS]);
     }
-    nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parent, n, dist, e, info);
+    nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parent, n, dist, ld, e, info);
     if ((rc = last_launch("nbr_prep_kernel"))) return rc;
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
     spdp_saa_partial* slots = partial ? reinterpret_cast<spdp_saa_partial*>(w + L.slots) : nullptr;
     unsigned long long* ovf = reinterpret_cast<unsigned long long*>(w + L.ovf);
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
     const int W = window_hint == 0 ? 32 : (window_hint <= 16 ? 16 : (window_hint <= 24 ? 24 : 32));
-    if (W == 16) rc = launch_nbr_t<16>(st, e, info, n, demand, ld, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
-    else if (W == 24) rc = launch_nbr_t<24>(st, e, info, n, demand, ld, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
-    else rc = launch_nbr_t<32>(st, e, info, n, demand, ld, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    if (W == 16) rc = launch_nbr_t<16>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    else if (W == 24) rc = launch_nbr_t<24>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    else rc = launch_nbr_t<32>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
     if (rc) return rc;
     return launch_finish(w, L, T, n, demand, ld, S, (uint32_t)Qe, cost, partial, false, st);
 }

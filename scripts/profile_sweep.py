@@ -18,6 +18,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--hint", type=int, default=None)
 ap.add_argument("--irp", action="store_true")
+ap.add_argument("--nbr", action="store_true", help="f3: values of tour 0 + neighbour evaluation of the population")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 if a.irp:
@@ -33,8 +34,14 @@ else:
     tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
     dist = torch.from_numpy(inst["dist"]).to(dev)
     h = a.hint if a.hint is not None else bench_config.HINT[a.config]
+    if a.nbr:
+        parent = tours[0].contiguous()
+        fwd, bwd = spdp.split_values(parent, dist, d, inst["Q"], S=cfg["S"])
     for _ in range(a.iters):
-        if cfg["T"] == 1:
+        if a.nbr:
+            spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False,
+                                       window_hint=h)
+        elif cfg["T"] == 1:
             spdp.split_eval(tours[0].contiguous(), dist, d, inst["Q"], S=cfg["S"], window_hint=h,
                             mean_window=bench_config.MEAN[a.config])
         else:

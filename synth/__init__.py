@@ -102,6 +102,29 @@ def perturb_tours(tour: np.ndarray, T: int, seed: int) -> np.ndarray:
     return out
 
 
+def local_move_tours(tour: np.ndarray, T: int, seed: int, radius: int = 10) -> np.ndarray:
+    """T tours: tour 0 as given, tours 1..T-1 = tour 0 + ONE seeded granular move (relocate of a
+    customer by at most `radius` positions, or a 2-opt reversal of at most radius + 1 positions),
+    the bounded neighbourhoods of HGS local search (f3 workload, DESIGN R23)."""
+    rng = np.random.default_rng(seed)
+    n = tour.shape[0]
+    out = np.empty((T, n), dtype=np.int32)
+    out[0] = tour
+    for t in range(1, T):
+        x = list(int(v) for v in tour)
+        if n >= 3:
+            a = int(rng.integers(0, n))
+            b = int(np.clip(a + rng.integers(-radius, radius + 1), 0, n - 1))
+            if rng.random() < 0.5:  # relocate
+                v = x.pop(a)
+                x.insert(b, v)
+            else:  # 2-opt
+                lo, hi = min(a, b), max(a, b)
+                x[lo:hi + 1] = x[lo:hi + 1][::-1]
+        out[t] = np.asarray(x, dtype=np.int32)
+    return out
+
+
 def irp_instance(M: int = 10, H: int = 30, U: int = 100, X: int = 100, I0: int = 50,
                  h: int = 1, b: int = 20, c: int = 1, mu_lo: int = 5, mu_hi: int = 30,
                  seed: int = 105, period: int = 3) -> dict:
