@@ -519,6 +519,25 @@ def measure_rows(spdp, torch, dev, pk):
                      "evals_per_s": cfg["T"] * cfg["S"] / ((ms_v + ms_nl) / 1e3),
                      "partials_equal_batch": bool(torch.equal(part, lpart))}}
     del d, fwd, bwd
+    # f4: C2 with a route-duration limit (1.5 x the largest out-and-back trip) and a fleet limit
+    # (capacity bound ceil(sum mu / Q) + 2 routes), each alone and together
+    cfg2 = synth.config_instance("C2")
+    inst2 = cfg2["inst"]
+    d = spdp.gen_demands(cfg2["model"], 0, cfg2["S"], device=dev)
+    tour2, dist2 = torch.from_numpy(inst2["tour"]).to(dev), torch.from_numpy(inst2["dist"]).to(dev)
+    trip = int(max(inst2["dist"][0, c] + inst2["dist"][c, 0] for c in inst2["tour"]))
+    kmin = int(np.ceil(inst2["nominal"].astype(np.int64).sum() / inst2["Q"]))
+    costl = torch.empty(cfg2["S"], dtype=torch.int32, device=dev)
+    partl = torch.zeros(6, dtype=torch.int64, device=dev)
+    f4 = {"Lmax": int(trip * 1.5), "K": kmin + 2}
+    for tag, L, K in (("duration", int(trip * 1.5), 0), ("fleet", -1, kmin + 2), ("both", int(trip * 1.5), kmin + 2)):
+        fn = lambda: spdp.split_eval_limits(tour2, dist2, d, inst2["Q"], max_duration=L, max_routes=K, S=cfg2["S"],
+                                            cost=costl, partial=partl)
+        ms = _time_events(fn, torch, dev, iters=3, warm=1)
+        f4[tag] = {"ms": ms, "evals_per_s": cfg2["S"] / (ms / 1e3),
+                   "infeasible": int(partl[1].item()), "kernel": spdp.last_kernel()}
+    rows["f4_limits_C2"] = f4
+    del d
     # f2: penalized split at C2 (lambda = 10 cost units per unit of overload, Q of C2)
     cfg2 = synth.config_instance("C2")
     inst2 = cfg2["inst"]

@@ -75,6 +75,8 @@ typedef enum {
 #define SPDP_F_SWEEP_INT   2u       /* register ring, exact int32, predicated min per candidate */
 #define SPDP_F_SWEEP_F32   4u       /* register ring, exact integer-valued fp32, FMA-pipe masking */
 #define SPDP_F_SWEEP_DEQUE 8u       /* monotone-deque sliding-window minimum, O(1) amortised */
+#define SPDP_F_SCRATCH_GLOBAL 16u  /* spdp_split_eval_limits: per-scenario DP arrays in the workspace
+                                       instead of shared memory (same results; for testing both paths) */
 /* bits 8..15 of flags: the expected MEAN window width i - mask(i) (0 = unknown; with
  * window_hint = 0 it is sampled).  A tuning hint like window_hint: it picks how many
  * candidates the sweep evaluates before its first warp vote, never the result. */
@@ -261,6 +263,30 @@ SPDP_API spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int
                                        const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
                                        int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
                                        void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream);
+
+/* f4 (DESIGN R24). Split with a route-duration limit and a fleet
+ * limit ("route length/duration constraints, if applicable"; PAPER:68
+ * "three vehicles available"):
+ *   route (p, i] admissible iff  sum_{k=p+1}^{i} q <= Q  and
+ *     t(p, i) = c_{0,s_{p+1}} + sum_{k=p+1}^{i-1} c_{s_k,s_{k+1}} + c_{s_i,0} <= max_duration
+ *   F_0(0) = 0, F_k(i) = min_{admissible (p, i]} F_{k-1}(p) + t(p, i),
+ *   cost[j] = min_{1 <= k <= max_routes} F_k(n)  of scenario j
+ * max_duration < 0: no duration limit; max_routes <= 0 (or >= n): no fleet limit
+ * (one pass of Eq. (3)).  SPDP_INFEASIBLE when no admissible split exists (a
+ * demand above Q, a customer whose out-and-back trip exceeds max_duration, or
+ * more routes needed than max_routes).  cost [S] int32 (may be NULL), partial:
+ * ONE spdp_saa_partial (may be NULL, overwritten).  One thread per scenario, the
+ * Eq. (2) masks computed once and reused by the max_routes passes; per-scenario
+ * DP arrays in shared memory when 3 (n+1) 4 B x 64 threads fit, else in the
+ * workspace (or always with SPDP_F_SCRATCH_GLOBAL).  n ld < 2^32; the int32
+ * range bound of spdp_split_eval applies.  ws: spdp_limits_workspace_bytes(n)
+ * bytes of device memory. */
+SPDP_API size_t spdp_limits_workspace_bytes(int32_t n);
+SPDP_API spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t* dist, int32_t n,
+                                   const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                                   int32_t max_duration, int32_t max_routes, int32_t* cost,
+                                   spdp_saa_partial* partial, void* ws, size_t ws_bytes, uint32_t flags,
+                                   spdp_stream_t stream);
 
 /* a6 standalone: SAA partial of a cost vector (SPDP_INFEASIBLE entries are
  * counted in n_infeas and excluded).  partial: DEVICE pointer to one struct. */

@@ -31,6 +31,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 SPDP_OK, SPDP_E_USAGE, SPDP_E_DATA, SPDP_E_RESOURCE, SPDP_E_CUDA = 0, 2, 3, 4, 5
 INFEASIBLE = 2**31 - 1
 F_VALIDATE = 1
+F_SCRATCH_GLOBAL = 16
 F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8}  # sweep algorithm flags (spdp.h)
 MAX_N = 16384
 
@@ -40,7 +41,8 @@ SYMBOLS = (
     "spdp_host_workspace_bytes", "spdp_split_eval_host", "spdp_irp_workspace_bytes", "spdp_irp_dp",
     "spdp_set_profile_events", "spdp_last_kernel", "spdp_routes_workspace_bytes", "spdp_split_routes",
     "spdp_split_eval_penalized", "spdp_values_workspace_bytes", "spdp_split_values",
-    "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours",
+    "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours", "spdp_limits_workspace_bytes",
+    "spdp_split_eval_limits",
 )
 
 
@@ -98,13 +100,16 @@ def _sig():
     L.spdp_neighbour_workspace_bytes.argtypes = [i32, i64, i32]
     L.spdp_neighbour_workspace_bytes.restype = sz
     L.spdp_split_eval_neighbours.argtypes = [P, P, P, P, i32, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
+    L.spdp_limits_workspace_bytes.argtypes = [i32]
+    L.spdp_limits_workspace_bytes.restype = sz
+    L.spdp_split_eval_limits.argtypes = [P, P, i32, P, i64, i64, i32, i32, i32, P, P, P, sz, u32, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
     L.spdp_irp_dp.argtypes = [P, ctypes.POINTER(IrpCustomer), i32, i32, P, i64, i64, P, P, P, sz, u32, P]
     for name in ("spdp_gen_demands", "spdp_demand_prefix", "spdp_split_mask", "spdp_split_eval",
                  "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean", "spdp_split_eval_host",
                  "spdp_irp_dp", "spdp_split_values", "spdp_split_eval_neighbours", "spdp_split_eval_penalized",
-                 "spdp_split_routes"):
+                 "spdp_split_routes", "spdp_split_eval_limits"):
         getattr(L, name).restype = st
 
 
@@ -377,6 +382,30 @@ def split_eval_neighbours(parent, fwd, bwd, tours, dist, demand, Q: int, S: int 
                                            _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
                                            ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_VALIDATE if validate else 0,
                                            _stream(dev)), "spdp_split_eval_neighbours")
+    return cost, partial
+
+
+def split_eval_limits(tour, dist, demand, Q: int, max_duration: int = -1, max_routes: int = 0,
+                      S: int | None = None, want_cost: bool = True, want_partial: bool = True, cost=None,
+                      partial=None, scratch_global: bool = False):
+    """f4: split costs with a route-duration limit (route cost <= max_duration; < 0: none) and at
+    most max_routes routes (<= 0: none) (spdp_split_eval_limits).  Returns (cost int32 [S], partial)."""
+    torch = _torch()
+    n, ld = demand.shape
+    S = ld if S is None else S
+    dev = demand.device
+    if want_cost and cost is None:
+        cost = torch.empty(S, dtype=torch.int32, device=dev)
+    if want_partial and partial is None:
+        partial = torch.zeros(6, dtype=torch.int64, device=dev)
+    ws = workspace(int(_lib.spdp_limits_workspace_bytes(n)), dev, tag="limits")
+    _check(_lib.spdp_split_eval_limits(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"),
+                                       ld, S, int(Q), int(max_duration), int(max_routes),
+                                       _dev_ptr(cost, "cost") if want_cost else None,
+                                       _dev_ptr(partial, "partial") if want_partial else None,
+                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                       F_SCRATCH_GLOBAL if scratch_global else 0, _stream(dev)),
+           "spdp_split_eval_limits")
     return cost, partial
 
 

@@ -290,6 +290,12 @@ __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
     }
 }
 
+spdp_status launch_tour_table(const int32_t* tours, int32_t T, const int32_t* parent, int32_t n, const int32_t* dist,
+                              int64_t ld, int4* etabs, int4* info, cudaStream_t st) {
+    nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parent, n, dist, ld, etabs, info);
+    return last_launch("nbr_prep_kernel");
+}
+
 static size_t etab_bytes(int32_t n, int32_t T) { return align_up(sizeof(int4) * (size_t)T * (size_t)(n + 1), 256); }
 
 static spdp_status check_common(const char* fn, int32_t n, int64_t S, int32_t Q, int64_t ld, const void* demand) {

@@ -57,4 +57,10 @@ spdp_status launch_finish(char* ws, const WsLayout& L, int32_t T, int32_t n, con
                           int64_t S, uint32_t Qe, int32_t* cost, spdp_saa_partial* partial, bool pdl,
                           cudaStream_t st);
 
+// nbr.cu: per-tour position tables e[t][i] = {row of sigma_i, A[i], B[i], row * ld (uint32)},
+// i = 0..n, for T tours [T][n]; with parent != NULL also info[t] = {common prefix length,
+// n - common suffix length} against the parent.  One warp per tour.
+spdp_status launch_tour_table(const int32_t* tours, int32_t T, const int32_t* parent, int32_t n, const int32_t* dist,
+                              int64_t ld, int4* etabs, int4* info, cudaStream_t st);
+
 }  // namespace spdp
