@@ -75,8 +75,8 @@ typedef enum {
 #define SPDP_F_SWEEP_INT   2u       /* register ring, exact int32, predicated min per candidate */
 #define SPDP_F_SWEEP_F32   4u       /* register ring, exact integer-valued fp32, FMA-pipe masking */
 #define SPDP_F_SWEEP_DEQUE 8u       /* monotone-deque sliding-window minimum, O(1) amortised */
-#define SPDP_F_SCRATCH_GLOBAL 16u  /* spdp_split_eval_limits: per-scenario DP arrays in the workspace
-                                       instead of shared memory (same results; for testing both paths) */
+#define SPDP_F_SCRATCH_GLOBAL 16u  /* spdp_split_eval_limits: every scenario through the general kernel
+                                       with its DP arrays in the workspace (same results; tests both paths) */
 /* bits 8..15 of flags: the expected MEAN window width i - mask(i) (0 = unknown; with
  * window_hint = 0 it is sampled).  A tuning hint like window_hint: it picks how many
  * candidates the sweep evaluates before its first warp vote, never the result. */
@@ -275,13 +275,15 @@ SPDP_API spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int
  * (one pass of Eq. (3)).  SPDP_INFEASIBLE when no admissible split exists (a
  * demand above Q, a customer whose out-and-back trip exceeds max_duration, or
  * more routes needed than max_routes).  cost [S] int32 (may be NULL), partial:
- * ONE spdp_saa_partial (may be NULL, overwritten).  One thread per scenario, the
- * Eq. (2) masks computed once and reused by the max_routes passes; per-scenario
- * DP arrays in shared memory when 3 (n+1) 4 B x 64 threads fit, else in the
- * workspace (or always with SPDP_F_SCRATCH_GLOBAL).  n ld < 2^32; the int32
- * range bound of spdp_split_eval applies.  ws: spdp_limits_workspace_bytes(n)
- * bytes of device memory. */
-SPDP_API size_t spdp_limits_workspace_bytes(int32_t n);
+ * ONE spdp_saa_partial (may be NULL, overwritten).  One thread per scenario: a
+ * 32-position ring kernel keeps the vehicle-count dimension to the band
+ * [kP(i), kP(i) + max_routes - kT] of the capacity bounds (kP = greedy route count
+ * of the prefix, kT of the tour); scenarios whose window or band outgrows it go to
+ * a general kernel (K passes, arrays of n+1 per scenario; SPDP_F_SCRATCH_GLOBAL
+ * sends every scenario there).  n ld < 2^32, S < 2^31; the int32 range bound of
+ * spdp_split_eval applies.  ws: spdp_limits_workspace_bytes(n, S) bytes of device
+ * memory. */
+SPDP_API size_t spdp_limits_workspace_bytes(int32_t n, int64_t S);
 SPDP_API spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t* dist, int32_t n,
                                    const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
                                    int32_t max_duration, int32_t max_routes, int32_t* cost,

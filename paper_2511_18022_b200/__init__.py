@@ -100,7 +100,7 @@ def _sig():
     L.spdp_neighbour_workspace_bytes.argtypes = [i32, i64, i32]
     L.spdp_neighbour_workspace_bytes.restype = sz
     L.spdp_split_eval_neighbours.argtypes = [P, P, P, P, i32, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
-    L.spdp_limits_workspace_bytes.argtypes = [i32]
+    L.spdp_limits_workspace_bytes.argtypes = [i32, i64]
     L.spdp_limits_workspace_bytes.restype = sz
     L.spdp_split_eval_limits.argtypes = [P, P, i32, P, i64, i64, i32, i32, i32, P, P, P, sz, u32, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
@@ -398,7 +398,7 @@ def split_eval_limits(tour, dist, demand, Q: int, max_duration: int = -1, max_ro
         cost = torch.empty(S, dtype=torch.int32, device=dev)
     if want_partial and partial is None:
         partial = torch.zeros(6, dtype=torch.int64, device=dev)
-    ws = workspace(int(_lib.spdp_limits_workspace_bytes(n)), dev, tag="limits")
+    ws = workspace(int(_lib.spdp_limits_workspace_bytes(n, S)), dev, tag="limits")
     _check(_lib.spdp_split_eval_limits(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"),
                                        ld, S, int(Q), int(max_duration), int(max_routes),
                                        _dev_ptr(cost, "cost") if want_cost else None,

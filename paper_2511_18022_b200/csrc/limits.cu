@@ -5,10 +5,10 @@
 //   t(p, i) = A[p] + B[i] <= Lmax  (duration = route cost, scenario-invariant);
 //   F_0(0) = 0,  F_k(i) = min_{admissible (p, i]} F_{k-1}(p) + t(p, i),
 //   cost = min_{k <= K} F_k(n)   (K <= 0: no fleet limit -> one pass of Eq. (3)).
-// The fleet limit adds the vehicle-count layer dimension to the layered DAG: K
-// passes of the Eq. (3) sweep, pass k reading F_{k-1}.  The masks mask(i) of
-// Eq. (2) do not depend on k: they are computed once per scenario (two pointers)
-// and reused by every pass.
+// The fleet limit adds the vehicle-count layer dimension to the layered DAG, kept
+// to the band of k that the capacity bounds allow (ring kernel below).  The masks
+// mask(i) of Eq. (2) do not depend on k: they are computed once per scenario (two
+// pointers) and reused for every k.
 #include <climits>
 
 #include "common.cuh"
@@ -18,40 +18,38 @@ namespace spdp {
 
 constexpr int kLimBig = 1 << 30;  // no admissible split (above every finite value, R17 range bound)
 constexpr int kLimThreads = 64;
-constexpr int kLimGlobalBlocksPerSm = 4;  // persistent grid of the workspace-scratch variant
+// persistent grid of the general kernel (its per-scenario arrays in the workspace): enough warps
+// to hide the latency of its serial loops, within a bounded workspace
+__host__ __device__ inline int lim_blocks_per_sm(int n) { return n <= 256 ? 16 : (n <= 2048 ? 8 : 2); }
 
-// One scenario per thread, grid-stride over scenarios.  Per-thread arrays of n+1 ints
-// (mask, F_a, F_b; element p of thread r at base[p * stride + r], conflict-free /
-// coalesced) live in shared memory (use_smem) or in the workspace.  The tour's
-// position table {row, A, B, row offset} is staged in shared memory.
+// The general kernel (any window, any number of routes): one scenario per thread,
+// grid-stride over the scenarios (or over the `list` of scenarios the ring kernel
+// deferred, `count` of them).  Per-thread arrays of n+1 ints (mask | kP << 16, F_a,
+// F_b; element p of thread r at base[p * stride + r], coalesced) live in the
+// workspace (shared memory would leave 1-2 CTAs per SM).  The tour's position table
+// {row, A, B, row offset} is staged in shared memory.
 __global__ void __launch_bounds__(kLimThreads) split_limits_kernel(const int4* __restrict__ e, int n,
                                                                   const uint16_t* __restrict__ demand, int64_t S, int Q,
                                                                   int Lmax, int K, int32_t* __restrict__ cost,
                                                                   spdp_saa_partial* __restrict__ partial, int* gscratch,
-                                                                  int use_smem) {
+                                                                  const int64_t* __restrict__ list,
+                                                                  const unsigned* __restrict__ count) {
     extern __shared__ int4 sm4[];
     __shared__ Part red[kLimThreads / 32];
     int4* tb = sm4;
     for (int i = threadIdx.x; i <= n; i += blockDim.x) tb[i] = e[i];
     __syncthreads();
-    int* arr;
-    int64_t stride;
-    int64_t r;
-    if (use_smem) {
-        arr = reinterpret_cast<int*>(sm4 + (n + 1));
-        stride = blockDim.x;
-        r = threadIdx.x;
-    } else {
-        arr = gscratch;
-        stride = (int64_t)gridDim.x * blockDim.x;
-        r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    }
+    int* arr = gscratch;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int* Mk = arr + r;
     int* Fa = arr + (int64_t)(n + 1) * stride + r;
     int* Fb = arr + 2 * (int64_t)(n + 1) * stride + r;
     const bool fleet = K > 0 && K < n;
     Part acc{0, 0, 0, 0, 0};
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nwork = list ? (int64_t)*count : S;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwork; w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = list ? list[w] : w;
         const uint16_t* dcol = demand + s;
         // tour-order prefix loads (in Fb) and the Eq. (2) masks
         int P = 0;
@@ -65,19 +63,27 @@ __global__ void __launch_bounds__(kLimThreads) split_limits_kernel(const int4* _
         }
         int result = SPDP_INFEASIBLE;
         if (!bad) {
-            int m = 0, Pm = 0;
+            // masks (low 16 bits) and kP(i), the greedy route count of the prefix (high 16 bits)
+            int m = 0, Pm = 0, kp = 0, load = Q + 1;
             for (int i = 1; i <= n; ++i) {
                 const int Pi = Fb[(int64_t)i * stride];
+                const int q = Pi - Fb[(int64_t)(i - 1) * stride];
+                load += q;
+                if (load > Q) {
+                    ++kp;
+                    load = q;
+                }
                 while (Pi - Pm > Q) Pm = Fb[(int64_t)(++m) * stride];
-                Mk[(int64_t)i * stride] = m;
+                Mk[(int64_t)i * stride] = m | (kp << 16);
             }
+            const int kT = kp;
             // one pass of the layered sweep: cur[i] = min_{admissible p} prev[p] + A[p] + B[i]
             auto pass = [&](const int* prev, int* cur) -> bool {
                 bool any = false;
                 for (int i = 1; i <= n; ++i) {
                     const int Bi = tb[i].z;
                     const int thr = Lmax - Bi;  // duration: A[p] <= Lmax - B[i]
-                    const int lo = Mk[(int64_t)i * stride];
+                    const int lo = Mk[(int64_t)i * stride] & 0xffff;
                     int best = kLimBig;
                     for (int p = i - 1; p >= lo; --p) {
                         const int Ap = tb[p].y;
@@ -95,20 +101,45 @@ __global__ void __launch_bounds__(kLimThreads) split_limits_kernel(const int4* _
                 Fa[0] = 0;
                 pass(Fa, Fa);
                 res = Fa[(int64_t)n * stride];
-            } else {
-                Fa[0] = 0;
-                for (int i = 1; i <= n; ++i) Fa[(int64_t)i * stride] = kLimBig;  // F_0
-                int* prev = Fa;
-                int* cur = Fb;  // (the prefix loads are no longer needed)
+            } else if (K < kT) {  // more routes needed than available (capacity bound)
                 res = kLimBig;
+            } else {
+                // pass k only visits the band of layers i with kP(i) <= k <= kP(i) + K - kT (the
+                // ring kernel's bound, see below); kP is nondecreasing, so the band is a range
+                // [lo_k, hi_k] moving right with k, and cells left behind are reset to infinity
+                const int slack = K - kT;
+                for (int i = 0; i <= n; ++i) {
+                    Fa[(int64_t)i * stride] = i == 0 ? 0 : kLimBig;  // F_0
+                    Fb[(int64_t)i * stride] = kLimBig;
+                }
+                int* prev = Fa;
+                int* cur = Fb;
+                res = kLimBig;
+                int lo = 1, hi = 0, lo2 = 1, lo1 = 1;  // lo2 / lo1: the bands' starts two / one passes ago
+                auto kp_at = [&](int i) -> int { return Mk[(int64_t)i * stride] >> 16; };
                 for (int k = 1; k <= K; ++k) {
-                    cur[0] = kLimBig;
-                    const bool any = pass(prev, cur);
-                    res = min(res, cur[(int64_t)n * stride]);
+                    while (lo <= n && kp_at(lo) < k - slack) ++lo;
+                    while (hi + 1 <= n && kp_at(hi + 1) <= k) ++hi;
+                    cur[0] = kLimBig;  // F_k(0), k >= 1
+                    for (int i = lo2; i < lo && i <= n; ++i) cur[(int64_t)i * stride] = kLimBig;
+                    for (int i = lo; i <= hi; ++i) {
+                        const int Bi = tb[i].z;
+                        const int thr = Lmax - Bi;
+                        const int mlo = Mk[(int64_t)i * stride] & 0xffff;
+                        int best = kLimBig;
+                        for (int p = i - 1; p >= mlo; --p) {
+                            const int Ap = tb[p].y;
+                            const int fp = prev[(int64_t)p * stride];
+                            if (Ap <= thr && fp < kLimBig) best = min(best, fp + Ap);
+                        }
+                        cur[(int64_t)i * stride] = best >= kLimBig ? kLimBig : best + Bi;
+                    }
+                    if (hi == n) res = min(res, cur[(int64_t)n * stride]);
                     int* tmp = prev;
                     prev = cur;
                     cur = tmp;
-                    if (!any) break;
+                    lo2 = lo1;
+                    lo1 = lo;
                 }
             }
             result = res >= kLimBig ? SPDP_INFEASIBLE : res;
@@ -128,6 +159,151 @@ __global__ void __launch_bounds__(kLimThreads) split_limits_kernel(const int4* _
     }
 }
 
+// The ring kernel (the common case): one scenario per thread; the last 32 positions
+// of the DP live in a per-thread shared-memory ring (slot p mod 32, [slot][tid]
+// layout: conflict-free).  Eq. (2) mask by two pointers over the ring's prefix loads.
+// Fleet limit (BW > 1): the vehicle-count dimension is kept to a band.  With kP(i) the
+// greedy (minimum, R5) number of capacity-feasible routes for the prefix 1..i and
+// kT = kP(n), F_k(i) is infinite for k < kP(i), and a state with k > kP(i) + K - kT
+// cannot complete within K routes (the suffix needs at least kT - kP(i)), so layer i
+// keeps k in [kP(i), kP(i) + K - kT] only: K - kT + 1 <= BW values per position (the
+// duration limit only removes routes, so these capacity bounds stay valid).  A
+// scenario whose window outgrows the ring or whose band exceeds BW is deferred to the
+// general kernel (list).  BW = 1 without a fleet limit (one value per position).
+constexpr int kRing = 32;
+
+template <int BW, int NT>
+__global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __restrict__ e, int n,
+                                                               const uint16_t* __restrict__ demand, int64_t S, int Q,
+                                                               int Lmax, int K, int32_t* __restrict__ cost,
+                                                               spdp_saa_partial* __restrict__ partial,
+                                                               int64_t* __restrict__ list, unsigned* __restrict__ count,
+                                                               int table_in_smem) {
+    constexpr bool FLEET = BW > 1;
+    extern __shared__ int4 sm4[];
+    __shared__ Part red[NT / 32];
+    const int tid = threadIdx.x;
+    int* ringP = reinterpret_cast<int*>(sm4);                  // [kRing][NT]
+    int* ringK = ringP + kRing * NT;                           // [kRing][NT]: kP(p) (fleet)
+    int* ringF = ringK + (FLEET ? kRing * NT : 0);             // [kRing][BW][NT]
+    const int4* tb = e;
+    if (table_in_smem) {
+        int4* st = reinterpret_cast<int4*>(ringF + kRing * BW * NT);
+        for (int i = tid; i <= n; i += NT) st[i] = e[i];
+        __syncthreads();
+        tb = st;
+    }
+    auto P_at = [&](int p) -> int& { return ringP[(p & (kRing - 1)) * NT + tid]; };
+    auto K_at = [&](int p) -> int& { return ringK[(p & (kRing - 1)) * NT + tid]; };
+    auto F_at = [&](int p, int b) -> int& { return ringF[((p & (kRing - 1)) * BW + b) * NT + tid]; };
+    Part acc{0, 0, 0, 0, 0};
+    const int64_t s = (int64_t)blockIdx.x * NT + tid;
+    if (s < S) {
+        const uint16_t* dcol = demand + s;
+        int result = SPDP_INFEASIBLE;
+        bool defer = false;
+        // capacity pre-pass: any demand above Q (R4) and kT = greedy route count of the whole tour
+        bool bad = false;
+        int kT = 0;
+        {
+            int load = Q + 1;
+            for (int i = 1; i <= n; ++i) {
+                const int q = dcol[(uint32_t)tb[i].w];
+                bad |= q > Q;
+                load += q;
+                if (load > Q) {
+                    ++kT;
+                    load = q;
+                }
+            }
+        }
+        const int slack = FLEET ? K - kT : 0;
+        if (!bad && slack >= 0) {
+            if (slack >= BW) {
+                defer = true;
+            } else {
+                P_at(0) = 0;
+                if (FLEET) {
+                    K_at(0) = 0;
+#pragma unroll
+                    for (int b = 0; b < BW; ++b) F_at(0, b) = b == 0 ? 0 : kLimBig;  // F_0(0) = 0
+                } else {
+                    F_at(0, 0) = 0;
+                }
+                int P = 0, m = 0, kp = 0, load = Q + 1;
+                for (int i = 1; i <= n && !defer; ++i) {
+                    const int4 ei = tb[i];
+                    const int q = dcol[(uint32_t)ei.w];
+                    P += q;
+                    load += q;
+                    if (load > Q) {  // greedy prefix route count kP(i)
+                        ++kp;
+                        load = q;
+                    }
+                    if (m < i - kRing) {  // the ring holds positions i-32..i-1 only: defer (conservative)
+                        defer = true;
+                        break;
+                    }
+                    while (P - P_at(m) > Q) ++m;  // mask(i), m <= i - 1 since q <= Q
+                    const int thr = Lmax - ei.z;  // duration: A[p] <= Lmax - B[i]
+                    int best[BW];
+#pragma unroll
+                    for (int b = 0; b < BW; ++b) best[b] = kLimBig;
+                    for (int p = i - 1; p >= m; --p) {
+                        const int Ap = tb[p].y;
+                        if (Ap > thr) continue;
+                        if (FLEET) {
+                            const int off = kp - 1 - K_at(p);  // F_{k-1}(p), k = kp + b: band index off + b
+#pragma unroll
+                            for (int b = 0; b < BW; ++b) {
+                                const int bb = off + b;
+                                if (bb >= 0 && bb < BW) {
+                                    const int fp = F_at(p, bb);
+                                    if (fp < kLimBig) best[b] = min(best[b], fp + Ap);
+                                }
+                            }
+                        } else {
+                            const int fp = F_at(p, 0);
+                            if (fp < kLimBig) best[0] = min(best[0], fp + Ap);
+                        }
+                    }
+                    // layer i overwrites slot i mod 32 (position i - 32 is out of every later window)
+                    P_at(i) = P;
+                    if (FLEET) K_at(i) = kp;
+#pragma unroll
+                    for (int b = 0; b < BW; ++b) {
+                        int v = best[b] >= kLimBig ? kLimBig : best[b] + ei.z;
+                        if (FLEET && (b > slack || kp + b > K)) v = kLimBig;  // outside the band
+                        F_at(i, b) = v;
+                    }
+                }
+                if (!defer) {
+                    int res = kLimBig;
+#pragma unroll
+                    for (int b = 0; b < BW; ++b) res = min(res, F_at(n, b));
+                    result = res >= kLimBig ? SPDP_INFEASIBLE : res;
+                }
+            }
+        }
+        if (defer) {
+            list[atomicAdd(count, 1u)] = s;
+        } else {
+            if (cost) cost[s] = result;
+            part_add_cost(acc, result, result != SPDP_INFEASIBLE);
+        }
+    }
+    if (partial) {
+        const Part t = block_sum(acc, red);
+        if (tid == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->n_feas), (unsigned long long)t.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->n_infeas), (unsigned long long)t.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sum), (unsigned long long)t.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_lo), (unsigned long long)t.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_hi), (unsigned long long)t.sq_hi);
+        }
+    }
+}
+
 static int lim_num_sms() {
     int dev = 0, v = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
@@ -135,19 +311,44 @@ static int lim_num_sms() {
 }
 
 static size_t lim_table_bytes(int32_t n) { return align_up(sizeof(int4) * (size_t)(n + 1), 256); }
-static size_t lim_smem_bytes(int32_t n, bool arrays) {
-    return sizeof(int4) * (size_t)(n + 1) + (arrays ? 3 * sizeof(int) * (size_t)(n + 1) * kLimThreads : 0);
+static size_t lim_scratch_bytes(int32_t n) {
+    const size_t threads = (size_t)lim_num_sms() * lim_blocks_per_sm(n) * kLimThreads;
+    return align_up(3 * sizeof(int) * (size_t)(n + 1) * threads, 256);
 }
 constexpr size_t kLimSmemCap = 200 * 1024;
+constexpr int kLimTableSmemMaxN = 2047;  // ring kernel: table staged in shared memory up to 32 KB
+
+template <int BW, int NT>
+static size_t ring_smem(int32_t n) {
+    return sizeof(int) * (size_t)kRing * NT * (BW + (BW > 1 ? 2 : 1)) +
+           (n <= kLimTableSmemMaxN ? sizeof(int4) * (size_t)(n + 1) : 0);
+}
+
+template <int BW, int NT>
+static spdp_status launch_ring(cudaStream_t st, const int4* e, int n, const uint16_t* demand, int64_t S, int Q, int Lmax,
+                               int K, int32_t* cost, spdp_saa_partial* partial, int64_t* list, unsigned* count) {
+    const size_t smem = ring_smem<BW, NT>(n);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t err = cudaFuncSetAttribute(split_limits_ring_kernel<BW, NT>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)ring_smem<BW, NT>(kLimTableSmemMaxN));
+        if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_limits_ring_kernel)");
+        attr = true;
+    }
+    split_limits_ring_kernel<BW, NT><<<(unsigned)ceil_div(S, NT), NT, smem, st>>>(
+        e, n, demand, S, Q, Lmax, K, cost, partial, list, count, n <= kLimTableSmemMaxN ? 1 : 0);
+    set_last_kernel("split_limits_ring_kernel<%d>", BW);
+    return last_launch("split_limits_ring_kernel");
+}
 
 }  // namespace spdp
 
 using namespace spdp;
 
-extern "C" size_t spdp_limits_workspace_bytes(int32_t n) {
-    if (n < 1) return 0;
-    const size_t threads = (size_t)lim_num_sms() * kLimGlobalBlocksPerSm * kLimThreads;
-    return lim_table_bytes(n) + align_up(3 * sizeof(int) * (size_t)(n + 1) * threads, 256);
+extern "C" size_t spdp_limits_workspace_bytes(int32_t n, int64_t S) {
+    if (n < 1 || S < 1) return 0;
+    return lim_table_bytes(n) + lim_scratch_bytes(n) + align_up(sizeof(int64_t) * (size_t)S, 256) + 256;
 }
 
 extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t* dist, int32_t n,
@@ -163,20 +364,34 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
     if (ld < S || (ld % 8) != 0) return fail(SPDP_E_USAGE, "%s: ld=%lld must be >= S and a multiple of 8", fn, (long long)ld);
     if (!tour || !dist || !demand || !ws) return fail(SPDP_E_USAGE, "%s: NULL required pointer", fn);
     if (((uintptr_t)demand & 15u) != 0) return fail(SPDP_E_USAGE, "%s: demand must be 16-byte aligned", fn);
-    if (ws_bytes < spdp_limits_workspace_bytes(n)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
+    if (ws_bytes < spdp_limits_workspace_bytes(n, S)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
     if ((uint64_t)n * (uint64_t)ld >= (1ull << 32)) return fail(SPDP_E_RESOURCE, "%s: n ld must stay below 2^32", fn);
+    if (S >= (1LL << 31)) return fail(SPDP_E_RESOURCE, "%s: S >= 2^31", fn);
     cudaStream_t st = (cudaStream_t)stream;
     char* w = static_cast<char*>(ws);
     int4* e = reinterpret_cast<int4*>(w);
     int* scratch = reinterpret_cast<int*>(w + lim_table_bytes(n));
+    int64_t* list = reinterpret_cast<int64_t*>(w + lim_table_bytes(n) + lim_scratch_bytes(n));
+    unsigned* count = reinterpret_cast<unsigned*>(w + lim_table_bytes(n) + lim_scratch_bytes(n) +
+                                                  align_up(sizeof(int64_t) * (size_t)S, 256));
     spdp_status rc = launch_tour_table(tour, 1, nullptr, n, dist, ld, e, nullptr, st);
     if (rc) return rc;
     if (partial && (rc = cuda_check(cudaMemsetAsync(partial, 0, sizeof(spdp_saa_partial), st), "cudaMemsetAsync(partial)")))
         return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
     const int Lmax = max_duration < 0 ? INT_MAX / 2 : max_duration;
-    const bool smem_ok = lim_smem_bytes(n, true) <= kLimSmemCap && !(flags & SPDP_F_SCRATCH_GLOBAL);
-    const size_t smem = lim_smem_bytes(n, smem_ok);
+    const bool fleet = max_routes > 0 && max_routes < n;
+    const int K = fleet ? max_routes : 0;
+    prof_begin(st);
+    // (1) the ring kernel for every scenario; (2) the general kernel for the ones it deferred
+    const bool general_only = (flags & SPDP_F_SCRATCH_GLOBAL) != 0;
+    if (!general_only) {
+        rc = fleet ? launch_ring<4, 128>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count)
+                   : launch_ring<1, 128>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count);
+        if (rc) return rc;
+    }
+    const size_t smem = sizeof(int4) * (size_t)(n + 1);
     if (smem > kLimSmemCap) return fail(SPDP_E_RESOURCE, "%s: n=%d too large for the staged table", fn, n);
     static bool attr = false;
     if (!attr) {
@@ -185,21 +400,14 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
         if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_limits_kernel)");
         attr = true;
     }
-    int per_sm = kLimGlobalBlocksPerSm;
-    if (smem_ok) {
-        int occ = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, split_limits_kernel, kLimThreads, smem) != cudaSuccess ||
-            occ < 1)
-            occ = 1;
-        per_sm = occ;
-    }
+    const int per_sm = lim_blocks_per_sm(n);
     int64_t grid = (int64_t)lim_num_sms() * per_sm;
     const int64_t need = ceil_div(S, kLimThreads);
     if (grid > need) grid = need;
-    prof_begin(st);
-    split_limits_kernel<<<(unsigned)grid, kLimThreads, smem, st>>>(e, n, demand, S, Qe, Lmax, max_routes, cost, partial,
-                                                                  scratch, smem_ok ? 1 : 0);
+    split_limits_kernel<<<(unsigned)grid, kLimThreads, smem, st>>>(e, n, demand, S, Qe, Lmax, K, cost, partial, scratch,
+                                                                  general_only ? nullptr : list,
+                                                                  general_only ? nullptr : count);
     prof_end(st);
-    set_last_kernel("split_limits_kernel<%s>", smem_ok ? "smem" : "global");
+    if (general_only) set_last_kernel("split_limits_kernel<global>");
     return last_launch("split_limits_kernel");
 }

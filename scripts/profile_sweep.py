@@ -19,6 +19,8 @@ ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--hint", type=int, default=None)
 ap.add_argument("--irp", action="store_true")
 ap.add_argument("--nbr", action="store_true", help="f3: values of tour 0 + neighbour evaluation of the population")
+ap.add_argument("--granular", action="store_true", help="f3 with the granular one-move population")
+ap.add_argument("--limits", action="store_true", help="f4: duration 1.5 x max trip + fleet ceil(sum mu / Q) + 2")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 if a.irp:
@@ -34,11 +36,19 @@ else:
     tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
     dist = torch.from_numpy(inst["dist"]).to(dev)
     h = a.hint if a.hint is not None else bench_config.HINT[a.config]
+    if a.granular:
+        tours = torch.from_numpy(synth.local_move_tours(inst["tour"], cfg["T"], 400)).to(dev)
+    if a.limits:
+        trip = int(max(inst["dist"][0, c] + inst["dist"][c, 0] for c in inst["tour"]))
+        kmin = int(np.ceil(inst["nominal"].astype(np.int64).sum() / inst["Q"]))
     if a.nbr:
         parent = tours[0].contiguous()
         fwd, bwd = spdp.split_values(parent, dist, d, inst["Q"], S=cfg["S"])
     for _ in range(a.iters):
-        if a.nbr:
+        if a.limits:
+            spdp.split_eval_limits(tours[0].contiguous(), dist, d, inst["Q"], max_duration=int(trip * 1.5),
+                                   max_routes=kmin + 2, S=cfg["S"])
+        elif a.nbr:
             spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False,
                                        window_hint=h)
         elif cfg["T"] == 1:

@@ -43,7 +43,7 @@ def _limits(inst, dem, frac_routes):
     trip = int(max(d[0, c] + d[c, 0] for c in t))
     kmin = int(np.ceil(inst["nominal"].astype(np.int64).sum() / inst["Q"]))
     return [(-1, 0), (trip, 0), (int(trip * 1.5), 0), (-1, kmin + frac_routes), (-1, 1),
-            (int(trip * 1.5), kmin + 2 * frac_routes)]
+            (int(trip * 1.5), kmin + 2 * frac_routes), (-1, kmin + 6)]  # (kmin + 6: bands wider than the ring's)
 
 
 @pytest.mark.parametrize("name,S,extra_q,glob", [("C1", 100, 0, False), ("C1", 100, 0, True), ("C2", 2_003, 0, False),
