@@ -87,3 +87,18 @@ def test_limits_edge_cases(spdp):
         cost, part = spdp.split_eval_limits(to_dev(np.array([1], dtype=np.int32)), to_dev(dist), to_dev(dem), 5,
                                             max_duration=Lmax, max_routes=K, S=3)
         assert cost.cpu().tolist() == want
+
+
+@pytest.mark.parametrize("n,S", [(1, 1), (2, 9), (5, 130), (40, 3)])
+def test_limits_tiny(spdp, n, S):
+    inst = synth.make_instance(n, seed=55 + n, r=2.0)
+    model = synth.demand_model(inst["nominal"], inst["Q"], seed=98)
+    dem = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
+    tour, dist, D = to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem)
+    trip = int(max(inst["dist"][0, c] + inst["dist"][c, 0] for c in inst["tour"]))
+    for Lmax, K in ((-1, 0), (trip, 0), (-1, 1), (-1, max(1, n // 2)), (2 * trip, max(1, n // 3))):
+        for g in (False, True):
+            cost, _ = spdp.split_eval_limits(tour, dist, D, inst["Q"], max_duration=Lmax, max_routes=K, S=S,
+                                             scratch_global=g)
+            want = as_i32(oracle.split_limits(inst["tour"], inst["dist"], dem, inst["Q"], Lmax=Lmax, K=K, S=S))
+            assert np.array_equal(cost.cpu().numpy().astype(np.int64), want), (Lmax, K, g)

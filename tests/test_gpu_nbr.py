@@ -124,3 +124,23 @@ def test_neighbours_usage_errors(spdp):
     with pytest.raises(spdp.SpdpError) as ei:
         spdp.split_eval_neighbours(parent, fwd, bwd, bad, dist, D, cfg["Q"], S=S, validate=True)
     assert ei.value.status == spdp.SPDP_E_DATA
+
+
+@pytest.mark.parametrize("n,S", [(1, 1), (2, 9), (3, 130), (40, 1)])
+def test_neighbours_tiny(spdp, n, S):
+    """n = 1 (the only candidate is the parent), n = 2 (every candidate a swap), a partial
+    128-scenario CTA and a single scenario; values and costs vs the oracle."""
+    rng = np.random.default_rng(n * 1000 + S)
+    inst = synth.make_instance(n, seed=77 + n, r=2.0)
+    model = synth.demand_model(inst["nominal"], inst["Q"], seed=99)
+    dem = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
+    parent = inst["tour"]
+    tours = np.ascontiguousarray(np.stack([parent] + [(rng.permutation(n) + 1).astype(np.int32) for _ in range(5)]))
+    P, dist, D = to_dev(parent), to_dev(inst["dist"]), to_dev(dem)
+    fwd, bwd = spdp.split_values(P, dist, D, inst["Q"], S=S)
+    wf, wb = oracle.split_values(parent, inst["dist"], dem, inst["Q"], S=S)
+    assert np.array_equal(fwd.cpu().numpy().T.astype(np.int64), as_i32(wf))
+    assert np.array_equal(bwd.cpu().numpy().T.astype(np.int64), as_i32(wb))
+    cost, _ = spdp.split_eval_neighbours(P, fwd, bwd, to_dev(tours), dist, D, inst["Q"], S=S, window_hint=16)
+    want = as_i32(oracle.split_tours(tours, inst["dist"], dem, inst["Q"], S=S))
+    assert np.array_equal(cost.cpu().numpy().astype(np.int64), want)
