@@ -1464,7 +1464,7 @@ static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
                                            a.cgs, a.tinfo, a.n, a.T, a.S, a.Q, (uint32_t)lim, a.cost, a.slots, a.ovf,
                                            a.hdr),
                                 "split_sweep_f2_kernel");
-    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d,%d,%d%s>", W, U0, UG, Cfg::kMinBlocks, NG, PAIR ? ",pair" : "");
+    set_last_kernel("split_sweep_f2_kernel<%d,%d,%d,%d,%d,%d>", W, U0, UG, MB, NG, PAIR ? 1 : 0);
     prof_end(st);
     return rc;
 }
