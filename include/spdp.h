@@ -77,6 +77,8 @@ typedef enum {
 #define SPDP_F_SWEEP_DEQUE 8u       /* monotone-deque sliding-window minimum, O(1) amortised */
 #define SPDP_F_SCRATCH_GLOBAL 16u  /* spdp_split_eval_limits: every scenario through the general kernel
                                        with its DP arrays in the workspace (same results; tests both paths) */
+#define SPDP_F_NBR_SMEM 32u        /* spdp_split_eval_neighbours: the shared-memory-ring kernel instead of
+                                       the register ring (same results) */
 /* bits 8..15 of flags: the expected MEAN window width i - mask(i) (0 = unknown; with
  * window_hint = 0 it is sampled).  A tuning hint like window_hint: it picks how many
  * candidates the sweep evaluates before its first warp vote, never the result. */
@@ -254,8 +256,9 @@ SPDP_API spdp_status spdp_split_values(const int32_t* tour, const int32_t* dist,
  * then takes cost = min_{s0 <= i <= E} f(i) + bwd[i] (every split has a route
  * boundary there).  Results (cost [T][S] int32, may be NULL; partial [T], may be
  * NULL, overwritten) are bit-identical to spdp_split_eval_batch on `tours`.
- * window_hint: as spdp_split_eval (selects the register ring: 16, 24 or 32;
- * wider windows are finished by the general kernel).  SPDP_F_VALIDATE checks the
+ * window_hint: 1..24 selects a 16-entry register ring, else 32 entries (with
+ * SPDP_F_NBR_SMEM: a shared-memory ring of 32, or 64 entries for hints above 32);
+ * wider windows are finished by the general kernel.  SPDP_F_VALIDATE checks the
  * candidates (not the parent).  ws: spdp_neighbour_workspace_bytes(n, S, T). */
 SPDP_API size_t spdp_neighbour_workspace_bytes(int32_t n, int64_t S, int32_t T);
 SPDP_API spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int32_t* fwd, const int32_t* bwd,

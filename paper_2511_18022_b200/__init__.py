@@ -32,6 +32,7 @@ SPDP_OK, SPDP_E_USAGE, SPDP_E_DATA, SPDP_E_RESOURCE, SPDP_E_CUDA = 0, 2, 3, 4, 5
 INFEASIBLE = 2**31 - 1
 F_VALIDATE = 1
 F_SCRATCH_GLOBAL = 16
+F_NBR_SMEM = 32
 F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8}  # sweep algorithm flags (spdp.h)
 MAX_N = 16384
 
@@ -362,9 +363,10 @@ def split_values(tour, dist, demand, Q: int, S: int | None = None, fwd=None, bwd
 
 def split_eval_neighbours(parent, fwd, bwd, tours, dist, demand, Q: int, S: int | None = None,
                           want_cost: bool = True, want_partial: bool = True, window_hint: int = 0,
-                          validate: bool = False, cost=None, partial=None):
+                          validate: bool = False, cost=None, partial=None, smem: bool = False):
     """f3: split costs of T candidate tours [T][n] from the parent's values (spdp_split_eval_neighbours);
-    bit-identical to split_eval_batch(tours, ...).  Returns (cost int32 [T][S], partial int64 [T][6])."""
+    bit-identical to split_eval_batch(tours, ...).  Returns (cost int32 [T][S], partial int64 [T][6]).
+    smem: the shared-memory-ring kernel instead of the register ring (same results)."""
     torch = _torch()
     n, ld = demand.shape
     T = tours.shape[0]
@@ -380,8 +382,9 @@ def split_eval_neighbours(parent, fwd, bwd, tours, dist, demand, Q: int, S: int 
                                            _dev_ptr(demand, "demand"), ld, S, int(Q),
                                            _dev_ptr(cost, "cost") if want_cost else None,
                                            _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
-                                           ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_VALIDATE if validate else 0,
-                                           _stream(dev)), "spdp_split_eval_neighbours")
+                                           ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                           (F_VALIDATE if validate else 0) | (F_NBR_SMEM if smem else 0), _stream(dev)),
+           "spdp_split_eval_neighbours")
     return cost, partial
 
 

@@ -296,6 +296,139 @@ spdp_status launch_tour_table(const int32_t* tours, int32_t T, const int32_t* pa
     return last_launch("nbr_prep_kernel");
 }
 
+
+// The same restarted sweep with the ring in shared memory ([W][NT] {G, Y} per CTA,
+// slot p mod W, conflict-free 8-byte rows): the layer loop is unrolled only by the
+// prefetch distance and the candidate scan is a loop of 4-candidate groups behind a
+// warp vote, so the code stays small (the register ring's unrolled W-layer body
+// overflows the instruction cache: ncu no_instruction stalls) and registers few.
+// Any power-of-two W (64 covers the C4 windows).
+template <int W, int NT>
+__global__ void __launch_bounds__(NT) split_nbr_smem_kernel(
+    const int4* __restrict__ etabs, const int4* __restrict__ info, int n, const uint16_t* __restrict__ demand,
+    int64_t S, int Q, const int32_t* __restrict__ fwd, const int32_t* __restrict__ bwd,
+    int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots, unsigned long long* __restrict__ ovf_list,
+    unsigned* __restrict__ ovf_count, int table_in_smem) {
+    static_assert((W & (W - 1)) == 0 && W >= 8, "W: a power of two");
+    __shared__ Part red[NT / 32];
+    extern __shared__ int4 sm4[];
+    int2* ring = reinterpret_cast<int2*>(sm4);  // [W][NT]
+    const int t = blockIdx.x;
+    const int4 in = info[t];
+    const int a = in.x, s0 = in.y;
+    const int4* tb = etabs + (int64_t)t * (n + 1);
+    if (table_in_smem) {
+        int4* st = sm4 + (W * NT) / 2;
+        for (int i = threadIdx.x; i <= n; i += NT) st[i] = tb[i];
+        __syncthreads();
+        tb = st;
+    }
+    const int tid = threadIdx.x;
+    auto R = [&](int p) -> int2& { return ring[(p & (W - 1)) * NT + tid]; };
+    const int64_t s = (int64_t)blockIdx.y * NT + tid;
+    const bool live = s < S;
+    const int64_t col = live ? s : S - 1;
+    const int32_t* fcol = fwd + col;
+    const int32_t* bcol = bwd + col;
+    const uint16_t* dcol = demand + col;
+    const uint32_t Su = (uint32_t)S;
+    const int pc = fcol[(uint32_t)n * Su];
+    int result = pc;
+    bool ovf = false;
+    if (a < n) {
+        {
+            int P = 0;
+            for (int k = 1; k <= W; ++k) {
+                const int p = a + 1 - k;
+                if (p >= 0) {
+                    const int4 ep = tb[p];
+                    R(p) = make_int2(fcol[(uint32_t)p * Su] + ep.y, P + Q);
+                    if (p >= 1) P -= dcol[(uint32_t)ep.w];
+                } else {
+                    R(p) = make_int2(INT_MAX, INT_MIN);
+                }
+            }
+        }
+        int qb[kNbrPf], bb[kNbrPf];
+#pragma unroll
+        for (int k = 0; k < kNbrPf; ++k) {
+            const int i = a + 1 + k;
+            qb[k] = 0;
+            bb[k] = 0;
+            if (i <= n) {
+                qb[k] = dcol[(uint32_t)tb[i].w];
+                if (i >= s0) bb[k] = bcol[(uint32_t)i * Su];
+            }
+        }
+        int P = 0, Ps = 0;
+        int gprev = R(a).x;  // g(a), age 1 of layer a + 1
+        int total = INT_MAX;
+        bool active = pc != SPDP_INFEASIBLE;
+        for (int base = a + 1;; base += kNbrPf) {
+#pragma unroll
+            for (int j = 0; j < kNbrPf; ++j) {
+                const int i = base + j;
+                if (i > n) break;  // warp-uniform
+                const int4 ei = tb[i];
+                const int q = qb[j];
+                const int bv = bb[j];
+                const int ia = i + kNbrPf;
+                if (ia <= n) {
+                    qb[j] = dcol[(uint32_t)tb[ia].w];
+                    if (ia >= s0) bb[j] = bcol[(uint32_t)ia * Su];
+                }
+                const int Pn = P + q;
+                if (i > s0 && Pn - Ps > Q) active = false;
+                int best = gprev, best1 = INT_MAX;  // age 1 is always in the window (q <= Q)
+                bool deep = true;
+                for (int k0 = 2; k0 <= W; k0 += 4) {
+                    if (!__any_sync(kFull, active && R(i - k0).y >= Pn)) {
+                        deep = false;
+                        break;
+                    }
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int k = k0 + v;
+                        if (k <= W) {
+                            const int2 c = R(i - k);
+                            if (c.y >= Pn) {
+                                if (v & 1) best1 = min(best1, c.x);
+                                else best = min(best, c.x);
+                            }
+                        }
+                    }
+                }
+                best = min(best, best1);
+                // the scan reached age W still inside the window and an older point exists
+                if (deep && active && R(i - W).y >= Pn && i - W >= 1) ovf = true;
+                if (active && i >= s0) total = min(total, best + ei.z + bv);
+                gprev = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
+                R(i) = make_int2(gprev, Pn + Q);  // (slot of position i - W, no longer needed)
+                if (i == s0 - 1) Ps = Pn;
+                P = Pn;
+            }
+            if (base + kNbrPf > n || !__any_sync(kFull, active && !ovf)) break;
+        }
+        result = pc == SPDP_INFEASIBLE ? pc : total;
+    }
+    const bool deferred = live && ovf;
+    if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
+    if (cost && live && !deferred) cost[(int64_t)t * S + s] = result;
+    if (slots) {
+        Part p{0, 0, 0, 0, 0};
+        if (live && !deferred) part_add_cost(p, result, result != SPDP_INFEASIBLE);
+        const Part r = block_sum(p, red);
+        if (threadIdx.x == 0) {
+            spdp_saa_partial* d = &slots[(int64_t)t * kSlots + (blockIdx.y % kSlots)];
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_feas), (unsigned long long)r.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->n_infeas), (unsigned long long)r.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sum), (unsigned long long)r.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_lo), (unsigned long long)r.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&d->sumsq_hi), (unsigned long long)r.sq_hi);
+        }
+    }
+}
+
 static size_t etab_bytes(int32_t n, int32_t T) { return align_up(sizeof(int4) * (size_t)T * (size_t)(n + 1), 256); }
 
 static spdp_status check_common(const char* fn, int32_t n, int64_t S, int32_t Q, int64_t ld, const void* demand) {
@@ -372,6 +505,32 @@ static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info
     return last_launch("split_nbr_kernel");
 }
 
+constexpr int kNbrSmemThreads = 128;
+
+template <int W>
+static spdp_status launch_nbr_smem_t(cudaStream_t st, const int4* e, const int4* info, int n, const uint16_t* demand,
+                                     int64_t S, int T, int Q, const int32_t* fwd, const int32_t* bwd, int32_t* cost,
+                                     spdp_saa_partial* slots, unsigned long long* ovf, unsigned* ovf_count) {
+    constexpr int NT = kNbrSmemThreads;
+    const bool tsm = n <= kNbrSmemMaxN;
+    const size_t ring = sizeof(int2) * (size_t)W * NT;
+    const size_t smem = ring + (tsm ? sizeof(int4) * (size_t)(n + 1) : 0);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t err = cudaFuncSetAttribute(split_nbr_smem_kernel<W, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(ring + sizeof(int4) * (kNbrSmemMaxN + 1)));
+        if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_nbr_smem_kernel)");
+        attr = true;
+    }
+    const dim3 grid((unsigned)T, (unsigned)ceil_div(S, NT));
+    prof_begin(st);
+    split_nbr_smem_kernel<W, NT><<<grid, NT, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf, ovf_count,
+                                                         tsm ? 1 : 0);
+    prof_end(st);
+    set_last_kernel("split_nbr_smem_kernel<%d>", W);
+    return last_launch("split_nbr_smem_kernel");
+}
+
 extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int32_t* fwd, const int32_t* bwd,
                                                   const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,
                                                   const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
@@ -411,10 +570,16 @@ extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const i
     spdp_saa_partial* slots = partial ? reinterpret_cast<spdp_saa_partial*>(w + L.slots) : nullptr;
     unsigned long long* ovf = reinterpret_cast<unsigned long long*>(w + L.ovf);
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
-    const int W = window_hint == 0 ? 32 : (window_hint <= 16 ? 16 : (window_hint <= 24 ? 24 : 32));
-    if (W == 16) rc = launch_nbr_t<16>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
-    else if (W == 24) rc = launch_nbr_t<24>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
-    else rc = launch_nbr_t<32>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    if (flags & SPDP_F_NBR_SMEM) {  // the shared-memory ring (W = 32, or 64 for hinted windows above 32)
+        rc = (window_hint > 32) ? launch_nbr_smem_t<64>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count)
+                                : launch_nbr_smem_t<32>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    } else {  // the register ring: 16 entries up to a hinted window of 24 (measured faster than 24 or 32
+              // entries at C3 even with the overflow lanes it sends to the finish kernel), else 32
+        if (window_hint != 0 && window_hint <= 24)
+            rc = launch_nbr_t<16>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+        else
+            rc = launch_nbr_t<32>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+    }
     if (rc) return rc;
     return launch_finish(w, L, T, n, demand, ld, S, (uint32_t)Qe, cost, partial, false, st);
 }

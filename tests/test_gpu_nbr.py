@@ -69,10 +69,11 @@ def _candidates(tour, T, seed):
     return np.ascontiguousarray(np.stack(out), dtype=np.int32)
 
 
+@pytest.mark.parametrize("smem", [False, True])
 @pytest.mark.parametrize("name,S,T,hint,extra_q", [
     ("C1", 100, 24, 0, 0), ("C2", 3_001, 40, 16, 0), ("C2", 2_003, 30, 24, 30), ("C3", 1_001, 40, 32, 0),
-    ("C3", 777, 20, 16, 0), ("C4", 203, 12, 16, 0), ("C4", 203, 12, 32, 0)])
-def test_neighbours_parity(spdp, name, S, T, hint, extra_q):
+    ("C3", 777, 20, 16, 0), ("C4", 203, 12, 16, 0), ("C4", 203, 12, 32, 0), ("C4", 203, 12, 64, 0)])
+def test_neighbours_parity(spdp, name, S, T, hint, extra_q, smem):
     """Bit-exact vs the oracle's split of every candidate (C4 with a 16-entry ring sends most
     lanes through the overflow path)."""
     cfg = synth.config_instance(name, S=S)
@@ -84,7 +85,7 @@ def test_neighbours_parity(spdp, name, S, T, hint, extra_q):
     parent, dist, D = to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem)
     fwd, bwd = spdp.split_values(parent, dist, D, cfg["Q"], S=S)
     cost, part = spdp.split_eval_neighbours(parent, fwd, bwd, to_dev(tours), dist, D, cfg["Q"], S=S,
-                                            window_hint=hint, validate=True)
+                                            window_hint=hint, validate=True, smem=smem)
     want = as_i32(oracle.split_tours(tours, inst["dist"], dem, cfg["Q"], S=S))
     got = cost.cpu().numpy().astype(np.int64)
     assert np.array_equal(got, want)
@@ -141,6 +142,8 @@ def test_neighbours_tiny(spdp, n, S):
     wf, wb = oracle.split_values(parent, inst["dist"], dem, inst["Q"], S=S)
     assert np.array_equal(fwd.cpu().numpy().T.astype(np.int64), as_i32(wf))
     assert np.array_equal(bwd.cpu().numpy().T.astype(np.int64), as_i32(wb))
-    cost, _ = spdp.split_eval_neighbours(P, fwd, bwd, to_dev(tours), dist, D, inst["Q"], S=S, window_hint=16)
     want = as_i32(oracle.split_tours(tours, inst["dist"], dem, inst["Q"], S=S))
-    assert np.array_equal(cost.cpu().numpy().astype(np.int64), want)
+    for smem in (False, True):
+        cost, _ = spdp.split_eval_neighbours(P, fwd, bwd, to_dev(tours), dist, D, inst["Q"], S=S, window_hint=16,
+                                             smem=smem)
+        assert np.array_equal(cost.cpu().numpy().astype(np.int64), want)
