@@ -1,0 +1,17 @@
+import sys, os
+sys.path.insert(0, os.getcwd())
+import numpy as np, torch, synth, bench_config, paper_2511_18022_b200 as spdp
+dev=torch.device("cuda")
+for name in ("C3","C2"):
+    cfg=synth.config_instance(name); inst=cfg["inst"]
+    d=spdp.gen_demands(cfg["model"],0,cfg["S"],device=dev)
+    tours=torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev); dist=torch.from_numpy(inst["dist"]).to(dev)
+    for h in (12, 16, 20, 24):
+        for mw in (0, bench_config.MEAN[name]):
+            fn=lambda: spdp.split_eval_batch(tours,dist,d,inst["Q"],S=cfg["S"],want_cost=False,window_hint=h,mean_window=mw)
+            for _ in range(2): fn()
+            a=torch.cuda.Event(enable_timing=True); b=torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(5): fn()
+            b.record(); torch.cuda.synchronize()
+            print(name, h, mw, spdp.last_kernel(), "%.4f ms" % (a.elapsed_time(b)/5))
