@@ -240,9 +240,11 @@ SPDP_API spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dist,
  * (Split = Eq. (1), of the sub-tour as a standalone problem).
  * int32 [n+1][S] each (DEVICE, caller-owned), SPDP_INFEASIBLE where the prefix /
  * suffix holds a demand above Q.  fwd[n] = bwd[0] = the spdp_split_eval cost.
- * One thread per scenario, any window width.  ws: spdp_values_workspace_bytes(n)
- * bytes of device memory.  Same argument rules as spdp_split_eval. */
-SPDP_API size_t spdp_values_workspace_bytes(int32_t n);
+ * One thread per scenario: a 32-entry register ring per direction, scenarios whose
+ * window outgrows it (or with a demand above Q) by a general kernel (any window).
+ * ws: spdp_values_workspace_bytes(n, S) bytes of device memory.  Same argument
+ * rules as spdp_split_eval; n ld < 2^32. */
+SPDP_API size_t spdp_values_workspace_bytes(int32_t n, int64_t S);
 SPDP_API spdp_status spdp_split_values(const int32_t* tour, const int32_t* dist, int32_t n,
                               const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
                               int32_t* fwd, int32_t* bwd, void* ws, size_t ws_bytes,

@@ -95,7 +95,7 @@ def _sig():
     L.spdp_routes_workspace_bytes.argtypes = [i32, i32]
     L.spdp_routes_workspace_bytes.restype = sz
     L.spdp_split_routes.argtypes = [P, P, i32, P, i64, i64, i32, P, i32, P, P, P, P, P, sz, P]
-    L.spdp_values_workspace_bytes.argtypes = [i32]
+    L.spdp_values_workspace_bytes.argtypes = [i32, i64]
     L.spdp_values_workspace_bytes.restype = sz
     L.spdp_split_values.argtypes = [P, P, i32, P, i64, i64, i32, P, P, P, sz, P]
     L.spdp_neighbour_workspace_bytes.argtypes = [i32, i64, i32]
@@ -354,7 +354,7 @@ def split_values(tour, dist, demand, Q: int, S: int | None = None, fwd=None, bwd
         fwd = torch.empty((n + 1, S), dtype=torch.int32, device=dev)
     if bwd is None:
         bwd = torch.empty((n + 1, S), dtype=torch.int32, device=dev)
-    ws = workspace(int(_lib.spdp_values_workspace_bytes(n)), dev, tag="values")
+    ws = workspace(int(_lib.spdp_values_workspace_bytes(n, S)), dev, tag="values")
     _check(_lib.spdp_split_values(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld, S,
                                   int(Q), _dev_ptr(fwd, "fwd"), _dev_ptr(bwd, "bwd"), ctypes.c_void_p(ws.data_ptr()),
                                   ws.numel(), _stream(dev)), "spdp_split_values")

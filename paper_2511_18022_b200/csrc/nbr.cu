@@ -25,6 +25,9 @@
 
 namespace spdp {
 
+constexpr int kNbrPf = 8;            // demand / b prefetch distance (layers)
+constexpr int kNbrSmemMaxN = 4095;  // position table in shared memory up to (n + 1) 16 B = 64 KB
+
 // Per-tour position table e[i], i = 0..n:  {row of customer sigma_i (i >= 1), A[i] (i < n),
 // B[i] (i >= 1), row * ld as a uint32 element offset (used when n ld < 2^32)}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
 // D[1] = 0, D[i] = D[i-1] + c_{s_{i-1},s_i}.
@@ -92,9 +95,12 @@ __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict_
 // where the prefix / suffix holds a demand above Q (DESIGN R4).
 __global__ void __launch_bounds__(256) split_values_kernel(const int4* __restrict__ e, int n,
                                                            const uint16_t* __restrict__ demand, int64_t ld, int64_t S,
-                                                           int Q, int32_t* fwd, int32_t* bwd) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= S) return;
+                                                           int Q, int32_t* fwd, int32_t* bwd,
+                                                           const int64_t* __restrict__ list,
+                                                           const unsigned* __restrict__ count) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= (list ? (int64_t)*count : S)) return;
+    const int64_t s = list ? list[w] : w;
     const uint16_t* dcol = demand + s;
     int32_t* fc = fwd + s;
     int32_t* bc = bwd + s;
@@ -140,6 +146,87 @@ __global__ void __launch_bounds__(256) split_values_kernel(const int4* __restric
     }
 }
 
+// The register-ring version of the same two passes (the common case): one scenario per
+// thread, a W-entry ring {value, load + Q} per direction, layers unrolled by W, demands
+// prefetched kNbrPf layers ahead.  Forward: G = f(p) + A[p], Y = P(p) + Q, window of
+// layer i = ring entries with Y >= P(i).  Backward (the mirror): H = b(j) + B[j], Y =
+// R(j) + Q with R(j) = sum_{k>j} q, window of position i = entries with Y >= R(i).  A
+// scenario whose window outgrows the ring (or that holds a demand above Q) is listed
+// for split_values_kernel.
+template <int W>
+__device__ __forceinline__ bool values_pass(const int4* __restrict__ e, int n, const uint16_t* __restrict__ dcol,
+                                            int Q, int32_t* __restrict__ outc, int64_t S, bool backward) {
+    int G[W], Y[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        G[k] = INT_MAX;
+        Y[k] = INT_MIN;
+    }
+    // position of step L: forward i = L + 1 (its g-entry at i-1 = L), backward i = n - 1 - L
+    auto qpos = [&](int L) -> int { return backward ? n - L : L + 1; };  // the demand entering step L
+    int qb[kNbrPf];
+#pragma unroll
+    for (int k = 0; k < kNbrPf; ++k) qb[k] = (k < n) ? (int)dcol[(uint32_t)e[qpos(k)].w] : 0;
+    // entry for the start point: forward p = 0 (f = 0, G = A[0]), backward j = n (b = 0, H = B[n])
+    int cur = backward ? e[n].z : e[0].y;
+    int P = 0;
+    bool ok = true;
+    for (int L0 = 0; L0 < n; L0 += W) {
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const int L = L0 + j;
+            if (L < n) {
+                const int q = qb[j % kNbrPf];
+                if (L + kNbrPf < n) qb[j % kNbrPf] = dcol[(uint32_t)e[qpos(L + kNbrPf)].w];
+                const int Pn = P + q;
+                ok &= q <= Q;
+                ok &= !(Y[j] >= Pn);  // the slot being overwritten (age W + 1) still in the window
+                G[j] = cur;
+                Y[j] = P + Q;
+                int best = cur;
+#pragma unroll
+                for (int k = 1; k < W; ++k) {
+                    const int sl = (j - k + W) % W;
+                    if (Y[sl] < Pn) break;  // the window is a contiguous run of the newest entries (R5)
+                    best = min(best, G[sl]);
+                }
+                const int i = backward ? n - 1 - L : L + 1;
+                const int4 ei = e[i];
+                // forward: f(i) = best + B[i], next entry g(i) = f(i) + A[i]
+                // backward: b(i) = best + A[i], next entry h(i) = b(i) + B[i]
+                const int val = backward ? best + ei.y : best + ei.z;
+                outc[(int64_t)i * S] = val;
+                cur = val + (backward ? ei.z : ei.y);
+                P = Pn;
+            }
+        }
+    }
+    return ok;
+}
+
+template <int W>
+__global__ void __launch_bounds__(128) split_values_ring_kernel(const int4* __restrict__ etab, int n,
+                                                                const uint16_t* __restrict__ demand, int64_t S, int Q,
+                                                                int32_t* __restrict__ fwd, int32_t* __restrict__ bwd,
+                                                                int64_t* __restrict__ list, unsigned* __restrict__ count,
+                                                                int table_in_smem) {
+    extern __shared__ int4 sm4[];
+    const int4* e = etab;
+    if (table_in_smem) {
+        for (int i = threadIdx.x; i <= n; i += blockDim.x) sm4[i] = etab[i];
+        __syncthreads();
+        e = sm4;
+    }
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const uint16_t* dcol = demand + s;
+    fwd[s] = 0;
+    bwd[(int64_t)n * S + s] = 0;
+    const bool okf = values_pass<W>(e, n, dcol, Q, fwd + s, S, false);
+    const bool okb = values_pass<W>(e, n, dcol, Q, bwd + s, S, true);
+    if (!(okf && okb)) list[atomicAdd(count, 1u)] = s;
+}
+
 // The restarted sweep: one scenario per thread, one candidate tour per blockIdx.x.
 // Ring of the last W split points p (slot (p - a - 1) mod W): {G = f(p) + A[p],
 // Y = P(p) + Q} with P relative to P(a) = 0; p is in the window of layer i iff
@@ -151,7 +238,6 @@ __global__ void __launch_bounds__(256) split_values_kernel(const int4* __restric
 // A lane whose window reaches past the ring is appended to the overflow list
 // (finished from scratch by split_finish_kernel on the candidate's own tables).
 constexpr int kNbrThreads = 128;
-constexpr int kNbrPf = 8;
 constexpr int kNbrU0 = 8;
 
 template <int W, bool SM>
@@ -446,9 +532,9 @@ static spdp_status check_common(const char* fn, int32_t n, int64_t S, int32_t Q,
 
 using namespace spdp;
 
-extern "C" size_t spdp_values_workspace_bytes(int32_t n) {
-    if (n < 1) return 0;
-    return etab_bytes(n, 1);
+extern "C" size_t spdp_values_workspace_bytes(int32_t n, int64_t S) {
+    if (n < 1 || S < 1) return 0;
+    return etab_bytes(n, 1) + align_up(sizeof(int64_t) * (size_t)S, 256) + 256;
 }
 
 extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dist, int32_t n, const uint16_t* demand,
@@ -458,17 +544,34 @@ extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dis
     spdp_status rc = check_common(fn, n, S, Q, ld, demand);
     if (rc) return rc;
     if (!tour || !dist || !demand || !fwd || !bwd || !ws) return fail(SPDP_E_USAGE, "%s: NULL required pointer", fn);
-    if (ws_bytes < spdp_values_workspace_bytes(n)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
+    if (ws_bytes < spdp_values_workspace_bytes(n, S)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
+    if ((uint64_t)n * (uint64_t)ld >= (1ull << 32)) return fail(SPDP_E_RESOURCE, "%s: n ld must stay below 2^32", fn);
     cudaStream_t st = (cudaStream_t)stream;
-    int4* e = static_cast<int4*>(ws);
+    char* w = static_cast<char*>(ws);
+    int4* e = reinterpret_cast<int4*>(w);
+    int64_t* list = reinterpret_cast<int64_t*>(w + etab_bytes(n, 1));
+    unsigned* count = reinterpret_cast<unsigned*>(w + etab_bytes(n, 1) + align_up(sizeof(int64_t) * (size_t)S, 256));
     nbr_prep_kernel<<<1, 32, 0, st>>>(tour, nullptr, n, dist, ld, e, nullptr);
     if ((rc = last_launch("nbr_prep_kernel"))) return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
     // Q above the largest possible load behaves as "everything fits"; clamp so sums stay in int32
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
+    const bool tsm = n <= kNbrSmemMaxN;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t err = cudaFuncSetAttribute(split_values_ring_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(sizeof(int4) * (kNbrSmemMaxN + 1)));
+        if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_values_ring_kernel)");
+        attr = true;
+    }
     prof_begin(st);
-    split_values_kernel<<<(unsigned)ceil_div(S, 256), 256, 0, st>>>(e, n, demand, ld, S, Qe, fwd, bwd);
+    split_values_ring_kernel<32><<<(unsigned)ceil_div(S, 128), 128, tsm ? sizeof(int4) * (size_t)(n + 1) : 0, st>>>(
+        e, n, demand, S, Qe, fwd, bwd, list, count, tsm ? 1 : 0);
+    if ((rc = last_launch("split_values_ring_kernel"))) return rc;
+    // the scenarios whose window outgrew the ring (or with a demand above Q): the general kernel
+    split_values_kernel<<<(unsigned)ceil_div(S, 256), 256, 0, st>>>(e, n, demand, ld, S, Qe, fwd, bwd, list, count);
     prof_end(st);
-    set_last_kernel("split_values_kernel");
+    set_last_kernel("split_values_ring_kernel<32>");
     return last_launch("split_values_kernel");
 }
 
@@ -477,7 +580,6 @@ extern "C" size_t spdp_neighbour_workspace_bytes(int32_t n, int64_t S, int32_t T
     return ws_layout(n, S, T).total + etab_bytes(n, T) + align_up(sizeof(int4) * (size_t)T, 256);
 }
 
-constexpr int kNbrSmemMaxN = 4095;  // position table in shared memory up to (n + 1) 16 B = 64 KB
 
 template <int W>
 static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info, int n, const uint16_t* demand,
