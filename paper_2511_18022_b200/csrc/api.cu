@@ -4,6 +4,10 @@
 #include <cstdarg>
 #include <cstdio>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "common.cuh"
 
 namespace spdp {
@@ -54,6 +58,53 @@ void prof_end(cudaStream_t st) {
 }  // namespace spdp
 
 using namespace spdp;
+
+static std::mutex g_setup_mu;
+static std::map<std::tuple<const void*, int, int, int, int, size_t>, int> g_setup;  // (func, dev, smem_max, carveout, threads, smem)
+static std::map<int, int> g_sms;
+
+spdp_status spdp::kernel_setup(const void* func, int smem_max, int carveout, int threads, size_t smem, int* blocks_per_sm,
+                         const char* what) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_check(e, what);
+    const auto key = std::make_tuple(func, dev, smem_max, carveout, threads, smem);
+    std::lock_guard<std::mutex> lock(g_setup_mu);
+    auto it = g_setup.find(key);
+    if (it != g_setup.end()) {
+        if (blocks_per_sm) *blocks_per_sm = it->second;
+        return SPDP_OK;
+    }
+    if (smem_max > 0) {
+        e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+        if (e != cudaSuccess) return cuda_check(e, what);
+    }
+    if (carveout >= 0) {
+        e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+        if (e != cudaSuccess) return cuda_check(e, what);
+    }
+    int b = 1;
+    if (threads > 0) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, func, threads, smem);
+        if (e != cudaSuccess) return cuda_check(e, what);
+        if (b < 1) b = 1;
+    }
+    g_setup[key] = b;
+    if (blocks_per_sm) *blocks_per_sm = b;
+    return SPDP_OK;
+}
+
+int spdp::device_sms() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    std::lock_guard<std::mutex> lock(g_setup_mu);
+    auto it = g_sms.find(dev);
+    if (it != g_sms.end()) return it->second;
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = v;
+    return v;
+}
 
 extern "C" int spdp_version(void) { return 100; }  // 0.1.0
 

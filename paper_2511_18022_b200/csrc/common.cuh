@@ -26,6 +26,15 @@ void prof_end(cudaStream_t st);
 // spdp_last_kernel(): record the name of the sweep kernel just enqueued.
 void set_last_kernel(const char* fmt, ...);
 
+// One-time setup per (kernel, device), thread-safe: raise the kernel's dynamic shared
+// memory limit to smem_max bytes and (carveout >= 0) set the preferred shared-memory
+// carveout in percent; with threads > 0 also return the resident CTAs per SM for
+// `threads` threads and `smem` bytes (>= 1) in *blocks_per_sm.
+spdp_status kernel_setup(const void* func, int smem_max, int carveout, int threads, size_t smem, int* blocks_per_sm,
+                         const char* what);
+// The SM count of the current device (cached per device).
+int device_sms();
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -312,12 +312,7 @@ static spdp_status launch_irp(const uint8_t* visit, const IrpCust* cust, int H, 
                               int64_t ld, int64_t S, long long* cost, cudaStream_t st) {
     const int warps = 4;
     const size_t smem = (size_t)warps * (sizeof(uint16_t) * H * 32 + sizeof(int32_t) * 32 * K);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(irp_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(irp)");
-        attr_set = true;
-    }
+    if (spdp_status e = kernel_setup((const void*)irp_kernel<K>, 200 * 1024, -1, 0, 0, nullptr, "irp_kernel setup")) return e;
     const int64_t ntask = ((S + 31) / 32) * M;
     int64_t blocks = ceil_div(ntask, warps);
     if (blocks > 148 * 16) blocks = 148 * 16;
@@ -376,13 +371,7 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     if (prefix_band && lane_smem_warp <= 48 * 1024 && irp_mode == 0) {
         // lazy-shift lane kernel: 4 warps per CTA, several CTAs per SM
         const int warps = 4;
-        static bool attr_lazy = false;
-        if (!attr_lazy) {
-            cudaError_t e = cudaFuncSetAttribute(irp_lazy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            if (e == cudaSuccess) e = cudaFuncSetAttribute(irp_lazy_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(irp_lazy)");
-            attr_lazy = true;
-        }
+        if ((rc = kernel_setup((const void*)irp_lazy_kernel, 200 * 1024, 100, 0, 0, nullptr, "irp_lazy setup"))) return rc;
         const int64_t ntile = (S + 31) / 32;
         const int64_t blocks = (ntile + warps - 1) / warps;
         prof_begin(st);
@@ -393,13 +382,7 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     } else if (prefix_band && lane_smem_warp <= 96 * 1024) {
         int warps = (int)((192 * 1024) / lane_smem_warp);
         warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaError_t e = cudaFuncSetAttribute(irp_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            if (e == cudaSuccess) e = cudaFuncSetAttribute(irp_lane_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(irp_lane)");
-            attr_set = true;
-        }
+        if ((rc = kernel_setup((const void*)irp_lane_kernel, 200 * 1024, 100, 0, 0, nullptr, "irp_lane setup"))) return rc;
         const int64_t ntile = (S + 31) / 32;
         int64_t blocks = (ntile + warps - 1) / warps;
         prof_begin(st);

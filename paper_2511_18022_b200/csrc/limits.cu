@@ -304,11 +304,7 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
     }
 }
 
-static int lim_num_sms() {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-}
+static int lim_num_sms() { return device_sms(); }
 
 static size_t lim_table_bytes(int32_t n) { return align_up(sizeof(int4) * (size_t)(n + 1), 256); }
 static size_t lim_scratch_bytes(int32_t n) {
@@ -328,14 +324,10 @@ template <int BW, int NT>
 static spdp_status launch_ring(cudaStream_t st, const int4* e, int n, const uint16_t* demand, int64_t S, int Q, int Lmax,
                                int K, int32_t* cost, spdp_saa_partial* partial, int64_t* list, unsigned* count) {
     const size_t smem = ring_smem<BW, NT>(n);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t err = cudaFuncSetAttribute(split_limits_ring_kernel<BW, NT>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)ring_smem<BW, NT>(kLimTableSmemMaxN));
-        if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_limits_ring_kernel)");
-        attr = true;
-    }
+    if (spdp_status e = kernel_setup((const void*)split_limits_ring_kernel<BW, NT>,
+                                     (int)ring_smem<BW, NT>(kLimTableSmemMaxN), -1, 0, 0, nullptr,
+                                     "split_limits_ring_kernel setup"))
+        return e;
     split_limits_ring_kernel<BW, NT><<<(unsigned)ceil_div(S, NT), NT, smem, st>>>(
         e, n, demand, S, Q, Lmax, K, cost, partial, list, count, n <= kLimTableSmemMaxN ? 1 : 0);
     set_last_kernel("split_limits_ring_kernel<%d>", BW);
@@ -393,13 +385,8 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
     }
     const size_t smem = sizeof(int4) * (size_t)(n + 1);
     if (smem > kLimSmemCap) return fail(SPDP_E_RESOURCE, "%s: n=%d too large for the staged table", fn, n);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t err = cudaFuncSetAttribute(split_limits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)kLimSmemCap);
-        if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_limits_kernel)");
-        attr = true;
-    }
+    if ((rc = kernel_setup((const void*)split_limits_kernel, (int)kLimSmemCap, -1, 0, 0, nullptr, "split_limits_kernel setup")))
+        return rc;
     const int per_sm = lim_blocks_per_sm(n);
     int64_t grid = (int64_t)lim_num_sms() * per_sm;
     const int64_t need = ceil_div(S, kLimThreads);

@@ -557,13 +557,9 @@ extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dis
     // Q above the largest possible load behaves as "everything fits"; clamp so sums stay in int32
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
     const bool tsm = n <= kNbrSmemMaxN;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t err = cudaFuncSetAttribute(split_values_ring_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)(sizeof(int4) * (kNbrSmemMaxN + 1)));
-        if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_values_ring_kernel)");
-        attr = true;
-    }
+    if ((rc = kernel_setup((const void*)split_values_ring_kernel<32>, (int)(sizeof(int4) * (kNbrSmemMaxN + 1)), -1, 0, 0,
+                           nullptr, "split_values_ring_kernel setup")))
+        return rc;
     prof_begin(st);
     split_values_ring_kernel<32><<<(unsigned)ceil_div(S, 128), 128, tsm ? sizeof(int4) * (size_t)(n + 1) : 0, st>>>(
         e, n, demand, S, Qe, fwd, bwd, list, count, tsm ? 1 : 0);
@@ -589,13 +585,9 @@ static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info
     prof_begin(st);
     if (n <= kNbrSmemMaxN) {
         const size_t smem = sizeof(int4) * (size_t)(n + 1);
-        static bool attr = false;
-        if (!attr) {
-            cudaError_t err = cudaFuncSetAttribute(split_nbr_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)(sizeof(int4) * (kNbrSmemMaxN + 1)));
-            if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_nbr_kernel)");
-            attr = true;
-        }
+        if (spdp_status e = kernel_setup((const void*)split_nbr_kernel<W, true>, (int)(sizeof(int4) * (kNbrSmemMaxN + 1)),
+                                         -1, 0, 0, nullptr, "split_nbr_kernel setup"))
+            return e;
         split_nbr_kernel<W, true><<<grid, kNbrThreads, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,
                                                                    ovf_count);
     } else {
@@ -617,13 +609,9 @@ static spdp_status launch_nbr_smem_t(cudaStream_t st, const int4* e, const int4*
     const bool tsm = n <= kNbrSmemMaxN;
     const size_t ring = sizeof(int2) * (size_t)W * NT;
     const size_t smem = ring + (tsm ? sizeof(int4) * (size_t)(n + 1) : 0);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t err = cudaFuncSetAttribute(split_nbr_smem_kernel<W, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)(ring + sizeof(int4) * (kNbrSmemMaxN + 1)));
-        if (err != cudaSuccess) return cuda_check(err, "cudaFuncSetAttribute(split_nbr_smem_kernel)");
-        attr = true;
-    }
+    if (spdp_status e = kernel_setup((const void*)split_nbr_smem_kernel<W, NT>, (int)(ring + sizeof(int4) * (kNbrSmemMaxN + 1)),
+                                     -1, 0, 0, nullptr, "split_nbr_smem_kernel setup"))
+        return e;
     const dim3 grid((unsigned)T, (unsigned)ceil_div(S, NT));
     prof_begin(st);
     split_nbr_smem_kernel<W, NT><<<grid, NT, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf, ovf_count,

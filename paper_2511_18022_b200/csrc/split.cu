@@ -1366,29 +1366,16 @@ struct SweepArgs {
     unsigned* hdr;
 };
 
-static int num_sms() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
-}
+static int num_sms() { return device_sms(); }
 
 // Launches the sweep: one wave of persistent CTAs (occupancy x SMs).
 template <int W>
 static spdp_status launch_sweep_t(cudaStream_t st, const SweepArgs& a) {
     auto kern = split_sweep_kernel<W>;
-    static int blocks_per_sm = 0;
-    if (blocks_per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SweepCfg<W>::kSmem);
-        if (e == cudaSuccess)  // all of the unified L1/smem as shared memory
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kSweepThreads, SweepCfg<W>::kSmem);
-        if (e != cudaSuccess) return cuda_check(e, "split_sweep setup");
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
+    int blocks_per_sm = 1;  // (all of the unified L1/smem as shared memory)
+    if (spdp_status e = kernel_setup((const void*)kern, (int)SweepCfg<W>::kSmem, 100, kSweepThreads, SweepCfg<W>::kSmem,
+                                     &blocks_per_sm, "split_sweep setup"))
+        return e;
     const int64_t ntiles = ((a.S + kTile - 1) / kTile) * a.T;
     int64_t grid = (int64_t)blocks_per_sm * num_sms();
     const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
@@ -1416,15 +1403,10 @@ static int sweep_mode() {  // 0 auto (ring int for W <= 32, deque above), 1 int,
 }
 
 static spdp_status launch_deque(cudaStream_t st, const SweepArgs& a) {
-    static int blocks_per_sm = 0;
-    if (blocks_per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(split_deque_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(split_deque_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, split_deque_kernel, kSweepThreads, DequeCfg::kSmem);
-        if (e != cudaSuccess) return cuda_check(e, "split_deque setup");
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
+    int blocks_per_sm = 1;
+    if (spdp_status e = kernel_setup((const void*)split_deque_kernel, 220 * 1024, 100, kSweepThreads, DequeCfg::kSmem,
+                                     &blocks_per_sm, "split_deque setup"))
+        return e;
     const int64_t ntiles = ((a.S + kTile - 1) / kTile) * a.T;
     int64_t grid = (int64_t)blocks_per_sm * num_sms();
     const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
@@ -1442,15 +1424,10 @@ template <int W, int U0, int UG, int MB = 0, int NG = W, bool PAIR = false>
 static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
     using Cfg = F2Cfg<W, MB>;
     auto kern = split_sweep_f2_kernel<W, U0, UG, MB, NG, PAIR>;
-    static int blocks_per_sm = 0;
-    if (blocks_per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kSweepThreads, Cfg::kSmem);
-        if (e != cudaSuccess) return cuda_check(e, "split_sweep_f2 setup");
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
+    int blocks_per_sm = 1;
+    if (spdp_status e = kernel_setup((const void*)kern, (int)Cfg::kSmem, 100, kSweepThreads, Cfg::kSmem, &blocks_per_sm,
+                                     "split_sweep_f2 setup"))
+        return e;
     const int64_t ntiles = ((a.S + kTile - 1) / kTile) * a.T;
     int64_t grid = (int64_t)blocks_per_sm * num_sms();
     const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
@@ -1536,15 +1513,10 @@ template <int W>
 static spdp_status launch_penalized_t(cudaStream_t st, const SweepArgs& a, int32_t lam) {
     using Cfg = F2Cfg<W, 0>;
     auto kern = split_penalized_kernel<W>;
-    static int blocks_per_sm = 0;
-    if (blocks_per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kSweepThreads, Cfg::kSmem);
-        if (e != cudaSuccess) return cuda_check(e, "split_penalized setup");
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
+    int blocks_per_sm = 1;
+    if (spdp_status e = kernel_setup((const void*)kern, (int)Cfg::kSmem, 100, kSweepThreads, Cfg::kSmem, &blocks_per_sm,
+                                     "split_penalized setup"))
+        return e;
     const int64_t ntiles = ((a.S + kTile - 1) / kTile) * a.T;
     int64_t grid = (int64_t)blocks_per_sm * num_sms();
     const int64_t need = (ntiles + kSweepWarps - 1) / kSweepWarps;
@@ -1639,14 +1611,11 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         if (rc) return rc;
         const size_t per_warp = 2 * sizeof(long long) * (size_t)(n + 1);
         const int warps = per_warp * 4 <= 192 * 1024 ? 4 : 1;
-        static bool attr_pen = false;
-        if (!attr_pen) {
-            cudaError_t e = cudaFuncSetAttribute(split_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(split_penalized_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(penalized finish)");
-            attr_pen = true;
-        }
+        if ((rc = kernel_setup((const void*)split_finish_kernel, 200 * 1024, -1, 0, 0, nullptr, "split_finish setup")))
+            return rc;
+        if ((rc = kernel_setup((const void*)split_penalized_finish_kernel, 200 * 1024, -1, 0, 0, nullptr,
+                               "split_penalized_finish setup")))
+            return rc;
         // SAA slots -> partial (no strict overflow list), then the deferred penalized scenarios
         rc = cuda_check(launch_pdl(split_finish_kernel, dim3(num_sms()), dim3(128), (size_t)0, st,
                                    partial ? slots : nullptr, (int)kSlots, T, (const int2*)tabs, (const int32_t*)g0, n,
@@ -1689,12 +1658,8 @@ spdp_status launch_finish(char* w, const WsLayout& L, int32_t T, int32_t n, cons
     // each with 12 (n+1) B of shared scratch for the rare windows wider than kOvfW)
     const size_t per_warp = 3 * sizeof(int) * (size_t)(n + 1);
     const int warps = per_warp * 4 <= 192 * 1024 ? 4 : 1;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(split_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(split_finish)");
-        attr_set = true;
-    }
+    if (spdp_status e = kernel_setup((const void*)split_finish_kernel, 200 * 1024, -1, 0, 0, nullptr, "split_finish setup"))
+        return e;
     const spdp_saa_partial* slots = partial ? reinterpret_cast<const spdp_saa_partial*>(w + L.slots) : nullptr;
     const int2* tabs = reinterpret_cast<const int2*>(w + L.tabs);
     const int32_t* g0 = reinterpret_cast<const int32_t*>(w + L.g0);
