@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--window-hint", type=int, default=None)
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every timed step from Python (default at N = 1: replay a CUDA graph of the step)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -261,6 +263,29 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
+    # At N = 1 the timed steps replay a CUDA graph of one step (the same three kernels with their
+    # programmatic-dependent-launch edges), so host launch overhead (ctypes marshalling, ~tens of
+    # us per step in Python) cannot leave the GPU idle between steps.
+    graph, launch_mode = None, "eager (one C-ABI call per step from Python)"
+    if world == 1 and not args.eager:
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            torch.cuda.synchronize(dev)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize(dev)
+            graph, launch_mode = g, "CUDA graph replay (one captured step per replay)"
+        except Exception as ex:  # keep the eager loop (and say why)
+            launch_mode = "eager (graph capture failed: %s)" % str(ex).splitlines()[0][:120]
+            torch.cuda.synchronize(dev)
+
+    def timed_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
 
     # algorithmic work: Eq. (3) candidates sum_i (i - mask(i)) from the standalone mask kernel (untimed)
     m = spdp.split_mask(tour, demand, Q, S=S_loc)
@@ -289,7 +314,7 @@ def main():
     # launch; an event recorded between them would serialise that)
     t_start.record(stream)
     for k in range(args.steps):
-        step()
+        timed_step()
     for ev in freed:  # the last all-reduces are part of the timed region
         if ev is not None:
             stream.wait_event(ev)
@@ -309,7 +334,7 @@ def main():
     soak_end = time.perf_counter() + 1.0
     while time.perf_counter() < soak_end:
         for _ in range(20):
-            step()
+            timed_step()
         torch.cuda.synchronize(dev)
     clocks = sampler.stop()
 
@@ -352,7 +377,8 @@ def main():
                               "demand %.0f MB/GPU fits L2 (126 MB): steps after the first read it from L2")
                              % (n * S_loc * 2 / 1e6),
                        "parallelism": "scenario-sharded dp%d, 1 int64 all-reduce/step (on a comm stream, "
-                                      "overlapped with the next step)" % world},
+                                      "overlapped with the next step)" % world,
+                       "launch": launch_mode},
             "roofline": roof, "clocks": clocks, "gpu_launches": 3 * args.steps}
 
     # ------------------------------------------------------------------ e2e through the C-ABI host entry
