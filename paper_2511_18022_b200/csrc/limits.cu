@@ -16,6 +16,7 @@
 
 namespace spdp {
 
+constexpr int kLimTableSmemMaxN = 2047;  // position table staged in shared memory up to 32 KB
 constexpr int kLimBig = 1 << 30;  // no admissible split (above every finite value, R17 range bound)
 constexpr int kLimThreads = 64;
 // persistent grid of the general kernel (its per-scenario arrays in the workspace): enough warps
@@ -36,9 +37,12 @@ __global__ void __launch_bounds__(kLimThreads) split_limits_kernel(const int4* _
                                                                   const unsigned* __restrict__ count) {
     extern __shared__ int4 sm4[];
     __shared__ Part red[kLimThreads / 32];
-    int4* tb = sm4;
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) tb[i] = e[i];
-    __syncthreads();
+    const int4* tb = e;  // staged in shared memory up to kLimTableSmemMaxN positions, else read through L1
+    if (n <= kLimTableSmemMaxN) {
+        for (int i = threadIdx.x; i <= n; i += blockDim.x) sm4[i] = e[i];
+        __syncthreads();
+        tb = sm4;
+    }
     int* arr = gscratch;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -310,7 +314,6 @@ static size_t lim_scratch_bytes(int32_t n) {
     return align_up(3 * sizeof(int) * (size_t)(n + 1) * threads, 256);
 }
 constexpr size_t kLimSmemCap = 200 * 1024;
-constexpr int kLimTableSmemMaxN = 2047;  // ring kernel: table staged in shared memory up to 32 KB
 
 template <int BW, int NT, int kRing>
 static size_t ring_smem(int32_t n) {
@@ -383,8 +386,7 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
                    : launch_ring<1, 128, 32>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count);
         if (rc) return rc;
     }
-    const size_t smem = sizeof(int4) * (size_t)(n + 1);
-    if (smem > kLimSmemCap) return fail(SPDP_E_RESOURCE, "%s: n=%d too large for the staged table", fn, n);
+    const size_t smem = n <= kLimTableSmemMaxN ? sizeof(int4) * (size_t)(n + 1) : 0;
     if ((rc = kernel_setup((const void*)split_limits_kernel, (int)kLimSmemCap, -1, 0, 0, nullptr, "split_limits_kernel setup")))
         return rc;
     const int per_sm = lim_blocks_per_sm(n);

@@ -80,3 +80,19 @@ def test_product_never_imports_oracle():
                 if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                     text = open(os.path.join(dirpath, f)).read()
                     assert not pat.search(text), os.path.join(dirpath, f)
+
+
+def test_usage_errors_of_the_next_rows(spdp):
+    """f3 / f4 entry points reject bad arguments on the host, before any device work."""
+    L = spdp.lib()
+    assert L.spdp_split_values(None, None, 10, None, 8, 8, 5, None, None, None, 0, None) == spdp.SPDP_E_USAGE
+    assert L.spdp_split_values(None, None, 0, None, 8, 8, 5, None, None, None, 0, None) == spdp.SPDP_E_USAGE
+    assert L.spdp_split_eval_neighbours(None, None, None, None, 4, None, 10, None, 8, 8, 5, None, None, 0, None, 0, 0,
+                                        None) == spdp.SPDP_E_USAGE
+    assert L.spdp_split_eval_neighbours(None, None, None, None, 0, None, 10, None, 8, 8, 5, None, None, 0, None, 0, 0,
+                                        None) == spdp.SPDP_E_USAGE
+    assert L.spdp_split_eval_limits(None, None, 10, None, 8, 8, 5, -1, 0, None, None, None, 0, 0, None) == spdp.SPDP_E_USAGE
+    assert L.spdp_split_eval_limits(None, None, 10, None, 8, 8, 0, -1, 0, None, None, None, 0, 0, None) == spdp.SPDP_E_USAGE
+    assert b"Q=0" in L.spdp_last_error()
+    assert L.spdp_values_workspace_bytes(0, 5) == 0 and L.spdp_values_workspace_bytes(10, 5) > 0
+    assert L.spdp_neighbour_workspace_bytes(10, 5, 0) == 0 and L.spdp_neighbour_workspace_bytes(10, 5, 3) > 0

@@ -102,3 +102,20 @@ def test_limits_tiny(spdp, n, S):
                                              scratch_global=g)
             want = as_i32(oracle.split_limits(inst["tour"], inst["dist"], dem, inst["Q"], Lmax=Lmax, K=K, S=S))
             assert np.array_equal(cost.cpu().numpy().astype(np.int64), want), (Lmax, K, g)
+
+
+def test_limits_large_n_table_in_global_memory(spdp):
+    """n above the shared-memory table size (the position table read through L1)."""
+    n, S = 2600, 17
+    inst = synth.make_instance(n, seed=2600, r=12.0)
+    model = synth.demand_model(inst["nominal"], inst["Q"], seed=97)
+    dem = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
+    tour, dist, D = to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem)
+    kmin = int(np.ceil(inst["nominal"].astype(np.int64).sum() / inst["Q"]))
+    trip = int(max(inst["dist"][0, c] + inst["dist"][c, 0] for c in inst["tour"]))
+    for Lmax, K in ((-1, 0), (2 * trip, 0), (-1, kmin + 2)):
+        for g in (False, True):
+            cost, _ = spdp.split_eval_limits(tour, dist, D, inst["Q"], max_duration=Lmax, max_routes=K, S=S,
+                                             scratch_global=g)
+            want = as_i32(oracle.split_limits(inst["tour"], inst["dist"], dem, inst["Q"], Lmax=Lmax, K=K, S=S))
+            assert np.array_equal(cost.cpu().numpy().astype(np.int64), want), (Lmax, K, g)

@@ -147,3 +147,20 @@ def test_neighbours_tiny(spdp, n, S):
         cost, _ = spdp.split_eval_neighbours(P, fwd, bwd, to_dev(tours), dist, D, inst["Q"], S=S, window_hint=16,
                                              smem=smem)
         assert np.array_equal(cost.cpu().numpy().astype(np.int64), want)
+
+
+def test_neighbours_large_n_table_in_global_memory(spdp):
+    """n above the shared-memory table size of the neighbour kernel (4095)."""
+    n, S = 4300, 9
+    inst = synth.make_instance(n, seed=4300, r=6.0)
+    model = synth.demand_model(inst["nominal"], inst["Q"], seed=96)
+    dem = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
+    tours = np.ascontiguousarray(synth.perturb_tours(inst["tour"], 4, 11))
+    P, dist, D = to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem)
+    fwd, bwd = spdp.split_values(P, dist, D, inst["Q"], S=S)
+    want = as_i32(oracle.split_tours(tours, inst["dist"], dem, inst["Q"], S=S))
+    assert np.array_equal(fwd.cpu().numpy()[-1].astype(np.int64), want[0])
+    for smem in (False, True):
+        cost, _ = spdp.split_eval_neighbours(P, fwd, bwd, to_dev(tours), dist, D, inst["Q"], S=S, window_hint=16,
+                                             smem=smem)
+        assert np.array_equal(cost.cpu().numpy().astype(np.int64), want)
