@@ -233,12 +233,16 @@ __global__ void __launch_bounds__(128) irp_lazy_kernel(const uint8_t* __restrict
     int32_t* A = vsm + (size_t)wid * (Umax + 1) * 32 + lane;  // A[x] at A[x * 32]
     constexpr int32_t kReal = 1 << 29;                        // values >= kReal are unreachable
     const int64_t ntile = (S + 31) / 32;
-    for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntile; tile += (int64_t)gridDim.x * nw) {
+    // one warp task = (32-scenario tile, customer): M times more independent warps than tiles, so
+    // the launch fills every SM several times over; the customer costs are summed with atomics
+    // into cost[] (zeroed by the host code)
+    for (int64_t task = (int64_t)blockIdx.x * nw + wid; task < ntile * M; task += (int64_t)gridDim.x * nw) {
+        const int64_t tile = task / M;
+        const int m = (int)(task - tile * M);
         const int64_t s0 = tile * 32;
         const bool live = s0 + lane < S;
         const int64_t s = live ? s0 + lane : S - 1;
-        long long total = 0;
-        for (int m = 0; m < M; ++m) {
+        {
             const IrpCust p = cust[m];
             const int U = p.U, B = U + 1;
             for (int y = 0; y <= U; ++y) A[y * 32] = (y == p.I0) ? 0 : kIrpInf;
@@ -286,9 +290,8 @@ __global__ void __launch_bounds__(128) irp_lazy_kernel(const uint8_t* __restrict
                 best = min(best, A[x * 32] + alpha * y + K);
                 x = (x + 1 == B) ? 0 : x + 1;
             }
-            total += best;
+            if (live) atomicAdd(reinterpret_cast<unsigned long long*>(&cost[s]), (unsigned long long)(long long)best);
         }
-        if (live) cost[s] = total;
     }
 }
 
@@ -372,8 +375,9 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
         // lazy-shift lane kernel: 4 warps per CTA, several CTAs per SM
         const int warps = 4;
         if ((rc = kernel_setup((const void*)irp_lazy_kernel, 200 * 1024, 100, 0, 0, nullptr, "irp_lazy setup"))) return rc;
-        const int64_t ntile = (S + 31) / 32;
-        const int64_t blocks = (ntile + warps - 1) / warps;
+        const int64_t ntask = ((S + 31) / 32) * M;
+        const int64_t blocks = (ntask + warps - 1) / warps;
+        if ((rc = cuda_check(cudaMemsetAsync(c, 0, sizeof(long long) * (size_t)S, st), "cudaMemsetAsync(cost)"))) return rc;
         prof_begin(st);
         irp_lazy_kernel<<<(unsigned)blocks, warps * 32, lane_smem_warp * warps, st>>>(dvisit, dcust, H, M, Umax, demand,
                                                                                      ld, S, c);
