@@ -614,10 +614,24 @@ def cpu_baseline(cfg, cost_dev, S, spdp, partial_dev):
     got = cost_dev.cpu().numpy().astype(np.int64)
     parity = bool(np.array_equal(got, want))
     est = spdp.saa_mean(partial_dev)
+    # the paper's 1-thread baseline: one host thread on a 10^5-scenario prefix
+    S1 = min(S, 100_000)
+    t0 = time.perf_counter()
+    oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], S=S1, threads=1)
+    t1 = time.perf_counter() - t0
+    cpu_model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": S / t, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": "all %d scenarios of the timed workload, once (oracle split + SAA; demands pre-generated "
                       "by the oracle's own generator)" % S,
-            "seconds": t, "parity_all_costs_bit_exact": parity, "saa_mean_equal": est["mean"] == w["mean"]}
+            "seconds": t, "parity_all_costs_bit_exact": parity, "saa_mean_equal": est["mean"] == w["mean"],
+            "cpu_model": cpu_model,
+            "single_thread": {"value": S1 / t1, "unit": UNIT, "cores": 1,
+                              "sample": "first %d scenarios, oracle split only" % S1}}
 
 
 if __name__ == "__main__":
