@@ -135,15 +135,15 @@ SPDP_API int spdp_version(void);
 SPDP_API const char* spdp_last_error(void);
 
 /* Measurement hook (bench.py): when both are non-NULL, every subsequent
- * spdp_split_eval / spdp_split_eval_batch / spdp_irp_dp call made by THIS
- * thread records `start_event` immediately before and `stop_event`
- * immediately after its dominant kernel (the sweep / IRP kernel), on the call's
- * stream.  Both are cudaEvent_t.  Pass NULL, NULL to clear.  Thread-local. */
+ * spdp_split_eval / _batch / _penalized / _neighbours / _limits, spdp_split_values
+ * or spdp_irp_dp call made by THIS thread records `start_event` immediately
+ * before and `stop_event` immediately after its dominant kernel(s) (the sweep /
+ * neighbour / limits / values / IRP kernels), on the call's stream.  Both are cudaEvent_t.  Pass NULL, NULL to clear.  Thread-local. */
 SPDP_API void spdp_set_profile_events(void* start_event, void* stop_event);
 
-/* Name of the sweep kernel (a5/a8 variant and its ring width) that the last
- * spdp_split_eval / spdp_split_eval_batch call on this thread enqueued, e.g.
- * "split_sweep_f2_kernel<20,3,2>"; "" before the first call.  Thread-local,
+/* Name of the dominant kernel (variant and ring width) that the last split call
+ * on this thread enqueued, e.g. "split_sweep_f2_kernel<20,3,1,0,20,0>" or
+ * "split_nbr_kernel<16,1>"; "" before the first call.  Thread-local,
  * owned by the library, valid until the next call on this thread.  For
  * reports (bench.py's roofline line); never needed for correctness. */
 SPDP_API const char* spdp_last_kernel(void);
