@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
 
 static int lim_num_sms() { return device_sms(); }
 
-static size_t lim_table_bytes(int32_t n) { return align_up(sizeof(int4) * (size_t)(n + 1), 256); }
+static size_t lim_table_bytes(int32_t n) { return align_up(sizeof(int4) * (size_t)tour_tab_stride(n), 256); }
 static size_t lim_scratch_bytes(int32_t n) {
     const size_t threads = (size_t)lim_num_sms() * lim_blocks_per_sm(n) * kLimThreads;
     return align_up(3 * sizeof(int) * (size_t)(n + 1) * threads, 256);

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict_
                                                       int4* __restrict__ etabs, int4* __restrict__ info) {
     const int t = blockIdx.x, lane = threadIdx.x;
     const int32_t* tour = tours + (int64_t)t * n;
-    int4* e = etabs + (int64_t)t * (n + 1);
+    int4* e = etabs + (int64_t)t * tour_tab_stride(n);
     const int64_t N1 = (int64_t)n + 1;
     auto node = [&](int i) -> int {  // customer at 0-based position i, clamped to 1..n
         const int c = tour[i];
@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict_
         carry += __shfl_sync(kFull, incl, 31);
     }
     if (lane == 0) e[0] = make_int4(0, dist[node(0)], 0, 0);  // A[0] = c_{0,s_1}
+    if (lane < kTourTabPad) e[n + 1 + lane] = make_int4(0, 0, 0, 0);  // padding (demand row 0)
     if (parent && info) {
         int a = n, last = -1;
         for (int b = 0; b < n; b += 32) {
@@ -231,17 +232,26 @@ __global__ void __launch_bounds__(128) split_values_ring_kernel(const int4* __re
 // Ring of the last W split points p (slot (p - a - 1) mod W): {G = f(p) + A[p],
 // Y = P(p) + Q} with P relative to P(a) = 0; p is in the window of layer i iff
 // Y >= P(i).  Seeded from the parent's f(a-W+1..a).  The candidate's position
-// table sits in shared memory (SM) or is read through L1; demands and b_parent of
-// the next kNbrPf layers are prefetched into static register slots (addresses:
-// one 32-bit multiply-add from the table's row offset / the layer index).  Ages
+// table sits in shared memory (SM) or is read through L1 (padded past n, so the
+// demand prefetch kNbrPf layers ahead needs no bounds check; addresses are one
+// 32-bit multiply-add from the row offset).  Phase A (layers a+1..s0-1, whole
+// W-layer chunks) is the plain Eq. (3) sweep; phase B (from the chunk holding s0)
+// adds the suffix combination min f(i) + b_parent(i), the per-lane stop once no
+// route starting before s0 reaches the layer, and the b_parent prefetch.  Ages
 // 2..kNbrU0+1 are scanned unconditionally, then groups of 4 behind a warp vote.
-// A lane whose window reaches past the ring is appended to the overflow list
+// A lane whose window reaches the oldest ring age is appended to the overflow list
 // (finished from scratch by split_finish_kernel on the candidate's own tables).
 constexpr int kNbrThreads = 128;
 constexpr int kNbrU0 = 8;
 
+__device__ __forceinline__ const void* mad_wide(uint32_t a, uint32_t b, const void* base) {
+    uint64_t r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(base));
+    return reinterpret_cast<const void*>(r);
+}
+
 template <int W, bool SM>
-__global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
+__global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kernel(
     const int4* __restrict__ etabs, const int4* __restrict__ info, int n, const uint16_t* __restrict__ demand,
     int64_t S, int Q, const int32_t* __restrict__ fwd, const int32_t* __restrict__ bwd,
     int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots, unsigned long long* __restrict__ ovf_list,
@@ -253,14 +263,19 @@ __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
     const int t = blockIdx.x;  // tours fastest: the CTAs resident together share scenario tiles (L2 reuse)
     const int4 in = info[t];
     const int a = in.x, s0 = in.y;
-    const int4* e = etabs + (int64_t)t * (n + 1);
+    const int stride = tour_tab_stride(n);
+    const int4* e = etabs + (int64_t)t * stride;
     if constexpr (SM) {
-        for (int i = threadIdx.x; i <= n; i += kNbrThreads) stab[i] = e[i];
+        for (int i = threadIdx.x; i < stride; i += kNbrThreads) stab[i] = e[i];
         __syncthreads();
     }
     auto tab = [&](int i) -> int4 {
         if constexpr (SM) return stab[i];
         else return __ldg(&e[i]);
+    };
+    auto rowoff = [&](int i) -> uint32_t {
+        if constexpr (SM) return (uint32_t)stab[i].w;
+        else return (uint32_t)__ldg(&e[i].w);
     };
     const int64_t s = (int64_t)blockIdx.y * kNbrThreads + threadIdx.x;
     const bool live = s < S;
@@ -268,11 +283,13 @@ __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
     const int32_t* fcol = fwd + col;
     const int32_t* bcol = bwd + col;
     const uint16_t* dcol = demand + col;
-    const uint32_t Su = (uint32_t)S;  // (n + 1) S < 2^32: row offsets of fwd / bwd in 32 bits
+    const uint32_t Su = (uint32_t)S, S4 = 4u * (uint32_t)S;  // (n + 1) S < 2^32, 4 S < 2^32
+    auto dem = [&](uint32_t off) -> int { return *static_cast<const uint16_t*>(mad_wide(off, 2u, dcol)); };
+    auto bwd_at = [&](int i) -> int { return *static_cast<const int32_t*>(mad_wide((uint32_t)i, S4, bcol)); };
     const int pc = fcol[(uint32_t)n * Su];  // the parent's cost: same customers, same feasibility (R4)
     int result = pc;
     bool ovf = false;
-    if (a < n) {  // (a, s0 are uniform per CTA; every lane enters: the loop votes over the full warp)
+    if (a < n) {  // (a, s0 are uniform per CTA; every lane enters: the loops vote over the full warp)
         int G[W], Y[W];
         {
             int P = 0;  // P(p) - P(a), walking p down from a
@@ -283,80 +300,100 @@ __global__ void __launch_bounds__(kNbrThreads) split_nbr_kernel(
                     const int4 ep = tab(p);
                     G[W - k] = fcol[(uint32_t)p * Su] + ep.y;
                     Y[W - k] = P + Q;
-                    if (p >= 1) P -= dcol[(uint32_t)ep.w];
+                    if (p >= 1) P -= dem((uint32_t)ep.w);
                 } else {
                     G[W - k] = INT_MAX;
                     Y[W - k] = INT_MIN;  // never in a window
                 }
             }
         }
-        int qb[kNbrPf], bb[kNbrPf];
+        int qb[kNbrPf];
+#pragma unroll
+        for (int k = 0; k < kNbrPf; ++k) qb[k] = dem(rowoff(a + 1 + k));  // (padded past n)
+        int P = 0;
+        // candidate scan of layer (slot j, load Pn): age 1 (slot j-1) is always in the window (q <= Q)
+        auto scan = [&](const int j, const int Pn, const bool active) -> int {
+            int best = G[(j - 1 + W) % W], best1 = INT_MAX;
+#pragma unroll
+            for (int k = 2; k < 2 + kNbrU0; ++k) {
+                const int sl = (j - k + W) % W;
+                if (Y[sl] >= Pn) {
+                    if (k & 1) best1 = min(best1, G[sl]);
+                    else best = min(best, G[sl]);
+                }
+            }
+#pragma unroll
+            for (int k0 = 2 + kNbrU0; k0 <= W; k0 += 4) {
+                if (!__any_sync(kFull, active && Y[(j - k0 + W) % W] >= Pn)) break;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int k = k0 + v;
+                    if (k <= W) {
+                        const int sl = (j - k + W) % W;
+                        if (Y[sl] >= Pn) {
+                            if (k & 1) best1 = min(best1, G[sl]);
+                            else best = min(best, G[sl]);
+                        }
+                    }
+                }
+            }
+            // age W (slot j) still in the window: the window may reach past the ring (conservative
+            // when that point is position 0; the finish kernel then recomputes the lane exactly)
+            if (active && Y[j] >= Pn) ovf = true;
+            return min(best, best1);
+        };
+        const bool feas = pc != SPDP_INFEASIBLE;  // an infeasible scenario only follows the warp
+        int base = a + 1;
+        // phase A: whole chunks before s0 -- the plain sweep
+        while (base + W <= s0) {
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const int i = base + j;
+                const int q = qb[j % kNbrPf];
+                qb[j % kNbrPf] = dem(rowoff(i + kNbrPf));
+                const int Pn = P + q;
+                const int best = scan(j, Pn, feas);
+                const int4 ei = tab(i);
+                G[j] = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
+                Y[j] = Pn + Q;
+                P = Pn;
+            }
+            base += W;
+        }
+        // phase B: from the chunk holding s0 to the stop
+        int bb[kNbrPf];
 #pragma unroll
         for (int k = 0; k < kNbrPf; ++k) {
-            const int i = a + 1 + k;
-            qb[k] = 0;
-            bb[k] = 0;
-            if (i <= n) {
-                qb[k] = dcol[(uint32_t)tab(i).w];
-                if (i >= s0) bb[k] = bcol[(uint32_t)i * Su];
-            }
+            const int i = base + k;
+            bb[k] = (i >= s0 && i <= n) ? bwd_at(i) : 0;
         }
-        int P = 0, Ps = 0;  // P(i) and P(s0 - 1) (= P(a) when s0 - 1 == a)
+        int Ps = P;  // P(s0 - 1) when base == s0; else set at layer s0 - 1 below
         int total = INT_MAX;
-        bool active = pc != SPDP_INFEASIBLE;  // an infeasible scenario only follows the warp
-        for (int base = a + 1;; base += W) {
+        bool active = feas;
+        for (;; base += W) {
 #pragma unroll
             for (int j = 0; j < W; ++j) {
                 const int i = base + j;
                 if (i > n) break;  // warp-uniform
-                const int4 ei = tab(i);
                 const int q = qb[j % kNbrPf];
                 const int bv = bb[j % kNbrPf];
                 const int ia = i + kNbrPf;
-                if (ia <= n) {
-                    qb[j % kNbrPf] = dcol[(uint32_t)tab(ia).w];
-                    if (ia >= s0) bb[j % kNbrPf] = bcol[(uint32_t)ia * Su];
-                }
+                qb[j % kNbrPf] = dem(rowoff(ia));
+                if (ia >= s0 && ia <= n) bb[j % kNbrPf] = bwd_at(ia);
                 const int Pn = P + q;
                 // no route starting before s0 reaches layer i: the boundary set [s0, i-1] is complete
                 if (i > s0 && Pn - Ps > Q) active = false;
-                int best = G[(j - 1 + W) % W];  // age 1: always in the window (q <= Q)
-                int best1 = INT_MAX;            // second min chain (odd ages)
-#pragma unroll
-                for (int k = 2; k < 2 + kNbrU0; ++k) {
-                    const int sl = (j - k + W) % W;
-                    if (Y[sl] >= Pn) {
-                        if (k & 1) best1 = min(best1, G[sl]);
-                        else best = min(best, G[sl]);
-                    }
-                }
-#pragma unroll
-                for (int k0 = 2 + kNbrU0; k0 <= W; k0 += 4) {
-                    if (!__any_sync(kFull, active && Y[(j - k0 + W) % W] >= Pn)) break;
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int k = k0 + v;
-                        if (k <= W) {
-                            const int sl = (j - k + W) % W;
-                            if (Y[sl] >= Pn) {
-                                if (k & 1) best1 = min(best1, G[sl]);
-                                else best = min(best, G[sl]);
-                            }
-                        }
-                    }
-                }
-                best = min(best, best1);
-                // age W (slot j) in the window and an older split point exists: past the ring
-                if (active && Y[j] >= Pn && i - W >= 1) ovf = true;
+                const int best = scan(j, Pn, active);
+                const int4 ei = tab(i);
                 if (active && i >= s0) total = min(total, best + ei.z + bv);
-                G[j] = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
+                G[j] = best + ei.y + ei.z;
                 Y[j] = Pn + Q;
                 if (i == s0 - 1) Ps = Pn;
                 P = Pn;
             }
             if (base + W > n || !__any_sync(kFull, active && !ovf)) break;
         }
-        result = pc == SPDP_INFEASIBLE ? pc : total;
+        result = feas ? total : pc;
     }
     const bool deferred = live && ovf;
     if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
@@ -382,7 +419,6 @@ spdp_status launch_tour_table(const int32_t* tours, int32_t T, const int32_t* pa
     return last_launch("nbr_prep_kernel");
 }
 
-
 // The same restarted sweep with the ring in shared memory ([W][NT] {G, Y} per CTA,
 // slot p mod W, conflict-free 8-byte rows): the layer loop is unrolled only by the
 // prefetch distance and the candidate scan is a loop of 4-candidate groups behind a
@@ -402,7 +438,7 @@ __global__ void __launch_bounds__(NT) split_nbr_smem_kernel(
     const int t = blockIdx.x;
     const int4 in = info[t];
     const int a = in.x, s0 = in.y;
-    const int4* tb = etabs + (int64_t)t * (n + 1);
+    const int4* tb = etabs + (int64_t)t * tour_tab_stride(n);
     if (table_in_smem) {
         int4* st = sm4 + (W * NT) / 2;
         for (int i = threadIdx.x; i <= n; i += NT) st[i] = tb[i];
@@ -515,7 +551,7 @@ __global__ void __launch_bounds__(NT) split_nbr_smem_kernel(
     }
 }
 
-static size_t etab_bytes(int32_t n, int32_t T) { return align_up(sizeof(int4) * (size_t)T * (size_t)(n + 1), 256); }
+static size_t etab_bytes(int32_t n, int32_t T) { return align_up(sizeof(int4) * (size_t)T * (size_t)tour_tab_stride(n), 256); }
 
 static spdp_status check_common(const char* fn, int32_t n, int64_t S, int32_t Q, int64_t ld, const void* demand) {
     if (n < 1) return fail(SPDP_E_USAGE, "%s: n=%d < 1", fn, n);
@@ -584,8 +620,8 @@ static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info
     const dim3 grid((unsigned)T, (unsigned)ceil_div(S, kNbrThreads));
     prof_begin(st);
     if (n <= kNbrSmemMaxN) {
-        const size_t smem = sizeof(int4) * (size_t)(n + 1);
-        if (spdp_status e = kernel_setup((const void*)split_nbr_kernel<W, true>, (int)(sizeof(int4) * (kNbrSmemMaxN + 1)),
+        const size_t smem = sizeof(int4) * (size_t)tour_tab_stride(n);
+        if (spdp_status e = kernel_setup((const void*)split_nbr_kernel<W, true>, (int)(sizeof(int4) * tour_tab_stride(kNbrSmemMaxN)),
                                          -1, 0, 0, nullptr, "split_nbr_kernel setup"))
             return e;
         split_nbr_kernel<W, true><<<grid, kNbrThreads, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,

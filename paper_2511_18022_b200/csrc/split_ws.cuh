@@ -57,6 +57,11 @@ spdp_status launch_finish(char* ws, const WsLayout& L, int32_t T, int32_t n, con
                           int64_t S, uint32_t Qe, int32_t* cost, spdp_saa_partial* partial, bool pdl,
                           cudaStream_t st);
 
+// Position tables of nbr.cu / limits.cu: n + 1 entries per tour plus kTourTabPad padding entries
+// (row offset 0: a valid demand row) so prefetches past position n need no bounds check.
+constexpr int kTourTabPad = 8;
+__host__ __device__ inline int tour_tab_stride(int n) { return n + 1 + kTourTabPad; }
+
 // nbr.cu: per-tour position tables e[t][i] = {row of sigma_i, A[i], B[i], row * ld (uint32)},
 // i = 0..n, for T tours [T][n]; with parent != NULL also info[t] = {common prefix length,
 // n - common suffix length} against the parent.  One warp per tour.
