@@ -28,8 +28,8 @@ namespace spdp {
 constexpr int kNbrPf = 8;            // demand / b prefetch distance (layers)
 constexpr int kNbrSmemMaxN = 4095;  // position table in shared memory up to (n + 1) 16 B = 64 KB
 
-// Per-tour position table e[i], i = 0..n:  {row of customer sigma_i (i >= 1), A[i] (i < n),
-// B[i] (i >= 1), row * ld as a uint32 element offset (used when n ld < 2^32)}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
+// Per-tour position table e[i], i = 0..n:  {Cg[i] = A[i] + B[i], A[i] (i < n), B[i] (i >= 1),
+// row * ld of customer sigma_i as a uint32 element offset (callers check n ld < 2^32)}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
 // D[1] = 0, D[i] = D[i-1] + c_{s_{i-1},s_i}.
 // info[t] = {a, s0, 0, 0}: a = common prefix length with the parent, s0 = n - common suffix
 // length (a = s0 = n: the tour equals the parent).  One warp per tour.
@@ -58,15 +58,15 @@ __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict_
         const long long D = carry + incl - arc;  // D[i+1]
         if (i < n) {
             int4 v;
-            v.x = c - 1;
             v.y = (i + 1 < n) ? (int)(dist[node(i + 1)] - (D + arc)) : 0;  // A[i+1] = c_{0,s_{i+2}} - D[i+2]
             v.z = (int)(D + dist[(int64_t)c * N1]);                          // B[i+1]
+            v.x = v.y + v.z;                                                 // Cg[i+1] = A + B: g(i+1) - min
             v.w = (int)(uint32_t)((uint64_t)(c - 1) * (uint64_t)ld);  // element offset of the row (n ld < 2^32)
             e[i + 1] = v;
         }
         carry += __shfl_sync(kFull, incl, 31);
     }
-    if (lane == 0) e[0] = make_int4(0, dist[node(0)], 0, 0);  // A[0] = c_{0,s_1}
+    if (lane == 0) e[0] = make_int4(dist[node(0)], dist[node(0)], 0, 0);  // A[0] = c_{0,s_1} (Cg[0] = A[0])
     if (lane < kTourTabPad) e[n + 1 + lane] = make_int4(0, 0, 0, 0);  // padding (demand row 0)
     if (parent && info) {
         int a = n, last = -1;
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) split_values_kernel(const int4* __restric
     const uint16_t* dcol = demand + s;
     int32_t* fc = fwd + s;
     int32_t* bc = bwd + s;
-    auto q_at = [&](int i) -> int { return dcol[(int64_t)__ldg(&e[i].x) * ld]; };  // q of position i >= 1
+    auto q_at = [&](int i) -> int { return dcol[(uint32_t)__ldg(&e[i].w)]; };  // q of position i >= 1
     // forward: f(i) = B[i] + min_{p in [m, i-1]} f(p) + A[p], m = mask(i)
     fc[0] = 0;
     {
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) split_values_kernel(const int4* __restric
         bool bad = false;
         for (int i = 1; i <= n; ++i) {
             const int4 ei = __ldg(&e[i]);
-            const int q = dcol[(int64_t)ei.x * ld];
+            const int q = dcol[(uint32_t)ei.w];
             bad |= q > Q;
             if (bad) {
                 fc[(int64_t)i * S] = SPDP_INFEASIBLE;
@@ -353,8 +353,7 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
                 qb[j % kNbrPf] = dem(rowoff(i + kNbrPf));
                 const int Pn = P + q;
                 const int best = scan(j, Pn, feas);
-                const int4 ei = tab(i);
-                G[j] = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
+                G[j] = best + tab(i).x;  // g(i) = f(i) + A[i] = best + Cg[i]
                 Y[j] = Pn + Q;
                 P = Pn;
             }
@@ -386,7 +385,7 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
                 const int best = scan(j, Pn, active);
                 const int4 ei = tab(i);
                 if (active && i >= s0) total = min(total, best + ei.z + bv);
-                G[j] = best + ei.y + ei.z;
+                G[j] = best + ei.x;
                 Y[j] = Pn + Q;
                 if (i == s0 - 1) Ps = Pn;
                 P = Pn;
@@ -524,7 +523,7 @@ __global__ void __launch_bounds__(NT) split_nbr_smem_kernel(
                 // the scan reached age W still inside the window and an older point exists
                 if (deep && active && R(i - W).y >= Pn && i - W >= 1) ovf = true;
                 if (active && i >= s0) total = min(total, best + ei.z + bv);
-                gprev = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
+                gprev = best + ei.x;  // g(i) = f(i) + A[i] = best + Cg[i]
                 R(i) = make_int2(gprev, Pn + Q);  // (slot of position i - W, no longer needed)
                 if (i == s0 - 1) Ps = Pn;
                 P = Pn;
