@@ -28,8 +28,9 @@ namespace spdp {
 constexpr int kNbrPf = 8;            // demand / b prefetch distance (layers)
 constexpr int kNbrSmemMaxN = 4095;  // position table in shared memory up to (n + 1) 16 B = 64 KB
 
-// Per-tour position table e[i], i = 0..n:  {Cg[i] = A[i] + B[i], A[i] (i < n), B[i] (i >= 1),
-// row * ld of customer sigma_i as a uint32 element offset (callers check n ld < 2^32)}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
+// Per-tour position table e[i], i = 0..n:  {float bits of Cg[i] 2^-24 with Cg = A + B (the fp32
+// phase of the neighbour sweep), A[i] (i < n), B[i] (i >= 1), row * ld of customer sigma_i as a
+// uint32 element offset (callers check n ld < 2^32)}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
 // D[1] = 0, D[i] = D[i-1] + c_{s_{i-1},s_i}.
 // info[t] = {a, s0, 0, 0}: a = common prefix length with the parent, s0 = n - common suffix
 // length (a = s0 = n: the tour equals the parent).  One warp per tour.
@@ -60,13 +61,13 @@ __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict_
             int4 v;
             v.y = (i + 1 < n) ? (int)(dist[node(i + 1)] - (D + arc)) : 0;  // A[i+1] = c_{0,s_{i+2}} - D[i+2]
             v.z = (int)(D + dist[(int64_t)c * N1]);                          // B[i+1]
-            v.x = v.y + v.z;                                                 // Cg[i+1] = A + B: g(i+1) - min
+            v.x = __float_as_int((float)(v.y + v.z) * 0x1p-24f);             // Cg[i+1] 2^-24 (exact when |Cg| < 2^24)
             v.w = (int)(uint32_t)((uint64_t)(c - 1) * (uint64_t)ld);  // element offset of the row (n ld < 2^32)
             e[i + 1] = v;
         }
         carry += __shfl_sync(kFull, incl, 31);
     }
-    if (lane == 0) e[0] = make_int4(dist[node(0)], dist[node(0)], 0, 0);  // A[0] = c_{0,s_1} (Cg[0] = A[0])
+    if (lane == 0) e[0] = make_int4(0, dist[node(0)], 0, 0);  // A[0] = c_{0,s_1}
     if (lane < kTourTabPad) e[n + 1 + lane] = make_int4(0, 0, 0, 0);  // padding (demand row 0)
     if (parent && info) {
         int a = n, last = -1;
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
     const int4* __restrict__ etabs, const int4* __restrict__ info, int n, const uint16_t* __restrict__ demand,
     int64_t S, int Q, const int32_t* __restrict__ fwd, const int32_t* __restrict__ bwd,
     int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots, unsigned long long* __restrict__ ovf_list,
-    unsigned* __restrict__ ovf_count) {
+    unsigned* __restrict__ ovf_count, const TourInfo* __restrict__ tinfo, int f32_loads) {
     static_assert(W % kNbrPf == 0, "the prefetch distance must divide the ring");
     static_assert(kNbrU0 % 4 == 0 && kNbrU0 < W, "unconditional ages");
     __shared__ Part red[kNbrThreads / 32];
@@ -344,6 +345,62 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
         };
         const bool feas = pc != SPDP_INFEASIBLE;  // an infeasible scenario only follows the warp
         int base = a + 1;
+        const TourInfo ti = tinfo[t];
+        if (f32_loads && ti.ok && base + W <= s0) {
+            // phase A in exact fp32, the candidate masking on the FMA pipe (as split_sweep_f2_kernel):
+            // G = (g + OFF) 2^-24 in [0, 1); loads as the bits of 2^23 + BIAS + P (+ Q), so P += q is an
+            // integer add on the bits; s = sat(P(i) - Y) is 0 inside the window and 1 outside, and
+            // G + s >= 1 > every in-window G.  (Host: (n + W) Qe + Q + 1 < 2^23; tour: TourInfo::ok.)
+            constexpr uint32_t kMagic = 0x4B000000u;
+            const uint32_t bias = (uint32_t)W * (uint32_t)Q + 1u;  // every seed load >= -W Q: bias + P >= 1
+            const float offf = (float)ti.off;
+            float Gf[W];
+            uint32_t Yb[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                Gf[k] = (Y[k] == INT_MIN) ? 0.0f : ((float)(G[k] + ti.off)) * 0x1p-24f;
+                Yb[k] = (Y[k] == INT_MIN) ? 0u : kMagic + bias + (uint32_t)Y[k];  // (float 0: never in a window)
+            }
+            uint32_t Pb = kMagic + bias + (uint32_t)P;
+            while (base + W <= s0) {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    const int i = base + j;
+                    const uint32_t q = (uint32_t)qb[j % kNbrPf];
+                    qb[j % kNbrPf] = dem(rowoff(i + kNbrPf));
+                    const uint32_t Pnb = Pb + q;
+                    const float Pn = __uint_as_float(Pnb);
+                    auto cand = [&](const int k) -> float {
+                        const int sl = (j - k + W) % W;
+                        return Gf[sl] + __saturatef(Pn - __uint_as_float(Yb[sl]));
+                    };
+                    float best = Gf[(j - 1 + W) % W];  // age 1
+#pragma unroll
+                    for (int k = 2; k < 2 + kNbrU0; k += 2) best = fminf(best, fminf(cand(k), cand(k + 1)));
+#pragma unroll
+                    for (int k0 = 2 + kNbrU0; k0 <= W; k0 += 4) {
+                        if (!__any_sync(kFull, feas && Yb[(j - k0 + W) % W] >= Pnb)) break;
+#pragma unroll
+                        for (int v = 0; v < 4; v += 2)
+                            if (k0 + v + 1 <= W) best = fminf(best, fminf(cand(k0 + v), cand(k0 + v + 1)));
+                            else if (k0 + v <= W) best = fminf(best, cand(k0 + v));
+                    }
+                    if (feas && Yb[j] >= Pnb) ovf = true;  // age W still in the window
+                    Gf[j] = best + __int_as_float(tab(i).x);  // + Cg[i] 2^-24
+                    Yb[j] = Pnb + (uint32_t)Q;
+                    Pb = Pnb;
+                }
+                base += W;
+            }
+            // back to the int32 ring for phase B
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                G[k] = (int)(Gf[k] * 0x1p24f) - ti.off;
+                Y[k] = (Yb[k] < kMagic) ? INT_MIN : (int)(Yb[k] - kMagic - bias);
+            }
+            P = (int)(Pb - kMagic - bias);
+            (void)offf;
+        }
         // phase A: whole chunks before s0 -- the plain sweep
         while (base + W <= s0) {
 #pragma unroll
@@ -353,7 +410,8 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
                 qb[j % kNbrPf] = dem(rowoff(i + kNbrPf));
                 const int Pn = P + q;
                 const int best = scan(j, Pn, feas);
-                G[j] = best + tab(i).x;  // g(i) = f(i) + A[i] = best + Cg[i]
+                const int4 ei = tab(i);
+                G[j] = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
                 Y[j] = Pn + Q;
                 P = Pn;
             }
@@ -385,7 +443,7 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
                 const int best = scan(j, Pn, active);
                 const int4 ei = tab(i);
                 if (active && i >= s0) total = min(total, best + ei.z + bv);
-                G[j] = best + ei.x;
+                G[j] = best + ei.y + ei.z;
                 Y[j] = Pn + Q;
                 if (i == s0 - 1) Ps = Pn;
                 P = Pn;
@@ -523,7 +581,7 @@ __global__ void __launch_bounds__(NT) split_nbr_smem_kernel(
                 // the scan reached age W still inside the window and an older point exists
                 if (deep && active && R(i - W).y >= Pn && i - W >= 1) ovf = true;
                 if (active && i >= s0) total = min(total, best + ei.z + bv);
-                gprev = best + ei.x;  // g(i) = f(i) + A[i] = best + Cg[i]
+                gprev = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
                 R(i) = make_int2(gprev, Pn + Q);  // (slot of position i - W, no longer needed)
                 if (i == s0 - 1) Ps = Pn;
                 P = Pn;
@@ -615,7 +673,8 @@ extern "C" size_t spdp_neighbour_workspace_bytes(int32_t n, int64_t S, int32_t T
 template <int W>
 static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info, int n, const uint16_t* demand,
                                 int64_t S, int T, int Q, const int32_t* fwd, const int32_t* bwd,
-                                int32_t* cost, spdp_saa_partial* slots, unsigned long long* ovf, unsigned* ovf_count) {
+                                int32_t* cost, spdp_saa_partial* slots, unsigned long long* ovf, unsigned* ovf_count,
+                                const TourInfo* tinfo, int f32_loads) {
     const dim3 grid((unsigned)T, (unsigned)ceil_div(S, kNbrThreads));
     prof_begin(st);
     if (n <= kNbrSmemMaxN) {
@@ -624,10 +683,10 @@ static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info
                                          -1, 0, 0, nullptr, "split_nbr_kernel setup"))
             return e;
         split_nbr_kernel<W, true><<<grid, kNbrThreads, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,
-                                                                   ovf_count);
+                                                                   ovf_count, tinfo, f32_loads);
     } else {
         split_nbr_kernel<W, false><<<grid, kNbrThreads, 0, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,
-                                                                 ovf_count);
+                                                                 ovf_count, tinfo, f32_loads);
     }
     prof_end(st);
     set_last_kernel("split_nbr_kernel<%d,%d>", W, n <= kNbrSmemMaxN ? 1 : 0);
@@ -700,10 +759,14 @@ extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const i
                                 : launch_nbr_smem_t<32>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
     } else {  // the register ring: 16 entries up to a hinted window of 24 (measured faster than 24 or 32
               // entries at C3 even with the overflow lanes it sends to the finish kernel), else 32
+        const TourInfo* tinfo = reinterpret_cast<const TourInfo*>(w + L.tinfo);
+        // the fp32 phase: every load value it forms, (n + W) Qe + Q + 1, below 2^23 (exact floats)
+        const int f32 = ((flags & SPDP_F_SWEEP_INT) == 0 &&
+                         ((int64_t)n + 32) * (int64_t)Qe + (int64_t)Qe + 1 < (1LL << 23)) ? 1 : 0;
         if (window_hint != 0 && window_hint <= 24)
-            rc = launch_nbr_t<16>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+            rc = launch_nbr_t<16>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count, tinfo, f32);
         else
-            rc = launch_nbr_t<32>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count);
+            rc = launch_nbr_t<32>(st, e, info, n, demand, S, T, Qe, fwd, bwd, cost, slots, ovf, ovf_count, tinfo, f32);
     }
     if (rc) return rc;
     return launch_finish(w, L, T, n, demand, ld, S, (uint32_t)Qe, cost, partial, false, st);

@@ -19,9 +19,9 @@ fwd, bwd = spdp.split_values(parent, dist, d, inst["Q"], S=cfg["S"])
 pops = {"C3": cfg["tours"], "granular": synth.local_move_tours(inst["tour"], cfg["T"], 400)}
 for name, tt in pops.items():
     tours = torch.from_numpy(np.ascontiguousarray(tt)).to(dev)
-    for h, smem in [(20, False), (32, False), (20, True)]:
+    for h, smem, io in [(20, False, False), (20, False, True), (20, True, False)]:
         fn = lambda: spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, d, inst["Q"], S=cfg["S"],
-                                                want_cost=False, window_hint=h, smem=smem)
+                                                want_cost=False, window_hint=h, smem=smem, int_only=io)
         for _ in range(2):
             fn()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -30,4 +30,4 @@ for name, tt in pops.items():
             fn()
         b.record()
         torch.cuda.synchronize()
-        print("%-9s hint=%2d %-26s %.3f ms" % (name, h, spdp.last_kernel(), a.elapsed_time(b) / 5))
+        print("%-9s hint=%2d int_only=%d %-26s %.3f ms" % (name, h, io, spdp.last_kernel(), a.elapsed_time(b) / 5))

@@ -69,11 +69,11 @@ def _candidates(tour, T, seed):
     return np.ascontiguousarray(np.stack(out), dtype=np.int32)
 
 
-@pytest.mark.parametrize("smem", [False, True])
+@pytest.mark.parametrize("smem,int_only", [(False, False), (False, True), (True, False)])
 @pytest.mark.parametrize("name,S,T,hint,extra_q", [
     ("C1", 100, 24, 0, 0), ("C2", 3_001, 40, 16, 0), ("C2", 2_003, 30, 24, 30), ("C3", 1_001, 40, 32, 0),
     ("C3", 777, 20, 16, 0), ("C4", 203, 12, 16, 0), ("C4", 203, 12, 32, 0), ("C4", 203, 12, 64, 0)])
-def test_neighbours_parity(spdp, name, S, T, hint, extra_q, smem):
+def test_neighbours_parity(spdp, name, S, T, hint, extra_q, smem, int_only):
     """Bit-exact vs the oracle's split of every candidate (C4 with a 16-entry ring sends most
     lanes through the overflow path)."""
     cfg = synth.config_instance(name, S=S)
@@ -85,7 +85,7 @@ def test_neighbours_parity(spdp, name, S, T, hint, extra_q, smem):
     parent, dist, D = to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem)
     fwd, bwd = spdp.split_values(parent, dist, D, cfg["Q"], S=S)
     cost, part = spdp.split_eval_neighbours(parent, fwd, bwd, to_dev(tours), dist, D, cfg["Q"], S=S,
-                                            window_hint=hint, validate=True, smem=smem)
+                                            window_hint=hint, validate=True, smem=smem, int_only=int_only)
     want = as_i32(oracle.split_tours(tours, inst["dist"], dem, cfg["Q"], S=S))
     got = cost.cpu().numpy().astype(np.int64)
     assert np.array_equal(got, want)
@@ -103,10 +103,13 @@ def test_neighbours_match_batch_at_full_C3(spdp):
     tours = to_dev(cfg["tours"])
     parent, dist = to_dev(inst["tour"]), to_dev(inst["dist"])
     fwd, bwd = spdp.split_values(parent, dist, D, cfg["Q"], S=S)
-    cost, part = spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, D, cfg["Q"], S=S, window_hint=24)
+    cost, part = spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, D, cfg["Q"], S=S, window_hint=20)
     bcost, bpart = spdp.split_eval_batch(tours, dist, D, cfg["Q"], S=S, window_hint=24)
     assert torch.equal(cost, bcost)
     assert torch.equal(part, bpart)
+    icost, ipart = spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, D, cfg["Q"], S=S, window_hint=20,
+                                              int_only=True)
+    assert torch.equal(icost, bcost) and torch.equal(ipart, bpart)
     cols = np.random.default_rng(5).choice(S, size=64, replace=False)
     dem = D.cpu().numpy().view(np.uint16)[:, cols]
     dem = np.ascontiguousarray(np.pad(dem, ((0, 0), (0, (-dem.shape[1]) % 8))))
