@@ -58,9 +58,11 @@ def _L():
         lib.oracle_split_penalized.argtypes = [i32, P, P, i32, i64, P, i64, i64, P, P, ctypes.c_int]
         lib.oracle_split_values.argtypes = [i32, P, P, i32, P, i64, i64, P, P, ctypes.c_int]
         lib.oracle_split_limits.argtypes = [i32, P, P, i32, i64, i32, P, i64, i64, P, P, P, ctypes.c_int]
+        lib.oracle_split_f32.argtypes = [i32, P, P, i32, P, i64, i64, P, ctypes.c_int]
+        lib.oracle_saa_f32.argtypes = [P, i64, P]
         lib.oracle_irp.argtypes = [i32, i32, P, P, P, i64, i64, P, ctypes.c_int]
         for name in ("oracle_gen_demands", "oracle_split_batch", "oracle_split_batch_tours", "oracle_split_penalized",
-                     "oracle_split_values", "oracle_split_limits",
+                     "oracle_split_values", "oracle_split_limits", "oracle_split_f32", "oracle_saa_f32",
                      "oracle_saa", "oracle_irp", "oracle_num_threads"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -216,6 +218,33 @@ def split_limits(tour, dist, demand, Q, Lmax: int = -1, K: int = 0, want_pred: b
     if rc:
         raise ValueError("oracle_split_limits rc=%d" % rc)
     return (cost, pred, kused) if want_pred else cost
+
+
+def split_f32(tour, dist, demand, Q, S: int | None = None, threads: int = 0) -> np.ndarray:
+    """a5 fp32 mode (DESIGN R25): real-valued costs dist (fp64 [(n+1)^2]); float32 [S] costs
+    (+inf = infeasible), each candidate one fp32 add of the route cost rounded once from fp64."""
+    tour = np.ascontiguousarray(tour, dtype=np.int32)
+    dist = np.ascontiguousarray(dist, dtype=np.float64)
+    demand = np.ascontiguousarray(demand, dtype=np.uint16)
+    n = tour.shape[0]
+    ld = demand.shape[1]
+    S = ld if S is None else S
+    cost = np.zeros(S, dtype=np.float32)
+    rc = _L().oracle_split_f32(n, _p(tour), _p(dist), int(Q), _p(demand), ld, int(S), _p(cost), int(threads))
+    if rc:
+        raise ValueError("oracle_split_f32 rc=%d" % rc)
+    return cost
+
+
+def saa_f32(cost) -> dict:
+    """SAA of float32 costs: sequential fp64 sums, two-pass variance."""
+    cost = np.ascontiguousarray(cost, dtype=np.float32)
+    out = np.zeros(7, dtype=np.float64)
+    rc = _L().oracle_saa_f32(_p(cost), cost.shape[0], _p(out))
+    if rc == 3:
+        raise ValueError("all scenarios infeasible (SPEC:287)")
+    return {"m": int(out[0]), "infeasible": int(out[1]), "mean": out[2], "var": out[3], "stderr": out[4],
+            "ci95_lo": out[5], "ci95_hi": out[6]}
 
 
 def split_tours(tours, dist, demand, Q, S: int | None = None, threads: int = 0) -> np.ndarray:

@@ -33,7 +33,10 @@
  *                            transposed costs; f(i) + b(i) >= cost, = at optimal boundaries
  *   oracle_split_limits      brute force over partitions with <= K routes of duration
  *                            <= Lmax; no limits = plain split; monotone in K and Lmax
+ *   oracle_split_f32         integer-valued costs = oracle_split exactly; real costs within the
+ *                            fp32 rounding bound of an fp64 brute force over partitions
  *   oracle_saa               Python statistics.fmean/variance (exact Fractions) on costs
+ *   oracle_saa_f32           Python statistics on exact Fractions within 1e-12 relative
  *   oracle_irp               brute force over all action sequences (pure Python, in
  *                            the test); two closed forms
  */
@@ -553,6 +556,88 @@ int oracle_saa(const int64_t* cost, int64_t S, double* out, uint64_t* sums_out)
     } else {
         out[3] = 0.0;
     }
+    out[4] = sqrt(out[3] / (double)m);
+    out[5] = out[2] - 1.96 * out[4];
+    out[6] = out[2] + 1.96 * out[4];
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a5 fp32 mode (SURVEY §8(a) a2/a5 "fp32 (one add + exact min)", §8(c3)    */
+/* "fp32 mode (secondary)"; DESIGN R25): real-valued costs c (fp64 input).   */
+/*   Dd[1] = 0, Dd[i] = Dd[i-1] + c[s_{i-1}][s_i]      (fp64, sequential)     */
+/*   T32(p,i) = (float)((c[0][s_{p+1}] + (Dd[i] - Dd[p+1])) + c[s_i][0])     */
+/*             (the route cost of Eq. (1), rounded ONCE to fp32)   */
+/*   f(0) = 0, f(i) = min_{mask(i) <= p <= i-1} fl32(f(p) + T32(p,i))         */
+/* Descending scan with the exact capacity break (as oracle_split_batch),    */
+/* each candidate one IEEE single add (SSE, -ffp-contract=off), exact min.   */
+/* cost[s] = f(n), +INFINITY when infeasible (a demand above Q, R4).          */
+/* ------------------------------------------------------------------------ */
+int oracle_split_f32(int32_t n, const int32_t* tour, const double* dist, int32_t Q,
+                     const uint16_t* demand, int64_t ld, int64_t S, float* cost, int threads)
+{
+    if (n < 1 || S < 0 || Q < 1 || ld < S) return 2;
+    const int64_t N1 = (int64_t)n + 1;
+    double* Dd = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    Dd[0] = 0.0;
+    Dd[1] = 0.0;
+    for (int32_t i = 2; i <= n; ++i) Dd[i] = Dd[i - 1] + dist[(int64_t)tour[i - 2] * N1 + tour[i - 1]];
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel
+#endif
+    {
+        int64_t* q = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+        float* f = (float*)malloc(sizeof(float) * (size_t)(n + 1));
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+        for (int64_t s = 0; s < S; ++s) {
+            for (int32_t k = 1; k <= n; ++k) q[k - 1] = demand[(int64_t)(tour[k - 1] - 1) * ld + s];
+            f[0] = 0.0f;
+            for (int32_t i = 1; i <= n; ++i) {
+                float best = INFINITY;
+                int64_t load = 0;
+                for (int32_t p = i - 1; p >= 0; --p) {
+                    load += q[p];                                   /* q_{sigma_{p+1}} */
+                    if (load > Q) break;
+                    const double t64 = (dist[0 * N1 + tour[p]] + (Dd[i] - Dd[p + 1])) + dist[(int64_t)tour[i - 1] * N1 + 0];
+                    const float t32 = (float)t64;
+                    const float cand = f[p] + t32;
+                    if (cand < best) best = cand;
+                }
+                f[i] = best;
+            }
+            cost[s] = f[n];
+        }
+        free(q);
+        free(f);
+    }
+    free(Dd);
+    return 0;
+}
+
+/* SAA of fp32 costs (SURVEY §8(c5) fp32 mode): over the finite costs, sequential */
+/* fp64 sums, two passes: mean = sum / m, var = sum (c - mean)^2 / (m - 1).       */
+/* out: as oracle_saa.                                                             */
+int oracle_saa_f32(const float* cost, int64_t S, double* out)
+{
+    int64_t m = 0, inf = 0;
+    double sum = 0.0;
+    for (int64_t s = 0; s < S; ++s) {
+        if (isinf(cost[s])) { inf++; continue; }
+        m++;
+        sum += (double)cost[s];
+    }
+    out[0] = (double)m;
+    out[1] = (double)inf;
+    if (m == 0) return 3;
+    const double mean = sum / (double)m;
+    double ss = 0.0;
+    for (int64_t s = 0; s < S; ++s)
+        if (!isinf(cost[s])) ss += ((double)cost[s] - mean) * ((double)cost[s] - mean);
+    out[2] = mean;
+    out[3] = m >= 2 ? ss / (double)(m - 1) : 0.0;
     out[4] = sqrt(out[3] / (double)m);
     out[5] = out[2] - 1.96 * out[4];
     out[6] = out[2] + 1.96 * out[4];
