@@ -564,6 +564,20 @@ def measure_rows(spdp, torch, dev, pk):
                    "infeasible": int(partl[1].item()), "kernel": spdp.last_kernel()}
     rows["f4_limits_C2"] = f4
     del d
+    # a5 fp32 mode at C2: real-valued (unrounded Euclidean, fp64) costs, float32 DP (DESIGN R25)
+    cfg2 = synth.config_instance("C2")
+    inst2 = cfg2["inst"]
+    d = spdp.gen_demands(cfg2["model"], 0, cfg2["S"], device=dev)
+    xy = np.asarray(inst2["coords"], dtype=np.float64)
+    distf = torch.from_numpy(np.ascontiguousarray(np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1)))).to(dev)
+    tour2 = torch.from_numpy(inst2["tour"]).to(dev)
+    costf = torch.empty(cfg2["S"], dtype=torch.float32, device=dev)
+    ms = _time_events(lambda: spdp.split_eval_f32(tour2, distf, d, inst2["Q"], S=cfg2["S"], cost=costf), torch, dev,
+                      iters=5)
+    est = spdp.saa_estimate_f32(costf)
+    rows["a5_f32_C2"] = {"ms": ms, "evals_per_s": cfg2["S"] / (ms / 1e3), "kernel": spdp.last_kernel(),
+                         "saa_mean": est["mean"]}
+    del d
     # f2: penalized split at C2 (lambda = 10 cost units per unit of overload, Q of C2)
     cfg2 = synth.config_instance("C2")
     inst2 = cfg2["inst"]

@@ -295,6 +295,27 @@ SPDP_API spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t* 
                                    spdp_saa_partial* partial, void* ws, size_t ws_bytes, uint32_t flags,
                                    spdp_stream_t stream);
 
+/* a5 fp32 mode (DESIGN R25): real-valued route costs.
+ * dist: DEVICE fp64 [(n+1)*(n+1)] row-major (c_{a,b} >= 0).  With the fp64 prefix
+ * Dd[1] = 0, Dd[i] = Dd[i-1] + c_{s_{i-1},s_i} (sequential) and the route cost of
+ * Eq. (1) rounded once, T32(p,i) = fl32((c_{0,s_{p+1}} + (Dd[i] - Dd[p+1])) + c_{s_i,0}):
+ *   f(0) = 0,  f(i) = min_{mask(i) <= p <= i-1} fl32(f(p) + T32(p,i))
+ *   cost[j] = f(n) of scenario j (float [S], +INFINITY when a demand exceeds Q).
+ * One IEEE single add per candidate and an exact min: bit-identical for every launch
+ * configuration.  One thread per scenario, any window.  ws: spdp_f32_workspace_bytes(n, S)
+ * bytes (the f rows [n+1][S] fp32 + the position table).  n ld < 2^32. */
+SPDP_API size_t spdp_f32_workspace_bytes(int32_t n, int64_t S);
+SPDP_API spdp_status spdp_split_eval_f32(const int32_t* tour, const double* dist, int32_t n,
+                                const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                                float* cost, void* ws, size_t ws_bytes, spdp_stream_t stream);
+
+/* SAA estimate of fp32 costs (SURVEY §8(c5) fp32 mode): over the finite costs, fp64 sums
+ * in two passes (mean, then the squared deviations), agreeing with a sequential fp64
+ * evaluation within 1e-9 relative.  cost: DEVICE float [S]; ws: 64 bytes of device
+ * memory; synchronizes `stream`; E_DATA when every cost is infinite. */
+SPDP_API spdp_status spdp_saa_estimate_f32(const float* cost, int64_t S, spdp_saa_estimate* out_h,
+                                  void* ws, size_t ws_bytes, spdp_stream_t stream);
+
 /* a6 standalone: SAA partial of a cost vector (SPDP_INFEASIBLE entries are
  * counted in n_infeas and excluded).  partial: DEVICE pointer to one struct. */
 SPDP_API spdp_status spdp_saa_reduce(const int32_t* cost, int64_t S, spdp_saa_partial* partial,

@@ -43,7 +43,7 @@ SYMBOLS = (
     "spdp_set_profile_events", "spdp_last_kernel", "spdp_routes_workspace_bytes", "spdp_split_routes",
     "spdp_split_eval_penalized", "spdp_values_workspace_bytes", "spdp_split_values",
     "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours", "spdp_limits_workspace_bytes",
-    "spdp_split_eval_limits",
+    "spdp_split_eval_limits", "spdp_f32_workspace_bytes", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
 )
 
 
@@ -104,13 +104,17 @@ def _sig():
     L.spdp_limits_workspace_bytes.argtypes = [i32, i64]
     L.spdp_limits_workspace_bytes.restype = sz
     L.spdp_split_eval_limits.argtypes = [P, P, i32, P, i64, i64, i32, i32, i32, P, P, P, sz, u32, P]
+    L.spdp_f32_workspace_bytes.argtypes = [i32, i64]
+    L.spdp_f32_workspace_bytes.restype = sz
+    L.spdp_split_eval_f32.argtypes = [P, P, i32, P, i64, i64, i32, P, P, sz, P]
+    L.spdp_saa_estimate_f32.argtypes = [P, i64, ctypes.POINTER(SaaEstimate), P, sz, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
     L.spdp_irp_dp.argtypes = [P, ctypes.POINTER(IrpCustomer), i32, i32, P, i64, i64, P, P, P, sz, u32, P]
     for name in ("spdp_gen_demands", "spdp_demand_prefix", "spdp_split_mask", "spdp_split_eval",
                  "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean", "spdp_split_eval_host",
                  "spdp_irp_dp", "spdp_split_values", "spdp_split_eval_neighbours", "spdp_split_eval_penalized",
-                 "spdp_split_routes", "spdp_split_eval_limits"):
+                 "spdp_split_routes", "spdp_split_eval_limits", "spdp_split_eval_f32", "spdp_saa_estimate_f32"):
         getattr(L, name).restype = st
 
 
@@ -413,6 +417,33 @@ def split_eval_limits(tour, dist, demand, Q: int, max_duration: int = -1, max_ro
                                        F_SCRATCH_GLOBAL if scratch_global else 0, _stream(dev)),
            "spdp_split_eval_limits")
     return cost, partial
+
+
+def split_eval_f32(tour, dist, demand, Q: int, S: int | None = None, cost=None):
+    """a5 fp32 mode (spdp_split_eval_f32): dist a CUDA float64 tensor [(n+1)^2] of real costs;
+    returns float32 costs [S] (+inf = infeasible)."""
+    torch = _torch()
+    n, ld = demand.shape
+    S = ld if S is None else S
+    dev = demand.device
+    if cost is None:
+        cost = torch.empty(S, dtype=torch.float32, device=dev)
+    ws = workspace(int(_lib.spdp_f32_workspace_bytes(n, S)), dev, tag="f32")
+    _check(_lib.spdp_split_eval_f32(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld,
+                                    S, int(Q), _dev_ptr(cost, "cost"), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                    _stream(dev)), "spdp_split_eval_f32")
+    return cost
+
+
+def saa_estimate_f32(cost) -> dict:
+    """SAA estimate of float32 costs on the device (spdp_saa_estimate_f32; synchronizes)."""
+    ws = workspace(64, cost.device, tag="saa_f32")
+    e = SaaEstimate()
+    _check(_lib.spdp_saa_estimate_f32(_dev_ptr(cost, "cost"), cost.numel(), ctypes.byref(e),
+                                      ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(cost.device)),
+           "spdp_saa_estimate_f32")
+    return {"m": e.m, "infeasible": e.infeasible, "mean": e.mean, "var": e.var, "stderr": e.std_err,
+            "ci95_lo": e.ci95_lo, "ci95_hi": e.ci95_hi}
 
 
 def saa_reduce(cost, partial=None):

@@ -1,0 +1,211 @@
+// f32.cu -- the fp32 mode of the split (SURVEY §8(a) a2 / a5 "fp32 (one add + exact min)",
+// §8(c3) "fp32 mode (secondary)"; DESIGN R25): real-valued route costs.
+//
+//   Dd[1] = 0, Dd[i] = Dd[i-1] + c[s_{i-1}][s_i]               (fp64, sequential: one thread)
+//   T32(p, i) = fl32((c[0][s_{p+1}] + (Dd[i] - Dd[p+1])) + c[s_i][0])   (Eq. (1)'s route cost,
+//               rounded once from fp64)
+//   f(0) = 0,  f(i) = min_{mask(i) <= p <= i-1} fl32(f(p) + T32(p, i))
+//
+// Unlike the integer mode the rounded route cost is not separable into A[p] + B[i], so each
+// candidate forms T32 from the tour's fp64 prefix table (two fp64 adds and one rounding, in
+// the oracle's order) and adds it to f(p) with one IEEE single add; the min is exact.  The
+// result is therefore bit-identical to oracle_split_f32 for any launch configuration.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace spdp {
+
+struct F32Pos {
+    double Dd, c0, ci0;  // Dd[i], c[0][s_i], c[s_i][0]
+    uint32_t rowoff;     // (s_i - 1) * ld (n ld < 2^32)
+    uint32_t pad;
+};
+
+constexpr int kF32SmemMaxN = 4095;  // position table in shared memory up to 128 KB
+
+__global__ void f32_prep_kernel(const int32_t* __restrict__ tour, int n, const double* __restrict__ dist, int64_t ld,
+                                F32Pos* __restrict__ tab) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int64_t N1 = (int64_t)n + 1;
+    auto node = [&](int i) -> int {  // customer at 0-based position i, clamped to 1..n
+        const int c = tour[i];
+        return c < 1 ? 1 : (c > n ? n : c);
+    };
+    double D = 0.0;
+    tab[0] = F32Pos{0.0, 0.0, 0.0, 0u, 0u};
+    for (int i = 1; i <= n; ++i) {
+        const int c = node(i - 1);
+        if (i >= 2) D = __dadd_rn(D, dist[(int64_t)node(i - 2) * N1 + c]);
+        tab[i] = F32Pos{D, dist[c], dist[(int64_t)c * N1], (uint32_t)((uint64_t)(c - 1) * (uint64_t)ld), 0u};
+    }
+}
+
+// One scenario per thread: two-pointer mask, f in the thread's own rows of the
+// workspace ([n+1][S] fp32, coalesced across the warp), any window.
+__global__ void __launch_bounds__(256) split_f32_kernel(const F32Pos* __restrict__ tab_g, int n,
+                                                        const uint16_t* __restrict__ demand, int64_t S, int Q,
+                                                        float* fsc, float* __restrict__ cost, int table_in_smem) {
+    extern __shared__ F32Pos ftab[];
+    const F32Pos* tab = tab_g;
+    if (table_in_smem) {
+        for (int i = threadIdx.x; i <= n; i += blockDim.x) ftab[i] = tab_g[i];
+        __syncthreads();
+        tab = ftab;
+    }
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const uint16_t* dcol = demand + s;
+    float* fc = fsc + s;
+    fc[0] = 0.0f;
+    int P = 0, Pm = 0, m = 0;
+    bool bad = false;
+    for (int i = 1; i <= n && !bad; ++i) {
+        const int q = dcol[tab[i].rowoff];
+        if (q > Q) {  // Eq. (2)'s set is empty from here on (DESIGN R4)
+            bad = true;
+            break;
+        }
+        P += q;
+        while (P - Pm > Q) Pm += dcol[tab[++m].rowoff];  // P(m) = sum_{k<=m} q; stops at m <= i-1
+        const double Di = tab[i].Dd, ci0 = tab[i].ci0;
+        float best = INFINITY;
+        for (int p = i - 1; p >= m; --p) {
+            const double t64 = __dadd_rn(__dadd_rn(tab[p + 1].c0, __dsub_rn(Di, tab[p + 1].Dd)), ci0);
+            best = fminf(best, __fadd_rn(fc[(int64_t)p * S], __double2float_rn(t64)));
+        }
+        fc[(int64_t)i * S] = best;
+    }
+    cost[s] = bad ? INFINITY : fc[(int64_t)n * S];
+}
+
+// SAA of fp32 costs in fp64, two passes (count + sum, then the squared deviations).
+__global__ void __launch_bounds__(256) saa_f32_pass(const float* __restrict__ cost, int64_t S, double* acc, int pass) {
+    __shared__ double sh[2][8];
+    double a = 0.0, b = 0.0;
+    const double mean = pass ? acc[1] / acc[0] : 0.0;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
+        const float c = cost[s];
+        if (isinf(c)) continue;  // infeasible (counted by count_inf_kernel)
+        if (pass) {
+            const double d = (double)c - mean;
+            a += d * d;
+        } else {
+            a += 1.0;
+            b += (double)c;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(kFull, a, o);
+        b += __shfl_xor_sync(kFull, b, o);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        sh[0][wid] = a;
+        sh[1][wid] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ta = 0.0, tb = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            ta += sh[0][w];
+            tb += sh[1][w];
+        }
+        if (pass) {
+            atomicAdd(&acc[2], ta);
+        } else {
+            atomicAdd(&acc[0], ta);  // feasible count
+            atomicAdd(&acc[1], tb);  // sum of costs
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) count_inf_kernel(const float* __restrict__ cost, int64_t S,
+                                                        unsigned long long* ninf) {
+    unsigned long long k = 0;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x)
+        k += isinf(cost[s]) ? 1ull : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(kFull, k, o);
+    if ((threadIdx.x & 31) == 0 && k) atomicAdd(ninf, k);
+}
+
+static size_t f32_table_bytes(int32_t n) { return align_up(sizeof(F32Pos) * (size_t)(n + 1), 256); }
+
+}  // namespace spdp
+
+using namespace spdp;
+
+extern "C" size_t spdp_f32_workspace_bytes(int32_t n, int64_t S) {
+    if (n < 1 || S < 1) return 0;
+    return f32_table_bytes(n) + align_up(sizeof(float) * (size_t)(n + 1) * (size_t)S, 256);
+}
+
+extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* dist, int32_t n, const uint16_t* demand,
+                                           int64_t ld, int64_t S, int32_t Q, float* cost, void* ws, size_t ws_bytes,
+                                           spdp_stream_t stream) {
+    const char* fn = "spdp_split_eval_f32";
+    if (n < 1) return fail(SPDP_E_USAGE, "%s: n=%d < 1", fn, n);
+    if (n > SPDP_MAX_N) return fail(SPDP_E_RESOURCE, "%s: n=%d > SPDP_MAX_N=%d", fn, n, SPDP_MAX_N);
+    if (S < 1) return fail(SPDP_E_USAGE, "%s: S=%lld < 1", fn, (long long)S);
+    if (Q < 1) return fail(SPDP_E_USAGE, "%s: Q=%d < 1 (SPEC:34)", fn, Q);
+    if (ld < S || (ld % 8) != 0) return fail(SPDP_E_USAGE, "%s: ld=%lld must be >= S and a multiple of 8", fn, (long long)ld);
+    if (!tour || !dist || !demand || !cost || !ws) return fail(SPDP_E_USAGE, "%s: NULL required pointer", fn);
+    if (ws_bytes < spdp_f32_workspace_bytes(n, S)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
+    if ((uint64_t)n * (uint64_t)ld >= (1ull << 32)) return fail(SPDP_E_RESOURCE, "%s: n ld must stay below 2^32", fn);
+    cudaStream_t st = (cudaStream_t)stream;
+    char* w = static_cast<char*>(ws);
+    F32Pos* tab = reinterpret_cast<F32Pos*>(w);
+    float* fsc = reinterpret_cast<float*>(w + f32_table_bytes(n));
+    f32_prep_kernel<<<1, 32, 0, st>>>(tour, n, dist, ld, tab);
+    spdp_status rc = last_launch("f32_prep_kernel");
+    if (rc) return rc;
+    const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
+    const bool tsm = n <= kF32SmemMaxN;
+    if ((rc = kernel_setup((const void*)split_f32_kernel, (int)(sizeof(F32Pos) * (kF32SmemMaxN + 1)), -1, 0, 0, nullptr,
+                           "split_f32_kernel setup")))
+        return rc;
+    prof_begin(st);
+    split_f32_kernel<<<(unsigned)ceil_div(S, 256), 256, tsm ? sizeof(F32Pos) * (size_t)(n + 1) : 0, st>>>(
+        tab, n, demand, S, Qe, fsc, cost, tsm ? 1 : 0);
+    prof_end(st);
+    set_last_kernel("split_f32_kernel");
+    return last_launch("split_f32_kernel");
+}
+
+extern "C" spdp_status spdp_saa_estimate_f32(const float* cost, int64_t S, spdp_saa_estimate* out, void* ws,
+                                             size_t ws_bytes, spdp_stream_t stream) {
+    const char* fn = "spdp_saa_estimate_f32";
+    if (!cost || !out || !ws || S < 1) return fail(SPDP_E_USAGE, "%s: bad arguments", fn);
+    if (ws_bytes < 64) return fail(SPDP_E_USAGE, "%s: workspace < 64 bytes", fn);
+    cudaStream_t st = (cudaStream_t)stream;
+    double* acc = static_cast<double*>(ws);  // [0] feasible count, [1] sum, [2] sum of squared deviations
+    unsigned long long* ninf = reinterpret_cast<unsigned long long*>(acc + 4);
+    spdp_status rc = cuda_check(cudaMemsetAsync(ws, 0, 64, st), "cudaMemsetAsync(acc)");
+    if (rc) return rc;
+    int64_t blocks = ceil_div(S, 256 * 8);
+    if (blocks > (int64_t)device_sms() * 8) blocks = (int64_t)device_sms() * 8;
+    saa_f32_pass<<<(unsigned)blocks, 256, 0, st>>>(cost, S, acc, 0);
+    if ((rc = last_launch("saa_f32_pass"))) return rc;
+    saa_f32_pass<<<(unsigned)blocks, 256, 0, st>>>(cost, S, acc, 1);
+    if ((rc = last_launch("saa_f32_pass"))) return rc;
+    count_inf_kernel<<<(unsigned)blocks, 256, 0, st>>>(cost, S, ninf);
+    if ((rc = last_launch("count_inf_kernel"))) return rc;
+    double h[5];
+    if ((rc = cuda_check(cudaMemcpyAsync(h, ws, sizeof(h), cudaMemcpyDeviceToHost, st), "memcpy(acc)"))) return rc;
+    if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
+    unsigned long long k;
+    memcpy(&k, &h[4], sizeof(k));
+    const int64_t m = (int64_t)h[0];
+    out->m = m;
+    out->infeasible = (int64_t)k;
+    if (m == 0) return fail(SPDP_E_DATA, "%s: all scenarios infeasible (SPEC:287)", fn);
+    out->mean = h[1] / (double)m;
+    out->var = m >= 2 ? h[2] / (double)(m - 1) : 0.0;
+    out->std_err = sqrt(out->var / (double)m);
+    out->ci95_lo = out->mean - 1.96 * out->std_err;
+    out->ci95_hi = out->mean + 1.96 * out->std_err;
+    return SPDP_OK;
+}
