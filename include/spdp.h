@@ -302,8 +302,10 @@ SPDP_API spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t* 
  *   f(0) = 0,  f(i) = min_{mask(i) <= p <= i-1} fl32(f(p) + T32(p,i))
  *   cost[j] = f(n) of scenario j (float [S], +INFINITY when a demand exceeds Q).
  * One IEEE single add per candidate and an exact min: bit-identical for every launch
- * configuration.  One thread per scenario, any window.  ws: spdp_f32_workspace_bytes(n, S)
- * bytes (the f rows [n+1][S] fp32 + the position table).  n ld < 2^32. */
+ * configuration.  One thread per scenario on a 32-entry register ring with the band table
+ * T32(i-k, i), k <= 32, formed once per call; scenarios with wider windows by a general
+ * kernel (any window).  ws: spdp_f32_workspace_bytes(n, S) bytes (the f rows [n+1][S] fp32
+ * of the general kernel, the tables, a deferral list).  n ld < 2^32. */
 SPDP_API size_t spdp_f32_workspace_bytes(int32_t n, int64_t S);
 SPDP_API spdp_status spdp_split_eval_f32(const int32_t* tour, const double* dist, int32_t n,
                                 const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,

@@ -10,6 +10,7 @@
 // candidate forms T32 from the tour's fp64 prefix table (two fp64 adds and one rounding, in
 // the oracle's order) and adds it to f(p) with one IEEE single add; the min is exact.  The
 // result is therefore bit-identical to oracle_split_f32 for any launch configuration.
+#include <climits>
 #include <cmath>
 #include <cstring>
 
@@ -42,11 +43,14 @@ __global__ void f32_prep_kernel(const int32_t* __restrict__ tour, int n, const d
     }
 }
 
-// One scenario per thread: two-pointer mask, f in the thread's own rows of the
-// workspace ([n+1][S] fp32, coalesced across the warp), any window.
+// The general kernel (any window; the scenarios the ring kernel deferred, or all of them): one
+// scenario per thread, two-pointer mask, f in the thread's own rows of the
+// workspace ([n+1][S] fp32, coalesced across the warp), T32 formed per candidate.
 __global__ void __launch_bounds__(256) split_f32_kernel(const F32Pos* __restrict__ tab_g, int n,
                                                         const uint16_t* __restrict__ demand, int64_t S, int Q,
-                                                        float* fsc, float* __restrict__ cost, int table_in_smem) {
+                                                        float* fsc, float* __restrict__ cost, int table_in_smem,
+                                                        const int64_t* __restrict__ list,
+                                                        const unsigned* __restrict__ count) {
     extern __shared__ F32Pos ftab[];
     const F32Pos* tab = tab_g;
     if (table_in_smem) {
@@ -54,8 +58,9 @@ __global__ void __launch_bounds__(256) split_f32_kernel(const F32Pos* __restrict
         __syncthreads();
         tab = ftab;
     }
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= S) return;
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= (list ? (int64_t)*count : S)) return;
+    const int64_t s = list ? list[w] : w;
     const uint16_t* dcol = demand + s;
     float* fc = fsc + s;
     fc[0] = 0.0f;
@@ -78,6 +83,100 @@ __global__ void __launch_bounds__(256) split_f32_kernel(const F32Pos* __restrict
         fc[(int64_t)i * S] = best;
     }
     cost[s] = bad ? INFINITY : fc[(int64_t)n * S];
+}
+
+// The band table of the ring kernel: tb[i][k - 1] = T32(i - k, i), k = 1..W (the route costs of
+// every candidate the ring can hold, scenario-invariant), formed in the oracle's fp64 order.
+__global__ void f32_band_kernel(const F32Pos* __restrict__ tab, int n, int W, float* __restrict__ tb) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)(n + 1) * W) return;
+    const int i = (int)(idx / W), k = (int)(idx % W) + 1;
+    float v = 0.0f;  // (k > i: no such split point; its ring slot is never in a window)
+    if (k <= i) {
+        const int p = i - k;
+        v = __double2float_rn(__dadd_rn(__dadd_rn(tab[p + 1].c0, __dsub_rn(tab[i].Dd, tab[p + 1].Dd)), tab[i].ci0));
+    }
+    tb[idx] = v;
+}
+
+// The ring kernel (the common case): one scenario per thread, a W-entry register ring of
+// {f(p), P(p) + Q} (slot p mod W), layers unrolled by W, each candidate one fp32 add of the
+// band-table entry and a masked min; ages 1..8 unconditionally, then groups of 4 behind a warp
+// vote.  A scenario whose window outgrows the ring is listed for the general kernel.
+constexpr int kF32W = 32;
+constexpr int kF32Pf = 8;
+constexpr int kF32BandSmemMaxN = 375;  // band table (n + 1) W 4 B staged in shared memory up to 48 KB
+
+__global__ void __launch_bounds__(256) split_f32_ring_kernel(const F32Pos* __restrict__ tab, const float* __restrict__ tb_g,
+                                                             int n, const uint16_t* __restrict__ demand, int64_t S,
+                                                             int Q, float* __restrict__ cost, int64_t* __restrict__ list,
+                                                             unsigned* __restrict__ count, int band_in_smem) {
+    constexpr int W = kF32W;
+    extern __shared__ float tbs[];
+    const float* tb = tb_g;
+    if (band_in_smem) {
+        for (int i = threadIdx.x; i < (n + 1) * W; i += blockDim.x) tbs[i] = tb_g[i];
+        __syncthreads();
+        tb = tbs;
+    }
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = s < S;
+    const uint16_t* dcol = demand + (live ? s : S - 1);
+    auto q_at = [&](int i) -> int { return i <= n ? (int)dcol[tab[i].rowoff] : 0; };
+    float F[W];
+    int Y[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        F[k] = 0.0f;
+        Y[k] = INT_MIN;  // no split point yet: never in a window
+    }
+    Y[0] = Q;  // position 0: f = 0, P = 0
+    int qb[kF32Pf];
+#pragma unroll
+    for (int k = 0; k < kF32Pf; ++k) qb[k] = q_at(1 + k);
+    int P = 0;
+    bool bad = false, ovf = false;
+    float fin = 0.0f;
+    for (int b = 1; b <= n; b += W) {  // layer i = b + j sits in slot (1 + j) mod W
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const int i = b + j;
+            if (i > n) break;  // warp-uniform
+            const int q = qb[j % kF32Pf];
+            qb[j % kF32Pf] = q_at(i + kF32Pf);
+            bad |= q > Q;
+            const int Pn = P + q;
+            const float* row = tb + (int64_t)i * W;
+            float best = INFINITY;
+#pragma unroll
+            for (int k = 1; k <= 8; ++k) {
+                const int sl = (1 + j - k + 2 * W) % W;
+                if (Y[sl] >= Pn) best = fminf(best, __fadd_rn(F[sl], row[k - 1]));
+            }
+#pragma unroll
+            for (int k0 = 9; k0 <= W; k0 += 4) {
+                if (!__any_sync(kFull, Y[(1 + j - k0 + 2 * W) % W] >= Pn)) break;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int k = k0 + v;
+                    if (k <= W) {
+                        const int sl = (1 + j - k + 2 * W) % W;
+                        if (Y[sl] >= Pn) best = fminf(best, __fadd_rn(F[sl], row[k - 1]));
+                    }
+                }
+            }
+            const int si = (1 + j) % W;  // = the slot of age W, overwritten now
+            ovf |= Y[si] >= Pn && i - W >= 1;  // an older split point may still be in the window
+            F[si] = best;
+            Y[si] = Pn + Q;
+            if (i == n) fin = best;
+            P = Pn;
+        }
+    }
+    if (!live) return;
+    if (bad) cost[s] = INFINITY;
+    else if (ovf) list[atomicAdd(count, 1u)] = s;
+    else cost[s] = fin;
 }
 
 // SAA of fp32 costs in fp64, two passes (count + sum, then the squared deviations).
@@ -132,7 +231,9 @@ __global__ void __launch_bounds__(256) count_inf_kernel(const float* __restrict_
     if ((threadIdx.x & 31) == 0 && k) atomicAdd(ninf, k);
 }
 
-static size_t f32_table_bytes(int32_t n) { return align_up(sizeof(F32Pos) * (size_t)(n + 1), 256); }
+static size_t f32_table_bytes(int32_t n) { return align_up(sizeof(F32Pos) * (size_t)(n + 1 + kF32Pf), 256); }
+static size_t f32_band_bytes(int32_t n) { return align_up(sizeof(float) * (size_t)(n + 1) * kF32W, 256); }
+static size_t f32_list_bytes(int64_t S) { return align_up(sizeof(int64_t) * (size_t)S, 256) + 256; }
 
 }  // namespace spdp
 
@@ -140,7 +241,8 @@ using namespace spdp;
 
 extern "C" size_t spdp_f32_workspace_bytes(int32_t n, int64_t S) {
     if (n < 1 || S < 1) return 0;
-    return f32_table_bytes(n) + align_up(sizeof(float) * (size_t)(n + 1) * (size_t)S, 256);
+    return f32_table_bytes(n) + f32_band_bytes(n) + f32_list_bytes(S) +
+           align_up(sizeof(float) * (size_t)(n + 1) * (size_t)S, 256);
 }
 
 extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* dist, int32_t n, const uint16_t* demand,
@@ -158,20 +260,32 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     cudaStream_t st = (cudaStream_t)stream;
     char* w = static_cast<char*>(ws);
     F32Pos* tab = reinterpret_cast<F32Pos*>(w);
-    float* fsc = reinterpret_cast<float*>(w + f32_table_bytes(n));
+    float* tb = reinterpret_cast<float*>(w + f32_table_bytes(n));
+    int64_t* list = reinterpret_cast<int64_t*>(w + f32_table_bytes(n) + f32_band_bytes(n));
+    unsigned* count = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(list) + align_up(sizeof(int64_t) * (size_t)S, 256));
+    float* fsc = reinterpret_cast<float*>(w + f32_table_bytes(n) + f32_band_bytes(n) + f32_list_bytes(S));
     f32_prep_kernel<<<1, 32, 0, st>>>(tour, n, dist, ld, tab);
     spdp_status rc = last_launch("f32_prep_kernel");
     if (rc) return rc;
+    const int64_t nb = (int64_t)(n + 1) * kF32W;
+    f32_band_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, st>>>(tab, n, kF32W, tb);
+    if ((rc = last_launch("f32_band_kernel"))) return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
+    const bool bsm = n <= kF32BandSmemMaxN;
+    prof_begin(st);
+    // (1) the ring kernel for every scenario; (2) the general kernel for the ones it deferred
+    split_f32_ring_kernel<<<(unsigned)ceil_div(S, 256), 256, bsm ? sizeof(float) * (size_t)nb : 0, st>>>(
+        tab, tb, n, demand, S, Qe, cost, list, count, bsm ? 1 : 0);
+    if ((rc = last_launch("split_f32_ring_kernel"))) return rc;
     const bool tsm = n <= kF32SmemMaxN;
     if ((rc = kernel_setup((const void*)split_f32_kernel, (int)(sizeof(F32Pos) * (kF32SmemMaxN + 1)), -1, 0, 0, nullptr,
                            "split_f32_kernel setup")))
         return rc;
-    prof_begin(st);
     split_f32_kernel<<<(unsigned)ceil_div(S, 256), 256, tsm ? sizeof(F32Pos) * (size_t)(n + 1) : 0, st>>>(
-        tab, n, demand, S, Qe, fsc, cost, tsm ? 1 : 0);
+        tab, n, demand, S, Qe, fsc, cost, tsm ? 1 : 0, list, count);
     prof_end(st);
-    set_last_kernel("split_f32_kernel");
+    set_last_kernel("split_f32_ring_kernel<%d>", kF32W);
     return last_launch("split_f32_kernel");
 }
 
