@@ -318,6 +318,13 @@ SPDP_API spdp_status spdp_split_eval_f32(const int32_t* tour, const double* dist
 SPDP_API spdp_status spdp_saa_estimate_f32(const float* cost, int64_t S, spdp_saa_estimate* out_h,
                                   void* ws, size_t ws_bytes, spdp_stream_t stream);
 
+/* The moments behind it, for a multi-rank estimate (asynchronous): moments (DEVICE double[4],
+ * overwritten) = {m, sum c, sum (c - center)^2, infeasible} over the finite costs.  Two passes
+ * across ranks (paper_2511_18022_b200.dist.saa_estimate_f32): all-reduce(SUM) of the pass with
+ * center 0 gives the global mean, all-reduce of the pass centred on it the squared deviations. */
+SPDP_API spdp_status spdp_saa_f32_moments(const float* cost, int64_t S, double center, double* moments,
+                                 spdp_stream_t stream);
+
 /* a6 standalone: SAA partial of a cost vector (SPDP_INFEASIBLE entries are
  * counted in n_infeas and excluded).  partial: DEVICE pointer to one struct. */
 SPDP_API spdp_status spdp_saa_reduce(const int32_t* cost, int64_t S, spdp_saa_partial* partial,

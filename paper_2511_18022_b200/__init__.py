@@ -44,6 +44,7 @@ SYMBOLS = (
     "spdp_split_eval_penalized", "spdp_values_workspace_bytes", "spdp_split_values",
     "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours", "spdp_limits_workspace_bytes",
     "spdp_split_eval_limits", "spdp_f32_workspace_bytes", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
+    "spdp_saa_f32_moments",
 )
 
 
@@ -108,13 +109,15 @@ def _sig():
     L.spdp_f32_workspace_bytes.restype = sz
     L.spdp_split_eval_f32.argtypes = [P, P, i32, P, i64, i64, i32, P, P, sz, P]
     L.spdp_saa_estimate_f32.argtypes = [P, i64, ctypes.POINTER(SaaEstimate), P, sz, P]
+    L.spdp_saa_f32_moments.argtypes = [P, i64, ctypes.c_double, P, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
     L.spdp_irp_dp.argtypes = [P, ctypes.POINTER(IrpCustomer), i32, i32, P, i64, i64, P, P, P, sz, u32, P]
     for name in ("spdp_gen_demands", "spdp_demand_prefix", "spdp_split_mask", "spdp_split_eval",
                  "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean", "spdp_split_eval_host",
                  "spdp_irp_dp", "spdp_split_values", "spdp_split_eval_neighbours", "spdp_split_eval_penalized",
-                 "spdp_split_routes", "spdp_split_eval_limits", "spdp_split_eval_f32", "spdp_saa_estimate_f32"):
+                 "spdp_split_routes", "spdp_split_eval_limits", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
+                 "spdp_saa_f32_moments"):
         getattr(L, name).restype = st
 
 
@@ -444,6 +447,16 @@ def saa_estimate_f32(cost) -> dict:
            "spdp_saa_estimate_f32")
     return {"m": e.m, "infeasible": e.infeasible, "mean": e.mean, "var": e.var, "stderr": e.std_err,
             "ci95_lo": e.ci95_lo, "ci95_hi": e.ci95_hi}
+
+
+def saa_f32_moments(cost, center: float = 0.0, out=None):
+    """{m, sum, sum (c - center)^2, infeasible} of float32 costs (DEVICE float64 [4], asynchronous)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(4, dtype=torch.float64, device=cost.device)
+    _check(_lib.spdp_saa_f32_moments(_dev_ptr(cost, "cost"), cost.numel(), float(center), _dev_ptr(out, "moments"),
+                                     _stream(cost.device)), "spdp_saa_f32_moments")
+    return out
 
 
 def saa_reduce(cost, partial=None):

@@ -179,56 +179,36 @@ __global__ void __launch_bounds__(256) split_f32_ring_kernel(const F32Pos* __res
     else cost[s] = fin;
 }
 
-// SAA of fp32 costs in fp64, two passes (count + sum, then the squared deviations).
-__global__ void __launch_bounds__(256) saa_f32_pass(const float* __restrict__ cost, int64_t S, double* acc, int pass) {
-    __shared__ double sh[2][8];
-    double a = 0.0, b = 0.0;
-    const double mean = pass ? acc[1] / acc[0] : 0.0;
+// SAA moments of fp32 costs in fp64: acc = {m, sum c, sum (c - center)^2, infeasible} over the
+// finite costs (block tree sums, one fp64 atomic per block and field).
+__global__ void __launch_bounds__(256) saa_f32_moments_kernel(const float* __restrict__ cost, int64_t S, double center,
+                                                              double* __restrict__ acc) {
+    __shared__ double sh[4][8];
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
         const float c = cost[s];
-        if (isinf(c)) continue;  // infeasible (counted by count_inf_kernel)
-        if (pass) {
-            const double d = (double)c - mean;
-            a += d * d;
-        } else {
-            a += 1.0;
-            b += (double)c;
+        if (isinf(c)) {
+            v[3] += 1.0;
+            continue;
         }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(kFull, a, o);
-        b += __shfl_xor_sync(kFull, b, o);
+        const double d = (double)c - center;
+        v[0] += 1.0;
+        v[1] += (double)c;
+        v[2] += d * d;
     }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) {
-        sh[0][wid] = a;
-        sh[1][wid] = b;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[f] += __shfl_xor_sync(kFull, v[f], o);
+        if (lane == 0) sh[f][wid] = v[f];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double ta = 0.0, tb = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-            ta += sh[0][w];
-            tb += sh[1][w];
-        }
-        if (pass) {
-            atomicAdd(&acc[2], ta);
-        } else {
-            atomicAdd(&acc[0], ta);  // feasible count
-            atomicAdd(&acc[1], tb);  // sum of costs
-        }
+    if (threadIdx.x < 4) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[threadIdx.x][w];
+        atomicAdd(&acc[threadIdx.x], t);
     }
-}
-
-__global__ void __launch_bounds__(256) count_inf_kernel(const float* __restrict__ cost, int64_t S,
-                                                        unsigned long long* ninf) {
-    unsigned long long k = 0;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x)
-        k += isinf(cost[s]) ? 1ull : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(kFull, k, o);
-    if ((threadIdx.x & 31) == 0 && k) atomicAdd(ninf, k);
 }
 
 static size_t f32_table_bytes(int32_t n) { return align_up(sizeof(F32Pos) * (size_t)(n + 1 + kF32Pf), 256); }
@@ -289,34 +269,39 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     return last_launch("split_f32_kernel");
 }
 
+extern "C" spdp_status spdp_saa_f32_moments(const float* cost, int64_t S, double center, double* moments,
+                                             spdp_stream_t stream) {
+    if (!cost || !moments || S < 1) return fail(SPDP_E_USAGE, "spdp_saa_f32_moments: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    spdp_status rc = cuda_check(cudaMemsetAsync(moments, 0, 4 * sizeof(double), st), "cudaMemsetAsync(moments)");
+    if (rc) return rc;
+    int64_t blocks = ceil_div(S, 256 * 8);
+    if (blocks > (int64_t)device_sms() * 8) blocks = (int64_t)device_sms() * 8;
+    saa_f32_moments_kernel<<<(unsigned)blocks, 256, 0, st>>>(cost, S, center, moments);
+    return last_launch("saa_f32_moments_kernel");
+}
+
 extern "C" spdp_status spdp_saa_estimate_f32(const float* cost, int64_t S, spdp_saa_estimate* out, void* ws,
                                              size_t ws_bytes, spdp_stream_t stream) {
     const char* fn = "spdp_saa_estimate_f32";
     if (!cost || !out || !ws || S < 1) return fail(SPDP_E_USAGE, "%s: bad arguments", fn);
     if (ws_bytes < 64) return fail(SPDP_E_USAGE, "%s: workspace < 64 bytes", fn);
     cudaStream_t st = (cudaStream_t)stream;
-    double* acc = static_cast<double*>(ws);  // [0] feasible count, [1] sum, [2] sum of squared deviations
-    unsigned long long* ninf = reinterpret_cast<unsigned long long*>(acc + 4);
-    spdp_status rc = cuda_check(cudaMemsetAsync(ws, 0, 64, st), "cudaMemsetAsync(acc)");
+    double* acc = static_cast<double*>(ws);
+    double h[4];
+    // pass 1: count and sum -> mean; pass 2: squared deviations about that mean (two-pass variance)
+    spdp_status rc = spdp_saa_f32_moments(cost, S, 0.0, acc, stream);
     if (rc) return rc;
-    int64_t blocks = ceil_div(S, 256 * 8);
-    if (blocks > (int64_t)device_sms() * 8) blocks = (int64_t)device_sms() * 8;
-    saa_f32_pass<<<(unsigned)blocks, 256, 0, st>>>(cost, S, acc, 0);
-    if ((rc = last_launch("saa_f32_pass"))) return rc;
-    saa_f32_pass<<<(unsigned)blocks, 256, 0, st>>>(cost, S, acc, 1);
-    if ((rc = last_launch("saa_f32_pass"))) return rc;
-    count_inf_kernel<<<(unsigned)blocks, 256, 0, st>>>(cost, S, ninf);
-    if ((rc = last_launch("count_inf_kernel"))) return rc;
-    double h[5];
-    if ((rc = cuda_check(cudaMemcpyAsync(h, ws, sizeof(h), cudaMemcpyDeviceToHost, st), "memcpy(acc)"))) return rc;
+    if ((rc = cuda_check(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st), "memcpy(moments)"))) return rc;
     if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
-    unsigned long long k;
-    memcpy(&k, &h[4], sizeof(k));
     const int64_t m = (int64_t)h[0];
     out->m = m;
-    out->infeasible = (int64_t)k;
+    out->infeasible = (int64_t)h[3];
     if (m == 0) return fail(SPDP_E_DATA, "%s: all scenarios infeasible (SPEC:287)", fn);
     out->mean = h[1] / (double)m;
+    if ((rc = spdp_saa_f32_moments(cost, S, out->mean, acc, stream))) return rc;
+    if ((rc = cuda_check(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st), "memcpy(moments)"))) return rc;
+    if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
     out->var = m >= 2 ? h[2] / (double)(m - 1) : 0.0;
     out->std_err = sqrt(out->var / (double)m);
     out->ci95_lo = out->mean - 1.96 * out->std_err;

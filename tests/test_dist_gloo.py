@@ -79,3 +79,60 @@ def test_shard_ranges_cover_exactly():
             assert rs[0][0] == 0 and rs[-1][1] == S
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert max(e - b for b, e in rs) - min(e - b for b, e in rs) <= 1
+
+
+def _np_moments(cost, center):
+    """Host stand-in for spdp_saa_f32_moments (no GPU in this container): {m, sum, ssdev, inf}."""
+    c = np.asarray(cost, dtype=np.float32)
+    fin = c[np.isfinite(c)].astype(np.float64)
+    return torch.tensor([float(fin.size), float(fin.sum()), float(((fin - center) ** 2).sum()),
+                         float(c.size - fin.size)], dtype=torch.float64)
+
+
+def _worker_f32(rank, world, port, S, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_18022_b200 import dist as pdist
+        cfg = synth.config_instance("C2", S=S)
+        inst = cfg["inst"]
+        xy = np.asarray(inst["coords"], dtype=np.float64)
+        distf = np.ascontiguousarray(np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1)))
+        b, e = pdist.shard_range(S, rank, world)
+        model = dict(cfg["model"])
+        model["q_cap"] = inst["Q"] + 20  # some infeasible scenarios
+        dem = oracle.gen_demands(model, b, e - b)
+        cost = oracle.split_f32(inst["tour"], distf, dem, inst["Q"])
+        est = pdist.saa_estimate_f32(cost, moments_fn=_np_moments)
+        q.put((rank, est["m"], est["infeasible"], est["mean"], est["var"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_fp32_saa_equals_single_process():
+    """The fp32-mode SAA over 2 ranks (two passes, one all-reduce each) agrees with the
+    single-process sequential-fp64 oracle within 1e-9 relative."""
+    S = 3001
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_f32, args=(r, 2, port, S, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = synth.config_instance("C2", S=S)
+    inst = cfg["inst"]
+    xy = np.asarray(inst["coords"], dtype=np.float64)
+    distf = np.ascontiguousarray(np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1)))
+    model = dict(cfg["model"])
+    model["q_cap"] = inst["Q"] + 20
+    w = oracle.saa_f32(oracle.split_f32(inst["tour"], distf, oracle.gen_demands(model, 0, S), inst["Q"]))
+    assert w["infeasible"] > 0
+    for rank, m, ninf, mean, var in res:
+        assert m == w["m"] and ninf == w["infeasible"]
+        assert abs(mean - w["mean"]) <= 1e-9 * w["mean"]
+        assert abs(var - w["var"]) <= 1e-9 * w["var"]

@@ -68,3 +68,21 @@ def test_split_f32_edge_cases(spdp):
     with pytest.raises(spdp.SpdpError) as ei:
         spdp.saa_estimate_f32(allinf)
     assert ei.value.status == spdp.SPDP_E_DATA
+
+
+def test_saa_f32_moments_and_dist_helper(spdp):
+    """The moments kernel behind the multi-rank fp32 SAA: single process, the dist helper's two
+    passes equal spdp_saa_estimate_f32."""
+    from paper_2511_18022_b200 import dist as pdist
+    rng = np.random.default_rng(3)
+    c = rng.uniform(5e4, 9e4, size=100_003).astype(np.float32)
+    c[::101] = np.inf
+    ct = torch.from_numpy(c).cuda()
+    m = spdp.saa_f32_moments(ct, 0.0).cpu().numpy()
+    fin = c[np.isfinite(c)].astype(np.float64)
+    assert m[0] == fin.size and m[3] == c.size - fin.size
+    assert abs(m[1] - fin.sum()) <= 1e-12 * fin.sum()
+    a = pdist.saa_estimate_f32(ct)
+    b = spdp.saa_estimate_f32(ct)
+    assert a["m"] == b["m"] and a["infeasible"] == b["infeasible"]
+    assert abs(a["mean"] - b["mean"]) <= 1e-13 * b["mean"] and abs(a["var"] - b["var"]) <= 1e-12 * b["var"]
