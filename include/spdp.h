@@ -311,6 +311,12 @@ SPDP_API spdp_status spdp_split_eval_f32(const int32_t* tour, const double* dist
                                 const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
                                 float* cost, void* ws, size_t ws_bytes, spdp_stream_t stream);
 
+/* a8 in fp32 mode: T tours [T][n] over the same demand set, cost [T][S] float (the tours run
+ * one after the other on `stream`, sharing the workspace of spdp_f32_workspace_bytes(n, S)). */
+SPDP_API spdp_status spdp_split_eval_batch_f32(const int32_t* tours, int32_t T, const double* dist, int32_t n,
+                                      const uint16_t* demand, int64_t ld, int64_t S, int32_t Q, float* cost,
+                                      void* ws, size_t ws_bytes, spdp_stream_t stream);
+
 /* SAA estimate of fp32 costs (SURVEY §8(c5) fp32 mode): over the finite costs, fp64 sums
  * in two passes (mean, then the squared deviations), agreeing with a sequential fp64
  * evaluation within 1e-9 relative.  cost: DEVICE float [S]; ws: 64 bytes of device

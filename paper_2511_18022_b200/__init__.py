@@ -44,7 +44,7 @@ SYMBOLS = (
     "spdp_split_eval_penalized", "spdp_values_workspace_bytes", "spdp_split_values",
     "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours", "spdp_limits_workspace_bytes",
     "spdp_split_eval_limits", "spdp_f32_workspace_bytes", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
-    "spdp_saa_f32_moments",
+    "spdp_saa_f32_moments", "spdp_split_eval_batch_f32",
 )
 
 
@@ -110,6 +110,7 @@ def _sig():
     L.spdp_split_eval_f32.argtypes = [P, P, i32, P, i64, i64, i32, P, P, sz, P]
     L.spdp_saa_estimate_f32.argtypes = [P, i64, ctypes.POINTER(SaaEstimate), P, sz, P]
     L.spdp_saa_f32_moments.argtypes = [P, i64, ctypes.c_double, P, P]
+    L.spdp_split_eval_batch_f32.argtypes = [P, i32, P, i32, P, i64, i64, i32, P, P, sz, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
     L.spdp_irp_dp.argtypes = [P, ctypes.POINTER(IrpCustomer), i32, i32, P, i64, i64, P, P, P, sz, u32, P]
@@ -117,7 +118,7 @@ def _sig():
                  "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean", "spdp_split_eval_host",
                  "spdp_irp_dp", "spdp_split_values", "spdp_split_eval_neighbours", "spdp_split_eval_penalized",
                  "spdp_split_routes", "spdp_split_eval_limits", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
-                 "spdp_saa_f32_moments"):
+                 "spdp_saa_f32_moments", "spdp_split_eval_batch_f32"):
         getattr(L, name).restype = st
 
 
@@ -435,6 +436,23 @@ def split_eval_f32(tour, dist, demand, Q: int, S: int | None = None, cost=None):
     _check(_lib.spdp_split_eval_f32(_dev_ptr(tour, "tour"), _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld,
                                     S, int(Q), _dev_ptr(cost, "cost"), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
                                     _stream(dev)), "spdp_split_eval_f32")
+    return cost
+
+
+def split_eval_batch_f32(tours, dist, demand, Q: int, S: int | None = None, cost=None):
+    """a8 in fp32 mode (spdp_split_eval_batch_f32): float32 costs [T][S] of T tours [T][n]."""
+    torch = _torch()
+    n, ld = demand.shape
+    T = tours.shape[0]
+    S = ld if S is None else S
+    dev = demand.device
+    if cost is None:
+        cost = torch.empty((T, S), dtype=torch.float32, device=dev)
+    ws = workspace(int(_lib.spdp_f32_workspace_bytes(n, S)), dev, tag="f32")
+    _check(_lib.spdp_split_eval_batch_f32(_dev_ptr(tours, "tours"), T, _dev_ptr(dist, "dist"), n,
+                                          _dev_ptr(demand, "demand"), ld, S, int(Q), _dev_ptr(cost, "cost"),
+                                          ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream(dev)),
+           "spdp_split_eval_batch_f32")
     return cost
 
 

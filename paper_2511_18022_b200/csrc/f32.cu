@@ -269,6 +269,20 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     return last_launch("split_f32_kernel");
 }
 
+extern "C" spdp_status spdp_split_eval_batch_f32(const int32_t* tours, int32_t T, const double* dist, int32_t n,
+                                                 const uint16_t* demand, int64_t ld, int64_t S, int32_t Q, float* cost,
+                                                 void* ws, size_t ws_bytes, spdp_stream_t stream) {
+    if (T < 1) return fail(SPDP_E_USAGE, "spdp_split_eval_batch_f32: T=%d < 1", T);
+    if (!tours || !cost) return fail(SPDP_E_USAGE, "spdp_split_eval_batch_f32: NULL required pointer");
+    // the tours one after the other on the stream (the workspace of one tour is reused)
+    for (int32_t t = 0; t < T; ++t) {
+        spdp_status rc = spdp_split_eval_f32(tours + (int64_t)t * n, dist, n, demand, ld, S, Q, cost + (int64_t)t * S, ws,
+                                             ws_bytes, stream);
+        if (rc) return rc;
+    }
+    return SPDP_OK;
+}
+
 extern "C" spdp_status spdp_saa_f32_moments(const float* cost, int64_t S, double center, double* moments,
                                              spdp_stream_t stream) {
     if (!cost || !moments || S < 1) return fail(SPDP_E_USAGE, "spdp_saa_f32_moments: bad arguments");

@@ -86,3 +86,15 @@ def test_saa_f32_moments_and_dist_helper(spdp):
     b = spdp.saa_estimate_f32(ct)
     assert a["m"] == b["m"] and a["infeasible"] == b["infeasible"]
     assert abs(a["mean"] - b["mean"]) <= 1e-13 * b["mean"] and abs(a["var"] - b["var"]) <= 1e-12 * b["var"]
+
+
+def test_split_batch_f32_parity(spdp):
+    cfg = synth.config_instance("C3", S=701)
+    inst, S = cfg["inst"], 701
+    dem = oracle.gen_demands(cfg["model"], 0, S, ld=spdp.padded_ld(S))
+    tours = np.ascontiguousarray(cfg["tours"][:9])
+    dist = real_dist(inst)
+    got = spdp.split_eval_batch_f32(to_dev(tours), to_dev(dist), to_dev(dem), cfg["Q"], S=S).cpu().numpy()
+    for t in range(tours.shape[0]):
+        want = oracle.split_f32(tours[t], dist, dem, cfg["Q"], S=S)
+        assert np.array_equal(got[t].view(np.uint32), want.view(np.uint32)), t
