@@ -118,7 +118,7 @@ def dist_env():
 
 def ncu_traffic(config_name: str):
     """dram bytes per sweep launch from the committed ncu --set full summary, if any."""
-    p = os.path.join(ROOT, "profiles", "ncu_sweep_%s.json" % config_name)
+    p = os.path.join(ROOT, "profiles", "r01_ncu_sweep_%s.json" % config_name)
     if not os.path.exists(p):
         return None
     try:
