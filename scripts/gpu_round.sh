@@ -29,6 +29,8 @@ for p in $PHASES; do
            -o $OUT/nbr_gran_C3 python scripts/profile_sweep.py --config C3 --nbr --granular --iters 2 > $OUT/ncu_fullgran.log 2>&1; echo "fullgran rc=$?" >> $OUT/status.txt ;;
     fulllim) timeout 900 ncu --set full --clock-control none --import-source on -k regex:split_limits_ring -s 1 -c 1 \
            -o $OUT/limits_C2 python scripts/profile_sweep.py --config C2 --limits --iters 2 > $OUT/ncu_fulllim.log 2>&1; echo "fulllim rc=$?" >> $OUT/status.txt ;;
+    fullf32) timeout 900 ncu --set full --clock-control none --import-source on -k regex:split_f32_ring -s 1 -c 1 \
+           -o $OUT/f32_C2 python scripts/profile_sweep.py --config C2 --f32 --iters 2 > $OUT/ncu_fullf32.log 2>&1; echo "fullf32 rc=$?" >> $OUT/status.txt ;;
     fullirp) timeout 900 ncu --set full --clock-control none --import-source on -k regex:irp_la -s 1 -c 1 \
            -o $OUT/irp_C5 python scripts/profile_sweep.py --irp --iters 2 > $OUT/ncu_fullirp.log 2>&1; echo "fullirp rc=$?" >> $OUT/status.txt ;;
     micro) ./scripts/micro_alu > $OUT/micro.txt 2>&1; echo "micro rc=$?" >> $OUT/status.txt ;;

@@ -21,6 +21,7 @@ ap.add_argument("--irp", action="store_true")
 ap.add_argument("--nbr", action="store_true", help="f3: values of tour 0 + neighbour evaluation of the population")
 ap.add_argument("--granular", action="store_true", help="f3 with the granular one-move population")
 ap.add_argument("--limits", action="store_true", help="f4: duration 1.5 x max trip + fleet ceil(sum mu / Q) + 2")
+ap.add_argument("--f32", action="store_true", help="fp32 mode with unrounded Euclidean costs")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 if a.irp:
@@ -45,7 +46,11 @@ else:
         parent = tours[0].contiguous()
         fwd, bwd = spdp.split_values(parent, dist, d, inst["Q"], S=cfg["S"])
     for _ in range(a.iters):
-        if a.limits:
+        if a.f32:
+            xy = np.asarray(inst["coords"], dtype=np.float64)
+            distf = torch.from_numpy(np.ascontiguousarray(np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1)))).to(dev)
+            spdp.split_eval_f32(tours[0].contiguous(), distf, d, inst["Q"], S=cfg["S"])
+        elif a.limits:
             spdp.split_eval_limits(tours[0].contiguous(), dist, d, inst["Q"], max_duration=int(trip * 1.5),
                                    max_routes=kmin + 2, S=cfg["S"])
         elif a.nbr:
