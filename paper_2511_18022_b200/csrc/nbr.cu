@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
     const int4* __restrict__ etabs, const int4* __restrict__ info, int n, const uint16_t* __restrict__ demand,
     int64_t S, int Q, const int32_t* __restrict__ fwd, const int32_t* __restrict__ bwd,
     int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots, unsigned long long* __restrict__ ovf_list,
-    unsigned* __restrict__ ovf_count, const TourInfo* __restrict__ tinfo, int f32_loads) {
+    unsigned* __restrict__ ovf_count, const TourInfo* __restrict__ tinfo, int f32_loads, int64_t s_off) {
     static_assert(W % kNbrPf == 0, "the prefetch distance must divide the ring");
     static_assert(kNbrU0 % 4 == 0 && kNbrU0 < W, "unconditional ages");
     __shared__ Part red[kNbrThreads / 32];
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
         if constexpr (SM) return (uint32_t)stab[i].w;
         else return (uint32_t)__ldg(&e[i].w);
     };
-    const int64_t s = (int64_t)blockIdx.y * kNbrThreads + threadIdx.x;
+    const int64_t s = s_off + (int64_t)blockIdx.y * kNbrThreads + threadIdx.x;  // (launches of <= 65535 tiles)
     const bool live = s < S;
     const int64_t col = live ? s : S - 1;
     const int32_t* fcol = fwd + col;
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(NT) split_nbr_smem_kernel(
     const int4* __restrict__ etabs, const int4* __restrict__ info, int n, const uint16_t* __restrict__ demand,
     int64_t S, int Q, const int32_t* __restrict__ fwd, const int32_t* __restrict__ bwd,
     int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots, unsigned long long* __restrict__ ovf_list,
-    unsigned* __restrict__ ovf_count, int table_in_smem) {
+    unsigned* __restrict__ ovf_count, int table_in_smem, int64_t s_off) {
     static_assert((W & (W - 1)) == 0 && W >= 8, "W: a power of two");
     __shared__ Part red[NT / 32];
     extern __shared__ int4 sm4[];
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(NT) split_nbr_smem_kernel(
     }
     const int tid = threadIdx.x;
     auto R = [&](int p) -> int2& { return ring[(p & (W - 1)) * NT + tid]; };
-    const int64_t s = (int64_t)blockIdx.y * NT + tid;
+    const int64_t s = s_off + (int64_t)blockIdx.y * NT + tid;
     const bool live = s < S;
     const int64_t col = live ? s : S - 1;
     const int32_t* fcol = fwd + col;
@@ -675,18 +675,22 @@ static spdp_status launch_nbr_t(cudaStream_t st, const int4* e, const int4* info
                                 int64_t S, int T, int Q, const int32_t* fwd, const int32_t* bwd,
                                 int32_t* cost, spdp_saa_partial* slots, unsigned long long* ovf, unsigned* ovf_count,
                                 const TourInfo* tinfo, int f32_loads) {
-    const dim3 grid((unsigned)T, (unsigned)ceil_div(S, kNbrThreads));
+    const int64_t ntile = ceil_div(S, kNbrThreads);
     prof_begin(st);
+    for (int64_t y0 = 0; y0 < ntile; y0 += 65535) {  // (grid.y <= 65535 tiles per launch)
+    const dim3 grid((unsigned)T, (unsigned)(ntile - y0 < 65535 ? ntile - y0 : 65535));
+    const int64_t s_off = y0 * kNbrThreads;
     if (n <= kNbrSmemMaxN) {
         const size_t smem = sizeof(int4) * (size_t)tour_tab_stride(n);
         if (spdp_status e = kernel_setup((const void*)split_nbr_kernel<W, true>, (int)(sizeof(int4) * tour_tab_stride(kNbrSmemMaxN)),
                                          -1, 0, 0, nullptr, "split_nbr_kernel setup"))
             return e;
         split_nbr_kernel<W, true><<<grid, kNbrThreads, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,
-                                                                   ovf_count, tinfo, f32_loads);
+                                                                   ovf_count, tinfo, f32_loads, s_off);
     } else {
         split_nbr_kernel<W, false><<<grid, kNbrThreads, 0, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,
-                                                                 ovf_count, tinfo, f32_loads);
+                                                                 ovf_count, tinfo, f32_loads, s_off);
+    }
     }
     prof_end(st);
     set_last_kernel("split_nbr_kernel<%d,%d>", W, n <= kNbrSmemMaxN ? 1 : 0);
@@ -706,10 +710,13 @@ static spdp_status launch_nbr_smem_t(cudaStream_t st, const int4* e, const int4*
     if (spdp_status e = kernel_setup((const void*)split_nbr_smem_kernel<W, NT>, (int)(ring + sizeof(int4) * (kNbrSmemMaxN + 1)),
                                      -1, 0, 0, nullptr, "split_nbr_smem_kernel setup"))
         return e;
-    const dim3 grid((unsigned)T, (unsigned)ceil_div(S, NT));
+    const int64_t ntile = ceil_div(S, NT);
     prof_begin(st);
-    split_nbr_smem_kernel<W, NT><<<grid, NT, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf, ovf_count,
-                                                         tsm ? 1 : 0);
+    for (int64_t y0 = 0; y0 < ntile; y0 += 65535) {  // (grid.y <= 65535 tiles per launch)
+        const dim3 grid((unsigned)T, (unsigned)(ntile - y0 < 65535 ? ntile - y0 : 65535));
+        split_nbr_smem_kernel<W, NT><<<grid, NT, smem, st>>>(e, info, n, demand, S, Q, fwd, bwd, cost, slots, ovf,
+                                                             ovf_count, tsm ? 1 : 0, y0 * NT);
+    }
     prof_end(st);
     set_last_kernel("split_nbr_smem_kernel<%d>", W);
     return last_launch("split_nbr_smem_kernel");
@@ -725,13 +732,12 @@ extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const i
     if (rc) return rc;
     if (T < 1) return fail(SPDP_E_USAGE, "%s: T=%d < 1", fn, T);
     if (T >= (1 << 23)) return fail(SPDP_E_RESOURCE, "%s: T=%d too large", fn, T);
-    if (ceil_div(S, kNbrThreads) >= 65536) return fail(SPDP_E_RESOURCE, "%s: S=%lld too large (grid)", fn, (long long)S);
     if (window_hint < 0) return fail(SPDP_E_USAGE, "%s: window_hint < 0", fn);
     if (!parent || !fwd || !bwd || !tours || !dist || !demand || !ws)
         return fail(SPDP_E_USAGE, "%s: NULL required pointer", fn);
     if (ws_bytes < spdp_neighbour_workspace_bytes(n, S, T)) return fail(SPDP_E_USAGE, "%s: workspace too small", fn);
-    if ((uint64_t)n * (uint64_t)ld >= (1ull << 32) || (uint64_t)(n + 1) * (uint64_t)S >= (1ull << 32))
-        return fail(SPDP_E_RESOURCE, "%s: n ld and (n + 1) S must stay below 2^32", fn);
+    if ((uint64_t)n * (uint64_t)ld >= (1ull << 32) || (uint64_t)(n + 1) * (uint64_t)S >= (1ull << 32) || S >= (1LL << 30))
+        return fail(SPDP_E_RESOURCE, "%s: n ld and (n + 1) S must stay below 2^32, S below 2^30", fn);
     cudaStream_t st = (cudaStream_t)stream;
     const WsLayout L = ws_layout(n, S, T);
     char* w = static_cast<char*>(ws);

@@ -167,3 +167,21 @@ def test_neighbours_large_n_table_in_global_memory(spdp):
         cost, _ = spdp.split_eval_neighbours(P, fwd, bwd, to_dev(tours), dist, D, inst["Q"], S=S, window_hint=16,
                                              smem=smem)
         assert np.array_equal(cost.cpu().numpy().astype(np.int64), want)
+
+
+def test_neighbours_more_scenario_tiles_than_one_grid(spdp):
+    """S above 65535 x 128 scenarios: the candidate kernels run as several launches; identical to
+    the batched sweep everywhere and to the oracle on sampled columns."""
+    cfg = synth.config_instance("C1", S=8_400_000)
+    inst, S = cfg["inst"], 65535 * 128 + 1_001
+    D = spdp.gen_demands(cfg["model"], 0, S)
+    tours = np.ascontiguousarray(synth.perturb_tours(inst["tour"], 6, 13))
+    P, dist, Tt = to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(tours)
+    fwd, bwd = spdp.split_values(P, dist, D, cfg["Q"], S=S)
+    cost, part = spdp.split_eval_neighbours(P, fwd, bwd, Tt, dist, D, cfg["Q"], S=S, window_hint=16)
+    bcost, bpart = spdp.split_eval_batch(Tt, dist, D, cfg["Q"], S=S, window_hint=16)
+    assert torch.equal(cost, bcost) and torch.equal(part, bpart)
+    cols = np.concatenate([np.arange(0, 40), np.arange(S - 40, S)])
+    dem = D.cpu().numpy().view(np.uint16)[:, cols]
+    want = as_i32(oracle.split_tours(tours, inst["dist"], np.ascontiguousarray(dem), cfg["Q"], S=cols.size))
+    assert np.array_equal(cost.cpu().numpy()[:, cols].astype(np.int64), want)
