@@ -263,6 +263,16 @@ SPDP_API spdp_status spdp_split_values(const int32_t* tour, const int32_t* dist,
  * wider windows are finished by the general kernel.  SPDP_F_VALIDATE checks the
  * candidates (not the parent).  ws: spdp_neighbour_workspace_bytes(n, S, T). */
 SPDP_API size_t spdp_neighbour_workspace_bytes(int32_t n, int64_t S, int32_t T);
+/* Several parents in one call (an HGS population's neighbourhoods): parents [P][n], fwd / bwd
+ * [P][n+1][S] (spdp_split_values of each parent, stacked), parent_of [T] int32 (DEVICE; the
+ * parent of candidate t, clamped to [0, P); may be NULL when P = 1).  Same results as P calls
+ * of spdp_split_eval_neighbours; same workspace size. */
+SPDP_API spdp_status spdp_split_eval_neighbours_multi(const int32_t* parents, int32_t P, const int32_t* parent_of,
+                                             const int32_t* fwd, const int32_t* bwd, const int32_t* tours,
+                                             int32_t T, const int32_t* dist, int32_t n, const uint16_t* demand,
+                                             int64_t ld, int64_t S, int32_t Q, int32_t* cost,
+                                             spdp_saa_partial* partial, int32_t window_hint, void* ws,
+                                             size_t ws_bytes, uint32_t flags, spdp_stream_t stream);
 SPDP_API spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int32_t* fwd, const int32_t* bwd,
                                        const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,
                                        const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,

@@ -44,7 +44,7 @@ SYMBOLS = (
     "spdp_split_eval_penalized", "spdp_values_workspace_bytes", "spdp_split_values",
     "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours", "spdp_limits_workspace_bytes",
     "spdp_split_eval_limits", "spdp_f32_workspace_bytes", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
-    "spdp_saa_f32_moments", "spdp_split_eval_batch_f32",
+    "spdp_saa_f32_moments", "spdp_split_eval_batch_f32", "spdp_split_eval_neighbours_multi",
 )
 
 
@@ -102,6 +102,8 @@ def _sig():
     L.spdp_neighbour_workspace_bytes.argtypes = [i32, i64, i32]
     L.spdp_neighbour_workspace_bytes.restype = sz
     L.spdp_split_eval_neighbours.argtypes = [P, P, P, P, i32, P, i32, P, i64, i64, i32, P, P, i32, P, sz, u32, P]
+    L.spdp_split_eval_neighbours_multi.argtypes = [P, i32, P, P, P, P, i32, P, i32, P, i64, i64, i32, P, P, i32, P, sz,
+                                                   u32, P]
     L.spdp_limits_workspace_bytes.argtypes = [i32, i64]
     L.spdp_limits_workspace_bytes.restype = sz
     L.spdp_split_eval_limits.argtypes = [P, P, i32, P, i64, i64, i32, i32, i32, P, P, P, sz, u32, P]
@@ -118,7 +120,8 @@ def _sig():
                  "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean", "spdp_split_eval_host",
                  "spdp_irp_dp", "spdp_split_values", "spdp_split_eval_neighbours", "spdp_split_eval_penalized",
                  "spdp_split_routes", "spdp_split_eval_limits", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
-                 "spdp_saa_f32_moments", "spdp_split_eval_batch_f32"):
+                 "spdp_saa_f32_moments", "spdp_split_eval_batch_f32",
+                 "spdp_split_eval_neighbours_multi"):
         getattr(L, name).restype = st
 
 
@@ -475,6 +478,32 @@ def saa_f32_moments(cost, center: float = 0.0, out=None):
     _check(_lib.spdp_saa_f32_moments(_dev_ptr(cost, "cost"), cost.numel(), float(center), _dev_ptr(out, "moments"),
                                      _stream(cost.device)), "spdp_saa_f32_moments")
     return out
+
+
+def split_eval_neighbours_multi(parents, parent_of, fwd, bwd, tours, dist, demand, Q: int, S: int | None = None,
+                                want_cost: bool = True, want_partial: bool = True, window_hint: int = 0,
+                                cost=None, partial=None):
+    """f3 with several parents (spdp_split_eval_neighbours_multi): parents int32 [P][n], parent_of int32 [T],
+    fwd / bwd int32 [P][n+1][S] (stacked split_values of each parent)."""
+    torch = _torch()
+    n, ld = demand.shape
+    T = tours.shape[0]
+    P = parents.shape[0]
+    S = ld if S is None else S
+    dev = demand.device
+    if want_cost and cost is None:
+        cost = torch.empty((T, S), dtype=torch.int32, device=dev)
+    if want_partial and partial is None:
+        partial = torch.zeros((T, 6), dtype=torch.int64, device=dev)
+    ws = workspace(int(_lib.spdp_neighbour_workspace_bytes(n, S, T)), dev, tag="nbr")
+    _check(_lib.spdp_split_eval_neighbours_multi(_dev_ptr(parents, "parents"), P, _dev_ptr(parent_of, "parent_of"),
+                                                 _dev_ptr(fwd, "fwd"), _dev_ptr(bwd, "bwd"), _dev_ptr(tours, "tours"), T,
+                                                 _dev_ptr(dist, "dist"), n, _dev_ptr(demand, "demand"), ld, S, int(Q),
+                                                 _dev_ptr(cost, "cost") if want_cost else None,
+                                                 _dev_ptr(partial, "partial") if want_partial else None,
+                                                 int(window_hint), ctypes.c_void_p(ws.data_ptr()), ws.numel(), 0,
+                                                 _stream(dev)), "spdp_split_eval_neighbours_multi")
+    return cost, partial
 
 
 def saa_reduce(cost, partial=None):

@@ -32,11 +32,13 @@ constexpr int kNbrSmemMaxN = 4095;  // position table in shared memory up to (n 
 // phase of the neighbour sweep), A[i] (i < n), B[i] (i >= 1), row * ld of customer sigma_i as a
 // uint32 element offset (callers check n ld < 2^32)}, A[p] = c_{0,s_{p+1}} - D[p+1], B[i] = D[i] + c_{s_i,0},
 // D[1] = 0, D[i] = D[i-1] + c_{s_{i-1},s_i}.
-// info[t] = {a, s0, 0, 0}: a = common prefix length with the parent, s0 = n - common suffix
-// length (a = s0 = n: the tour equals the parent).  One warp per tour.
-__global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict__ tours, const int32_t* __restrict__ parent,
+// info[t] = {a, s0, parent index, 0}: a = common prefix length with the tour's parent
+// (parents[parent_of[t]], or parents[0]), s0 = n - common suffix length (a = s0 = n: the tour
+// equals its parent).  One warp per tour.
+__global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict__ tours, const int32_t* __restrict__ parents,
                                                       int n, const int32_t* __restrict__ dist, int64_t ld,
-                                                      int4* __restrict__ etabs, int4* __restrict__ info) {
+                                                      int4* __restrict__ etabs, int4* __restrict__ info,
+                                                      const int32_t* __restrict__ parent_of, int P) {
     const int t = blockIdx.x, lane = threadIdx.x;
     const int32_t* tour = tours + (int64_t)t * n;
     int4* e = etabs + (int64_t)t * tour_tab_stride(n);
@@ -69,7 +71,10 @@ __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict_
     }
     if (lane == 0) e[0] = make_int4(0, dist[node(0)], 0, 0);  // A[0] = c_{0,s_1}
     if (lane < kTourTabPad) e[n + 1 + lane] = make_int4(0, 0, 0, 0);  // padding (demand row 0)
-    if (parent && info) {
+    if (parents && info) {
+        int par = parent_of ? parent_of[t] : 0;
+        par = par < 0 ? 0 : (par >= P ? P - 1 : par);  // (clamped: a bad index cannot read out of bounds)
+        const int32_t* parent = parents + (int64_t)par * n;
         int a = n, last = -1;
         for (int b = 0; b < n; b += 32) {
             const int i = b + lane;
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(32) nbr_prep_kernel(const int32_t* __restrict_
                 break;
             }
         }
-        if (lane == 0) info[t] = make_int4(a, a < n ? last + 1 : n, 0, 0);
+        if (lane == 0) info[t] = make_int4(a, a < n ? last + 1 : n, par, 0);
     }
 }
 
@@ -281,8 +286,9 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
     const int64_t s = s_off + (int64_t)blockIdx.y * kNbrThreads + threadIdx.x;  // (launches of <= 65535 tiles)
     const bool live = s < S;
     const int64_t col = live ? s : S - 1;
-    const int32_t* fcol = fwd + col;
-    const int32_t* bcol = bwd + col;
+    const int64_t pbase = (int64_t)in.z * (int64_t)(n + 1) * S;  // the tour's parent's value rows
+    const int32_t* fcol = fwd + pbase + col;
+    const int32_t* bcol = bwd + pbase + col;
     const uint16_t* dcol = demand + col;
     const uint32_t Su = (uint32_t)S, S4 = 4u * (uint32_t)S;  // (n + 1) S < 2^32, 4 S < 2^32
     auto dem = [&](uint32_t off) -> int { return *static_cast<const uint16_t*>(mad_wide(off, 2u, dcol)); };
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
 
 spdp_status launch_tour_table(const int32_t* tours, int32_t T, const int32_t* parent, int32_t n, const int32_t* dist,
                               int64_t ld, int4* etabs, int4* info, cudaStream_t st) {
-    nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parent, n, dist, ld, etabs, info);
+    nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parent, n, dist, ld, etabs, info, nullptr, 1);
     return last_launch("nbr_prep_kernel");
 }
 
@@ -507,8 +513,9 @@ __global__ void __launch_bounds__(NT) split_nbr_smem_kernel(
     const int64_t s = s_off + (int64_t)blockIdx.y * NT + tid;
     const bool live = s < S;
     const int64_t col = live ? s : S - 1;
-    const int32_t* fcol = fwd + col;
-    const int32_t* bcol = bwd + col;
+    const int64_t pbase = (int64_t)in.z * (int64_t)(n + 1) * S;  // the tour's parent's value rows
+    const int32_t* fcol = fwd + pbase + col;
+    const int32_t* bcol = bwd + pbase + col;
     const uint16_t* dcol = demand + col;
     const uint32_t Su = (uint32_t)S;
     const int pc = fcol[(uint32_t)n * Su];
@@ -644,7 +651,7 @@ extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dis
     int4* e = reinterpret_cast<int4*>(w);
     int64_t* list = reinterpret_cast<int64_t*>(w + etab_bytes(n, 1));
     unsigned* count = reinterpret_cast<unsigned*>(w + etab_bytes(n, 1) + align_up(sizeof(int64_t) * (size_t)S, 256));
-    nbr_prep_kernel<<<1, 32, 0, st>>>(tour, nullptr, n, dist, ld, e, nullptr);
+    nbr_prep_kernel<<<1, 32, 0, st>>>(tour, nullptr, n, dist, ld, e, nullptr, nullptr, 1);
     if ((rc = last_launch("nbr_prep_kernel"))) return rc;
     if ((rc = cuda_check(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
     // Q above the largest possible load behaves as "everything fits"; clamp so sums stay in int32
@@ -722,12 +729,16 @@ static spdp_status launch_nbr_smem_t(cudaStream_t st, const int4* e, const int4*
     return last_launch("split_nbr_smem_kernel");
 }
 
-extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int32_t* fwd, const int32_t* bwd,
-                                                  const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,
-                                                  const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
-                                                  int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
-                                                  void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream) {
+extern "C" spdp_status spdp_split_eval_neighbours_multi(const int32_t* parents, int32_t P, const int32_t* parent_of,
+                                                        const int32_t* fwd, const int32_t* bwd, const int32_t* tours,
+                                                        int32_t T, const int32_t* dist, int32_t n, const uint16_t* demand,
+                                                        int64_t ld, int64_t S, int32_t Q, int32_t* cost,
+                                                        spdp_saa_partial* partial, int32_t window_hint, void* ws,
+                                                        size_t ws_bytes, uint32_t flags, spdp_stream_t stream) {
     const char* fn = "spdp_split_eval_neighbours";
+    const int32_t* parent = parents;
+    if (P < 1) return fail(SPDP_E_USAGE, "%s: P=%d < 1", fn, P);
+    if (P > 1 && !parent_of) return fail(SPDP_E_USAGE, "%s: parent_of is NULL with P=%d parents", fn, P);
     spdp_status rc = check_common(fn, n, S, Q, ld, demand);
     if (rc) return rc;
     if (T < 1) return fail(SPDP_E_USAGE, "%s: T=%d < 1", fn, T);
@@ -754,7 +765,7 @@ extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const i
         if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
         if (h[HDR_STATUS]) return fail(SPDP_E_DATA, "%s: invalid candidate tour or costs (status %u)", fn, h[HDR_STATUS]);
     }
-    nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parent, n, dist, ld, e, info);
+    nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parents, n, dist, ld, e, info, parent_of, P);
     if ((rc = last_launch("nbr_prep_kernel"))) return rc;
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
     spdp_saa_partial* slots = partial ? reinterpret_cast<spdp_saa_partial*>(w + L.slots) : nullptr;
@@ -776,4 +787,13 @@ extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const i
     }
     if (rc) return rc;
     return launch_finish(w, L, T, n, demand, ld, S, (uint32_t)Qe, cost, partial, false, st);
+}
+
+extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int32_t* fwd, const int32_t* bwd,
+                                                  const int32_t* tours, int32_t T, const int32_t* dist, int32_t n,
+                                                  const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
+                                                  int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
+                                                  void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream) {
+    return spdp_split_eval_neighbours_multi(parent, 1, nullptr, fwd, bwd, tours, T, dist, n, demand, ld, S, Q, cost,
+                                            partial, window_hint, ws, ws_bytes, flags, stream);
 }

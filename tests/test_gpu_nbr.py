@@ -185,3 +185,33 @@ def test_neighbours_more_scenario_tiles_than_one_grid(spdp):
     dem = D.cpu().numpy().view(np.uint16)[:, cols]
     want = as_i32(oracle.split_tours(tours, inst["dist"], np.ascontiguousarray(dem), cfg["Q"], S=cols.size))
     assert np.array_equal(cost.cpu().numpy()[:, cols].astype(np.int64), want)
+
+
+def test_neighbours_several_parents(spdp):
+    """P = 3 parents (random tours) with their candidates interleaved: = the oracle's split of
+    every candidate and = three single-parent calls."""
+    cfg = synth.config_instance("C3", S=1_003)
+    inst, S = cfg["inst"], 1_003
+    dem = oracle.gen_demands(cfg["model"], 0, S, ld=spdp.padded_ld(S))
+    D, dist = to_dev(dem), to_dev(inst["dist"])
+    rng = np.random.default_rng(21)
+    parents = np.ascontiguousarray(np.stack([inst["tour"]] + [(rng.permutation(inst["n"]) + 1).astype(np.int32)
+                                                             for _ in range(2)]))
+    kids, pof = [], []
+    for k in range(3):
+        for c in synth.local_move_tours(parents[k], 6, 30 + k):
+            kids.append(c)
+            pof.append(k)
+    order = rng.permutation(len(kids))
+    tours = np.ascontiguousarray(np.stack([kids[i] for i in order]))
+    pof = np.ascontiguousarray(np.array([pof[i] for i in order], dtype=np.int32))
+    vals = [spdp.split_values(to_dev(parents[k]), dist, D, cfg["Q"], S=S) for k in range(3)]
+    fwd = torch.stack([v[0] for v in vals]).contiguous()
+    bwd = torch.stack([v[1] for v in vals]).contiguous()
+    cost, part = spdp.split_eval_neighbours_multi(to_dev(parents), to_dev(pof), fwd, bwd, to_dev(tours), dist, D,
+                                                  cfg["Q"], S=S, window_hint=16)
+    want = as_i32(oracle.split_tours(tours, inst["dist"], dem, cfg["Q"], S=S))
+    assert np.array_equal(cost.cpu().numpy().astype(np.int64), want)
+    p = part.cpu().numpy()
+    for t in range(tours.shape[0]):
+        assert tuple(int(v) for v in p[t, :5]) == _partial_expect(want[t])
