@@ -407,22 +407,7 @@ __global__ void __launch_bounds__(kNbrThreads, (W <= 16 ? 6 : 1)) split_nbr_kern
             P = (int)(Pb - kMagic - bias);
             (void)offf;
         }
-        // phase A: whole chunks before s0 -- the plain sweep
-        while (base + W <= s0) {
-#pragma unroll
-            for (int j = 0; j < W; ++j) {
-                const int i = base + j;
-                const int q = qb[j % kNbrPf];
-                qb[j % kNbrPf] = dem(rowoff(i + kNbrPf));
-                const int Pn = P + q;
-                const int best = scan(j, Pn, feas);
-                const int4 ei = tab(i);
-                G[j] = best + ei.y + ei.z;  // g(i) = f(i) + A[i]
-                Y[j] = Pn + Q;
-                P = Pn;
-            }
-            base += W;
-        }
+        // (without the fp32 phase, phase B runs every layer: one int32 body keeps the code small)
         // phase B: from the chunk holding s0 to the stop
         int bb[kNbrPf];
 #pragma unroll
