@@ -339,7 +339,9 @@ def main():
     clocks = sampler.stop()
 
     ms_step = t_start.elapsed_time(t_end) / args.steps
-    sweep_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev_s, ev_e))
+    sweep_all = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
+    sweep_ms = statistics.mean(sweep_all)
+    sweep_med = statistics.median(sweep_all)
     if world > 1:
         ms_step = pdist.max_over_ranks(ms_step, device=dev)
         sweep_ms = pdist.max_over_ranks(sweep_ms, device=dev)
@@ -359,7 +361,7 @@ def main():
         roof = {"bound": "alu", "achieved": alu_achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tcand/s",
                 "frac": alu_achieved / alu_peak}
     roof.update({"traffic": ncu_traffic(args.config), "kernel": spdp.last_kernel(),
-                 "kernel_ms": sweep_ms, "kernel_timing": "CUDA events around the sweep launch, mean of a second "
+                 "kernel_ms": sweep_ms, "kernel_ms_median": sweep_med, "kernel_timing": "CUDA events around the sweep launch, mean of a second "
                                                          "pass of the K timed steps",
                  "bytes_alg_per_launch": bytes_alg, "candidates_per_launch": cand,
                  "hbm_frac": hbm_achieved / pk["hbm_gbs"], "alu_frac": alu_achieved / alu_peak,
