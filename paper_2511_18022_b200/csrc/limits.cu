@@ -306,6 +306,107 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
     }
 }
 
+// Without a fleet limit: the duration-limited Eq. (3) sweep on a 32-entry REGISTER ring (the
+// integer sweep's structure).  The duration test of a candidate depends only on the layer i and
+// the age k (t(i-k, i) = A[i-k] + B[i] is scenario-invariant), so it is a per-layer bitmask
+// dm[i] (bit k-1: route (i-k, i] within Lmax) built once per call into the table's .x field;
+// per candidate the window test and the (warp-uniform) mask bit, then a predicated min.  Values
+// G = F + A with F = +inf kept at kLimBig (a layer may have no admissible split).  A scenario
+// whose window outgrows the ring is deferred to the general kernel.
+__global__ void limits_dmask_kernel(int4* __restrict__ tab, int n, int Lmax) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    unsigned dm = 0u;
+    if (i >= 1) {
+        const int Bi = tab[i].z;
+        for (int k = 1; k <= 32 && k <= i; ++k)
+            if (tab[i - k].y <= Lmax - Bi) dm |= 1u << (k - 1);
+    }
+    tab[i].x = (int)dm;
+}
+
+__global__ void __launch_bounds__(256) split_limits_reg_kernel(const int4* __restrict__ tab, int n,
+                                                               const uint16_t* __restrict__ demand, int64_t S, int Q,
+                                                               int32_t* __restrict__ cost,
+                                                               spdp_saa_partial* __restrict__ partial,
+                                                               int64_t* __restrict__ list, unsigned* __restrict__ count) {
+    constexpr int W = 32;
+    __shared__ Part red[8];
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = s < S;
+    const uint16_t* dcol = demand + (live ? s : S - 1);
+    auto q_at = [&](int i) -> int { return i <= n ? (int)dcol[(uint32_t)__ldg(&tab[i].w)] : 0; };
+    int G[W], Y[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        G[k] = kLimBig;
+        Y[k] = INT_MIN;  // no split point yet
+    }
+    G[0] = __ldg(&tab[0].y);  // position 0: F = 0, G = A[0]
+    Y[0] = Q;
+    int qb[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) qb[k] = q_at(1 + k);
+    int P = 0, fin = kLimBig;
+    bool bad = false, ovf = false;
+    for (int b = 1; b <= n; b += W) {  // layer i = b + j sits in slot (1 + j) mod W
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const int i = b + j;
+            if (i > n) break;  // warp-uniform
+            const int q = qb[j % 8];
+            qb[j % 8] = q_at(i + 8);
+            bad |= q > Q;
+            const int Pn = P + q;
+            const int4 ei = __ldg(&tab[i]);
+            const unsigned dm = (unsigned)ei.x;
+            int best = kLimBig;
+#pragma unroll
+            for (int k = 1; k <= 8; ++k) {
+                const int sl = (1 + j - k + 2 * W) % W;
+                if (((dm >> (k - 1)) & 1u) && Y[sl] >= Pn) best = min(best, G[sl]);
+            }
+#pragma unroll
+            for (int k0 = 9; k0 <= W; k0 += 4) {
+                if (!__any_sync(kFull, Y[(1 + j - k0 + 2 * W) % W] >= Pn)) break;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int k = k0 + v;
+                    const int sl = (1 + j - k + 2 * W) % W;
+                    if (((dm >> (k - 1)) & 1u) && Y[sl] >= Pn) best = min(best, G[sl]);
+                }
+            }
+            const int si = (1 + j) % W;  // = the slot of age W, overwritten now
+            ovf |= Y[si] >= Pn && i - W >= 1;
+            const int F = best >= kLimBig ? kLimBig : best + ei.z;  // F(i) = min G + B[i]
+            G[si] = F >= kLimBig ? kLimBig : F + ei.y;              // G(i) = F(i) + A[i]
+            Y[si] = Pn + Q;
+            if (i == n) fin = F;
+            P = Pn;
+        }
+    }
+    Part acc{0, 0, 0, 0, 0};
+    if (live) {
+        if (ovf && !bad) {
+            list[atomicAdd(count, 1u)] = s;
+        } else {
+            const int result = (bad || fin >= kLimBig) ? SPDP_INFEASIBLE : fin;
+            if (cost) cost[s] = result;
+            part_add_cost(acc, result, result != SPDP_INFEASIBLE);
+        }
+    }
+    if (partial) {
+        const Part t = block_sum(acc, red);
+        if (threadIdx.x == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->n_feas), (unsigned long long)t.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->n_infeas), (unsigned long long)t.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sum), (unsigned long long)t.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_lo), (unsigned long long)t.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_hi), (unsigned long long)t.sq_hi);
+        }
+    }
+}
+
 static int lim_num_sms() { return device_sms(); }
 
 static size_t lim_table_bytes(int32_t n) { return align_up(sizeof(int4) * (size_t)tour_tab_stride(n), 256); }
@@ -382,8 +483,16 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
     if (!general_only) {
         // fleet: 4 vehicle counts per position on a 16-position ring (48 KB per CTA, 16 warps per SM;
         // measured at C2, K = 27: 4.9 ms vs 7.2 ms with a 32-position ring and 8.6 ms with 8 counts)
-        rc = fleet ? launch_ring<4, 128, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count)
-                   : launch_ring<1, 128, 32>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count);
+        if (fleet) {
+            rc = launch_ring<4, 128, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count);
+        } else {  // duration only (or no limit): the register ring with the per-layer duration bitmask
+            limits_dmask_kernel<<<(unsigned)ceil_div(n + 1, 256), 256, 0, st>>>(e, n, Lmax);
+            if ((rc = last_launch("limits_dmask_kernel"))) return rc;
+            split_limits_reg_kernel<<<(unsigned)ceil_div(S, 256), 256, 0, st>>>(e, n, demand, S, Qe, cost, partial,
+                                                                              list, count);
+            set_last_kernel("split_limits_reg_kernel<32>");
+            rc = last_launch("split_limits_reg_kernel");
+        }
         if (rc) return rc;
     }
     const size_t smem = n <= kLimTableSmemMaxN ? sizeof(int4) * (size_t)(n + 1) : 0;
