@@ -290,8 +290,9 @@ SPDP_API spdp_status spdp_split_eval_neighbours(const int32_t* parent, const int
  * (one pass of Eq. (3)).  SPDP_INFEASIBLE when no admissible split exists (a
  * demand above Q, a customer whose out-and-back trip exceeds max_duration, or
  * more routes needed than max_routes).  cost [S] int32 (may be NULL), partial:
- * ONE spdp_saa_partial (may be NULL, overwritten).  One thread per scenario: a
- * 32-position ring kernel keeps the vehicle-count dimension to the band
+ * ONE spdp_saa_partial (may be NULL, overwritten).  One thread per scenario: without a
+ * fleet limit a register-ring sweep with a per-layer duration bitmask; with one, a
+ * 16-position shared-memory ring kernel keeps the vehicle-count dimension to the band
  * [kP(i), kP(i) + max_routes - kT] of the capacity bounds (kP = greedy route count
  * of the prefix, kT of the tour); scenarios whose window or band outgrows it go to
  * a general kernel (K passes, arrays of n+1 per scenario; SPDP_F_SCRATCH_GLOBAL
