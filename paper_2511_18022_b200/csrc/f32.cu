@@ -114,15 +114,20 @@ __global__ void __launch_bounds__(256) split_f32_ring_kernel(const F32Pos* __res
     constexpr int W = kF32W;
     extern __shared__ float tbs[];
     const float* tb = tb_g;
+    uint32_t* rows = reinterpret_cast<uint32_t*>(tbs + (n + 1) * W);  // row offsets, padded with 0
     if (band_in_smem) {
         for (int i = threadIdx.x; i < (n + 1) * W; i += blockDim.x) tbs[i] = tb_g[i];
+        for (int i = threadIdx.x; i < n + 1 + kF32Pf; i += blockDim.x) rows[i] = i <= n ? tab[i].rowoff : 0u;
         __syncthreads();
         tb = tbs;
     }
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = s < S;
     const uint16_t* dcol = demand + (live ? s : S - 1);
-    auto q_at = [&](int i) -> int { return i <= n ? (int)dcol[tab[i].rowoff] : 0; };
+    auto q_at = [&](int i) -> int {
+        if (band_in_smem) return (int)dcol[rows[i]];  // (padded past n: row 0)
+        return i <= n ? (int)dcol[tab[i].rowoff] : 0;
+    };
     float F[W];
     int Y[W];
 #pragma unroll
@@ -255,7 +260,8 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     const bool bsm = n <= kF32BandSmemMaxN;
     prof_begin(st);
     // (1) the ring kernel for every scenario; (2) the general kernel for the ones it deferred
-    split_f32_ring_kernel<<<(unsigned)ceil_div(S, 256), 256, bsm ? sizeof(float) * (size_t)nb : 0, st>>>(
+    split_f32_ring_kernel<<<(unsigned)ceil_div(S, 256), 256,
+                            bsm ? sizeof(float) * (size_t)nb + sizeof(uint32_t) * (size_t)(n + 1 + kF32Pf) : 0, st>>>(
         tab, tb, n, demand, S, Qe, cost, list, count, bsm ? 1 : 0);
     if ((rc = last_launch("split_f32_ring_kernel"))) return rc;
     const bool tsm = n <= kF32SmemMaxN;
