@@ -227,11 +227,12 @@ __global__ void __launch_bounds__(128) split_values_ring_kernel(const int4* __re
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= S) return;
     const uint16_t* dcol = demand + s;
-    fwd[s] = 0;
-    bwd[(int64_t)n * S + s] = 0;
-    const bool okf = values_pass<W>(e, n, dcol, Q, fwd + s, S, false);
-    const bool okb = values_pass<W>(e, n, dcol, Q, bwd + s, S, true);
-    if (!(okf && okb)) list[atomicAdd(count, 1u)] = s;
+    // blockIdx.y: the forward (0) or the backward (1) pass -- two independent threads per scenario
+    const bool backward = blockIdx.y != 0;
+    int32_t* out = backward ? bwd : fwd;
+    out[(backward ? (int64_t)n * S : 0) + s] = 0;
+    // (a scenario deferred by both passes is listed twice: the general kernel writes the same values)
+    if (!values_pass<W>(e, n, dcol, Q, out + s, S, backward)) list[atomicAdd(count, 1u)] = s;
 }
 
 // The restarted sweep: one scenario per thread, one candidate tour per blockIdx.x.
@@ -619,7 +620,7 @@ using namespace spdp;
 
 extern "C" size_t spdp_values_workspace_bytes(int32_t n, int64_t S) {
     if (n < 1 || S < 1) return 0;
-    return etab_bytes(n, 1) + align_up(sizeof(int64_t) * (size_t)S, 256) + 256;
+    return etab_bytes(n, 1) + align_up(sizeof(int64_t) * 2 * (size_t)S, 256) + 256;
 }
 
 extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dist, int32_t n, const uint16_t* demand,
@@ -635,7 +636,7 @@ extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dis
     char* w = static_cast<char*>(ws);
     int4* e = reinterpret_cast<int4*>(w);
     int64_t* list = reinterpret_cast<int64_t*>(w + etab_bytes(n, 1));
-    unsigned* count = reinterpret_cast<unsigned*>(w + etab_bytes(n, 1) + align_up(sizeof(int64_t) * (size_t)S, 256));
+    unsigned* count = reinterpret_cast<unsigned*>(w + etab_bytes(n, 1) + align_up(sizeof(int64_t) * 2 * (size_t)S, 256));
     nbr_prep_kernel<<<1, 32, 0, st>>>(tour, nullptr, n, dist, ld, e, nullptr, nullptr, 1);
     if ((rc = last_launch("nbr_prep_kernel"))) return rc;
     if ((rc = cuda_check(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
@@ -646,11 +647,11 @@ extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dis
                            nullptr, "split_values_ring_kernel setup")))
         return rc;
     prof_begin(st);
-    split_values_ring_kernel<32><<<(unsigned)ceil_div(S, 128), 128, tsm ? sizeof(int4) * (size_t)(n + 1) : 0, st>>>(
+    split_values_ring_kernel<32><<<dim3((unsigned)ceil_div(S, 128), 2), 128, tsm ? sizeof(int4) * (size_t)(n + 1) : 0, st>>>(
         e, n, demand, S, Qe, fwd, bwd, list, count, tsm ? 1 : 0);
     if ((rc = last_launch("split_values_ring_kernel"))) return rc;
     // the scenarios whose window outgrew the ring (or with a demand above Q): the general kernel
-    split_values_kernel<<<(unsigned)ceil_div(S, 256), 256, 0, st>>>(e, n, demand, ld, S, Qe, fwd, bwd, list, count);
+    split_values_kernel<<<(unsigned)ceil_div(2 * S, 256), 256, 0, st>>>(e, n, demand, ld, S, Qe, fwd, bwd, list, count);
     prof_end(st);
     set_last_kernel("split_values_ring_kernel<32>");
     return last_launch("split_values_kernel");
