@@ -539,12 +539,21 @@ def measure_rows(spdp, torch, dev, pk):
                                                        window_hint=h, mean_window=bench_config.MEAN["C3"]),
                          torch, dev, iters=6)
     _, lpart = spdp.split_eval_batch(ltours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h)
+    # SPDP_F_NBR_AUTO (reads the spans back, one sync): the batched sweep for the C3 population
+    ms_auto_c3 = _time_events(lambda: spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, d, inst["Q"],
+                                                                 S=cfg["S"], want_cost=False, partial=part,
+                                                                 window_hint=h, auto=True,
+                                                                 mean_window=bench_config.MEAN["C3"]), torch, dev, iters=4)
+    ms_auto_gr = _time_events(lambda: spdp.split_eval_neighbours(parent, fwd, bwd, ltours, dist, d, inst["Q"],
+                                                                 S=cfg["S"], want_cost=False, partial=part,
+                                                                 window_hint=h, auto=True,
+                                                                 mean_window=bench_config.MEAN["C3"]), torch, dev, iters=4)
     rows["f3_neighbours_C3"] = {
         "ms": ms_v + ms_n, "values_ms": ms_v, "neighbours_ms": ms_n, "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
         "evals_per_s": cfg["T"] * cfg["S"] / ((ms_v + ms_n) / 1e3), "mean_changed_span": span(cfg["tours"]),
-        "partials_equal_batch": equal_c3, "kernel": kern,
+        "partials_equal_batch": equal_c3, "kernel": kern, "auto_neighbours_ms": ms_auto_c3,
         "granular": {"neighbours_ms": ms_nl, "ms": ms_v + ms_nl, "batch_ms": ms_bl, "mean_changed_span": span(lt),
-                     "evals_per_s": cfg["T"] * cfg["S"] / ((ms_v + ms_nl) / 1e3),
+                     "evals_per_s": cfg["T"] * cfg["S"] / ((ms_v + ms_nl) / 1e3), "auto_neighbours_ms": ms_auto_gr,
                      "partials_equal_batch": bool(torch.equal(part, lpart))}}
     del d, fwd, bwd
     # f4: C2 with a route-duration limit (1.5 x the largest out-and-back trip) and a fleet limit

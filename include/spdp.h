@@ -79,6 +79,9 @@ typedef enum {
                                        with its DP arrays in the workspace (same results; tests both paths) */
 #define SPDP_F_NBR_SMEM 32u        /* spdp_split_eval_neighbours: the shared-memory-ring kernel instead of
                                        the register ring (same results) */
+#define SPDP_F_NBR_AUTO 64u        /* spdp_split_eval_neighbours(_multi): read the candidates' changed spans
+                                       back (synchronizes) and run spdp_split_eval_batch instead when they
+                                       average more than 40 % of the tour (the measured crossover) */
 /* bits 8..15 of flags: the expected MEAN window width i - mask(i) (0 = unknown; with
  * window_hint = 0 it is sampled).  A tuning hint like window_hint: it picks how many
  * candidates the sweep evaluates before its first warp vote, never the result. */

@@ -33,6 +33,7 @@ INFEASIBLE = 2**31 - 1
 F_VALIDATE = 1
 F_SCRATCH_GLOBAL = 16
 F_NBR_SMEM = 32
+F_NBR_AUTO = 64
 F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8}  # sweep algorithm flags (spdp.h)
 MAX_N = 16384
 
@@ -375,11 +376,12 @@ def split_values(tour, dist, demand, Q: int, S: int | None = None, fwd=None, bwd
 def split_eval_neighbours(parent, fwd, bwd, tours, dist, demand, Q: int, S: int | None = None,
                           want_cost: bool = True, want_partial: bool = True, window_hint: int = 0,
                           validate: bool = False, cost=None, partial=None, smem: bool = False,
-                          int_only: bool = False):
+                          int_only: bool = False, auto: bool = False, mean_window: int = 0):
     """f3: split costs of T candidate tours [T][n] from the parent's values (spdp_split_eval_neighbours);
     bit-identical to split_eval_batch(tours, ...).  Returns (cost int32 [T][S], partial int64 [T][6]).
     smem: the shared-memory-ring kernel instead of the register ring; int_only: no exact-fp32 phase
-    (SPDP_F_SWEEP_INT); same results either way."""
+    (SPDP_F_SWEEP_INT); auto: the batched sweep when the changed spans are long (SPDP_F_NBR_AUTO,
+    synchronizes; mean_window is then its tuning hint as in split_eval_batch); same results in every case."""
     torch = _torch()
     n, ld = demand.shape
     T = tours.shape[0]
@@ -396,7 +398,8 @@ def split_eval_neighbours(parent, fwd, bwd, tours, dist, demand, Q: int, S: int 
                                            _dev_ptr(cost, "cost") if want_cost else None,
                                            _dev_ptr(partial, "partial") if want_partial else None, int(window_hint),
                                            ctypes.c_void_p(ws.data_ptr()), ws.numel(),
-                                           (F_VALIDATE if validate else 0) | (F_NBR_SMEM if smem else 0) | (F_SWEEP["int"] if int_only else 0),
+                                           (F_VALIDATE if validate else 0) | (F_NBR_SMEM if smem else 0) | (F_SWEEP["int"] if int_only else 0)
+                                           | (F_NBR_AUTO if auto else 0) | _mean_flag(mean_window),
                                            _stream(dev)),
            "spdp_split_eval_neighbours")
     return cost, partial

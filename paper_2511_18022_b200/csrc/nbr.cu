@@ -19,6 +19,7 @@
 // where f(i) for i = a+1..E comes from the Eq. (3) sweep restarted at layer a+1
 // on a ring seeded with f_parent(a-W+1..a) -- O(s0 - a + window) layers instead of n.
 #include <climits>
+#include <vector>
 
 #include "common.cuh"
 #include "split_ws.cuh"
@@ -26,6 +27,7 @@
 namespace spdp {
 
 constexpr int kNbrPf = 8;            // demand / b prefetch distance (layers)
+constexpr double kNbrAutoSpan = 0.40;  // SPDP_F_NBR_AUTO: mean changed span / n above which the batch is faster
 constexpr int kNbrSmemMaxN = 4095;  // position table in shared memory up to (n + 1) 16 B = 64 KB
 
 // Per-tour position table e[i], i = 0..n:  {float bits of Cg[i] 2^-24 with Cg = A + B (the fp32
@@ -753,6 +755,20 @@ extern "C" spdp_status spdp_split_eval_neighbours_multi(const int32_t* parents, 
     }
     nbr_prep_kernel<<<T, 32, 0, st>>>(tours, parents, n, dist, ld, e, info, parent_of, P);
     if ((rc = last_launch("nbr_prep_kernel"))) return rc;
+    if (flags & SPDP_F_NBR_AUTO) {
+        // whole-call choice: when the candidates' changed spans average more than kNbrAutoSpan of the
+        // tour, the batched sweep is faster (measured crossover at C3): read the spans back
+        std::vector<int4> h((size_t)T);
+        if ((rc = cuda_check(cudaMemcpyAsync(h.data(), info, sizeof(int4) * (size_t)T, cudaMemcpyDeviceToHost, st),
+                             "memcpy(info)")))
+            return rc;
+        if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
+        double span = 0.0;
+        for (int32_t t = 0; t < T; ++t) span += (double)(h[(size_t)t].y - h[(size_t)t].x);
+        if (span > kNbrAutoSpan * (double)T * (double)n)
+            return spdp_split_eval_batch(tours, T, dist, n, demand, ld, S, Q, cost, partial, window_hint, ws, ws_bytes,
+                                         flags & ~(SPDP_F_NBR_AUTO | SPDP_F_NBR_SMEM | SPDP_F_VALIDATE), stream);
+    }
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
     spdp_saa_partial* slots = partial ? reinterpret_cast<spdp_saa_partial*>(w + L.slots) : nullptr;
     unsigned long long* ovf = reinterpret_cast<unsigned long long*>(w + L.ovf);

@@ -110,6 +110,16 @@ def test_neighbours_match_batch_at_full_C3(spdp):
     icost, ipart = spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, D, cfg["Q"], S=S, window_hint=20,
                                               int_only=True)
     assert torch.equal(icost, bcost) and torch.equal(ipart, bpart)
+    # SPDP_F_NBR_AUTO: the C3 population's long spans switch the call to the batched sweep (same results)
+    acost, apart = spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, D, cfg["Q"], S=S, window_hint=20,
+                                              auto=True)
+    assert torch.equal(acost, bcost) and torch.equal(apart, bpart)
+    assert spdp.last_kernel().startswith("split_sweep")
+    gt = to_dev(synth.local_move_tours(inst["tour"], 64, 5))
+    gcost, gpart = spdp.split_eval_neighbours(parent, fwd, bwd, gt, dist, D, cfg["Q"], S=S, window_hint=20, auto=True)
+    assert spdp.last_kernel().startswith("split_nbr")
+    g2, gp2 = spdp.split_eval_batch(gt, dist, D, cfg["Q"], S=S, window_hint=20)
+    assert torch.equal(gcost, g2) and torch.equal(gpart, gp2)
     cols = np.random.default_rng(5).choice(S, size=64, replace=False)
     dem = D.cpu().numpy().view(np.uint16)[:, cols]
     dem = np.ascontiguousarray(np.pad(dem, ((0, 0), (0, (-dem.shape[1]) % 8))))
