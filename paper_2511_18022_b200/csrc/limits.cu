@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
     }
     auto P_at = [&](int p) -> int& { return ringP[(p & (kRing - 1)) * NT + tid]; };
     auto K_at = [&](int p) -> int& { return ringK[(p & (kRing - 1)) * NT + tid]; };
-    auto F_at = [&](int p, int b) -> int& { return ringF[((p & (kRing - 1)) * BW + b) * NT + tid]; };
+    // F of one (slot, thread): BW contiguous ints ([kRing][NT][BW]: one 16-byte load when BW = 4)
+    auto F_at = [&](int p, int b) -> int& { return ringF[((p & (kRing - 1)) * NT + tid) * BW + b]; };
     Part acc{0, 0, 0, 0, 0};
     const int64_t s = (int64_t)blockIdx.x * NT + tid;
     if (s < S) {
@@ -254,7 +255,26 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
                     for (int p = i - 1; p >= m; --p) {
                         const int Ap = tb[p].y;
                         if (Ap > thr) continue;
-                        if (FLEET) {
+                        if constexpr (BW % 4 == 0) {
+                            // a feasible route (p, i] holds at most one greedy route start, so
+                            // d = kP(i) - kP(p) is 0 or 1 for every in-window p: F_{k-1}(p), k = kP(i) + b,
+                            // is band entry b - 1 + d -- a select between two fixed registers
+                            const int d = kp - K_at(p);
+                            int v[BW];
+#pragma unroll
+                            for (int b4 = 0; b4 < BW; b4 += 4) {
+                                const int4 f4 = *reinterpret_cast<const int4*>(&F_at(p, b4));
+                                v[b4] = f4.x;
+                                v[b4 + 1] = f4.y;
+                                v[b4 + 2] = f4.z;
+                                v[b4 + 3] = f4.w;
+                            }
+#pragma unroll
+                            for (int b = 0; b < BW; ++b) {
+                                const int c = d ? v[b] : (b ? v[b - 1] : kLimBig);
+                                if (c < kLimBig) best[b] = min(best[b], c + Ap);
+                            }
+                        } else if (FLEET) {
                             const int off = kp - 1 - K_at(p);  // F_{k-1}(p), k = kp + b: band index off + b
 #pragma unroll
                             for (int b = 0; b < BW; ++b) {
@@ -481,10 +501,10 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
     // (1) the ring kernel for every scenario; (2) the general kernel for the ones it deferred
     const bool general_only = (flags & SPDP_F_SCRATCH_GLOBAL) != 0;
     if (!general_only) {
-        // fleet: 4 vehicle counts per position on a 16-position ring (48 KB per CTA, 16 warps per SM;
-        // measured at C2, K = 27: 4.9 ms vs 7.2 ms with a 32-position ring and 8.6 ms with 8 counts)
+        // fleet: 8 vehicle counts per position on a 16-position ring, 64 threads per CTA (measured at C2:
+        // K = 27 3.9 ms, K = 31 5.4 ms; 4 counts: 3.7 / 7.6 ms -- wider bands defer fewer scenarios)
         if (fleet) {
-            rc = launch_ring<4, 128, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count);
+            rc = launch_ring<8, 64, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count);
         } else {  // duration only (or no limit): the register ring with the per-layer duration bitmask
             limits_dmask_kernel<<<(unsigned)ceil_div(n + 1, 256), 256, 0, st>>>(e, n, Lmax);
             if ((rc = last_launch("limits_dmask_kernel"))) return rc;
