@@ -66,3 +66,38 @@ def test_full_size_sampled(spdp, name):
     for t in (0, T - 1):
         ref = spdp.saa_reduce(cost[t].contiguous())
         assert torch.equal(ref.cpu(), part[t].cpu())
+
+
+def test_c2_full_next_rows_sampled(spdp):
+    """The NEXT rows and the fp32 mode at C2's full size (10^6 scenarios), in the bench's
+    launch configuration, on sampled scenarios the oracle evaluates one by one."""
+    cfg = synth.config_instance("C2")
+    inst, S = cfg["inst"], cfg["S"]
+    d = spdp.gen_demands(cfg["model"], 0, S)
+    tour, dist = torch.from_numpy(inst["tour"]).cuda(), torch.from_numpy(inst["dist"]).cuda()
+    rng = np.random.default_rng(1)
+    idx = np.unique(np.concatenate([rng.integers(0, S, size=120), [0, S - 1]]))
+    dem = _sample_cols(cfg["model"], idx)
+    Q = inst["Q"]
+    # f2 penalized (lambda = 10)
+    pc, _ = spdp.split_eval_penalized(tour, dist, d, Q, 10, S=S, window_hint=bench_config.HINT["C2"])
+    assert np.array_equal(pc.cpu().numpy()[idx].astype(np.int64), oracle.split_penalized(inst["tour"], inst["dist"],
+                                                                                        dem, Q, 10))
+    # f4 duration and fleet limits (the bench row's limits)
+    trip = int(max(inst["dist"][0, c] + inst["dist"][c, 0] for c in inst["tour"]))
+    kmin = int(np.ceil(inst["nominal"].astype(np.int64).sum() / Q))
+    for L, K in ((int(trip * 1.5), 0), (-1, kmin + 2)):
+        lc, _ = spdp.split_eval_limits(tour, dist, d, Q, max_duration=L, max_routes=K, S=S)
+        want = oracle.split_limits(inst["tour"], inst["dist"], dem, Q, Lmax=L, K=K)
+        want = np.where(want == oracle.INF, 2**31 - 1, want)
+        assert np.array_equal(lc.cpu().numpy()[idx].astype(np.int64), want), (L, K)
+    # f3 values of the tour
+    fwd, bwd = spdp.split_values(tour, dist, d, Q, S=S)
+    wf, wb = oracle.split_values(inst["tour"], inst["dist"], dem, Q)
+    assert np.array_equal(fwd.cpu().numpy()[:, idx].T.astype(np.int64), wf)
+    assert np.array_equal(bwd.cpu().numpy()[:, idx].T.astype(np.int64), wb)
+    # fp32 mode with unrounded Euclidean costs
+    xy = np.asarray(inst["coords"], dtype=np.float64)
+    distf = np.ascontiguousarray(np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1)))
+    c32 = spdp.split_eval_f32(tour, torch.from_numpy(distf).cuda(), d, Q, S=S).cpu().numpy()
+    assert np.array_equal(c32[idx].view(np.uint32), oracle.split_f32(inst["tour"], distf, dem, Q).view(np.uint32))
