@@ -101,3 +101,18 @@ def test_c2_full_next_rows_sampled(spdp):
     distf = np.ascontiguousarray(np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1)))
     c32 = spdp.split_eval_f32(tour, torch.from_numpy(distf).cuda(), d, Q, S=S).cpu().numpy()
     assert np.array_equal(c32[idx].view(np.uint32), oracle.split_f32(inst["tour"], distf, dem, Q).view(np.uint32))
+
+
+def test_c5_irp_full_sampled(spdp):
+    """The IRP row at C5's full size (10^5 scenarios, the bench's launch) on sampled scenarios."""
+    cfg = synth.irp_config()
+    irp, S = cfg["irp"], cfg["S"]
+    H, M = irp["H"], irp["M"]
+    d = spdp.gen_demands(cfg["model"], 0, S)
+    cost, part = spdp.irp_dp(irp["visit"], irp["cust"], d, H, M, S=S)
+    rng = np.random.default_rng(2)
+    idx = np.unique(np.concatenate([rng.integers(0, S, size=40), [0, S - 1]]))
+    dem = _sample_cols(cfg["model"], idx)
+    want = oracle.irp(H, M, irp["visit"], irp["cust"], dem)
+    assert np.array_equal(cost.cpu().numpy()[idx], want)
+    assert int(part.cpu().numpy()[2]) == int(cost.sum().item())
