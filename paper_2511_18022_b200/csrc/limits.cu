@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(kLimThreads) split_limits_kernel(const int4* _
 // keeps k in [kP(i), kP(i) + K - kT] only: K - kT + 1 <= BW values per position (the
 // duration limit only removes routes, so these capacity bounds stay valid).  A
 // scenario whose window outgrows the ring or whose band exceeds BW is deferred to the
-// general kernel (list).  BW = 1 without a fleet limit (one value per position).
+// general kernel (list).  (Without a fleet limit the register-ring kernel below is used;
+// BW = 1 here is kept for that case's shared-memory variant.)  F of a (slot, thread) is BW
+// contiguous ints, so a BW % 4 == 0 band loads with 16-byte accesses.
 template <int BW, int NT, int kRing>
 __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __restrict__ e, int n,
                                                                const uint16_t* __restrict__ demand, int64_t S, int Q,
