@@ -71,10 +71,13 @@ typedef enum {
 #define SPDP_F_VALIDATE 1u          /* check tour permutation, dist >= 0 and the int32 range
                                        bound on the device; synchronizes; E_DATA on failure */
 /* sweep algorithm (spdp_split_eval / _batch); all give bit-identical results.
- * Default (none set): register-ring Eq. (3) sweep for windows <= 32, deque otherwise. */
+ * Default (none set): the packed-u16 register ring for windows <= 32 when its load check passes
+ * (else the packed-fp32 or int ring), the deque for wider windows. */
 #define SPDP_F_SWEEP_INT   2u       /* register ring, exact int32, predicated min per candidate */
 #define SPDP_F_SWEEP_F32   4u       /* register ring, exact integer-valued fp32, FMA-pipe masking */
 #define SPDP_F_SWEEP_DEQUE 8u       /* monotone-deque sliding-window minimum, O(1) amortised */
+#define SPDP_F_SWEEP_U16 128u       /* register ring, two scenarios per lane in packed u16 halves
+                                       (windows 9..32, 12 (Q + 1) <= 2^15; else as the default) */
 #define SPDP_F_SCRATCH_GLOBAL 16u  /* spdp_split_eval_limits: every scenario through the general kernel
                                        with its DP arrays in the workspace (same results; tests both paths) */
 #define SPDP_F_NBR_SMEM 32u        /* spdp_split_eval_neighbours: the shared-memory-ring kernel instead of

@@ -34,7 +34,7 @@ F_VALIDATE = 1
 F_SCRATCH_GLOBAL = 16
 F_NBR_SMEM = 32
 F_NBR_AUTO = 64
-F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8}  # sweep algorithm flags (spdp.h)
+F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8, "u16": 128}  # sweep algorithm flags (spdp.h)
 MAX_N = 16384
 
 SYMBOLS = (
@@ -267,7 +267,7 @@ def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool
                want_partial: bool = True, window_hint: int = 0, validate: bool = False, cost=None, partial=None,
                algo: str | None = None, mean_window: int = 0):
     """Per-scenario split costs (int32 [S], INFEASIBLE sentinel) and the SAA partial (int64 [6]).
-    algo: None/"auto", "int", "f32" or "deque" (identical results; see spdp.h)."""
+    algo: None/"auto", "int", "f32", "deque" or "u16" (identical results; see spdp.h)."""
     torch = _torch()
     n, ld = demand.shape
     S = ld if S is None else S

@@ -43,7 +43,10 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     long long* wsum = reinterpret_cast<long long*>(smem_raw);              // 32 warp sums
     long long* dn = wsum + 32;                                             // D[n]
     int* cmx = reinterpret_cast<int*>(dn + 1);                             // block max of the used costs
-    unsigned* seen = reinterpret_cast<unsigned*>(smem_raw + 34 * sizeof(long long));  // bitmap
+    // ext: [0] NS = sum of max(0, -Cg), [1] max(0, max Cg), [2] the largest sum of max(0, Cg) over
+    // kU16Check consecutive layers, [3] B[n] (the packed-u16 sweep's range constants, TourInfo)
+    int* ext = reinterpret_cast<int*>(smem_raw + 34 * sizeof(long long));
+    unsigned* seen = reinterpret_cast<unsigned*>(smem_raw + 36 * sizeof(long long));  // bitmap
     pdl_trigger();  // the sweep's CTAs may launch now (they wait for this grid's completion)
     const int t = blockIdx.x;
     const int32_t* tour = tours + (int64_t)t * n;
@@ -60,6 +63,7 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
         for (int i = tid; i < kSlots; i += nt) slots[(int64_t)t * kSlots + i] = spdp_saa_partial{0, 0, 0, 0, 0, 0};
     if (tid == 0) {
         *cmx = 0;
+        ext[0] = ext[1] = ext[2] = ext[3] = 0;
         if (partial) partial[t] = spdp_saa_partial{0, 0, 0, 0, 0, 0};  // the finish kernel accumulates
     }
     if (validate) {
@@ -119,8 +123,9 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     // every table entry of this thread's positions in one pass (dist re-reads hit L1):
     // tab[i] = {row, Cg}, the int / fp32 Cg planes and the demand row pointer
     const int cs = cg_stride(n);
-    int32_t* cgi = cgs + (int64_t)t * 2 * cs;  // plane 0: int Cg, plane 1: fp32 Cg / 2^24 (exact when ok)
+    int32_t* cgi = cgs + (int64_t)t * kCgPlanes * cs;  // plane 0: int Cg, 1: fp32 Cg / 2^24, 2: packed u16 pair
     const uint16_t** rowp = rowps + (int64_t)t * (n + kTabPad);
+    int ns_local = 0, cgpos_max = 0;
     for (int i = lo; i < hi; ++i) {
         const int a = node(i);
         const int ca0 = dist[(int64_t)a * N1];
@@ -137,8 +142,18 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
         tab[i] = e;
         cgi[i] = e.y;
         cgi[cs + i] = __float_as_int((float)e.y * 0x1p-24f);
+        if (i + 1 < n) {
+            cgi[2 * cs + i] = (int32_t)((uint32_t)e.y * 0x10001u);  // the pair {Cg, Cg} as one 32-bit add
+            ns_local = min(ns_local + max(0, -e.y), 1 << 16);
+            cgpos_max = max(cgpos_max, e.y);
+        } else {
+            cgi[2 * cs + i] = 0;  // layer n: B[n] is added in int32 at the end
+            ext[3] = e.y;
+        }
         rowp[i] = demand + (int64_t)e.x * ld;
     }
+    if (ns_local) atomicAdd(&ext[0], ns_local);
+    if (cgpos_max) atomicMax(&ext[1], cgpos_max);
     for (int i = n + tid; i < cs; i += nt) {  // padding (rows: row 0; Cg: 0)
         if (i < n + kTabPad) {
             tab[i] = make_int2(0, 0);
@@ -146,12 +161,23 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
         }
         cgi[i] = 0;
         cgi[cs + i] = 0;
+        cgi[2 * cs + i] = 0;
     }
     for (int i = cs + tid; i < n + kTabPad; i += nt) {
         tab[i] = make_int2(0, 0);
         rowp[i] = demand;
     }
     if (tid == 0) g0[t] = dist[node(0)];
+    __syncthreads();
+    {  // the largest sum of max(0, Cg) over kU16Check consecutive layers (plane 0 is complete)
+        int wmax = 0;
+        for (int i = lo; i < min(hi, n - 1); ++i) {
+            int sum = 0;
+            for (int k = i; k < min(i + kU16Check, n - 1); ++k) sum += max(0, cgi[k]);
+            wmax = max(wmax, min(sum, 1 << 20));
+        }
+        if (wmax) atomicMax(&ext[2], wmax);
+    }
     __syncthreads();
     if (tid == 0) {  // g0f = (g0 + OFF) / 2^24
         const long long OFF = *dn, cm = *cmx;
@@ -160,6 +186,12 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
         ti.off = (int)(OFF < INT_MAX ? OFF : INT_MAX);
         // g + OFF <= (2n + 1) cmax + OFF and f(n) + OFF <= 2 n cmax + OFF: all below 2^24
         ti.ok = ((2LL * n + 2) * cm + OFF < (1LL << 24)) ? 1 : 0;
+        // packed-u16 sweep: values relative to a base stay in [0, 0x7FFF]
+        const int ns = ext[0], cgp = ext[1], win = ext[2];
+        ti.ns16 = ns < 0x7FFF ? ns : 0x7FFF;
+        ti.thr16 = 0x7FFF - (win < 0x7FFF ? win : 0x7FFF);
+        ti.ok16 = ((long long)ns + cgp + win <= 0x7FFF) ? 1 : 0;
+        ti.bn = ext[3];
         ti.pad = 0;
         tinfo[t] = ti;
     }
@@ -311,7 +343,7 @@ struct F2Stream {  // dynamic copy-cursor state only (constants stay kernel para
 #pragma unroll
             for (int cb = 0; cb < W / 4; cb += 32)
                 if (cb + lane < W / 4)
-                    cp_async16(sb + kRowsBytes + (cb + lane) * 16, cgf + (int64_t)ct * 2 * cgs_stride + r0 + (cb + lane) * 4);
+                    cp_async16(sb + kRowsBytes + (cb + lane) * 16, cgf + (int64_t)ct * kCgPlanes * cgs_stride + r0 + (cb + lane) * 4);
         }
         cp_async_commit();
         ++c;
@@ -1350,22 +1382,6 @@ __global__ void __launch_bounds__(256) saa_reduce_kernel(const int32_t* __restri
 }
 
 // ---------------------------------------------------------------- host dispatch
-struct SweepArgs {
-    const uint16_t* const* rowp;
-    const int2* tabs;
-    const int32_t* cgs;
-    const int32_t* g0;
-    const TourInfo* tinfo;
-    int n, T;
-    const uint16_t* demand;
-    int64_t ld, S;
-    uint32_t Q;
-    int32_t* cost;
-    spdp_saa_partial* slots;
-    unsigned long long* ovf;
-    unsigned* hdr;
-};
-
 static int num_sms() { return device_sms(); }
 
 // Launches the sweep: one wave of persistent CTAs (occupancy x SMs).
@@ -1387,19 +1403,6 @@ static spdp_status launch_sweep_t(cudaStream_t st, const SweepArgs& a) {
     set_last_kernel("split_sweep_kernel<%d,int>", W);
     prof_end(st);
     return rc;
-}
-
-// Tuning knob (environment, read once): SPDP_SWEEP=auto|int|f32 selects the candidate arithmetic.
-static int sweep_mode() {  // 0 auto (ring int for W <= 32, deque above), 1 int, 2 f32, 3 deque
-    static int m = [] {
-        const char* e = getenv("SPDP_SWEEP");
-        if (!e) return 0;
-        if (!strcmp(e, "int")) return 1;
-        if (!strcmp(e, "f32")) return 2;
-        if (!strcmp(e, "deque")) return 3;
-        return 0;
-    }();
-    return m;
 }
 
 static spdp_status launch_deque(cudaStream_t st, const SweepArgs& a) {
@@ -1446,47 +1449,16 @@ static spdp_status launch_sweep_f2_t(cudaStream_t st, const SweepArgs& a) {
     return rc;
 }
 
-// Tuning knob (environment, read once): SPDP_F2=<U0><UG> picks the candidate grouping of the
-// W=16/20 packed-fp32 sweeps (pairs scanned unconditionally, pairs per warp vote); default 31.
-static int f2_cfg() {
-    static int m = [] {
-        const char* e = getenv("SPDP_F2");
-        return e ? atoi(e) : 0;
-    }();
-    return m;
-}
-
 static spdp_status launch_sweep(int W, bool f32, cudaStream_t st, const SweepArgs& a, int mean_w) {
     if (f32) {
         // unconditional candidate pairs U0 ~ 0.8 x the mean window (measured: C2, mean 3.75 -> 3;
         // C3, mean 7.7 -> 6); an SPDP_F2 setting overrides
-        const bool wide = mean_w >= 6 && f2_cfg() == 0;
+        const bool wide = mean_w >= 6;
         switch (W) {
             case 8: return launch_sweep_f2_t<8, 2, 1>(st, a);
-            case 16:
-                if (wide) return launch_sweep_f2_t<16, 5, 1>(st, a);
-                switch (f2_cfg()) {
-                    case 21: return launch_sweep_f2_t<16, 2, 1>(st, a);
-                    case 32: return launch_sweep_f2_t<16, 3, 2>(st, a);
-                    case 41: return launch_sweep_f2_t<16, 4, 1>(st, a);
-                    case 314: return launch_sweep_f2_t<16, 3, 1, 4>(st, a);
-                    case 324: return launch_sweep_f2_t<16, 3, 2, 4>(st, a);
-                    default: return launch_sweep_f2_t<16, 3, 1>(st, a);
-                }
-            case 20:
-                if (wide) return launch_sweep_f2_t<20, 6, 2, 0, 20, true>(st, a);  // (pairs: -1.4 % at C3)
-                switch (f2_cfg()) {
-                    case 21: return launch_sweep_f2_t<20, 2, 1>(st, a);
-                    case 32: return launch_sweep_f2_t<20, 3, 2>(st, a);
-                    case 41: return launch_sweep_f2_t<20, 4, 1>(st, a);
-                    case 42: return launch_sweep_f2_t<20, 4, 2>(st, a);
-                    case 324: return launch_sweep_f2_t<20, 3, 2, 4>(st, a);
-                    case 3199: return launch_sweep_f2_t<20, 3, 1, 0, 20, true>(st, a);
-                    case 51: return launch_sweep_f2_t<20, 5, 1>(st, a);
-                    case 52: return launch_sweep_f2_t<20, 5, 2>(st, a);
-                    case 62: return launch_sweep_f2_t<20, 6, 2>(st, a);
-                    default: return launch_sweep_f2_t<20, 3, 1>(st, a);
-                }
+            case 16: return wide ? launch_sweep_f2_t<16, 5, 1>(st, a) : launch_sweep_f2_t<16, 3, 1>(st, a);
+            case 20:  // (pairs: -1.4 % at C3)
+                return wide ? launch_sweep_f2_t<20, 6, 2, 0, 20, true>(st, a) : launch_sweep_f2_t<20, 3, 1>(st, a);
             case 24: return wide ? launch_sweep_f2_t<24, 6, 2, 0, 24, true>(st, a) : launch_sweep_f2_t<24, 3, 1>(st, a);
             default: return wide ? launch_sweep_f2_t<32, 8, 2>(st, a) : launch_sweep_f2_t<32, 4, 2>(st, a);
         }
@@ -1597,12 +1569,16 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     // (the packed-fp32 sweep keeps loads as 2^23 + P + Q, exact below 2^24)
     const int64_t qeff = Qe < 65535u ? (int64_t)Qe : 65535;
     const bool f32_loads_exact = ((int64_t)n + 64) * qeff + 2 * (int64_t)Qe + 2 < (1LL << 23);
-    int mode = sweep_mode();
+    int mode = 0;  // 0 auto, 1 int ring, 2 packed-fp32 ring, 3 deque, 4 packed-u16 ring
     if (flags & SPDP_F_SWEEP_INT) mode = 1;
     if (flags & SPDP_F_SWEEP_F32) mode = 2;
     if (flags & SPDP_F_SWEEP_DEQUE) mode = 3;
-    // default for windows <= 32: the packed-fp32 ring when its loads are exact, else the int ring
-    const bool use_f32 = W <= 32 && f32_loads_exact && S < (1LL << 31) && (mode == 2 || mode == 0);
+    if (flags & SPDP_F_SWEEP_U16) mode = 4;
+    // default for windows <= 32: the packed-u16 ring (two scenarios per lane) when its load range
+    // check passes, else the packed-fp32 ring when its loads are exact, else the int ring
+    const bool u16_ok = ((W <= 32 && W >= 16) || mode == 4) && u16_loads_ok(n, Qe) && S < (1LL << 31);  // TUNING (temporary)
+    const bool use_u16 = u16_ok && (mode == 4 || mode == 0);
+    const bool use_f32 = W <= 32 && f32_loads_exact && S < (1LL << 31) && (mode == 2 || mode == 0 || mode == 4);
     // windows wider than the largest cheap register ring: the O(1)-amortised deque sweep
     // (measured 4.8x faster than the W=64 ring at n=1000, slower at small windows)
     if (lam >= 0) {  // f2 penalized split (DESIGN R22)
@@ -1633,6 +1609,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     // the O(1)-amortised deque for windows wider than the largest cheap ring, or for mean windows
     // >= 12 (measured crossover: deque 10.3 vs ring 7.4 ms at mean 7.7 (C3), 0.23 vs 1.4 ms at 15)
     if (mode == 3 || (mode == 0 && (W > 32 || mean_w >= 12))) rc = launch_deque(st, args);
+    else if (use_u16) rc = launch_sweep_u16(W, mean_w, st, args);
     else rc = launch_sweep(W, use_f32, st, args, mean_w);
     if (rc) return rc;
     return launch_finish(w, L, T, n, demand, ld, S, Qe, cost, partial, true, st);
@@ -1642,7 +1619,7 @@ spdp_status launch_tour_prep(const int32_t* tours, int32_t T, int32_t n, const i
                              const uint16_t* demand, int64_t ld, char* w, const WsLayout& L,
                              spdp_saa_partial* partial, bool zero_slots, bool validate, cudaStream_t st) {
     const int threads = n >= 2048 ? 1024 : 256;
-    const size_t smem = 34 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
+    const size_t smem = 36 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
     tour_prep_kernel<<<T, threads, smem, st>>>(
         tours, n, dist, reinterpret_cast<int2*>(w + L.tabs), reinterpret_cast<int32_t*>(w + L.g0), demand, ld,
         reinterpret_cast<const uint16_t**>(w + L.rowp), reinterpret_cast<TourInfo*>(w + L.tinfo),
@@ -1800,7 +1777,7 @@ extern "C" spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dis
     spdp_status rc;
     {
         const int threads = n >= 2048 ? 1024 : 256;
-        const size_t smem = 34 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
+        const size_t smem = 36 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
         tour_prep_kernel<<<1, threads, smem, st>>>(tour, n, dist, tabs, g0, demand, ld, rowp, tinfo,
                                                    reinterpret_cast<int32_t*>(w + L.cgs), nullptr, hdr, nullptr, 0);
         if ((rc = last_launch("tour_prep_kernel"))) return rc;

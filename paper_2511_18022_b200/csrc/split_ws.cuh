@@ -10,16 +10,27 @@ namespace spdp {
 // Per-tour info for the fp32 sweep: g0f = (g(0) + OFF) / 2^24 (float bits),
 // off = OFF = D[n] (makes every g(p) + OFF >= 0), ok = every value the fp32
 // sweep forms is an integer (times 2^-24) below 2^24, hence exact.
+// The packed-u16 sweep (split_u16.cu) keeps g relative to a per-scenario base in 15 bits:
+// ns16 = NS = sum of max(0, -Cg) over the tour's layers (the most the window minimum can ever
+// fall, DESIGN §6 "packed-u16"), thr16 = 0x7FFF - (largest sum of max(0, Cg) over kU16Check
+// consecutive layers): a value at or below thr16 at a range check stays below 2^15 until the
+// next check; ok16 = every value the sweep forms fits (NS + max Cg + that sum <= 0x7FFF).
+// bn = B[n] = D[n] + c_{s_n,0} (added in int32 at the end).
 struct TourInfo {
-    int32_t g0f_bits, off, ok, pad;
+    int32_t g0f_bits, off, ok, ns16, thr16, ok16, bn, pad;
 };
+
+// Range-check interval of the packed-u16 sweep (layers); tour_prep_kernel's thr16 assumes it.
+constexpr int kU16Check = 10;
 
 constexpr int kTabPad = 64;       // padding rows after each tour table
 constexpr int kSlots = 32;  // SAA partial slots per tour (spread the sweep's atomics)
 
-// Cg planes: per tour [2][cg_stride(n)] int32 (plane 0 int Cg, plane 1 fp32 Cg / 2^24 bits), zero padded;
+// Cg planes: per tour [kCgPlanes][cg_stride(n)] int32 (plane 0 int Cg, plane 1 fp32 Cg / 2^24 bits,
+// plane 2 the packed-u16 pair Cg * 0x10001 (0 at layer n and in the padding)), zero padded;
 // the stride keeps every chunk's W-entry slice 16-byte aligned for the bulk copies.
 __host__ __device__ inline int cg_stride(int n) { return (n + kTabPad + 7) & ~7; }
+constexpr int kCgPlanes = 3;
 
 struct WsLayout {
     size_t hdr, g0, tinfo, tabs, rowp, cgs, slots, ovf, total;
@@ -33,7 +44,7 @@ inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
     L.tinfo = off; off = align_up(off + sizeof(TourInfo) * (size_t)T, 256);
     L.tabs = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
     L.rowp = off; off = align_up(off + sizeof(uint64_t) * (size_t)T * (size_t)(n + kTabPad), 256);
-    L.cgs = off; off = align_up(off + sizeof(int32_t) * 2 * (size_t)T * (size_t)cg_stride(n), 256);
+    L.cgs = off; off = align_up(off + sizeof(int32_t) * kCgPlanes * (size_t)T * (size_t)cg_stride(n), 256);
     L.slots = off; off = align_up(off + sizeof(spdp_saa_partial) * (size_t)T * (size_t)kSlots, 256);
     L.ovf = off; off = align_up(off + sizeof(unsigned long long) * (size_t)T * (size_t)S, 256);
     L.total = off;
@@ -43,6 +54,28 @@ inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
 // header words
 enum { HDR_OVF_COUNT = 0, HDR_STATUS = 1, HDR_SAMPLE_W = 2, HDR_TILE = 3, HDR_SAMPLE_SUM = 4 /* u64 */, HDR_SAMPLE_CNT = 6 };
 enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
+
+// Arguments of the sweep launchers (split.cu, split_u16.cu).
+struct SweepArgs {
+    const uint16_t* const* rowp;
+    const int2* tabs;
+    const int32_t* cgs;
+    const int32_t* g0;
+    const TourInfo* tinfo;
+    int n, T;
+    const uint16_t* demand;
+    int64_t ld, S;
+    uint32_t Q;
+    int32_t* cost;
+    spdp_saa_partial* slots;
+    unsigned long long* ovf;
+    unsigned* hdr;
+};
+
+// split_u16.cu: the packed-u16 sweep (two scenarios per lane).  u16_loads_ok(): its load
+// range check (host side); launch_sweep_u16: W in {16, 20, 24, 32}, mean_w picks the grouping.
+bool u16_loads_ok(int n, uint32_t Q);
+spdp_status launch_sweep_u16(int W, int mean_w, cudaStream_t st, const SweepArgs& a);
 
 // Host launchers (split.cu).
 // tour_prep_kernel over T tours into the workspace (tables, g0, row pointers, Cg

@@ -37,7 +37,7 @@ def test_c2_full_all_costs_and_saa(spdp):
     assert np.array_equal(d.cpu().numpy().view(np.uint16)[:, :S], dem)
     want = oracle.split(inst["tour"], inst["dist"], dem, inst["Q"])
     w = oracle.saa(want)
-    for algo in (None, "f32", "deque"):  # None = the launch configuration bench.py times
+    for algo in (None, "f32", "deque", "u16"):  # None = the launch configuration bench.py times
         cost, part = spdp.split_eval(tour, dist, d, inst["Q"], S=S, window_hint=bench_config.HINT["C2"], algo=algo)
         got = cost.cpu().numpy().astype(np.int64)
         assert np.array_equal(got, want), algo

@@ -69,7 +69,7 @@ def test_prefix_and_mask(spdp):
 
 
 # ------------------------------------------------------------------ a5 / a6 single tour
-ALGOS = (None, "int", "f32", "deque")
+ALGOS = (None, "int", "f32", "deque", "u16")
 
 
 def _check_split(spdp, inst, dem, S, hints=(0, 8, 16, 32, 64), Q=None, algos=ALGOS):

@@ -53,7 +53,7 @@ def test_random_instances_every_entry_point(spdp, seed):
     n, S, Q, dist, tour, dem = _instance(rng)
     T, D, dd = to_dev(tour), to_dev(dem), to_dev(dist)
     want = as_i32(oracle.split(tour, dist, dem, Q, S=S))
-    for algo in (None, "int", "f32", "deque"):
+    for algo in (None, "int", "f32", "deque", "u16"):
         for hint in (0, 8, 20, 32, 64):
             cost, _ = spdp.split_eval(T, dd, D, Q, S=S, window_hint=hint, algo=algo)
             assert np.array_equal(cost.cpu().numpy().astype(np.int64), want), (algo, hint)
