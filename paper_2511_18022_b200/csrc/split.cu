@@ -1576,7 +1576,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
     if (flags & SPDP_F_SWEEP_U16) mode = 4;
     // default for windows <= 32: the packed-u16 ring (two scenarios per lane) when its load range
     // check passes, else the packed-fp32 ring when its loads are exact, else the int ring
-    const bool u16_ok = ((W <= 32 && W >= 16) || mode == 4) && u16_loads_ok(n, Qe) && S < (1LL << 31);  // TUNING (temporary)
+    const bool u16_ok = W <= 32 && W >= 16 && u16_loads_ok(n, Qe) && S < (1LL << 31);
     const bool use_u16 = u16_ok && (mode == 4 || mode == 0);
     const bool use_f32 = W <= 32 && f32_loads_exact && S < (1LL << 31) && (mode == 2 || mode == 0 || mode == 4);
     // windows wider than the largest cheap register ring: the O(1)-amortised deque sweep
