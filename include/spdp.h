@@ -85,6 +85,8 @@ typedef enum {
 #define SPDP_F_NBR_AUTO 64u        /* spdp_split_eval_neighbours(_multi): read the candidates' changed spans
                                        back (synchronizes) and run spdp_split_eval_batch instead when they
                                        average more than 40 % of the tour (the measured crossover) */
+#define SPDP_F_IRP_EAGER 65536u    /* spdp_irp_dp: the eager-shift lane kernel instead of the lazily shifted
+                                       value functions (same results) */
 /* bits 8..15 of flags: the expected MEAN window width i - mask(i) (0 = unknown; with
  * window_hint = 0 it is sampled).  A tuning hint like window_hint: it picks how many
  * candidates the sweep evaluates before its first warp vote, never the result. */
@@ -348,6 +350,13 @@ SPDP_API spdp_status spdp_saa_estimate_f32(const float* cost, int64_t S, spdp_sa
 SPDP_API spdp_status spdp_saa_f32_moments(const float* cost, int64_t S, double center, double* moments,
                                  spdp_stream_t stream);
 
+/* fp32-mode SAA finalize (host, synchronous): from the SUMMED pass-1 moments m1
+ * (HOST double[4], spdp_saa_f32_moments with center 0, all-reduced over ranks) the count,
+ * infeasible count and mean -- the centre of pass 2 -- and, when m2 (HOST double[4], the summed
+ * pass centred on that mean) is non-NULL, also var (m - 1 denominator), std_err and the 95 %
+ * interval; with m2 NULL those stay NaN.  E_DATA when no cost is finite. */
+SPDP_API spdp_status spdp_saa_finalize_f32(const double* m1, const double* m2, spdp_saa_estimate* out_h);
+
 /* a6 standalone: SAA partial of a cost vector (SPDP_INFEASIBLE entries are
  * counted in n_infeas and excluded).  partial: DEVICE pointer to one struct. */
 SPDP_API spdp_status spdp_saa_reduce(const int32_t* cost, int64_t S, spdp_saa_partial* partial,
@@ -376,8 +385,10 @@ SPDP_API spdp_status spdp_split_eval_host(const int32_t* tour_h, const int32_t* 
  * cost[j] = sum_m min_J V_H[J] (int64 [S], overwritten).  visit_h: HOST uint8 [M][H]
  * (z_{m,t}); cust_h: HOST array [M]; both are copied into `ws` (size from
  * spdp_irp_workspace_bytes).  demand: uint16 [H*M][ld], row t*M + m.
- * U <= 1023 and H (c X + h U + b 65535) < 2^29 (else E_RESOURCE).
- * partial (may be NULL): SAA partial of the S costs (DEVICE pointer). */
+ * U <= 1023 and H (c X + h U + b 65535) < 2^29 per customer (else E_RESOURCE).
+ * partial (may be NULL): SAA partial of the S costs (DEVICE pointer); needs the sum of those
+ * per-customer bounds below 2^31 (cost^2 must fit the summable int64 halves), else E_RESOURCE.
+ * flags: SPDP_F_IRP_EAGER selects the eager-shift kernel (same results). */
 SPDP_API size_t spdp_irp_workspace_bytes(int32_t H, int32_t M, int64_t S);
 SPDP_API spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_customer* cust_h, int32_t H, int32_t M,
                         const uint16_t* demand, int64_t ld, int64_t S, int64_t* cost,

@@ -34,7 +34,8 @@ F_VALIDATE = 1
 F_SCRATCH_GLOBAL = 16
 F_NBR_SMEM = 32
 F_NBR_AUTO = 64
-F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8, "u16": 128}  # sweep algorithm flags (spdp.h)
+F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8, "u16": 128}
+F_IRP_EAGER = 65536  # sweep algorithm flags (spdp.h)
 MAX_N = 16384
 
 SYMBOLS = (
@@ -45,7 +46,7 @@ SYMBOLS = (
     "spdp_split_eval_penalized", "spdp_values_workspace_bytes", "spdp_split_values",
     "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours", "spdp_limits_workspace_bytes",
     "spdp_split_eval_limits", "spdp_f32_workspace_bytes", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
-    "spdp_saa_f32_moments", "spdp_split_eval_batch_f32", "spdp_split_eval_neighbours_multi",
+    "spdp_saa_f32_moments", "spdp_saa_finalize_f32", "spdp_split_eval_batch_f32", "spdp_split_eval_neighbours_multi",
 )
 
 
@@ -113,6 +114,7 @@ def _sig():
     L.spdp_split_eval_f32.argtypes = [P, P, i32, P, i64, i64, i32, P, P, sz, P]
     L.spdp_saa_estimate_f32.argtypes = [P, i64, ctypes.POINTER(SaaEstimate), P, sz, P]
     L.spdp_saa_f32_moments.argtypes = [P, i64, ctypes.c_double, P, P]
+    L.spdp_saa_finalize_f32.argtypes = [P, P, ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_batch_f32.argtypes = [P, i32, P, i32, P, i64, i64, i32, P, P, sz, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
@@ -121,7 +123,7 @@ def _sig():
                  "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean", "spdp_split_eval_host",
                  "spdp_irp_dp", "spdp_split_values", "spdp_split_eval_neighbours", "spdp_split_eval_penalized",
                  "spdp_split_routes", "spdp_split_eval_limits", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
-                 "spdp_saa_f32_moments", "spdp_split_eval_batch_f32",
+                 "spdp_saa_f32_moments", "spdp_saa_finalize_f32", "spdp_split_eval_batch_f32",
                  "spdp_split_eval_neighbours_multi"):
         getattr(L, name).restype = st
 
@@ -198,15 +200,34 @@ def _mean_flag(mean_window: int) -> int:
 
 
 def workspace(nbytes: int, device, tag: str = "split"):
-    """Cached per-device scratch buffer (torch uint8), grown on demand."""
+    """Cached scratch buffer (torch uint8) per (device, current stream, tag), grown on demand.
+
+    spdp.h forbids one workspace in two concurrent calls: keying by the stream gives calls on
+    different streams (or threads using different streams) their own buffers.  A grown buffer's
+    predecessor is released only after the stream has finished with it (record_stream), and a
+    captured CUDA graph keeps referring to the buffer it was captured with -- replay it only while
+    that buffer is alive (a graph pins its workspace; bench.py holds a reference)."""
     torch = _torch()
     dev = torch.device(device)
-    key = (dev.index if dev.index is not None else torch.cuda.current_device(), tag)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    stream = torch.cuda.current_stream(idx)
+    key = (idx, stream.cuda_stream, tag)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
+        if buf is not None:
+            buf.record_stream(stream)  # the caching allocator reuses it only after the stream's queued work
         buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
         _WS[key] = buf
     return buf
+
+
+def _default_S(demand, S):
+    """The scenario count of a demand matrix: S if given, else the true count recorded by
+    gen_demands / empty_demand (not the padded row length ld, whose padding columns would be
+    evaluated as extra all-zero scenarios), else ld."""
+    if S is not None:
+        return int(S)
+    return int(getattr(demand, "_spdp_S", demand.shape[1]))
 
 
 def workspace_bytes(n: int, S: int, T: int = 1) -> int:
@@ -218,9 +239,12 @@ def padded_ld(S: int) -> int:
 
 
 def empty_demand(n: int, S: int, device):
-    """u16 demand matrix [n][ld] (stored as torch.int16), ld = S rounded up to 8."""
+    """u16 demand matrix [n][ld] (stored as torch.int16), ld = S rounded up to 8; the true S is
+    recorded on the tensor (the default S of every call that takes it)."""
     torch = _torch()
-    return torch.zeros((n, padded_ld(S)), dtype=torch.int16, device=device)
+    out = torch.zeros((n, padded_ld(S)), dtype=torch.int16, device=device)
+    out._spdp_S = int(S)
+    return out
 
 
 # ------------------------------------------------------------------ a1
@@ -237,6 +261,7 @@ def gen_demands(model: dict, s_begin: int, S: int, device="cuda", out=None):
                     q_cap=int(model["q_cap"]), stream_tag=int(model.get("stream_tag", 0)), seed=int(model["seed"]))
     _check(_lib.spdp_gen_demands(ctypes.byref(m), int(s_begin), int(S), _dev_ptr(out, "out"), out.shape[1],
                                  _stream(out.device)), "spdp_gen_demands")
+    out._spdp_S = int(S)
     out._spdp_nominal = nominal  # keep alive until the stream has consumed it
     return out
 
@@ -245,7 +270,7 @@ def gen_demands(model: dict, s_begin: int, S: int, device="cuda", out=None):
 def demand_prefix(tour, demand, S: int | None = None):
     torch = _torch()
     n, ld = demand.shape
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     out = torch.empty((n + 1, S), dtype=torch.int32, device=demand.device)
     _check(_lib.spdp_demand_prefix(_dev_ptr(tour, "tour"), n, _dev_ptr(demand, "demand"), ld, S,
                                    _dev_ptr(out, "prefix"), _stream(demand.device)), "spdp_demand_prefix")
@@ -255,7 +280,7 @@ def demand_prefix(tour, demand, S: int | None = None):
 def split_mask(tour, demand, Q: int, S: int | None = None):
     torch = _torch()
     n, ld = demand.shape
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     out = torch.empty((n, S), dtype=torch.int32, device=demand.device)
     _check(_lib.spdp_split_mask(_dev_ptr(tour, "tour"), n, _dev_ptr(demand, "demand"), ld, S, int(Q),
                                 _dev_ptr(out, "mask"), _stream(demand.device)), "spdp_split_mask")
@@ -270,7 +295,7 @@ def split_eval(tour, dist, demand, Q: int, S: int | None = None, want_cost: bool
     algo: None/"auto", "int", "f32", "deque" or "u16" (identical results; see spdp.h)."""
     torch = _torch()
     n, ld = demand.shape
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if want_cost and cost is None:
         cost = torch.empty(S, dtype=torch.int32, device=dev)
@@ -293,7 +318,7 @@ def split_eval_penalized(tour, dist, demand, Q: int, lam: int, S: int | None = N
     """f2: penalized split costs (int32 [S]) and the SAA partial (spdp_split_eval_penalized)."""
     torch = _torch()
     n, ld = demand.shape
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if want_cost and cost is None:
         cost = torch.empty(S, dtype=torch.int32, device=dev)
@@ -314,7 +339,7 @@ def split_routes(tour, dist, demand, Q: int, scen, S: int | None = None):
     nroutes int32 [K], maxload int32 [K]); pred[k][i] = last split point of prefix i."""
     torch = _torch()
     n, ld = demand.shape
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     K = int(scen.shape[0])
     cost = torch.empty(K, dtype=torch.int32, device=dev)
@@ -337,7 +362,7 @@ def split_eval_batch(tours, dist, demand, Q: int, S: int | None = None, want_cos
     torch = _torch()
     n, ld = demand.shape
     T = tours.shape[0]
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if want_cost and cost is None:
         cost = torch.empty((T, S), dtype=torch.int32, device=dev)
@@ -360,7 +385,7 @@ def split_values(tour, dist, demand, Q: int, S: int | None = None, fwd=None, bwd
     bwd[i] = Split of the customers after position i (INFEASIBLE sentinel)."""
     torch = _torch()
     n, ld = demand.shape
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if fwd is None:
         fwd = torch.empty((n + 1, S), dtype=torch.int32, device=dev)
@@ -385,7 +410,7 @@ def split_eval_neighbours(parent, fwd, bwd, tours, dist, demand, Q: int, S: int 
     torch = _torch()
     n, ld = demand.shape
     T = tours.shape[0]
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if want_cost and cost is None:
         cost = torch.empty((T, S), dtype=torch.int32, device=dev)
@@ -412,7 +437,7 @@ def split_eval_limits(tour, dist, demand, Q: int, max_duration: int = -1, max_ro
     most max_routes routes (<= 0: none) (spdp_split_eval_limits).  Returns (cost int32 [S], partial)."""
     torch = _torch()
     n, ld = demand.shape
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if want_cost and cost is None:
         cost = torch.empty(S, dtype=torch.int32, device=dev)
@@ -434,7 +459,7 @@ def split_eval_f32(tour, dist, demand, Q: int, S: int | None = None, cost=None):
     returns float32 costs [S] (+inf = infeasible)."""
     torch = _torch()
     n, ld = demand.shape
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if cost is None:
         cost = torch.empty(S, dtype=torch.float32, device=dev)
@@ -450,7 +475,7 @@ def split_eval_batch_f32(tours, dist, demand, Q: int, S: int | None = None, cost
     torch = _torch()
     n, ld = demand.shape
     T = tours.shape[0]
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if cost is None:
         cost = torch.empty((T, S), dtype=torch.float32, device=dev)
@@ -483,6 +508,22 @@ def saa_f32_moments(cost, center: float = 0.0, out=None):
     return out
 
 
+def saa_finalize_f32(m1, m2=None) -> dict:
+    """fp32-mode SAA estimate (spdp_saa_finalize_f32, host) from summed pass-1 moments m1 and,
+    optionally, the pass-2 moments m2 centred on the pass-1 mean (float64 [4] each, any device)."""
+    a1 = np.ascontiguousarray(m1.detach().cpu().numpy() if hasattr(m1, "detach") else m1, dtype=np.float64).reshape(4)
+    a2 = None
+    if m2 is not None:
+        a2 = np.ascontiguousarray(m2.detach().cpu().numpy() if hasattr(m2, "detach") else m2,
+                                  dtype=np.float64).reshape(4)
+    e = SaaEstimate()
+    _check(_lib.spdp_saa_finalize_f32(a1.ctypes.data_as(ctypes.c_void_p),
+                                      a2.ctypes.data_as(ctypes.c_void_p) if a2 is not None else None,
+                                      ctypes.byref(e)), "spdp_saa_finalize_f32")
+    return {"m": e.m, "infeasible": e.infeasible, "mean": e.mean, "var": e.var, "stderr": e.std_err,
+            "ci95_lo": e.ci95_lo, "ci95_hi": e.ci95_hi}
+
+
 def split_eval_neighbours_multi(parents, parent_of, fwd, bwd, tours, dist, demand, Q: int, S: int | None = None,
                                 want_cost: bool = True, want_partial: bool = True, window_hint: int = 0,
                                 cost=None, partial=None):
@@ -492,7 +533,7 @@ def split_eval_neighbours_multi(parents, parent_of, fwd, bwd, tours, dist, deman
     n, ld = demand.shape
     T = tours.shape[0]
     P = parents.shape[0]
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     if want_cost and cost is None:
         cost = torch.empty((T, S), dtype=torch.int32, device=dev)
@@ -552,7 +593,7 @@ def split_eval_host(tour_h, dist_h, demand_h, Q: int, S: int | None = None, cost
         return a.ctypes.data_as(ctypes.c_void_p)
 
     n, ld = demand_h.shape
-    S = ld if S is None else S
+    S = _default_S(demand_h, S)
     ws = workspace(host_workspace_bytes(n, S), device, tag="host")
     e = SaaEstimate()
     _check(_lib.spdp_split_eval_host(hptr(tour_h, "tour"), hptr(dist_h, "dist"), n, hptr(demand_h, "demand"), ld, S,
@@ -565,11 +606,12 @@ def split_eval_host(tour_h, dist_h, demand_h, Q: int, S: int | None = None, cost
 
 # ------------------------------------------------------------------ a9 + a10
 def irp_dp(visit, cust, demand, H: int, M: int, S: int | None = None, want_partial: bool = True, cost=None,
-           partial=None):
-    """IRP recourse cost per scenario (int64 [S]); visit u8 [M][H] and cust int32 [M][6] on the host."""
+           partial=None, eager: bool = False):
+    """IRP recourse cost per scenario (int64 [S]); visit u8 [M][H] and cust int32 [M][6] on the host.
+    eager: the eager-shift kernel (SPDP_F_IRP_EAGER; same results)."""
     torch = _torch()
     ld = demand.shape[1]
-    S = ld if S is None else S
+    S = _default_S(demand, S)
     dev = demand.device
     visit = np.ascontiguousarray(visit, dtype=np.uint8)
     cust = np.ascontiguousarray(cust, dtype=np.int32)
@@ -581,5 +623,6 @@ def irp_dp(visit, cust, demand, H: int, M: int, S: int | None = None, want_parti
     ws = workspace(int(_lib.spdp_irp_workspace_bytes(H, M, S)), dev, tag="irp")
     _check(_lib.spdp_irp_dp(visit.ctypes.data_as(ctypes.c_void_p), carr, H, M, _dev_ptr(demand, "demand"), ld, S,
                             _dev_ptr(cost, "cost"), _dev_ptr(partial, "partial") if want_partial else None,
-                            ctypes.c_void_p(ws.data_ptr()), ws.numel(), 0, _stream(dev)), "spdp_irp_dp")
+                            ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_IRP_EAGER if eager else 0, _stream(dev)),
+           "spdp_irp_dp")
     return cost, partial

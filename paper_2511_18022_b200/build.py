@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -32,11 +33,24 @@ def _deps():
     return _sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "spdp.h"), __file__]
 
 
+def _src_hash() -> str:
+    """sha256 over every source the library is built from (paths and contents) and the flags."""
+    h = hashlib.sha256()
+    h.update(" ".join(ARCH + FLAGS).encode())
+    for p in sorted(_deps()):
+        h.update(os.path.relpath(p, HERE).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    """The in-tree library was built from exactly the current sources (a content hash recorded
+    next to it at build time -- not file times, which a copied tree does not preserve reliably)."""
+    if not (os.path.exists(LIB) and os.path.exists(LIB + ".sha256")):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(p) <= t for p in _deps())
+    with open(LIB + ".sha256") as f:
+        return f.read().strip() == _src_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -64,6 +78,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))
     os.replace(tmp, LIB)
+    with open(LIB + ".sha256", "w") as f:
+        f.write(_src_hash() + "\n")
     return LIB
 
 

@@ -301,6 +301,27 @@ extern "C" spdp_status spdp_saa_f32_moments(const float* cost, int64_t S, double
     return last_launch("saa_f32_moments_kernel");
 }
 
+// fp32-mode SAA finalize (host): from the summed pass-1 moments {m, sum c, -, infeasible} the
+// count and mean; with the pass-2 moments (centred on that mean) also the unbiased variance,
+// standard error and 95 % interval (the sample average of the second-stage costs).
+extern "C" spdp_status spdp_saa_finalize_f32(const double* m1, const double* m2, spdp_saa_estimate* out) {
+    const char* fn = "spdp_saa_finalize_f32";
+    if (!m1 || !out) return fail(SPDP_E_USAGE, "%s: NULL pointer", fn);
+    if (!(m1[0] >= 0.0) || !(m1[3] >= 0.0)) return fail(SPDP_E_USAGE, "%s: negative counts", fn);
+    const int64_t m = (int64_t)llround(m1[0]);
+    out->m = m;
+    out->infeasible = (int64_t)llround(m1[3]);
+    out->mean = out->var = out->std_err = out->ci95_lo = out->ci95_hi = NAN;
+    if (m == 0) return fail(SPDP_E_DATA, "%s: all scenarios infeasible (SPEC:287)", fn);
+    out->mean = m1[1] / (double)m;
+    if (!m2) return SPDP_OK;
+    out->var = m >= 2 ? m2[2] / (double)(m - 1) : 0.0;
+    out->std_err = sqrt(out->var / (double)m);
+    out->ci95_lo = out->mean - 1.96 * out->std_err;
+    out->ci95_hi = out->mean + 1.96 * out->std_err;
+    return SPDP_OK;
+}
+
 extern "C" spdp_status spdp_saa_estimate_f32(const float* cost, int64_t S, spdp_saa_estimate* out, void* ws,
                                              size_t ws_bytes, spdp_stream_t stream) {
     const char* fn = "spdp_saa_estimate_f32";
@@ -308,23 +329,15 @@ extern "C" spdp_status spdp_saa_estimate_f32(const float* cost, int64_t S, spdp_
     if (ws_bytes < 64) return fail(SPDP_E_USAGE, "%s: workspace < 64 bytes", fn);
     cudaStream_t st = (cudaStream_t)stream;
     double* acc = static_cast<double*>(ws);
-    double h[4];
+    double h1[4], h2[4];
     // pass 1: count and sum -> mean; pass 2: squared deviations about that mean (two-pass variance)
     spdp_status rc = spdp_saa_f32_moments(cost, S, 0.0, acc, stream);
     if (rc) return rc;
-    if ((rc = cuda_check(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st), "memcpy(moments)"))) return rc;
+    if ((rc = cuda_check(cudaMemcpyAsync(h1, acc, sizeof(h1), cudaMemcpyDeviceToHost, st), "memcpy(moments)"))) return rc;
     if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
-    const int64_t m = (int64_t)h[0];
-    out->m = m;
-    out->infeasible = (int64_t)h[3];
-    if (m == 0) return fail(SPDP_E_DATA, "%s: all scenarios infeasible (SPEC:287)", fn);
-    out->mean = h[1] / (double)m;
+    if ((rc = spdp_saa_finalize_f32(h1, nullptr, out))) return rc;
     if ((rc = spdp_saa_f32_moments(cost, S, out->mean, acc, stream))) return rc;
-    if ((rc = cuda_check(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st), "memcpy(moments)"))) return rc;
+    if ((rc = cuda_check(cudaMemcpyAsync(h2, acc, sizeof(h2), cudaMemcpyDeviceToHost, st), "memcpy(moments)"))) return rc;
     if ((rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize"))) return rc;
-    out->var = m >= 2 ? h[2] / (double)(m - 1) : 0.0;
-    out->std_err = sqrt(out->var / (double)m);
-    out->ci95_lo = out->mean - 1.96 * out->std_err;
-    out->ci95_hi = out->mean + 1.96 * out->std_err;
-    return SPDP_OK;
+    return spdp_saa_finalize_f32(h1, h2, out);
 }

@@ -318,7 +318,7 @@ static spdp_status launch_irp(const uint8_t* visit, const IrpCust* cust, int H, 
     if (spdp_status e = kernel_setup((const void*)irp_kernel<K>, 200 * 1024, -1, 0, 0, nullptr, "irp_kernel setup")) return e;
     const int64_t ntask = ((S + 31) / 32) * M;
     int64_t blocks = ceil_div(ntask, warps);
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > (int64_t)device_sms() * 16) blocks = (int64_t)device_sms() * 16;
     prof_begin(st);
     irp_kernel<K><<<(unsigned)blocks, warps * 32, smem, st>>>(visit, cust, H, M, demand, ld, S, cost);
     spdp_status rc = last_launch("irp_kernel");
@@ -340,12 +340,12 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
                                    const uint16_t* demand, int64_t ld, int64_t S, int64_t* cost,
                                    spdp_saa_partial* partial, void* ws, size_t ws_bytes, uint32_t flags,
                                    spdp_stream_t stream) {
-    (void)flags;
     if (H < 1 || M < 1 || S < 1) return fail(SPDP_E_USAGE, "spdp_irp_dp: H, M, S must be >= 1");
     if (!visit_h || !cust_h || !demand || !cost || !ws) return fail(SPDP_E_USAGE, "spdp_irp_dp: NULL pointer");
     if (ld < S) return fail(SPDP_E_USAGE, "spdp_irp_dp: ld < S");
     if (ws_bytes < spdp_irp_workspace_bytes(H, M, S)) return fail(SPDP_E_USAGE, "spdp_irp_dp: workspace too small");
     int Umax = 0;
+    long long total_bound = 0;  // bound on a scenario's cost (the sum over customers)
     for (int m = 0; m < M; ++m) {
         const spdp_irp_customer& c = cust_h[m];
         if (c.U < 0 || c.X < 0 || c.I0 < 0 || c.I0 > c.U || c.h < 0 || c.b < 0 || c.c < 0)
@@ -353,8 +353,14 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
         // every reachable value <= H (c X + h U + b 65535) must stay below 2^29
         const long long bound = (long long)H * ((long long)c.c * c.X + (long long)c.h * c.U + (long long)c.b * 65535LL);
         if (bound >= (1LL << 29)) return fail(SPDP_E_RESOURCE, "spdp_irp_dp: cost bound %lld exceeds int32 kernel range", bound);
+        total_bound += bound;
         Umax = c.U > Umax ? c.U : Umax;
     }
+    // the SAA partial squares each cost into the summable {sumsq_lo, sumsq_hi} halves, which stay
+    // exact while cost^2 < 2^62 (spdp_saa_partial): reject larger totals rather than wrap
+    if (partial && total_bound >= (1LL << 31))
+        return fail(SPDP_E_RESOURCE, "spdp_irp_dp: cost bound %lld (sum over customers) >= 2^31: the SAA partial "
+                    "would overflow (pass partial = NULL and reduce the int64 costs elsewhere)", total_bound);
     if (Umax + 1 > 32 * 32) return fail(SPDP_E_RESOURCE, "spdp_irp_dp: U=%d > 1023", Umax);
     cudaStream_t st = (cudaStream_t)stream;
     char* w = static_cast<char*>(ws);
@@ -367,10 +373,7 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     bool prefix_band = true;  // every customer's delivery band is [0, y] (or empty)
     for (int m = 0; m < M; ++m) prefix_band &= (cust_h[m].X == 0 || cust_h[m].X >= cust_h[m].U);
     const size_t lane_smem_warp = sizeof(int32_t) * 32 * (size_t)(Umax + 1);
-    static const int irp_mode = [] {  // tuning knob: SPDP_IRP=lane selects the eager-shift kernel
-        const char* e = getenv("SPDP_IRP");
-        return (e && !strcmp(e, "lane")) ? 1 : 0;
-    }();
+    const int irp_mode = (flags & SPDP_F_IRP_EAGER) ? 1 : 0;  // the eager-shift lane kernel instead of the lazy one
     if (prefix_band && lane_smem_warp <= 48 * 1024 && irp_mode == 0) {
         // lazy-shift lane kernel: 4 warps per CTA, several CTAs per SM
         const int warps = 4;
@@ -408,8 +411,8 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     if (partial) {
         if ((rc = cuda_check(cudaMemsetAsync(partial, 0, sizeof(spdp_saa_partial), st), "memset partial"))) return rc;
         int64_t blocks = ceil_div(S, 256 * 8);
-        if (blocks > 148 * 8) blocks = 148 * 8;
-        irp_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(c, S, partial);
+        if (blocks > (int64_t)device_sms() * 8) blocks = (int64_t)device_sms() * 8;
+        irp_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(c, S, partial);  // (|cost| < 2^31: checked above)
         if ((rc = last_launch("irp_reduce_kernel"))) return rc;
     }
     return SPDP_OK;

@@ -1811,7 +1811,7 @@ extern "C" spdp_status spdp_saa_reduce(const int32_t* cost, int64_t S, spdp_saa_
     spdp_status rc = cuda_check(cudaMemsetAsync(partial, 0, sizeof(spdp_saa_partial), st), "cudaMemsetAsync(partial)");
     if (rc || S == 0) return rc;
     int64_t blocks = ceil_div(S, 256 * 8);
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > (int64_t)device_sms() * 8) blocks = (int64_t)device_sms() * 8;
     saa_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(cost, S, partial);
     return last_launch("saa_reduce_kernel");
 }

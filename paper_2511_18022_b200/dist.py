@@ -39,26 +39,21 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
 
 def saa_estimate_f32(cost, group=None, moments_fn=None) -> dict:
     """fp32-mode SAA estimate over the costs of ALL ranks (DESIGN R25): two passes, each one
-    all-reduce(SUM) of 4 doubles -- {m, sum} gives the global mean, then the squared deviations
-    about it (the two-pass variance of the single-GPU spdp_saa_estimate_f32).  moments_fn(cost,
-    center) -> float64 tensor [4] defaults to the device kernel (spdp_saa_f32_moments)."""
-    import math
-
+    all-reduce(SUM) of 4 doubles -- {m, sum} gives the global mean (spdp_saa_finalize_f32), then
+    the squared deviations about it; the estimate itself is spdp_saa_finalize_f32 of the two
+    summed passes (this function only moves the moments).  moments_fn(cost, center) -> float64
+    tensor [4] defaults to the device kernel (spdp_saa_f32_moments)."""
     import torch.distributed as dist
+
+    from paper_2511_18022_b200 import saa_finalize_f32
     if moments_fn is None:
         from paper_2511_18022_b200 import saa_f32_moments as moments_fn
     multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
     m1 = moments_fn(cost, 0.0)
     if multi:
         dist.all_reduce(m1, op=dist.ReduceOp.SUM, group=group)
-    m = int(round(float(m1[0])))
-    if m == 0:
-        raise ValueError("all scenarios infeasible (SPEC:287)")
-    mean = float(m1[1]) / m
-    m2 = moments_fn(cost, mean)
+    center = saa_finalize_f32(m1)["mean"]
+    m2 = moments_fn(cost, center)
     if multi:
         dist.all_reduce(m2, op=dist.ReduceOp.SUM, group=group)
-    var = float(m2[2]) / (m - 1) if m >= 2 else 0.0
-    se = math.sqrt(var / m)
-    return {"m": m, "infeasible": int(round(float(m1[3]))), "mean": mean, "var": var, "stderr": se,
-            "ci95_lo": mean - 1.96 * se, "ci95_hi": mean + 1.96 * se}
+    return saa_finalize_f32(m1, m2)

@@ -109,3 +109,45 @@ def test_saa_f32_against_exact_fractions():
     # identical costs: variance 0
     assert oracle.saa_f32(np.full(10, 3.5, dtype=np.float32))["var"] == 0.0
     assert statistics.fmean([1.0, 2.0]) == oracle.saa_f32(np.array([1.0, 2.0], dtype=np.float32))["mean"]
+
+
+def _bf32_leftfold(tour, q, dist, Q):
+    """R25 written out over every contiguous partition: each route's cost formed in fp64 from the
+    sequential fp64 tour prefix Dd, c_{0,s_{p+1}} + (Dd[i] - Dd[p+1]) + c_{s_i,0} left to right,
+    rounded once to fp32; the routes' costs summed left to right in fp32 (one rounding per add);
+    the minimum over the capacity-feasible partitions.  Round-to-nearest is monotone, so this
+    minimum is EXACTLY the value of the DP min_p fl32(f(p) + T32(p, i)) -- bit for bit."""
+    n = len(tour)
+    Dd = [0.0] * (n + 1)  # Dd[k], k = 1..n (1-based positions): arcs before position k
+    for k in range(2, n + 1):
+        Dd[k] = Dd[k - 1] + float(dist[tour[k - 2], tour[k - 1]])
+    best = np.float32(np.inf)
+    for cuts in itertools.product((0, 1), repeat=n - 1):
+        bounds, start = [], 1
+        for k, cut in enumerate(cuts, start=1):
+            if cut:
+                bounds.append((start, k))
+                start = k + 1
+        bounds.append((start, n))
+        if any(sum(q[k - 1] for k in range(a, b + 1)) > Q for a, b in bounds):
+            continue
+        acc = np.float32(0.0)
+        for a, b in bounds:  # route = positions a..b = p + 1..i
+            t64 = (float(dist[0, tour[a - 1]]) + (Dd[b] - Dd[a])) + float(dist[tour[b - 1], 0])
+            acc = np.float32(acc + np.float32(t64))
+        best = min(best, acc)
+    return best
+
+
+def test_f32_bit_exact_against_fp32_left_fold_brute_force():
+    rng = np.random.default_rng(55)
+    checked = 0
+    for _ in range(60):
+        n = int(rng.integers(1, 10))
+        tour, dist, Q, q, dem = _case(rng, n, 3, real=True, qmax=10)
+        c32 = oracle.split_f32(tour, dist, dem, Q, S=3)
+        for s in range(3):
+            want = _bf32_leftfold(tour, q[s], dist, Q)
+            assert np.float32(c32[s]).tobytes() == want.tobytes(), (n, s, c32[s], want)
+            checked += np.isfinite(want)
+    assert checked > 100
