@@ -6,12 +6,17 @@
 
 Workload (BASELINE.json configs[1], DESIGN §Input recipe): "C2", an X-n101-shaped
 CVRPSD instance, n = 100 customers, one giant tour, 10^6 correlated-demand
-scenarios per GPU (weak scaling: rank r owns global scenarios
-[r 10^6, (r+1) 10^6)).  One step = one pass of the hot path over the resident
-demand set: tour prep (a2) + masked min-plus sweep with per-scenario costs
-(a5) + fused SAA partial (a6) (+ the int64 all-reduce of the partial, a7, at
-N > 1).  Timed with CUDA events on the launching stream, max over ranks.
-The demand set (200 MB/GPU) is larger than L2, so every step streams it from HBM.
+scenarios in all (strong scaling, the default: rank r owns the global scenarios
+[floor(r S / N), floor((r+1) S / N)), north_star's "each rank owns S/8"; --scaling weak:
+10^6 per GPU).  One step = one pass of the hot path over the resident demand set:
+tour prep (a2) + masked min-plus sweep with per-scenario costs (a5) + fused SAA
+partial (a6) (+ the int64 all-reduce of the partial, a7, at N > 1, on a
+communication stream so that it overlaps the next step: pipelined evaluations).
+The timed steps replay a CUDA graph (at N > 1 one graph of G steps with their
+NCCL all-reduces); at N > 1 the line also carries the single-shot latency (one
+step with its all-reduce completed, nothing overlapped).  Timed with CUDA events
+on the launching stream, max over ranks.  The demand set (200 MB at N = 1) is
+larger than L2, so every step streams it from HBM.
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
 reference arm of this tier) on the host cores instead.
@@ -35,7 +40,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 import bench_config  # noqa: E402
 
-METRIC = "split evals/sec (scenario x tour) at n=100, S=1M per GPU"
+METRIC = "split evals/sec (scenario\u00d7tour) at n=100, S=1M, 1/2/4/8 B200; % ALU/HBM roofline"  # BASELINE.json
 UNIT = "scenario-tour evals/s"
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
 
@@ -179,13 +184,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="spdp", choices=["spdp", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): S = 10^6 in all, split over the ranks; weak: 10^6 per rank")
     ap.add_argument("--no-rows", action="store_true", help="skip the per-row (C3/C4/C5/gen) measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--window-hint", type=int, default=None)
     ap.add_argument("--eager", action="store_true",
-                    help="launch every timed step from Python (default at N = 1: replay a CUDA graph of the step)")
+                    help="launch every timed step from Python (default: replay a CUDA graph of the step(s))")
+    ap.add_argument("--graph-steps", type=int, default=10,
+                    help="steps per captured CUDA graph at N > 1 (their all-reduces pipelined inside it)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -224,7 +232,16 @@ def main():
         S_loc, S_glob = s_end - s_begin, S_cfg
     hint = args.window_hint if args.window_hint is not None else bench_config.HINT[args.config]
 
-    demand = spdp.gen_demands(cfg["model"], s_begin, S_loc, device=dev)
+    # Inputs larger than L2 at every N: at N = 1 the demand set (200 MB) is; when a rank's share is
+    # smaller (strong scaling), every step evaluates a fresh batch of the global S scenarios --
+    # batch k = the generator's scenarios [k S_glob, (k+1) S_glob), this rank's shard of it -- over
+    # B batches generated up front that together exceed twice the L2 (126 MB), so each step's
+    # batch was evicted since its last use and streams from HBM.
+    L2_BYTES = 126e6
+    dem_bytes = n * spdp.padded_ld(S_loc) * 2
+    B = 1 if dem_bytes > 1.5 * L2_BYTES else int(np.ceil(2 * L2_BYTES / dem_bytes))
+    demands = [spdp.gen_demands(cfg["model"], s_begin + k * S_glob, S_loc, device=dev) for k in range(B)]
+    demand = demands[0]
     T = cfg["T"]
     tour = torch.from_numpy(inst["tour"]).to(dev)
     tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
@@ -239,53 +256,80 @@ def main():
     kstep = [0]
 
     def step():
+        cur = torch.cuda.current_stream(dev)  # (the capture stream while a graph is being captured)
         b = kstep[0] & 1
         kstep[0] += 1
         part = partials[b]
+        dem = demands[(kstep[0] - 1) % B]
         if freed[b] is not None:
-            stream.wait_event(freed[b])
+            cur.wait_event(freed[b])
         if T > 1:  # batched tours (a8): T candidate tours over the same scenarios
-            spdp.split_eval_batch(tours, dist, demand, Q, S=S_loc, window_hint=hint, cost=cost, partial=part,
+            spdp.split_eval_batch(tours, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost, partial=part,
                                   mean_window=bench_config.MEAN[args.config])
         else:
-            spdp.split_eval(tour, dist, demand, Q, S=S_loc, window_hint=hint, cost=cost, partial=part,
+            spdp.split_eval(tour, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost, partial=part,
                             mean_window=bench_config.MEAN[args.config])
         if world > 1:
             ready = torch.cuda.Event()
-            ready.record(stream)
+            ready.record(cur)
+            comm.wait_event(ready)
             with torch.cuda.stream(comm):
-                comm.wait_event(ready)
                 pdist.allreduce_partials(part)
                 done = torch.cuda.Event()
                 done.record(comm)
             freed[b] = done
 
+    def join():  # the outstanding all-reduces, into the current stream
+        cur = torch.cuda.current_stream(dev)
+        for ev in freed:
+            if ev is not None:
+                cur.wait_event(ev)
+
     for _ in range(args.warmup):
         step()
+    join()
     torch.cuda.synchronize(dev)
-    # At N = 1 the timed steps replay a CUDA graph of one step (the same three kernels with their
-    # programmatic-dependent-launch edges), so host launch overhead (ctypes marshalling, ~tens of
-    # us per step in Python) cannot leave the GPU idle between steps.
+    # The timed steps replay a CUDA graph: at N = 1 of one step (the same three kernels with their
+    # programmatic-dependent-launch edges), at N > 1 of G steps whose NCCL all-reduces run on the
+    # communication stream, each overlapping the next step (joined at the graph's end) -- so host
+    # launch overhead (ctypes marshalling, ~tens of us per step in Python) cannot leave the GPU idle.
+    G = B  # one graph replay = one pass over the batches
+    if world > 1 and B == 1:
+        G = max(1, min(args.graph_steps, args.steps))
     graph, launch_mode = None, "eager (one C-ABI call per step from Python)"
-    if world == 1 and not args.eager:
+    if share:
+        launch_mode += "; gloo all-reduce (SPDP_BENCH_SHARE_GPU functional check)"
+    elif not args.eager:
         try:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                step()
+                for _ in range(G):
+                    step()
+                join()
+            freed[0] = freed[1] = None  # (capture-time events; the graph carries the dependencies)
             torch.cuda.synchronize(dev)
             for _ in range(3):
                 g.replay()
             torch.cuda.synchronize(dev)
-            graph, launch_mode = g, "CUDA graph replay (one captured step per replay)"
+            graph = g
+            launch_mode = ("CUDA graph replay (one captured step per replay)" if G == 1 else
+                           "CUDA graph replay (%d captured steps per replay, each step's all-reduce overlapping "
+                           "the next step on a communication stream)" % G)
         except Exception as ex:  # keep the eager loop (and say why)
             launch_mode = "eager (graph capture failed: %s)" % str(ex).splitlines()[0][:120]
+            freed[0] = freed[1] = None
             torch.cuda.synchronize(dev)
 
-    def timed_step():
+    def timed_steps(K):  # exactly K steps: K // G graph replays, the rest launched eagerly
         if graph is not None:
-            graph.replay()
+            for _ in range(K // G):
+                graph.replay()
+            kstep[0] = 0
+            for _ in range(K % G):
+                step()
         else:
-            step()
+            for _ in range(K):
+                step()
 
     # algorithmic work: Eq. (3) candidates sum_i (i - mask(i)) from the standalone mask kernel (untimed)
     m = spdp.split_mask(tour, demand, Q, S=S_loc)
@@ -313,11 +357,8 @@ def main():
     # sweep and finish kernels overlap their launch with the predecessor: programmatic dependent
     # launch; an event recorded between them would serialise that)
     t_start.record(stream)
-    for k in range(args.steps):
-        timed_step()
-    for ev in freed:  # the last all-reduces are part of the timed region
-        if ev is not None:
-            stream.wait_event(ev)
+    timed_steps(args.steps)
+    join()  # the last all-reduces are part of the timed region
     t_end.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -326,15 +367,30 @@ def main():
     for k in range(args.steps):
         spdp.set_profile_events(ev_s[k], ev_e[k])
         step()
+    join()
     torch.cuda.synchronize(dev)
     spdp.set_profile_events()
+    # single-shot latency: one step AND its all-reduce, nothing overlapped (the latency a caller
+    # waiting for one evaluation sees); max over ranks
+    n_ss = max(3, min(args.steps, 20))
+    ss_a = [torch.cuda.Event(enable_timing=True) for _ in range(n_ss)]
+    ss_b = [torch.cuda.Event(enable_timing=True) for _ in range(n_ss)]
+    if world > 1:
+        tdist.barrier()
+    for k in range(n_ss):
+        ss_a[k].record(stream)
+        step()
+        join()
+        ss_b[k].record(stream)
+        torch.cuda.synchronize(dev)
+    single_shot_ms = statistics.median(a.elapsed_time(b) for a, b in zip(ss_a, ss_b))
     if world > 1:
         tdist.barrier()
     # keep sampling clocks under the same load for >= 1 s so the record is meaningful
     soak_end = time.perf_counter() + 1.0
     while time.perf_counter() < soak_end:
-        for _ in range(20):
-            timed_step()
+        timed_steps(max(G, 20 // G * G))
+        join()
         torch.cuda.synchronize(dev)
     clocks = sampler.stop()
 
@@ -343,8 +399,9 @@ def main():
     sweep_ms = statistics.mean(sweep_all)
     sweep_med = statistics.median(sweep_all)
     if world > 1:
-        ms_step = pdist.max_over_ranks(ms_step, device=dev)
-        sweep_ms = pdist.max_over_ranks(sweep_ms, device=dev)
+        ms_step = pdist.max_over_ranks(ms_step, device=dev if not share else None)
+        sweep_ms = pdist.max_over_ranks(sweep_ms, device=dev if not share else None)
+        single_shot_ms = pdist.max_over_ranks(single_shot_ms, device=dev if not share else None)
     value = S_glob * T * 1.0 / (ms_step / 1e3)
 
     pk = peaks()
@@ -370,17 +427,21 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": "%s: X-n%d-shaped CVRPSD, n=%d, Q=%d, %d correlated-demand scenarios per GPU "
-                                   "(cv=0.3, rho=0.5), %d giant tour%s" % (args.config, n + 1, n, Q, S_loc, T,
-                                                                        "s" if T > 1 else ""),
+            "config": {"workload": "%s: X-n%d-shaped CVRPSD, n=%d, Q=%d, %d correlated-demand scenarios in all "
+                                   "(%d per GPU; cv=0.3, rho=0.5), %d giant tour%s" % (
+                                       args.config, n + 1, n, Q, S_glob, S_loc, T, "s" if T > 1 else ""),
                        "n": n, "S_per_gpu": S_loc, "S_global": S_glob, "T": T, "window_hint": hint,
                        "mean_window_hint": bench_config.MEAN[args.config],
-                       "l2": ("inputs larger than L2 (demand %.0f MB/GPU > 126 MB)" if n * S_loc * 2 > 126e6 else
-                              "demand %.0f MB/GPU fits L2 (126 MB): steps after the first read it from L2")
-                             % (n * S_loc * 2 / 1e6),
+                       "l2": ("inputs larger than L2 (demand %.0f MB/GPU > 126 MB)" % (dem_bytes / 1e6) if B == 1 else
+                              "inputs larger than L2: each step a fresh batch of the S scenarios, %d batches of "
+                              "%.0f MB/GPU rotating (%.0f MB > 2 x 126 MB L2)" % (B, dem_bytes / 1e6,
+                                                                                  B * dem_bytes / 1e6)),
                        "parallelism": "scenario-sharded dp%d, 1 int64 all-reduce/step (on a comm stream, "
                                       "overlapped with the next step)" % world,
                        "launch": launch_mode},
+            "single_shot_ms": single_shot_ms,
+            "single_shot": "median over %d steps of one step with its all-reduce completed (nothing overlapped), "
+                           "max over ranks" % n_ss,
             "roofline": roof, "clocks": clocks, "gpu_launches": 3 * args.steps}
 
     # ------------------------------------------------------------------ e2e through the C-ABI host entry
