@@ -141,6 +141,27 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         "r"(parity), "r"(10000000u)
         : "memory");
 }
+// one try of the same wait (true: the phase has completed); a warp loops on it through a vote,
+// so the compiler knows the warp leaves the loop converged (no divergence checks, BRA.DIV, on the
+// warp votes that follow)
+__device__ __forceinline__ bool mbar_try_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(10000000u)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+    while (!__all_sync(kFull, mbar_try_sleep(bar, parity))) {
+    }
+    __syncwarp();
+}
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -185,28 +206,34 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
     __syncthreads();
     pdl_wait();  // tables, counters and partial slots come from tour_prep_kernel
 
-    if (wid == kU16Cons) {
+    // (a vote, not a plain branch on wid: the compiler then knows each role runs whole warps, and the
+    // consumers' warp votes need no divergence checks, BRA.DIV)
+    if (__any_sync(kFull, wid == kU16Cons)) {
         // ---------------- producer: one lane fills the stages in order -----------------------------
         // per chunk: W/4 gathers of 4 tour-ordered rows x 256 scenarios (the tile of all consumers),
-        // one bulk copy of the W Cg pairs, the header; completion on the stage's full barrier
-        if (lane == 0) {
-            int t = -1, b = 0, c = nchunks, st = 0;
-            unsigned r = 0u;
-            for (;;) {
-                mbar_wait_sleep(&empty[st], (r & 1u) ^ 1u);  // the consumers released the previous use (round r - 1)
-                if (c == nchunks) {                      // the next tile
-                    const unsigned id = atomicAdd(hdr + HDR_TILE, 1u);
-                    t = id < ntiles ? (int)(id / ntile_s) : -1;
-                    b = id < ntiles ? (int)(id - (uint32_t)t * ntile_s) : 0;
-                    c = 0;
-                }
-                unsigned char* sb = smem_raw + (size_t)st * Cfg::kStageBytes;
-                uint64_t* fb = &full[st];
-                *reinterpret_cast<int4*>(sb + Cfg::kHdrOff) = make_int4(t, b, c, 0);
-                if (t < 0) {  // no tiles left: an arrival without data tells the consumers to stop
-                    mbar_arrive(fb);
-                    break;
-                }
+        // one bulk copy of the W Cg pairs, the header; completion on the stage's full barrier.  The
+        // whole warp runs the loop (lane 0 issues): no lane exits early, so the compiler keeps every
+        // warp of the kernel provably converged.
+        int t = -1, b = 0, c = nchunks, st = 0;
+        unsigned r = 0u;
+        for (;;) {
+            mbar_wait_warp(&empty[st], (r & 1u) ^ 1u);  // the consumers released the previous use (round r - 1)
+            if (c == nchunks) {                           // the next tile
+                unsigned id = 0;
+                if (lane == 0) id = atomicAdd(hdr + HDR_TILE, 1u);
+                id = __shfl_sync(kFull, id, 0);
+                t = id < ntiles ? (int)(id / ntile_s) : -1;
+                b = id < ntiles ? (int)(id - (uint32_t)t * ntile_s) : 0;
+                c = 0;
+            }
+            unsigned char* sb = smem_raw + (size_t)st * Cfg::kStageBytes;
+            uint64_t* fb = &full[st];
+            if (lane == 0) *reinterpret_cast<int4*>(sb + Cfg::kHdrOff) = make_int4(t, b, c, 0);
+            if (__any_sync(kFull, t < 0)) {  // no tiles left: an arrival without data tells the consumers to stop
+                if (lane == 0) mbar_arrive(fb);
+                break;
+            }
+            if (lane == 0) {
                 mbar_arrive_expect_tx(fb, (uint32_t)(Cfg::kRowsBytes + W * 4));
                 const int r0 = c * W;
                 const int2* tab = tabs + (int64_t)t * (n + kTabPad) + r0;  // (padded past n)
@@ -219,17 +246,17 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
                 }
                 bulk_g2s_plain(sb + Cfg::kCgOff, cgs + (int64_t)t * kCgPlanes * cgs_stride + 2 * cgs_stride + r0, W * 4,
                                fb);
-                ++c;
-                if (++st == NS) {
-                    st = 0;
-                    ++r;
-                }
+            }
+            __syncwarp();
+            ++c;
+            if (++st == NS) {
+                st = 0;
+                ++r;
             }
         }
-        return;
-    }
-
+    } else {
     // ---------------- consumer warp wid ---------------------------------------------------------
+    __syncwarp();
     const int slot = (blockIdx.x * kU16Cons + wid) % kSlots;
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
     const int rem = n % W;
@@ -272,7 +299,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
     unsigned cr = 0u;   // round (parity of the full barrier's phase)
     for (;;) {
         unsigned char* sb = smem_raw + (size_t)cs * Cfg::kStageBytes;
-        mbar_wait_sleep(&full[cs], cr & 1u);
+        mbar_wait_warp(&full[cs], cr & 1u);
         const int4 th = *reinterpret_cast<const int4*>(sb + Cfg::kHdrOff);
         if (__all_sync(kFull, th.x < 0)) break;  // (a vote: keeps the warp provably converged)
         const int t = th.x;
@@ -410,7 +437,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
             }
             if (__all_sync(kFull, ++c >= nchunks)) break;
             sb = smem_raw + (size_t)cs * Cfg::kStageBytes;
-            mbar_wait_sleep(&full[cs], cr & 1u);
+            mbar_wait_warp(&full[cs], cr & 1u);
         }
         uint32_t val = gprev;  // rem == 0: the last layer computed position n
         if (rem != 0) {        // else position n sits in ring slot rem (pushed by the first padded layer)
@@ -448,6 +475,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
         }
     }
     if (slots) flush();
+    }  // (no early return in either role: the compiler keeps each warp provably converged)
 }
 
 bool u16_loads_ok(int n, uint32_t Q) {
@@ -489,7 +517,7 @@ static spdp_status launch_u16_t(cudaStream_t st, const SweepArgs& a) {
     CUtensorMap map;
     if (spdp_status e = make_demand_map(&map, a.demand, a.ld, a.S, a.n)) return e;
     const int64_t ntiles = ((a.S + kU16Tile - 1) / kU16Tile) * a.T;
-    int64_t grid = (int64_t)blocks_per_sm * device_sms();
+    int64_t grid = (int64_t)blocks_per_sm * device_sms();  // (measured: 4-5 CTAs per SM saturate it)
     if (grid > ntiles) grid = ntiles;
     const uint32_t Q = a.Q, pthr = 0x7fffu - Q - (uint32_t)kU16Check * (Q + 1u);
     const U16Consts kc{0xffffffffu, 1u, (Q + 0x8000u) * 0x10001u, ((0x10000u - (Q + 1u)) & 0xffffu) * 0x10001u,

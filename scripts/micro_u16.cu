@@ -128,6 +128,52 @@ __global__ void k_novote(unsigned* out, unsigned m1, unsigned seed) {
     if (s == 0x12345u) out[0] = s;
 }
 
+
+// candidate idiom variants (per pair of candidates of one scenario pair):
+//  (b) 2 IMAD + 2 LOP3 + 2 VIMNMX.U16x2 (2-input folds)
+__global__ void k_cand2(unsigned* out, unsigned m1, unsigned seed) {
+    unsigned Yg[CH], G[CH], best[CH / 2];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        Yg[c] = seed * (c + 1) + threadIdx.x;
+        G[c] = seed ^ (c * 0x9E3779B9u);
+    }
+#pragma unroll
+    for (int c = 0; c < CH / 2; ++c) best[c] = 0xffffffffu;
+    unsigned P = seed;
+    for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH / 2; ++c) {
+            const unsigned d0 = imad(P, m1, Yg[2 * c]);
+            const unsigned d1 = imad(P, m1, Yg[2 * c + 1]);
+            best[c] = __vminu2(__vminu2(best[c], lop3(G[2 * c], d0, 0x80008000u)), lop3(G[2 * c + 1], d1, 0x80008000u));
+        }
+        P += 0x00010001u;
+    }
+    unsigned s = 0;
+#pragma unroll
+    for (int c = 0; c < CH / 2; ++c) s ^= best[c];
+    if (s == 0x12345u) out[0] = s;
+}
+//  (c) tree fold: 6 keys -> min3(min3(k0,k1,k2), min3(k3,k4,k5)) + accumulate: 6 IMAD + 6 LOP3 + 3 VIMNMX3
+__global__ void k_cand3(unsigned* out, unsigned m1, unsigned seed) {
+    unsigned Yg[6], G[6], best = 0xffffffffu;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        Yg[c] = seed * (c + 1) + threadIdx.x;
+        G[c] = seed ^ (c * 0x9E3779B9u);
+    }
+    unsigned P = seed;
+    for (int i = 0; i < ITERS; ++i) {
+        unsigned k[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) k[c] = lop3(G[c], imad(P, m1, Yg[c]), 0x80008000u);
+        best = __vimin3_u16x2(best, __vimin3_u16x2(k[0], k[1], k[2]), __vimin3_u16x2(k[3], k[4], k[5]));
+        P += 0x00010001u;
+    }
+    if (best == 0x12345u) out[0] = best;
+}
+
 template <typename K>
 static void run(K kern, const char* name, double instr_per_iter_per_thread, unsigned* d, double clk_ghz) {
     const int blocks = 148 * 8, threads = 256;
@@ -171,6 +217,8 @@ int main() {
     run(k_vmin3_lop3, "VIMNMX3.U16x2 + LOP3 interleaved (per instr)", 2 * CH, d, ghz);
     run(k_vmin3_imad, "VIMNMX3.U16x2 + IMAD interleaved (per instr)", 2 * CH, d, ghz);
     run(k_cand, "candidate pair idiom: IMAD+LOP3 x2 + VIMNMX3 (per instr)", 5.0 * CH / 2 + 1.0, d, ghz);
+    run(k_cand2, "candidate pair: IMAD+LOP3 x2 + 2 VIMNMX.U16x2 (per instr)", 6.0 * CH / 2 + 1.0, d, ghz);
+    run(k_cand3, "6 candidates: 6 IMAD + 6 LOP3 + 3 VIMNMX3 tree (per instr)", 16.0, d, ghz);
     run(k_vote, "8 LOP3 + VOTE.ANY + BRA per iteration (per LOP3)", CH, d, ghz);
     run(k_novote, "8 LOP3 + uniform BRA per iteration (per LOP3)", CH, d, ghz);
     cudaError_t e = cudaGetLastError();
