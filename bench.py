@@ -540,9 +540,14 @@ def measure_rows(spdp, torch, dev, pk):
     idx = torch.arange(1, 101, device=dev, dtype=torch.int64).unsqueeze(1)
     cand16 = int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item())
     del m
+    bytes16 = 100 * cfg2["S"] * 2 + cfg2["S"] * 4
     rows["a5_C2_r16"] = {"ms": ms, "Q": inst16["Q"], "evals_per_s": cfg2["S"] / (ms / 1e3), "kernel": spdp.last_kernel(),
+                         "bound": "hbm", "bytes_alg": bytes16,
+                         "hbm_frac": bytes16 / (ms / 1e3) / (pk["hbm_gbs"] * 1e9),
                          "candidates": cand16,
-                         "alu_frac": cand16 / (ms / 1e3) / (N_SM * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6)}
+                         "candidates_note": "Eq. (3) window sum; the deque sweep does O(1) amortised work per "
+                                            "layer, so its bound is the demand stream (hbm_frac), not these",
+                         "alu_frac_of_window_sum": cand16 / (ms / 1e3) / (N_SM * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6)}
     del d
     # a8: batched tours (C3) and a5 at n=1000 (C4, 1 GPU)
     for name in ("C3", "C4"):
@@ -556,15 +561,26 @@ def measure_rows(spdp, torch, dev, pk):
         fn = lambda: spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, partial=part,
                                            window_hint=h, mean_window=bench_config.MEAN[name])
         ms = _time_events(fn, torch, dev, iters=6)
-        m = spdp.split_mask(tours[0].contiguous(), d, inst["Q"], S=cfg["S"])
+        kern = spdp.last_kernel()
+        # exact Eq. (3) candidate count: the window sum of EVERY tour (standalone mask kernel, untimed)
         idx = torch.arange(1, cfg["n"] + 1, device=dev, dtype=torch.int64).unsqueeze(1)
-        cand0 = int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item())
+        cand = 0
+        for t in range(cfg["T"]):
+            m = spdp.split_mask(tours[t].contiguous(), d, inst["Q"], S=cfg["S"])
+            cand += int(((idx - m.to(torch.int64)) * (m >= 0)).sum().item())
         del m
         alu_peak = N_SM * ALU_LANES_PER_SM_CLK * pk["sm_max_mhz"] * 1e6
-        cand = cand0 * cfg["T"]  # tours differ by a few moves: window statistics ~ tour 0
-        rows["a8_batch_%s" % name if cfg["T"] > 1 else "a5_%s" % name] = {
-            "ms": ms, "evals_per_s": cfg["T"] * cfg["S"] / (ms / 1e3), "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
-            "candidates_est": cand, "alu_frac_est": cand / (ms / 1e3) / alu_peak}
+        bytes_ = cfg["n"] * cfg["S"] * 2 + cfg["T"] * cfg["S"] * 4 * 0  # (want_cost=False: no cost stream)
+        row = {"ms": ms, "evals_per_s": cfg["T"] * cfg["S"] / (ms / 1e3), "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
+               "kernel": kern, "candidates": cand, "alu_frac": cand / (ms / 1e3) / alu_peak,
+               "bytes_alg": bytes_, "hbm_frac": bytes_ / (ms / 1e3) / (pk["hbm_gbs"] * 1e9)}
+        if "deque" in kern:
+            row["bound"] = "hbm"
+            row["candidates_note"] = ("Eq. (3) window sum; the deque sweep does O(1) amortised work per layer, so "
+                                      "its bound is the demand stream (hbm_frac)")
+        else:
+            row["bound"] = "alu"
+        rows["a8_batch_%s" % name if cfg["T"] > 1 else "a5_%s" % name] = row
         del d
     # f3: the C3 population evaluated from tour 0's prefix / suffix values (spdp_split_values once,
     # then spdp_split_eval_neighbours over the 256 candidates): same costs as a8, fewer layers
@@ -683,8 +699,17 @@ def measure_rows(spdp, torch, dev, pk):
     costb = torch.empty(c5["S"], dtype=torch.int64, device=dev)
     fn = lambda: spdp.irp_dp(irp["visit"], irp["cust"], d, irp["H"], irp["M"], S=c5["S"], cost=costb)
     ms = _time_events(fn, torch, dev, iters=3)
-    rows["a9_a10_irp_C5"] = {"ms": ms, "scenarios_per_s": c5["S"] / (ms / 1e3),
-                             "states_per_s": c5["S"] * irp["M"] * irp["H"] * 101 / (ms / 1e3)}
+    # roofline: the demand stream (H M u16 per scenario) + the int64 cost; work = the (scenario,
+    # customer, period) DP stages, each over U + 1 inventory states (the lazy kernel shifts instead of
+    # rewriting the state vector on a no-delivery period, so the states are an upper bound of its work)
+    bytes_irp = irp["H"] * irp["M"] * c5["S"] * 2 + c5["S"] * 8
+    U = int(irp["cust"][0, 0])
+    rows["a9_a10_irp_C5"] = {"ms": ms, "scenarios_per_s": c5["S"] / (ms / 1e3), "kernel": spdp.last_kernel(),
+                             "stages_per_s": c5["S"] * irp["M"] * irp["H"] / (ms / 1e3),
+                             "states_per_s": c5["S"] * irp["M"] * irp["H"] * (U + 1) / (ms / 1e3),
+                             "bytes_alg": bytes_irp, "hbm_frac": bytes_irp / (ms / 1e3) / (pk["hbm_gbs"] * 1e9),
+                             "bound": "alu (issue): 60 MB of demand against ~10^8 state updates; hbm_frac shows "
+                                      "how far the data stream is from limiting it"}
     return rows
 
 

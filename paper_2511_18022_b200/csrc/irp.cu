@@ -322,6 +322,7 @@ static spdp_status launch_irp(const uint8_t* visit, const IrpCust* cust, int H, 
     prof_begin(st);
     irp_kernel<K><<<(unsigned)blocks, warps * 32, smem, st>>>(visit, cust, H, M, demand, ld, S, cost);
     spdp_status rc = last_launch("irp_kernel");
+    set_last_kernel("irp_kernel<%d>", K);
     prof_end(st);
     return rc;
 }
@@ -385,6 +386,7 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
         irp_lazy_kernel<<<(unsigned)blocks, warps * 32, lane_smem_warp * warps, st>>>(dvisit, dcust, H, M, Umax, demand,
                                                                                      ld, S, c);
         rc = last_launch("irp_lazy_kernel");
+        set_last_kernel("irp_lazy_kernel");
         prof_end(st);
     } else if (prefix_band && lane_smem_warp <= 96 * 1024) {
         int warps = (int)((192 * 1024) / lane_smem_warp);
@@ -396,6 +398,7 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
         irp_lane_kernel<<<(unsigned)blocks, warps * 32, lane_smem_warp * warps, st>>>(dvisit, dcust, H, M, Umax, demand,
                                                                                      ld, S, c);
         rc = last_launch("irp_lane_kernel");
+        set_last_kernel("irp_lane_kernel");
         prof_end(st);
     } else {
     if ((rc = cuda_check(cudaMemsetAsync(cost, 0, sizeof(int64_t) * (size_t)S, st), "memset cost"))) return rc;
