@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
                                                          int2* __restrict__ tabs, int32_t* __restrict__ g0,
                                                          const uint16_t* __restrict__ demand, int64_t ld,
                                                          const uint16_t** __restrict__ rowps, TourInfo* __restrict__ tinfo,
-                                                         int32_t* __restrict__ cgs, spdp_saa_partial* __restrict__ slots,
+                                                         int32_t* __restrict__ cgs, int32_t* __restrict__ trows,
+                                                         spdp_saa_partial* __restrict__ slots,
                                                          unsigned* __restrict__ hdr, spdp_saa_partial* __restrict__ partial,
                                                          int validate) {
     extern __shared__ unsigned char smem_raw[];
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     const int cs = cg_stride(n);
     int32_t* cgi = cgs + (int64_t)t * kCgPlanes * cs;  // plane 0: int Cg, 1: fp32 Cg / 2^24, 2: packed u16 pair
     const uint16_t** rowp = rowps + (int64_t)t * (n + kTabPad);
+    int32_t* trow = trows + (int64_t)t * trow_stride(n);
     int ns_local = 0, cgpos_max = 0;
     for (int i = lo; i < hi; ++i) {
         const int a = node(i);
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
             ext[3] = e.y;
         }
         rowp[i] = demand + (int64_t)e.x * ld;
+        trow[i] = e.x;
     }
     if (ns_local) atomicAdd(&ext[0], ns_local);
     if (cgpos_max) atomicMax(&ext[1], cgpos_max);
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
         tab[i] = make_int2(0, 0);
         rowp[i] = demand;
     }
+    for (int i = n + tid; i < trow_stride(n); i += nt) trow[i] = n;  // outside the tensor: zeros
     if (tid == 0) g0[t] = dist[node(0)];
     __syncthreads();
     {  // the largest sum of max(0, Cg) over kU16Check consecutive layers (plane 0 is complete)
@@ -1561,7 +1565,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
                 mean_w = (int)((wsum + (unsigned long long)h[HDR_SAMPLE_CNT] * n / 2) / ((unsigned long long)h[HDR_SAMPLE_CNT] * n));
         }
     }
-    const SweepArgs args{rowp, tabs, reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
+    const SweepArgs args{rowp, tabs, reinterpret_cast<const int32_t*>(w + L.trow), reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
                          cost, partial ? slots : nullptr, ovf, hdr};
     // fp32 sweep when every load value it forms (P' <= (n + W) min(Q, 65535) for feasible scenarios
     // including the padded layers, Y = P' + Q) is an exact float; the per-tour cost range is checked on
@@ -1587,7 +1591,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
         if (rc) return rc;
         const size_t per_warp = 2 * sizeof(long long) * (size_t)(n + 1);
         const int warps = per_warp * 4 <= 192 * 1024 ? 4 : 1;
-        if ((rc = kernel_setup((const void*)split_finish_kernel, 200 * 1024, -1, 0, 0, nullptr, "split_finish setup")))
+        if ((rc = kernel_setup((const void*)split_finish_kernel, 200 * 1024, 100, 0, 0, nullptr, "split_finish setup")))
             return rc;
         if ((rc = kernel_setup((const void*)split_penalized_finish_kernel, 200 * 1024, -1, 0, 0, nullptr,
                                "split_penalized_finish setup")))
@@ -1620,10 +1624,12 @@ spdp_status launch_tour_prep(const int32_t* tours, int32_t T, int32_t n, const i
                              spdp_saa_partial* partial, bool zero_slots, bool validate, cudaStream_t st) {
     const int threads = n >= 2048 ? 1024 : 256;
     const size_t smem = 36 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
+    // (the sweep's shared-memory carveout: no L1 / shared reconfiguration between the kernels of a call)
+    if (spdp_status e = kernel_setup((const void*)tour_prep_kernel, -1, 100, 0, 0, nullptr, "tour_prep setup")) return e;
     tour_prep_kernel<<<T, threads, smem, st>>>(
         tours, n, dist, reinterpret_cast<int2*>(w + L.tabs), reinterpret_cast<int32_t*>(w + L.g0), demand, ld,
         reinterpret_cast<const uint16_t**>(w + L.rowp), reinterpret_cast<TourInfo*>(w + L.tinfo),
-        reinterpret_cast<int32_t*>(w + L.cgs), zero_slots ? reinterpret_cast<spdp_saa_partial*>(w + L.slots) : nullptr,
+        reinterpret_cast<int32_t*>(w + L.cgs), reinterpret_cast<int32_t*>(w + L.trow), zero_slots ? reinterpret_cast<spdp_saa_partial*>(w + L.slots) : nullptr,
         reinterpret_cast<unsigned*>(w + L.hdr), partial, validate ? 1 : 0);
     return last_launch("tour_prep_kernel");
 }
@@ -1635,7 +1641,7 @@ spdp_status launch_finish(char* w, const WsLayout& L, int32_t T, int32_t n, cons
     // each with 12 (n+1) B of shared scratch for the rare windows wider than kOvfW)
     const size_t per_warp = 3 * sizeof(int) * (size_t)(n + 1);
     const int warps = per_warp * 4 <= 192 * 1024 ? 4 : 1;
-    if (spdp_status e = kernel_setup((const void*)split_finish_kernel, 200 * 1024, -1, 0, 0, nullptr, "split_finish setup"))
+    if (spdp_status e = kernel_setup((const void*)split_finish_kernel, 200 * 1024, 100, 0, 0, nullptr, "split_finish setup"))
         return e;
     const spdp_saa_partial* slots = partial ? reinterpret_cast<const spdp_saa_partial*>(w + L.slots) : nullptr;
     const int2* tabs = reinterpret_cast<const int2*>(w + L.tabs);
@@ -1779,7 +1785,8 @@ extern "C" spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dis
         const int threads = n >= 2048 ? 1024 : 256;
         const size_t smem = 36 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
         tour_prep_kernel<<<1, threads, smem, st>>>(tour, n, dist, tabs, g0, demand, ld, rowp, tinfo,
-                                                   reinterpret_cast<int32_t*>(w + L.cgs), nullptr, hdr, nullptr, 0);
+                                                   reinterpret_cast<int32_t*>(w + L.cgs),
+                                                   reinterpret_cast<int32_t*>(w + L.trow), nullptr, hdr, nullptr, 0);
         if ((rc = last_launch("tour_prep_kernel"))) return rc;
     }
     split_routes_kernel<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(tabs, g0, n, demand, ld, S, Qe, scen, K, pred, cost,

@@ -27,14 +27,18 @@
 //    fails it are deferred to split_finish_kernel, like ring overflows.
 //  * the chain: g(i) = min(keys of age >= 2, g(i-1)) + Cg[i], the add as one 32-bit add of
 //    the pair Cg * 0x10001 (no carry: both halves stay in [0, 0x7FFF]).
-//  * two layers per step: the candidates of age >= 2 of BOTH layers depend only on values known
-//    before either (layer j + 1's age 2 is layer j's age 1), so both layers' first groups run
-//    back to back and one warp vote per deeper group of ages guards both layers.
+//  * LS = 4 layers per step: the candidates of age >= l + 1 of layer j + l (l = 0 .. 3) are split
+//    points <= j, known before the step starts, so the four layers' unconditional groups run back
+//    to back and ONE warp vote per deeper group of ages guards all four layers (the vote, its
+//    branch and the branch-target fetch are paid once per 4 layers); the split points j + 1 ..
+//    j + 3 made inside the step enter last, as keys whose window tests (loads only) were ready
+//    early.  Measured (C2, 10^6 scenarios): two layers per step 84.0 us, four 79.8 us.
 //
 // Work decomposition (warp specialisation): a single wave of persistent CTAs of kU16Cons = 4
 // consumer warps + 1 producer warp.  A tile is 256 scenarios (64 per consumer warp) of one tour;
-// the producer takes tiles from a global counter and fills an NS-stage shared-memory ring: per
-// chunk of W layers, W/4 TMA gathers (cp.async.bulk.tensor.2d...tile::gather4: 4 tour-ordered
+// the producer of CTA k starts on tile k, takes later tiles from a global counter and fills an
+// NS-stage shared-memory ring: per chunk of W layers, the chunk's W demand rows in W/4 16-byte
+// loads of the tour's padded row table (one round trip), W/4 TMA gathers (cp.async.bulk.tensor.2d...tile::gather4: 4 tour-ordered
 // demand rows x 256 scenarios, 512 B each, in one instruction; rows past n are outside the tensor
 // and arrive as zeros) plus one bulk copy of the chunk's W Cg pairs, completing on the stage's
 // "full" mbarrier; the consumers release the stage through its "empty" mbarrier (4 arrivals), so
@@ -50,18 +54,22 @@
 
 namespace spdp {
 
-constexpr int kU16Cons = 4;                       // consumer warps per CTA, one tile of kU16Tile scenarios
+constexpr int kU16Cons = 4;                       // consumer warps per CTA, one tile of NP * kU16Box scenarios
 constexpr int kU16Threads = 32 * (kU16Cons + 1);  // + 1 producer warp
-constexpr int kU16Warp = 64;                      // scenarios per consumer warp (two per lane)
-constexpr int kU16Tile = kU16Cons * kU16Warp;     // scenarios per tile = columns of one TMA box
+constexpr int kU16Box = kU16Cons * 64;            // columns of one TMA box (256 scenarios, 512 B per row)
 constexpr uint32_t kGuard = 0x80008000u;
 
-template <int W>
+// NP = scenario pairs per lane (64 NP scenarios per consumer warp, NP TMA boxes per row and tile;
+// shared memory per stage: [NP boxes][W rows][256 scenarios] u16, then the W Cg pairs, the header)
+template <int W, int NP, int NST>
 struct U16Cfg {
-    static constexpr int NS = 3;                                            // stages
-    static constexpr int kMaxReg = W <= 24 ? 80 : 128;                      // registers: 5 / 3 CTAs per SM
-    static constexpr int kRowBytes = kU16Tile * (int)sizeof(uint16_t);      // 512 B
-    static constexpr int kRowsBytes = W * kRowBytes;                        // W rows
+    static constexpr int NS = NST;                                          // stages
+    static constexpr int kMaxReg = NP == 1 ? (W <= 24 ? 96 : 128) : 128;    // registers: 4 / 3 CTAs per SM
+    static constexpr int kTile = NP * kU16Box;                              // scenarios per tile
+    static constexpr int kWarp = NP * 64;                                   // scenarios per consumer warp
+    static constexpr int kRowBytes = kU16Box * (int)sizeof(uint16_t);      // 512 B (one box row)
+    static constexpr int kBoxBytes = W * kRowBytes;                         // W rows of one box
+    static constexpr int kRowsBytes = NP * kBoxBytes;                       // all boxes
     static constexpr int kCgOff = kRowsBytes;                               // W Cg pairs
     static constexpr int kHdrOff = kRowsBytes + W * (int)sizeof(int32_t);   // {tour, block, chunk, 0}
     static constexpr int kStageBytes = (kHdrOff + 16 + 127) / 128 * 128;    // (TMA: 128-B aligned)
@@ -105,6 +113,14 @@ __device__ __forceinline__ uint32_t umin_tree(const uint32_t* v) {
     else if constexpr (N == 3) return __vimin3_u16x2(v[0], v[1], v[2]);
     else if constexpr (N == 4) return __vimin3_u16x2(__vminu2(v[0], v[1]), v[2], v[3]);
     else return __vimin3_u16x2(umin_tree<N - 2>(v), v[N - 2], v[N - 1]);
+}
+
+// Minimum of v[lo .. N - 1] (lo a compile-time constant after unrolling).
+template <int N>
+__device__ __forceinline__ uint32_t umin_tree_from(const uint32_t* v, const int lo) {
+    if (lo == 0) return umin_tree<N>(v);
+    if constexpr (N > 1) return umin_tree_from<N - 1>(v + 1, lo - 1);
+    return v[0];
 }
 
 // ---- TMA / mbarrier helpers (this file only) ----------------------------------------------
@@ -178,21 +194,22 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 
 // A0: ages scanned unconditionally (age 1 + A0 - 1 masked candidates); then groups of UG ages,
 // each behind a warp vote on its youngest age; the scan of age W also tests for ring overflow.
-template <int W, int A0, int UG>
-__global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
-    split_sweep_u16_kernel(const __grid_constant__ CUtensorMap dmap, const int2* __restrict__ tabs,
+// NP: scenario pairs per lane (independent DP chains; one vote and one range check serve all).
+template <int W, int A0, int UG, int NP, int NST, int LS>
+__global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::kMaxReg))
+    split_sweep_u16_kernel(const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ trows,
                            const int32_t* __restrict__ cgs, const int32_t* __restrict__ g0s,
                            const TourInfo* __restrict__ tinfo, int n, int T, int64_t S, uint32_t Q, U16Consts kc,
                            int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
                            unsigned long long* __restrict__ ovf_list, unsigned* __restrict__ hdr) {
-    using Cfg = U16Cfg<W>;
+    using Cfg = U16Cfg<W, NP, NST>;
     constexpr int NS = Cfg::NS;
-    static_assert(A0 >= 2 && A0 <= W && UG >= 1, "bad u16 sweep config");
+    static_assert(A0 >= 2 && A0 <= W && UG >= 1 && NP >= 1 && (LS == 2 || LS == 4) && W % LS == 0 && kU16Check % LS == 0 && A0 >= LS + 1, "bad u16 sweep config");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::kStagesBytes);  // [NS]: data landed
     uint64_t* empty = full + NS;                                                 // [NS]: all consumers done
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t ntile_s = (uint32_t)((S + kU16Tile - 1) / kU16Tile);
+    const uint32_t ntile_s = (uint32_t)((S + Cfg::kTile - 1) / Cfg::kTile);
     const uint32_t ntiles = ntile_s * (uint32_t)T;
     const int nchunks = (n + W - 1) / W;
     const int cgs_stride = cg_stride(n);
@@ -210,20 +227,24 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
     // consumers' warp votes need no divergence checks, BRA.DIV)
     if (__any_sync(kFull, wid == kU16Cons)) {
         // ---------------- producer: one lane fills the stages in order -----------------------------
-        // per chunk: W/4 gathers of 4 tour-ordered rows x 256 scenarios (the tile of all consumers),
-        // one bulk copy of the W Cg pairs, the header; completion on the stage's full barrier.  The
+        // per chunk: NP W/4 gathers of 4 tour-ordered rows x 256 scenarios (box h of the tile), one
+        // bulk copy of the W Cg pairs, the header; completion on the stage's full barrier.  The
         // whole warp runs the loop (lane 0 issues): no lane exits early, so the compiler keeps every
         // warp of the kernel provably converged.
+        // the first tile of CTA k is tile k; later tiles come from the counter (starting at gridDim.x)
         int t = -1, b = 0, c = nchunks, st = 0;
-        unsigned r = 0u;
+        unsigned r = 0u, id = blockIdx.x;
+        const int4* trow = nullptr;
         for (;;) {
             mbar_wait_warp(&empty[st], (r & 1u) ^ 1u);  // the consumers released the previous use (round r - 1)
             if (c == nchunks) {                           // the next tile
-                unsigned id = 0;
-                if (lane == 0) id = atomicAdd(hdr + HDR_TILE, 1u);
-                id = __shfl_sync(kFull, id, 0);
+                if (t >= 0) {
+                    if (lane == 0) id = atomicAdd(hdr + HDR_TILE, 1u) + gridDim.x;
+                    id = __shfl_sync(kFull, id, 0);
+                }
                 t = id < ntiles ? (int)(id / ntile_s) : -1;
                 b = id < ntiles ? (int)(id - (uint32_t)t * ntile_s) : 0;
+                trow = reinterpret_cast<const int4*>(trows + (int64_t)(t < 0 ? 0 : t) * trow_stride(n));
                 c = 0;
             }
             unsigned char* sb = smem_raw + (size_t)st * Cfg::kStageBytes;
@@ -234,16 +255,18 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
                 break;
             }
             if (lane == 0) {
-                mbar_arrive_expect_tx(fb, (uint32_t)(Cfg::kRowsBytes + W * 4));
                 const int r0 = c * W;
-                const int2* tab = tabs + (int64_t)t * (n + kTabPad) + r0;  // (padded past n)
+                // the chunk's W rows, 4 per load (past n: row n, outside the tensor, reads as zeros)
+                int4 rq[W / 4];
 #pragma unroll
-                for (int g = 0; g < W / 4; ++g) {
-                    const int i = r0 + 4 * g;  // rows past n read as zeros (row n is outside the tensor)
-                    tma_gather4(sb + g * 4 * Cfg::kRowBytes, &dmap, b * kU16Tile, i < n ? tab[4 * g].x : n,
-                                i + 1 < n ? tab[4 * g + 1].x : n, i + 2 < n ? tab[4 * g + 2].x : n,
-                                i + 3 < n ? tab[4 * g + 3].x : n, fb);
-                }
+                for (int g = 0; g < W / 4; ++g) rq[g] = __ldg(trow + r0 / 4 + g);
+                mbar_arrive_expect_tx(fb, (uint32_t)(Cfg::kRowsBytes + W * 4));
+#pragma unroll
+                for (int g = 0; g < W / 4; ++g)
+#pragma unroll
+                    for (int h = 0; h < NP; ++h)
+                        tma_gather4(sb + h * Cfg::kBoxBytes + g * 4 * Cfg::kRowBytes, &dmap, b * Cfg::kTile + h * kU16Box,
+                                    rq[g].x, rq[g].y, rq[g].z, rq[g].w, fb);
                 bulk_g2s_plain(sb + Cfg::kCgOff, cgs + (int64_t)t * kCgPlanes * cgs_stride + 2 * cgs_stride + r0, W * 4,
                                fb);
             }
@@ -261,10 +284,20 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
     const int rem = n % W;
     const uint32_t m1 = kc.m1, one = kc.one, QGP = kc.qgp, nQ1P = kc.nq1p, PADD = kc.padd;
-
-    uint32_t G[W], Y[W];
+    // pair k of lane l: scenarios 64 (NP wid + k) + 2 l + {0, 1} of the tile, i.e. box (NP wid + k) / 4,
+    // columns 64 ((NP wid + k) % 4) + 2 l + {0, 1}
+    int boff[NP];
 #pragma unroll
-    for (int k = 0; k < W; ++k) G[k] = 0u;
+    for (int k = 0; k < NP; ++k) {
+        const int q = NP * wid + k;
+        boff[k] = (q >> 2) * Cfg::kBoxBytes + (q & 3) * 128 + 4 * lane;
+    }
+
+    uint32_t G[NP][W], Y[NP][W];
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+#pragma unroll
+        for (int a = 0; a < W; ++a) G[k][a] = 0u;
 
     struct LanePart {
         int nf, ni;
@@ -303,7 +336,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
         const int4 th = *reinterpret_cast<const int4*>(sb + Cfg::kHdrOff);
         if (__all_sync(kFull, th.x < 0)) break;  // (a vote: keeps the warp provably converged)
         const int t = th.x;
-        const int64_t s0 = (int64_t)th.y * kU16Tile + wid * kU16Warp;  // this warp's 64 scenarios
+        const int64_t s0 = (int64_t)th.y * Cfg::kTile + wid * Cfg::kWarp;  // this warp's 64 NP scenarios
         if (__any_sync(kFull, t != acc_t)) {  // a new tour: flush its predecessor's SAA sums, load its constants
             if (slots) flush();
             acc_t = t;
@@ -314,120 +347,191 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
                                  (0x7fffu - (uint32_t)ti.thr16) * 0x10001u, g0s[t] - (int32_t)ns, ti.bn, ti.ok16};
             __syncwarp();
         }
-        int32_t blo = tc->base0, bhi = blo;
+        int32_t blo[NP], bhi[NP];
+        uint32_t P[NP], gprev[NP], qmax[NP], ovfb[NP];
 #pragma unroll
-        for (int k = 0; k < W; ++k) Y[k] = 0x7fff7fffu;  // no window ever reaches an empty slot
-        uint32_t P = 0u, gprev = tc->nsP, qmax = 0u, ovfb = 0u;
+        for (int k = 0; k < NP; ++k) {
+            blo[k] = bhi[k] = tc->base0;
+#pragma unroll
+            for (int a = 0; a < W; ++a) Y[k][a] = 0x7fff7fffu;  // no window ever reaches an empty slot
+            P[k] = 0u;
+            gprev[k] = tc->nsP;
+            qmax[k] = 0u;
+            ovfb[k] = 0u;
+        }
 
         for (int c = 0;;) {
-            const uint32_t* bufw = reinterpret_cast<const uint32_t*>(sb + wid * kU16Warp * 2) + lane;  // row stride 128 words
             const uint32_t* cgc = reinterpret_cast<const uint32_t*>(sb + Cfg::kCgOff);
             const bool pad_chunk = (c + 1) * W > n;  // rows past n (zero demand): no overflow test there
-            // the key of the candidate of age a (>= 2) at layer jj: G inside the window, >= 0x8000 outside;
-            // d (bit 15 of a half set iff inside) is returned for the votes
-            auto cand = [&](const int jj, const uint32_t Pn, const int a, uint32_t& d) -> uint32_t {
+            // the key of the candidate of age a (>= 2) at layer jj of pair k: G inside the window, >= 0x8000
+            // outside; d (bit 15 of a half set iff inside) is returned for the votes
+            auto cand = [&](const int k, const int jj, const uint32_t Pn, const int a, uint32_t& d) -> uint32_t {
                 const int s = (jj - a + 1 + 2 * W) % W;
-                d = imad_u32(Pn, m1, Y[s]);
-                return key_of(G[s], d);
+                d = imad_u32(Pn, m1, Y[k][s]);
+                return key_of(G[k][s], d);
             };
             // the window of layer jj reaches the oldest ring age W: the ring may miss older candidates
-            auto overflow = [&](const int jj, const uint32_t d) {
-                if (!pad_chunk || c * W + jj < n) ovfb |= d & kGuard;
+            auto overflow = [&](const int k, const int jj, const uint32_t d) {
+                if (!pad_chunk || c * W + jj < n) ovfb[k] |= d & kGuard;
             };
-            // the unconditional ages 2..A0 of layer jj, folded
-            auto first_group = [&](const int jj, const uint32_t Pn) -> uint32_t {
+            // the unconditional ages lo..A0 of layer jj, folded (lo >= 2)
+            auto first_group = [&](const int k, const int jj, const uint32_t Pn, const int lo) -> uint32_t {
                 uint32_t key[A0 - 1];
 #pragma unroll
-                for (int k = 2; k <= A0; ++k) {
+                for (int a = 2; a <= A0; ++a) {
+                    if (a < lo) {
+                        key[a - 2] = 0xffffffffu;
+                        continue;
+                    }
                     uint32_t d;
-                    key[k - 2] = cand(jj, Pn, k, d);
-                    if (k == W) overflow(jj, d);
+                    key[a - 2] = cand(k, jj, Pn, a, d);
+                    if (a == W) overflow(k, jj, d);
                 }
-                return umin_tree<A0 - 1>(key);
+                return umin_tree_from<A0 - 1>(key, lo - 2);
             };
             // the keys of a group (ages a0 + 1 .. a0 + UG - 1; age a0's key k0 done by the caller) folded into a
-            auto group_rest = [&](const int jj, const uint32_t Pn, const int a0, uint32_t a, const uint32_t k0) {
+            auto group_rest = [&](const int k, const int jj, const uint32_t Pn, const int a0, uint32_t a,
+                                  const uint32_t k0) {
                 uint32_t key[UG + 1];
                 key[0] = a;
                 key[1] = k0;
 #pragma unroll
-                for (int k = 1; k < UG; ++k) {
-                    if (a0 + k <= W) {
+                for (int u = 1; u < UG; ++u) {
+                    if (a0 + u <= W) {
                         uint32_t d;
-                        key[k + 1] = cand(jj, Pn, a0 + k, d);
-                        if (a0 + k == W) overflow(jj, d);
+                        key[u + 1] = cand(k, jj, Pn, a0 + u, d);
+                        if (a0 + u == W) overflow(k, jj, d);
                     } else {
-                        key[k + 1] = 0xffffffffu;
+                        key[u + 1] = 0xffffffffu;
                     }
                 }
                 return umin_tree<UG + 1>(key);
             };
-            // every kU16Check layers: rebase values and loads if either approaches 2^15 (see the header)
-            auto range_check = [&](const uint32_t gm) {
-                const uint32_t tv = (gprev + tc->GADD) | (P + PADD);
+            // every kU16Check layers: rebase values and loads if either approaches 2^15 (see the header);
+            // one vote for all pairs (a rebase is valid at any layer, so pairs that do not need one may take it)
+            auto range_check = [&](const uint32_t* gm) {
+                uint32_t tv = 0u;
+#pragma unroll
+                for (int k = 0; k < NP; ++k) tv |= (gprev[k] + tc->GADD) | (P[k] + PADD);
                 if (__any_sync(kFull, (tv & kGuard) != 0u)) {
-                    // values: base += b = max(gm - NS, 0); older values below it saturate at 0
-                    const uint32_t b = __viaddmax_s16x2(gm, tc->nNSP, 0u);
-                    const uint32_t nb = __vsub2(0u, b);
 #pragma unroll
-                    for (int k = 0; k < W; ++k) G[k] = __viaddmax_s16x2(G[k], nb, 0u);
-                    gprev = __viaddmax_s16x2(gprev, nb, 0u);
-                    blo += (int32_t)(b & 0xffffu);
-                    bhi += (int32_t)(b >> 16);
-                    // loads: P -= bp = max(P - Q - 1, 0); a Y below bp is out of every window: 0x7fff
-                    const uint32_t bp = __viaddmax_s16x2(P, nQ1P, 0u);
-                    const uint32_t nbp = __vsub2(0u, bp);
+                    for (int k = 0; k < NP; ++k) {
+                        // values: base += b = max(gm - NS, 0); older values below it saturate at 0
+                        const uint32_t b = __viaddmax_s16x2(gm[k], tc->nNSP, 0u);
+                        const uint32_t nb = __vsub2(0u, b);
 #pragma unroll
-                    for (int k = 0; k < W; ++k) Y[k] = __viaddmax_u16x2(Y[k], nbp, 0x7fff7fffu);
-                    P = __vadd2(P, nbp);
+                        for (int a = 0; a < W; ++a) G[k][a] = __viaddmax_s16x2(G[k][a], nb, 0u);
+                        gprev[k] = __viaddmax_s16x2(gprev[k], nb, 0u);
+                        blo[k] += (int32_t)(b & 0xffffu);
+                        bhi[k] += (int32_t)(b >> 16);
+                        // loads: P -= bp = max(P - Q - 1, 0); a Y below bp is out of every window: 0x7fff
+                        const uint32_t bp = __viaddmax_s16x2(P[k], nQ1P, 0u);
+                        const uint32_t nbp = __vsub2(0u, bp);
+#pragma unroll
+                        for (int a = 0; a < W; ++a) Y[k][a] = __viaddmax_u16x2(Y[k][a], nbp, 0x7fff7fffu);
+                        P[k] = __vadd2(P[k], nbp);
+                    }
                 }
             };
             // demands loaded two layers ahead (the LDS latency stays off the layer chain), Cg pairs
             // four at a time
-            uint32_t qbuf[2];
-            qbuf[0] = bufw[0];
-            qbuf[1] = bufw[Cfg::kRowBytes / 4];
+            uint32_t qbuf[NP][2];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                qbuf[k][0] = *reinterpret_cast<const uint32_t*>(sb + boff[k]);
+                qbuf[k][1] = *reinterpret_cast<const uint32_t*>(sb + boff[k] + Cfg::kRowBytes);
+            }
             uint4 cg4 = make_uint4(0u, 0u, 0u, 0u);
             auto cg_of = [&](const int j) -> uint32_t {
                 if (j % 4 == 0) cg4 = *reinterpret_cast<const uint4*>(cgc + j);
                 return (j % 4 == 0) ? cg4.x : (j % 4 == 1) ? cg4.y : (j % 4 == 2) ? cg4.z : cg4.w;
             };
-            auto q_of = [&](const int j) -> uint32_t {
-                const uint32_t q = qbuf[j % 2];
-                if (j + 2 < W) qbuf[j % 2] = bufw[(j + 2) * (Cfg::kRowBytes / 4)];
+            auto q_of = [&](const int k, const int j) -> uint32_t {
+                const uint32_t q = qbuf[k][j % 2];
+                if (j + 2 < W) qbuf[k][j % 2] = *reinterpret_cast<const uint32_t*>(sb + boff[k] + (j + 2) * Cfg::kRowBytes);
                 return q;
             };
+            // steps of LS layers: every candidate of age >= l + 2 of layer j + l (a split point <= j - 1) and
+            // the age-(l + 1) one (split point j, the previous step's last value) are known when the step
+            // starts, so all LS layers' first groups and voted groups run back to back, behind ONE vote per
+            // group; the split points j + 1 .. j + LS - 1 produced inside the step are folded in last
+            // (their loads, hence their window tests, are known early; only the LOP3 waits for the value)
 #pragma unroll
-            for (int j = 0; j < W; j += 2) {
-                const uint32_t q0 = q_of(j), q1 = q_of(j + 1);
-                const uint32_t cg0 = cg_of(j), cg1 = cg_of(j + 1);
-                qmax = __vimax3_u16x2(qmax, q0, q1);
-                Y[j] = imad_u32(P, one, QGP);  // split point of layer j's age 1 (FMA pipe)
-                G[j] = gprev;
-                const uint32_t Pn0 = P + q0, Pn1 = Pn0 + q1;
-                uint32_t a0 = first_group(j, Pn0), a1 = first_group(j + 1, Pn1);
+            for (int j = 0; j < W; j += LS) {
+                uint32_t cgv[LS];
+#pragma unroll
+                for (int l = 0; l < LS; ++l) cgv[l] = cg_of(j + l);
+                uint32_t Pn[NP][LS], a[NP][LS];
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    uint32_t qv[LS];
+#pragma unroll
+                    for (int l = 0; l < LS; ++l) qv[l] = q_of(k, j + l);
+#pragma unroll
+                    for (int l = 0; l < LS; l += 2) qmax[k] = __vimax3_u16x2(qmax[k], qv[l], qv[l + 1]);
+                    Y[k][j] = imad_u32(P[k], one, QGP);  // split point j (FMA pipe)
+                    G[k][j] = gprev[k];
+                    Pn[k][0] = P[k] + qv[0];
+#pragma unroll
+                    for (int l = 1; l < LS; ++l) Pn[k][l] = Pn[k][l - 1] + qv[l];
+                }
+#pragma unroll
+                for (int k = 0; k < NP; ++k)
+#pragma unroll
+                    for (int l = 0; l < LS; ++l) a[k][l] = first_group(k, j + l, Pn[k][l], l + 1 > 2 ? l + 1 : 2);
 #pragma unroll
                 for (int gi = 0; gi < W; ++gi) {  // groups of UG ages behind one vote on their youngest
                     const int ag = A0 + 1 + gi * UG;
                     if (ag > W) break;
-                    uint32_t d0, d1;
-                    const uint32_t k0 = cand(j, Pn0, ag, d0), k1 = cand(j + 1, Pn1, ag, d1);
-                    if (!__any_sync(kFull, ((d0 | d1) & kGuard) != 0u)) break;
-                    if (ag == W) {
-                        overflow(j, d0);
-                        overflow(j + 1, d1);
-                    }
-                    a0 = group_rest(j, Pn0, ag, a0, k0);
-                    a1 = group_rest(j + 1, Pn1, ag, a1, k1);
+                    uint32_t dd[NP][LS], kk[NP][LS], dor = 0u;
+#pragma unroll
+                    for (int k = 0; k < NP; ++k)
+#pragma unroll
+                        for (int l = 0; l < LS; ++l) {
+                            kk[k][l] = cand(k, j + l, Pn[k][l], ag, dd[k][l]);
+                            dor |= dd[k][l];
+                        }
+                    if (!__any_sync(kFull, (dor & kGuard) != 0u)) break;
+#pragma unroll
+                    for (int k = 0; k < NP; ++k)
+#pragma unroll
+                        for (int l = 0; l < LS; ++l) {
+                            if (ag == W) overflow(k, j + l, dd[k][l]);
+                            a[k][l] = group_rest(k, j + l, Pn[k][l], ag, a[k][l], kk[k][l]);
+                        }
                 }
-                // age 1 (p = i - 1) is always in the window when q <= Q (q > Q: qmax, DESIGN R4)
-                const uint32_t g0 = __vminu2(a0, gprev) + cg0;
-                G[j + 1] = g0;  // (after layer j read slot j + 1 as its age W)
-                Y[j + 1] = imad_u32(Pn0, one, QGP);
-                const uint32_t gm1 = __vminu2(a1, g0);
-                gprev = gm1 + cg1;
-                P = Pn1;
-                if ((j + 1) % kU16Check == kU16Check - 1 || j + 1 == W - 1) range_check(gm1);
+                uint32_t gmlast[NP];
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    // gn[m], yn[m]: split point j + m (m = 0: from the ring; 1 .. LS: produced here)
+                    uint32_t gn[LS + 1], yn[LS + 1];
+                    gn[0] = gprev[k];
+                    yn[0] = Y[k][j];
+#pragma unroll
+                    for (int l = 0; l < LS; ++l) {
+                        uint32_t m = a[k][l];
+                        // in-step ages 2 .. l of layer j + l (split points j + 1 .. j + l - 1; LS <= 4: l <= 3)
+                        if (l == 2) {
+                            m = __vminu2(m, key_of(gn[1], imad_u32(Pn[k][l], m1, yn[1])));
+                        } else if (l == 3) {
+                            m = __vimin3_u16x2(m, key_of(gn[2], imad_u32(Pn[k][l], m1, yn[2])),
+                                               key_of(gn[1], imad_u32(Pn[k][l], m1, yn[1])));
+                        }
+                        // age 1 (split point j + l) is always in the window when q <= Q (q > Q: qmax, DESIGN R4)
+                        const uint32_t gm = __vminu2(m, gn[l]);
+                        gn[l + 1] = gm + cgv[l];
+                        yn[l + 1] = imad_u32(Pn[k][l], one, QGP);
+                        if (l == LS - 1) gmlast[k] = gm;
+                    }
+#pragma unroll
+                    for (int l = 1; l < LS; ++l) {  // (after every read of these slots' previous contents)
+                        G[k][j + l] = gn[l];
+                        Y[k][j + l] = yn[l];
+                    }
+                    gprev[k] = gn[LS];
+                    P[k] = Pn[k][LS - 1];
+                }
+                if ((j + LS) % kU16Check == 0 || j + LS == W) range_check(gmlast);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[cs]);  // the stage may be refilled once every consumer is done
@@ -439,38 +543,41 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__(U16Cfg<W>::kMaxReg)
             sb = smem_raw + (size_t)cs * Cfg::kStageBytes;
             mbar_wait_warp(&full[cs], cr & 1u);
         }
-        uint32_t val = gprev;  // rem == 0: the last layer computed position n
-        if (rem != 0) {        // else position n sits in ring slot rem (pushed by the first padded layer)
-#pragma unroll
-            for (int k = 0; k < W; ++k)
-                if (k == rem) val = G[k];
-        }
         const bool ok = tc->ok != 0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int64_t s = s0 + 2 * lane + h;
-            const bool live = s < S;
-            const uint32_t sh = 16u * (uint32_t)h;
-            const bool bad = ((qmax >> sh) & 0xffffu) > Q;
-            // (a demand above Q in the LOW half can carry into the high half: recompute the high one)
-            const bool tainted = h == 1 && (qmax & 0xffffu) > Q;
-            const bool ovf = ((ovfb >> sh) & 0x8000u) != 0u;
-            const int fval = (int)((val >> sh) & 0xffffu) + (h ? bhi : blo) + tc->bn;
-            const bool deferred = live && (ovf || !ok || tainted) && !bad;
-            if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
-            if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
-            if (live && !deferred) {
-                LanePart pa = *accp;
-                if (bad) {
-                    pa.ni += 1;
-                } else {
-                    const unsigned long long sq = (unsigned long long)fval * (unsigned long long)fval;
-                    pa.nf += 1;
-                    pa.sum += fval;
-                    pa.sqlo += (long long)(sq & 0xffffffffull);
-                    pa.sqhi += (long long)(sq >> 32);
+        for (int k = 0; k < NP; ++k) {
+            uint32_t val = gprev[k];  // rem == 0: the last layer computed position n
+            if (rem != 0) {           // else position n sits in ring slot rem (pushed by the first padded layer)
+#pragma unroll
+                for (int a = 0; a < W; ++a)
+                    if (a == rem) val = G[k][a];
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t s = s0 + 64 * k + 2 * lane + h;
+                const bool live = s < S;
+                const uint32_t sh = 16u * (uint32_t)h;
+                const bool bad = ((qmax[k] >> sh) & 0xffffu) > Q;
+                // (a demand above Q in the LOW half can carry into the high half: recompute the high one)
+                const bool tainted = h == 1 && (qmax[k] & 0xffffu) > Q;
+                const bool ovf = ((ovfb[k] >> sh) & 0x8000u) != 0u;
+                const int fval = (int)((val >> sh) & 0xffffu) + (h ? bhi[k] : blo[k]) + tc->bn;
+                const bool deferred = live && (ovf || !ok || tainted) && !bad;
+                if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
+                if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
+                if (live && !deferred) {
+                    LanePart pa = *accp;
+                    if (bad) {
+                        pa.ni += 1;
+                    } else {
+                        const unsigned long long sq = (unsigned long long)fval * (unsigned long long)fval;
+                        pa.nf += 1;
+                        pa.sum += fval;
+                        pa.sqlo += (long long)(sq & 0xffffffffull);
+                        pa.sqhi += (long long)(sq >> 32);
+                    }
+                    *accp = pa;
                 }
-                *accp = pa;
             }
         }
     }
@@ -497,7 +604,7 @@ static spdp_status make_demand_map(CUtensorMap* map, const uint16_t* demand, int
     if (!encode) return fail(SPDP_E_CUDA, "split_sweep_u16: cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)n};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(uint16_t)};
-    const cuuint32_t box[2] = {(cuuint32_t)kU16Tile, 1u};
+    const cuuint32_t box[2] = {(cuuint32_t)kU16Box, 1u};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(demand), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -506,51 +613,57 @@ static spdp_status make_demand_map(CUtensorMap* map, const uint16_t* demand, int
     return SPDP_OK;
 }
 
-template <int W, int A0, int UG>
+template <int W, int A0, int UG, int LS>
 static spdp_status launch_u16_t(cudaStream_t st, const SweepArgs& a) {
-    using Cfg = U16Cfg<W>;
-    auto kern = split_sweep_u16_kernel<W, A0, UG>;
+    constexpr int NP = 1, NST = 3;
+    using Cfg = U16Cfg<W, NP, NST>;
+    auto kern = split_sweep_u16_kernel<W, A0, UG, NP, NST, LS>;
     int blocks_per_sm = 1;
     if (spdp_status e = kernel_setup((const void*)kern, (int)Cfg::kSmem, 100, kU16Threads, Cfg::kSmem, &blocks_per_sm,
                                      "split_sweep_u16 setup"))
         return e;
     CUtensorMap map;
     if (spdp_status e = make_demand_map(&map, a.demand, a.ld, a.S, a.n)) return e;
-    const int64_t ntiles = ((a.S + kU16Tile - 1) / kU16Tile) * a.T;
+    const int64_t ntiles = ((a.S + Cfg::kTile - 1) / Cfg::kTile) * a.T;
     int64_t grid = (int64_t)blocks_per_sm * device_sms();  // (measured: 4-5 CTAs per SM saturate it)
     if (grid > ntiles) grid = ntiles;
     const uint32_t Q = a.Q, pthr = 0x7fffu - Q - (uint32_t)kU16Check * (Q + 1u);
     const U16Consts kc{0xffffffffu, 1u, (Q + 0x8000u) * 0x10001u, ((0x10000u - (Q + 1u)) & 0xffffu) * 0x10001u,
                        (0x7fffu - pthr) * 0x10001u};
     prof_begin(st);
-    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kU16Threads), Cfg::kSmem, st, map, a.tabs,
+    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kU16Threads), Cfg::kSmem, st, map, a.trows,
                                            a.cgs, a.g0, a.tinfo, a.n, a.T, a.S, a.Q, kc, a.cost, a.slots, a.ovf, a.hdr),
                                 "split_sweep_u16_kernel");
-    set_last_kernel("split_sweep_u16_kernel<%d,%d,%d>", W, A0, UG);
+    set_last_kernel("split_sweep_u16_kernel<%d,%d,%d,%d>", W, A0, UG, LS);
     prof_end(st);
     return rc;
+}
+
+template <int LS>
+static spdp_status launch_u16_ls(int W, int A0, cudaStream_t st, const SweepArgs& a) {
+    switch (W) {
+        case 16: return A0 <= 6 ? launch_u16_t<16, 6, 2, LS>(st, a) : A0 <= 8 ? launch_u16_t<16, 8, 2, LS>(st, a)
+                                                                              : launch_u16_t<16, 10, 2, LS>(st, a);
+        case 20:
+            switch (A0 < 6 ? 6 : (A0 > 12 ? 12 : A0)) {
+                case 6: return launch_u16_t<20, 6, 2, LS>(st, a);
+                case 7: return launch_u16_t<20, 7, 2, LS>(st, a);
+                case 8: return launch_u16_t<20, 8, 2, LS>(st, a);
+                case 9: return launch_u16_t<20, 9, 2, LS>(st, a);
+                case 10: return launch_u16_t<20, 10, 2, LS>(st, a);
+                default: return launch_u16_t<20, 12, 2, LS>(st, a);
+            }
+        case 24: return A0 <= 8 ? launch_u16_t<24, 8, 2, LS>(st, a) : A0 <= 10 ? launch_u16_t<24, 10, 2, LS>(st, a)
+                                                                               : launch_u16_t<24, 12, 2, LS>(st, a);
+        default: return A0 <= 8 ? launch_u16_t<32, 8, 2, LS>(st, a) : launch_u16_t<32, 12, 3, LS>(st, a);
+    }
 }
 
 spdp_status launch_sweep_u16(int W, int mean_w, cudaStream_t st, const SweepArgs& a) {
     // unconditional ages (age 1 + A0 - 1 masked candidates) ~ the expected mean window + 4
     // (SPDP_F_MEAN_WINDOW; C2: mean 4 -> 8, C3: mean 8 -> 12), the rest in voted pairs
     const int A0 = mean_w <= 0 ? 8 : (mean_w + 4 < 5 ? 5 : mean_w + 4);
-    switch (W) {
-        case 16: return A0 <= 6 ? launch_u16_t<16, 6, 2>(st, a) : A0 <= 8 ? launch_u16_t<16, 8, 2>(st, a)
-                                                                          : launch_u16_t<16, 10, 2>(st, a);
-        case 20:
-            switch (A0 < 6 ? 6 : (A0 > 12 ? 12 : A0)) {
-                case 6: return launch_u16_t<20, 6, 2>(st, a);
-                case 7: return launch_u16_t<20, 7, 2>(st, a);
-                case 8: return launch_u16_t<20, 8, 2>(st, a);
-                case 9: return launch_u16_t<20, 9, 2>(st, a);
-                case 10: return launch_u16_t<20, 10, 2>(st, a);
-                default: return launch_u16_t<20, 12, 2>(st, a);
-            }
-        case 24: return A0 <= 8 ? launch_u16_t<24, 8, 2>(st, a) : A0 <= 10 ? launch_u16_t<24, 10, 2>(st, a)
-                                                                           : launch_u16_t<24, 12, 2>(st, a);
-        default: return A0 <= 8 ? launch_u16_t<32, 8, 2>(st, a) : launch_u16_t<32, 12, 3>(st, a);
-    }
+    return launch_u16_ls<4>(W, A0, st, a);
 }
 
 }  // namespace spdp

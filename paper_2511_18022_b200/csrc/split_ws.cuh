@@ -21,7 +21,7 @@ struct TourInfo {
 };
 
 // Range-check interval of the packed-u16 sweep (layers); tour_prep_kernel's thr16 assumes it.
-constexpr int kU16Check = 10;
+constexpr int kU16Check = 8;
 
 constexpr int kTabPad = 64;       // padding rows after each tour table
 constexpr int kSlots = 32;  // SAA partial slots per tour (spread the sweep's atomics)
@@ -32,8 +32,13 @@ constexpr int kSlots = 32;  // SAA partial slots per tour (spread the sweep's at
 __host__ __device__ inline int cg_stride(int n) { return (n + kTabPad + 7) & ~7; }
 constexpr int kCgPlanes = 3;
 
+// Demand row of every tour position for the TMA sweep (split_u16.cu): per tour trow_stride(n)
+// int32 entries, row of sigma_{i+1} at i < n, then n (a row outside the demand tensor: reads as
+// zeros); 16-byte aligned rows of the table, so a producer reads 4 positions per load.
+__host__ __device__ inline int trow_stride(int n) { return (n + kTabPad + 3) & ~3; }
+
 struct WsLayout {
-    size_t hdr, g0, tinfo, tabs, rowp, cgs, slots, ovf, total;
+    size_t hdr, g0, tinfo, tabs, rowp, cgs, trow, slots, ovf, total;
 };
 
 inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
@@ -45,6 +50,7 @@ inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
     L.tabs = off; off = align_up(off + sizeof(int2) * (size_t)T * (size_t)(n + kTabPad), 256);
     L.rowp = off; off = align_up(off + sizeof(uint64_t) * (size_t)T * (size_t)(n + kTabPad), 256);
     L.cgs = off; off = align_up(off + sizeof(int32_t) * kCgPlanes * (size_t)T * (size_t)cg_stride(n), 256);
+    L.trow = off; off = align_up(off + sizeof(int32_t) * (size_t)T * (size_t)trow_stride(n), 256);
     L.slots = off; off = align_up(off + sizeof(spdp_saa_partial) * (size_t)T * (size_t)kSlots, 256);
     L.ovf = off; off = align_up(off + sizeof(unsigned long long) * (size_t)T * (size_t)S, 256);
     L.total = off;
@@ -59,6 +65,7 @@ enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
 struct SweepArgs {
     const uint16_t* const* rowp;
     const int2* tabs;
+    const int32_t* trows;
     const int32_t* cgs;
     const int32_t* g0;
     const TourInfo* tinfo;
