@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace spdp {
 
@@ -26,20 +27,32 @@ struct F32Pos {
 
 constexpr int kF32SmemMaxN = 4095;  // position table in shared memory up to 128 KB
 
-__global__ void f32_prep_kernel(const int32_t* __restrict__ tour, int n, const double* __restrict__ dist, int64_t ld,
-                                F32Pos* __restrict__ tab) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(256) f32_prep_kernel(const int32_t* __restrict__ tour, int n,
+                                                       const double* __restrict__ dist, int64_t ld,
+                                                       F32Pos* __restrict__ tab) {
+    if (blockIdx.x != 0) return;
     const int64_t N1 = (int64_t)n + 1;
     auto node = [&](int i) -> int {  // customer at 0-based position i, clamped to 1..n
         const int c = tour[i];
         return c < 1 ? 1 : (c > n ? n : c);
     };
-    double D = 0.0;
-    tab[0] = F32Pos{0.0, 0.0, 0.0, 0u, 0u};
-    for (int i = 1; i <= n; ++i) {
+    // every position's costs in parallel (Dd temporarily holds the arc into position i)
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+        if (i == 0) {
+            tab[0] = F32Pos{0.0, 0.0, 0.0, 0u, 0u};
+            continue;
+        }
         const int c = node(i - 1);
-        if (i >= 2) D = __dadd_rn(D, dist[(int64_t)node(i - 2) * N1 + c]);
-        tab[i] = F32Pos{D, dist[c], dist[(int64_t)c * N1], (uint32_t)((uint64_t)(c - 1) * (uint64_t)ld), 0u};
+        const double arc = i >= 2 ? dist[(int64_t)node(i - 2) * N1 + c] : 0.0;
+        tab[i] = F32Pos{arc, dist[c], dist[(int64_t)c * N1], (uint32_t)((uint64_t)(c - 1) * (uint64_t)ld), 0u};
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    // Dd[1] = 0, Dd[i] = Dd[i-1] + c[s_{i-1}][s_i]: the fp64 sum in the oracle's (sequential) order
+    double D = 0.0;
+    for (int i = 1; i <= n; ++i) {
+        if (i >= 2) D = __dadd_rn(D, tab[i].Dd);
+        tab[i].Dd = D;
     }
 }
 
@@ -85,103 +98,250 @@ __global__ void __launch_bounds__(256) split_f32_kernel(const F32Pos* __restrict
     cost[s] = bad ? INFINITY : fc[(int64_t)n * S];
 }
 
-// The band table of the ring kernel: tb[i][k - 1] = T32(i - k, i), k = 1..W (the route costs of
-// every candidate the ring can hold, scenario-invariant), formed in the oracle's fp64 order.
-__global__ void f32_band_kernel(const F32Pos* __restrict__ tab, int n, int W, float* __restrict__ tb) {
+// ---------------------------------------------------------------- the TMA-fed fp32 ring sweep
+// The common case (every scenario whose loads stay below 2^30; the rest, and the scenarios this
+// kernel lists, go through split_f32_kernel): the packed-u16 sweep's work decomposition (split_u16.cu: persistent CTAs of 4 consumer
+// warps + 1 producer warp, the producer gathering 4 tour-ordered demand rows x 128 scenarios per
+// TMA instruction into an NS-stage shared-memory ring) with one scenario per lane and fp32 values.
+// Per lane a W-entry register ring of {f(p), Y(p) = P(p) + Q} (split point p in slot p mod W).
+// Candidate p of layer i (age k = i - p): val = fl32(f(p) + T32(p, i)) (one IEEE add of the
+// band-table entry, staged per chunk next to the demand rows); d = Y(p) - P(i) >= 0 iff p is in
+// the window, so d's sign bit is set exactly outside it, and
+//   key = bits(val) | (d & 0x80000000)      (one LOP3)
+// orders like val inside the window (val >= 0: IEEE order of non-negative floats is the order of
+// their bit patterns) and above every in-window key outside it: the masked min of Eq. (3) is an
+// unsigned 3-input integer min (VIMNMX3) of keys, exact.  Two layers per step (the candidates of
+// age >= 2 of both are known before either), ages 1..A0 unconditionally, then groups of UG ages
+// behind one warp vote; a window that reaches age W lists the scenario for split_f32_kernel.
+constexpr int kF32Cons = 4;                      // consumer warps per CTA
+constexpr int kF32Threads = 32 * (kF32Cons + 1);
+constexpr int kF32Tile = 32 * kF32Cons;          // scenarios per tile = TMA box columns
+constexpr int kF32TW = 20;                       // ring width of the TMA sweep
+constexpr int kF32TA0 = 8;                       // unconditional ages
+
+template <int W, int NST>
+struct F32TCfg {
+    static constexpr int NS = NST;
+    static constexpr int kRowBytes = kF32Tile * 2;                // 256 B
+    static constexpr int kRowsBytes = W * kRowBytes;
+    static constexpr int kBandOff = kRowsBytes;                   // W layers x W ages fp32
+    static constexpr int kBandBytes = W * W * 4;
+    static constexpr int kHdrOff = kBandOff + kBandBytes;         // {tile, chunk}
+    static constexpr int kStageBytes = (kHdrOff + 16 + 127) / 128 * 128;
+    static constexpr size_t kSmem = (size_t)NS * kStageBytes + 2 * NS * sizeof(uint64_t);
+    static_assert(W % 4 == 0, "W must be a multiple of 4");
+};
+
+// band rows of the TMA sweep: tbw[i][k - 1] = T32(i - k, i), k = 1..W, rows i = 0 .. n + W (zero
+// past n and for k > i), so a chunk's W rows are one contiguous bulk copy
+__global__ void f32_bandw_kernel(const F32Pos* __restrict__ tab, int n, int W, float* __restrict__ tb) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)(n + 1) * W) return;
+    if (idx >= (int64_t)(n + 1 + W) * W) return;
     const int i = (int)(idx / W), k = (int)(idx % W) + 1;
-    float v = 0.0f;  // (k > i: no such split point; its ring slot is never in a window)
-    if (k <= i) {
+    float v = 0.0f;
+    if (i <= n && k <= i) {
         const int p = i - k;
         v = __double2float_rn(__dadd_rn(__dadd_rn(tab[p + 1].c0, __dsub_rn(tab[i].Dd, tab[p + 1].Dd)), tab[i].ci0));
     }
     tb[idx] = v;
 }
 
-// The ring kernel (the common case): one scenario per thread, a W-entry register ring of
-// {f(p), P(p) + Q} (slot p mod W), layers unrolled by W, each candidate one fp32 add of the
-// band-table entry and a masked min; ages 1..8 unconditionally, then groups of 4 behind a warp
-// vote.  A scenario whose window outgrows the ring is listed for the general kernel.
-constexpr int kF32W = 32;
-constexpr int kF32Pf = 8;
-constexpr int kF32BandSmemMaxN = 375;  // band table (n + 1) W 4 B staged in shared memory up to 48 KB
+// rows of the TMA gathers: trow[i] = demand row of tour position i + 1 (i < n), n past the end
+__global__ void f32_trow_kernel(const int32_t* __restrict__ tour, int n, int len, int32_t* __restrict__ trow) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    int r = n;
+    if (i < n) {
+        const int c = tour[i];
+        r = (c < 1 ? 1 : (c > n ? n : c)) - 1;
+    }
+    trow[i] = r;
+}
 
-__global__ void __launch_bounds__(256) split_f32_ring_kernel(const F32Pos* __restrict__ tab, const float* __restrict__ tb_g,
-                                                             int n, const uint16_t* __restrict__ demand, int64_t S,
-                                                             int Q, float* __restrict__ cost, int64_t* __restrict__ list,
-                                                             unsigned* __restrict__ count, int band_in_smem) {
-    constexpr int W = kF32W;
-    extern __shared__ float tbs[];
-    const float* tb = tb_g;
-    uint32_t* rows = reinterpret_cast<uint32_t*>(tbs + (n + 1) * W);  // row offsets, padded with 0
-    if (band_in_smem) {
-        for (int i = threadIdx.x; i < (n + 1) * W; i += blockDim.x) tbs[i] = tb_g[i];
-        for (int i = threadIdx.x; i < n + 1 + kF32Pf; i += blockDim.x) rows[i] = i <= n ? tab[i].rowoff : 0u;
-        __syncthreads();
-        tb = tbs;
+__device__ __forceinline__ uint32_t f32_key(float val, uint32_t d) {
+    uint32_t k;
+    asm("lop3.b32 %0, %1, %2, %3, 0xF8;" : "=r"(k) : "r"(__float_as_uint(val)), "r"(d), "r"(0x80000000u));
+    return k;  // val | (d & 0x80000000)
+}
+
+template <int N>
+__device__ __forceinline__ uint32_t umin_tree32(const uint32_t* v) {
+    if constexpr (N == 1) return v[0];
+    else if constexpr (N == 2) return min(v[0], v[1]);
+    else if constexpr (N == 3) return __vimin3_u32(v[0], v[1], v[2]);
+    else return __vimin3_u32(umin_tree32<N - 2>(v), v[N - 2], v[N - 1]);
+}
+
+template <int W, int A0, int UG, int NST>
+__global__ void __launch_bounds__(kF32Threads) split_f32_tma_kernel(
+    const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ trow, const float* __restrict__ tbw, int n,
+    int64_t S, int Q, float* __restrict__ cost, int64_t* __restrict__ list, unsigned* __restrict__ count) {
+    using Cfg = F32TCfg<W, NST>;
+    constexpr int NS = Cfg::NS;
+    static_assert(A0 >= 2 && A0 <= W && UG >= 1, "bad fp32 sweep config");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NS * Cfg::kStageBytes);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t ntiles = (uint32_t)((S + kF32Tile - 1) / kF32Tile);
+    const int nchunks = (n + W - 1) / W;
+    if (tid == 0) {
+        for (int k = 0; k < NS; ++k) {
+            mbar_init(&full[k], 1);
+        }
+        fence_mbar_init();
     }
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = s < S;
-    const uint16_t* dcol = demand + (live ? s : S - 1);
-    auto q_at = [&](int i) -> int {
-        if (band_in_smem) return (int)dcol[rows[i]];  // (padded past n: row 0)
-        return i <= n ? (int)dcol[tab[i].rowoff] : 0;
-    };
-    float F[W];
-    int Y[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-        F[k] = 0.0f;
-        Y[k] = INT_MIN;  // no split point yet: never in a window
-    }
-    Y[0] = Q;  // position 0: f = 0, P = 0
-    int qb[kF32Pf];
-#pragma unroll
-    for (int k = 0; k < kF32Pf; ++k) qb[k] = q_at(1 + k);
-    int P = 0;
-    bool bad = false, ovf = false;
-    float fin = 0.0f;
-    for (int b = 1; b <= n; b += W) {  // layer i = b + j sits in slot (1 + j) mod W
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-            const int i = b + j;
-            if (i > n) break;  // warp-uniform
-            const int q = qb[j % kF32Pf];
-            qb[j % kF32Pf] = q_at(i + kF32Pf);
-            bad |= q > Q;
-            const int Pn = P + q;
-            const float* row = tb + (int64_t)i * W;
-            float best = INFINITY;
-#pragma unroll
-            for (int k = 1; k <= 8; ++k) {
-                const int sl = (1 + j - k + 2 * W) % W;
-                if (Y[sl] >= Pn) best = fminf(best, __fadd_rn(F[sl], row[k - 1]));
-            }
-#pragma unroll
-            for (int k0 = 9; k0 <= W; k0 += 4) {
-                if (!__any_sync(kFull, Y[(1 + j - k0 + 2 * W) % W] >= Pn)) break;
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const int k = k0 + v;
-                    if (k <= W) {
-                        const int sl = (1 + j - k + 2 * W) % W;
-                        if (Y[sl] >= Pn) best = fminf(best, __fadd_rn(F[sl], row[k - 1]));
-                    }
+    __syncthreads();
+    if (__any_sync(kFull, wid == kF32Cons)) {
+        // ---- producer (see split_sweep_u16_kernel): tile blockIdx.x first, then the counter count[1]
+        int c = nchunks, st = 0, tile = -1;
+        unsigned r = 0u, id = blockIdx.x;
+        for (;;) {
+            if (r > 0) stage_acquire(st, 32 * (kF32Cons + 1));  // the consumers released the previous use (round r - 1)
+            if (c == nchunks) {
+                if (tile >= 0) {
+                    if (lane == 0) id = atomicAdd(count + 1, 1u) + gridDim.x;
+                    id = __shfl_sync(kFull, id, 0);
                 }
+                tile = id < ntiles ? (int)id : -1;
+                c = 0;
             }
-            const int si = (1 + j) % W;  // = the slot of age W, overwritten now
-            ovf |= Y[si] >= Pn && i - W >= 1;  // an older split point may still be in the window
-            F[si] = best;
-            Y[si] = Pn + Q;
-            if (i == n) fin = best;
-            P = Pn;
+            unsigned char* sb = smem_raw + (size_t)st * Cfg::kStageBytes;
+            uint64_t* fb = &full[st];
+            if (lane == 0) *reinterpret_cast<int4*>(sb + Cfg::kHdrOff) = make_int4(tile, c, 0, 0);
+            if (__any_sync(kFull, tile < 0)) {
+                if (lane == 0) mbar_arrive(fb);
+                break;
+            }
+            if (lane == 0) {
+                const int r0 = c * W;  // layers r0 + 1 .. r0 + W: tour positions r0 .. r0 + W - 1
+                int4 rq[W / 4];
+#pragma unroll
+                for (int g = 0; g < W / 4; ++g) rq[g] = __ldg(reinterpret_cast<const int4*>(trow + r0) + g);
+                mbar_arrive_expect_tx(fb, (uint32_t)(Cfg::kRowsBytes + Cfg::kBandBytes));
+#pragma unroll
+                for (int g = 0; g < W / 4; ++g)
+                    tma_gather4(sb + g * 4 * Cfg::kRowBytes, &dmap, tile * kF32Tile, rq[g].x, rq[g].y, rq[g].z, rq[g].w,
+                                fb);
+                bulk_g2s_plain(sb + Cfg::kBandOff, tbw + (int64_t)(r0 + 1) * W, Cfg::kBandBytes, fb);
+            }
+            __syncwarp();
+            ++c;
+            if (++st == NS) {
+                st = 0;
+                ++r;
+            }
+        }
+    } else {
+        __syncwarp();
+        float F[W];
+        int32_t Y[W];
+        int cs = 0;
+        unsigned cr = 0u;
+        for (;;) {
+            unsigned char* sb = smem_raw + (size_t)cs * Cfg::kStageBytes;
+            mbar_wait_warp(&full[cs], cr & 1u);
+            const int4 th = *reinterpret_cast<const int4*>(sb + Cfg::kHdrOff);
+            if (__all_sync(kFull, th.x < 0)) break;
+            const int64_t s = (int64_t)th.x * kF32Tile + wid * 32 + lane;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                F[k] = 0.0f;
+                Y[k] = -(1 << 30) - 1;  // no split point: never in a window (d < 0)
+            }
+            Y[0] = Q;  // split point 0: f = 0, P = 0
+            int32_t P = 0;
+            uint32_t qmax = 0u, ovf = 0u;
+            float fin = 0.0f;
+            for (int c = 0;;) {
+                const uint16_t* rows = reinterpret_cast<const uint16_t*>(sb) + wid * 32 + lane;
+                const float* band = reinterpret_cast<const float*>(sb + Cfg::kBandOff);
+                const bool last = c == nchunks - 1;
+                const int ilast = n - c * W;  // local index (1-based) of layer n in the last chunk
+                // layer jj (local, 0-based; global i = c W + jj + 1) uses slot (1 + jj - k) mod W for age k
+                auto cand = [&](const int jj, const int32_t Pn, const int k, uint32_t& d) -> uint32_t {
+                    const int sl = (1 + jj - k + 2 * W) % W;
+                    d = (uint32_t)(Y[sl] - Pn);
+                    return f32_key(__fadd_rn(F[sl], band[jj * W + k - 1]), d);
+                };
+                // age W inside the window of a real layer i > W (i <= n): an older split point may be too
+                auto overflow = [&](const int jj, const uint32_t d0, const uint32_t d1) {
+                    if (c >= 1 && (!last || jj + 1 <= ilast)) ovf |= ~d0;
+                    if (c >= 1 && (!last || jj + 2 <= ilast)) ovf |= ~d1;
+                };
+                uint32_t qn = rows[0];
+#pragma unroll
+                for (int j = 0; j < W; j += 2) {
+                    const uint32_t q0 = qn, q1 = rows[(j + 1) * kF32Tile];
+                    if (j + 2 < W) qn = rows[(j + 2) * kF32Tile];
+                    qmax = max(qmax, max(q0, q1));
+                    const int32_t Pn0 = P + (int32_t)q0, Pn1 = Pn0 + (int32_t)q1;
+                    // ages 2 .. A0 of both layers (split points <= the step's first layer - 1)
+                    uint32_t k0[A0 - 1], k1[A0 - 1];
+#pragma unroll
+                    for (int k = 2; k <= A0; ++k) {  // (A0 < W: no overflow test here)
+                        uint32_t d0, d1;
+                        k0[k - 2] = cand(j, Pn0, k, d0);
+                        k1[k - 2] = cand(j + 1, Pn1, k, d1);
+                    }
+                    uint32_t a0 = umin_tree32<A0 - 1>(k0), a1 = umin_tree32<A0 - 1>(k1);
+#pragma unroll
+                    for (int gi = 0; gi < W; ++gi) {
+                        const int ag = A0 + 1 + gi * UG;
+                        if (ag > W) break;
+                        uint32_t d0, d1;
+                        const uint32_t g0 = cand(j, Pn0, ag, d0), g1 = cand(j + 1, Pn1, ag, d1);
+                        if (!__any_sync(kFull, ((d0 & d1) >> 31) == 0u)) break;  // some lane has age ag inside
+                        uint32_t e0[UG + 1], e1[UG + 1];
+                        e0[0] = a0;
+                        e1[0] = a1;
+                        e0[1] = g0;
+                        e1[1] = g1;
+#pragma unroll
+                        for (int u = 1; u < UG; ++u) {
+                            if (ag + u <= W) {
+                                uint32_t dd0, dd1;
+                                e0[u + 1] = cand(j, Pn0, ag + u, dd0);
+                                e1[u + 1] = cand(j + 1, Pn1, ag + u, dd1);
+                                if (ag + u == W) overflow(j, dd0, dd1);
+                            } else {
+                                e0[u + 1] = e1[u + 1] = 0xffffffffu;
+                            }
+                        }
+                        if (ag == W) overflow(j, d0, d1);
+                        a0 = umin_tree32<UG + 1>(e0);
+                        a1 = umin_tree32<UG + 1>(e1);
+                    }
+                    // age 1 of layer j: split point i - 1 (always inside when q <= Q; q > Q: qmax)
+                    const int s0 = (1 + j - 1 + 2 * W) % W, s1 = (1 + j + 2 * W) % W, s2 = (2 + j) % W;
+                    const float f0 = __uint_as_float(min(a0, __float_as_uint(__fadd_rn(F[s0], band[j * W]))));
+                    F[s1] = f0;  // split point of layer j (its slot held age W of layer j, read above)
+                    Y[s1] = Pn0 + Q;
+                    const float f1 = __uint_as_float(min(a1, __float_as_uint(__fadd_rn(f0, band[(j + 1) * W]))));
+                    F[s2] = f1;
+                    Y[s2] = Pn1 + Q;
+                    if (last) {
+                        if (j + 1 == ilast) fin = f0;
+                        if (j + 2 == ilast) fin = f1;
+                    }
+                    P = Pn1;
+                }
+                stage_release(cs, 32 * (kF32Cons + 1));
+                if (++cs == NS) {
+                    cs = 0;
+                    ++cr;
+                }
+                if (__all_sync(kFull, ++c >= nchunks)) break;
+                sb = smem_raw + (size_t)cs * Cfg::kStageBytes;
+                mbar_wait_warp(&full[cs], cr & 1u);
+            }
+            if (s < S) {
+                // the window of some real layer reached age W: an older split point may be inside
+                if (qmax > (uint32_t)Q) cost[s] = INFINITY;  // Eq. (2)'s set is empty at some layer (R4)
+                else if (ovf & 0x80000000u) list[atomicAdd(count, 1u)] = s;
+                else cost[s] = fin;
+            }
         }
     }
-    if (!live) return;
-    if (bad) cost[s] = INFINITY;
-    else if (ovf) list[atomicAdd(count, 1u)] = s;
-    else cost[s] = fin;
 }
 
 // SAA moments of fp32 costs in fp64: acc = {m, sum c, sum (c - center)^2, infeasible} over the
@@ -216,9 +376,11 @@ __global__ void __launch_bounds__(256) saa_f32_moments_kernel(const float* __res
     }
 }
 
-static size_t f32_table_bytes(int32_t n) { return align_up(sizeof(F32Pos) * (size_t)(n + 1 + kF32Pf), 256); }
-static size_t f32_band_bytes(int32_t n) { return align_up(sizeof(float) * (size_t)(n + 1) * kF32W, 256); }
+static size_t f32_table_bytes(int32_t n) { return align_up(sizeof(F32Pos) * (size_t)(n + 1 + 8), 256); }
 static size_t f32_list_bytes(int64_t S) { return align_up(sizeof(int64_t) * (size_t)S, 256) + 256; }
+static int f32_tw_chunks(int32_t n) { return (n + kF32TW - 1) / kF32TW; }
+static size_t f32_trow_bytes(int32_t n) { return align_up(sizeof(int32_t) * (size_t)(f32_tw_chunks(n) * kF32TW + 4), 256); }
+static size_t f32_bandw_bytes(int32_t n) { return align_up(sizeof(float) * (size_t)(n + 1 + kF32TW) * kF32TW, 256); }
 
 }  // namespace spdp
 
@@ -226,8 +388,8 @@ using namespace spdp;
 
 extern "C" size_t spdp_f32_workspace_bytes(int32_t n, int64_t S) {
     if (n < 1 || S < 1) return 0;
-    return f32_table_bytes(n) + f32_band_bytes(n) + f32_list_bytes(S) +
-           align_up(sizeof(float) * (size_t)(n + 1) * (size_t)S, 256);
+    return f32_table_bytes(n) + f32_list_bytes(S) +
+           align_up(sizeof(float) * (size_t)(n + 1) * (size_t)S, 256) + f32_trow_bytes(n) + f32_bandw_bytes(n);
 }
 
 extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* dist, int32_t n, const uint16_t* demand,
@@ -245,25 +407,50 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     cudaStream_t st = (cudaStream_t)stream;
     char* w = static_cast<char*>(ws);
     F32Pos* tab = reinterpret_cast<F32Pos*>(w);
-    float* tb = reinterpret_cast<float*>(w + f32_table_bytes(n));
-    int64_t* list = reinterpret_cast<int64_t*>(w + f32_table_bytes(n) + f32_band_bytes(n));
+    int64_t* list = reinterpret_cast<int64_t*>(w + f32_table_bytes(n));
     unsigned* count = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(list) + align_up(sizeof(int64_t) * (size_t)S, 256));
-    float* fsc = reinterpret_cast<float*>(w + f32_table_bytes(n) + f32_band_bytes(n) + f32_list_bytes(S));
-    f32_prep_kernel<<<1, 32, 0, st>>>(tour, n, dist, ld, tab);
+    float* fsc = reinterpret_cast<float*>(w + f32_table_bytes(n) + f32_list_bytes(S));
+    f32_prep_kernel<<<1, 256, 0, st>>>(tour, n, dist, ld, tab);
     spdp_status rc = last_launch("f32_prep_kernel");
     if (rc) return rc;
-    const int64_t nb = (int64_t)(n + 1) * kF32W;
-    f32_band_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, st>>>(tab, n, kF32W, tb);
-    if ((rc = last_launch("f32_band_kernel"))) return rc;
-    if ((rc = cuda_check(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(count, 0, 2 * sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
-    const bool bsm = n <= kF32BandSmemMaxN;
-    prof_begin(st);
-    // (1) the ring kernel for every scenario; (2) the general kernel for the ones it deferred
-    split_f32_ring_kernel<<<(unsigned)ceil_div(S, 256), 256,
-                            bsm ? sizeof(float) * (size_t)nb + sizeof(uint32_t) * (size_t)(n + 1 + kF32Pf) : 0, st>>>(
-        tab, tb, n, demand, S, Qe, cost, list, count, bsm ? 1 : 0);
-    if ((rc = last_launch("split_f32_ring_kernel"))) return rc;
+    // the TMA sweep keeps Y = P + Q and P(i) - Y in int32: every load it forms (including the padded
+    // layers' zero demands) is at most (n + W) min(Q, 65535) (larger demands make the scenario
+    // infeasible, and its value is not used), so Y < 2^30 + Q suffices
+    const int64_t qcap = Qe < 65535 ? Qe : 65535;
+    const bool tma = ((int64_t)n + kF32TW) * qcap + Qe < (1LL << 30);
+    int32_t* trow = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(fsc) + align_up(sizeof(float) * (size_t)(n + 1) * (size_t)S, 256));
+    float* tbw = reinterpret_cast<float*>(reinterpret_cast<char*>(trow) + f32_trow_bytes(n));
+    if (tma) {
+        const int len = f32_tw_chunks(n) * kF32TW + 4;
+        f32_trow_kernel<<<(unsigned)ceil_div(len, 256), 256, 0, st>>>(tour, n, len, trow);
+        if ((rc = last_launch("f32_trow_kernel"))) return rc;
+        const int64_t nbw = (int64_t)(n + 1 + kF32TW) * kF32TW;
+        f32_bandw_kernel<<<(unsigned)ceil_div(nbw, 256), 256, 0, st>>>(tab, n, kF32TW, tbw);
+        if ((rc = last_launch("f32_bandw_kernel"))) return rc;
+        auto go = [&](auto kern, size_t smem) -> spdp_status {
+            int bps = 1;
+            spdp_status r2;
+            if ((r2 = kernel_setup((const void*)kern, (int)smem, 100, kF32Threads, smem, &bps, "split_f32_tma setup")))
+                return r2;
+            CUtensorMap map;
+            if ((r2 = make_demand_map(&map, demand, ld, S, n, kF32Tile))) return r2;
+            const int64_t ntiles = ceil_div(S, kF32Tile);
+            int64_t grid = (int64_t)bps * device_sms();
+            if (grid > ntiles) grid = ntiles;
+            prof_begin(st);
+            kern<<<(unsigned)grid, kF32Threads, smem, st>>>(map, trow, tbw, n, S, Qe, cost, list, count);
+            return last_launch("split_f32_tma_kernel");
+        };
+        rc = go(split_f32_tma_kernel<kF32TW, kF32TA0, 2, 3>, F32TCfg<kF32TW, 3>::kSmem);
+        if (rc) return rc;
+        set_last_kernel("split_f32_tma_kernel<%d,%d,%d>", kF32TW, kF32TA0, 2);
+    } else {  // (loads near 2^30: every scenario through the general kernel)
+        prof_begin(st);
+        list = nullptr;
+        set_last_kernel("split_f32_kernel");
+    }
     const bool tsm = n <= kF32SmemMaxN;
     if ((rc = kernel_setup((const void*)split_f32_kernel, (int)(sizeof(F32Pos) * (kF32SmemMaxN + 1)), -1, 0, 0, nullptr,
                            "split_f32_kernel setup")))
@@ -271,7 +458,6 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     split_f32_kernel<<<(unsigned)ceil_div(S, 256), 256, tsm ? sizeof(F32Pos) * (size_t)(n + 1) : 0, st>>>(
         tab, n, demand, S, Qe, fsc, cost, tsm ? 1 : 0, list, count);
     prof_end(st);
-    set_last_kernel("split_f32_ring_kernel<%d>", kF32W);
     return last_launch("split_f32_kernel");
 }
 

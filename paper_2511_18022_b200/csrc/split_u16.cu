@@ -41,16 +41,16 @@
 // loads of the tour's padded row table (one round trip), W/4 TMA gathers (cp.async.bulk.tensor.2d...tile::gather4: 4 tour-ordered
 // demand rows x 256 scenarios, 512 B each, in one instruction; rows past n are outside the tensor
 // and arrive as zeros) plus one bulk copy of the chunk's W Cg pairs, completing on the stage's
-// "full" mbarrier; the consumers release the stage through its "empty" mbarrier (4 arrivals), so
-// a fast warp runs up to NS - 1 chunks ahead of the slowest.  The consumers carry no copy code:
+// "full" mbarrier; the consumers release the stage by arriving on its named hardware barrier
+// (tma.cuh stage_release; the producer waits there in bar.sync, parked without polling), so a
+// fast warp runs up to NS - 1 chunks ahead of the slowest.  The consumers carry no copy code:
 // per chunk they wait on one barrier and arrive on another.
-#include <cudaTypedefs.h>
-
 #include <climits>
 #include <cstring>
 
 #include "common.cuh"
 #include "split_ws.cuh"
+#include "tma.cuh"
 
 namespace spdp {
 
@@ -89,14 +89,6 @@ struct U16Consts {
                     // is set iff P > pthr (a load rebase is due)
 };
 
-// d = a * b + c on the FMA pipe (b is a runtime multiplier, so ptxas cannot turn the multiply-add
-// into an IADD3 on the ALU pipe, which the candidate LOP3 / VIMNMX3 already load)
-__device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t d;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
-
 // key = G | (~d & 0x80008000) as one LOP3 (an explicit lop3, so ptxas cannot split it around
 // the vote branch that tests d)
 __device__ __forceinline__ uint32_t key_of(uint32_t G, uint32_t d) {
@@ -123,84 +115,6 @@ __device__ __forceinline__ uint32_t umin_tree_from(const uint32_t* v, const int 
     return v[0];
 }
 
-// ---- TMA / mbarrier helpers (this file only) ----------------------------------------------
-// 4 rows r0..r3 x box columns starting at col of the 2-D demand tensor -> 4 consecutive boxes in
-// shared memory; completion as transaction bytes on bar
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int col, int r0, int r1, int r2, int r3,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// wait for the phase with the given parity to complete, the warp suspended in the barrier unit
-// meanwhile (a suspend-time hint instead of the default short limit: no spinning instructions
-// steal the consumers' issue slots)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(10000000u)
-        : "memory");
-}
-// one try of the same wait (true: the phase has completed); a warp loops on it through a vote,
-// so the compiler knows the warp leaves the loop converged (no divergence checks, BRA.DIV, on the
-// warp votes that follow)
-__device__ __forceinline__ bool mbar_try_sleep(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(10000000u)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
-    while (!__all_sync(kFull, mbar_try_sleep(bar, parity))) {
-    }
-    __syncwarp();
-}
-// the producer's wait for a stage to be released: a non-blocking test, then timed sleeps (a warp
-// suspended in try_wait is woken by every barrier event of the SM and re-polls: measured 76 polls,
-// ~450 issue slots, per chunk; a stage is released about every 2 us, so a 256 ns back-off costs
-// nothing and leaves the issue slots to the consumers)
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-    while (!__all_sync(kFull, mbar_test(bar, parity))) __nanosleep(256);
-    __syncwarp();
-}
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
 // A0: ages scanned unconditionally (age 1 + A0 - 1 masked candidates); then groups of UG ages,
 // each behind a warp vote on its youngest age; the scan of age W also tests for ring overflow.
 // NP: scenario pairs per lane (independent DP chains; one vote and one range check serve all).
@@ -216,7 +130,6 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
     static_assert(A0 >= 2 && A0 <= W && UG >= 1 && NP >= 1 && (LS == 2 || LS == 4) && W % LS == 0 && kU16Check % LS == 0 && A0 >= LS + 1, "bad u16 sweep config");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::kStagesBytes);  // [NS]: data landed
-    uint64_t* empty = full + NS;                                                 // [NS]: all consumers done
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t ntile_s = (uint32_t)((S + Cfg::kTile - 1) / Cfg::kTile);
     const uint32_t ntiles = ntile_s * (uint32_t)T;
@@ -225,7 +138,6 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
     if (tid == 0) {
         for (int k = 0; k < NS; ++k) {
             mbar_init(&full[k], 1);
-            mbar_init(&empty[k], kU16Cons);
         }
         fence_mbar_init();
     }
@@ -245,7 +157,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
         unsigned r = 0u, id = blockIdx.x;
         const int4* trow = nullptr;
         for (;;) {
-            mbar_wait_backoff(&empty[st], (r & 1u) ^ 1u);  // the consumers released the previous use (round r - 1)
+            if (r > 0) stage_acquire(st, 32 * (kU16Cons + 1));  // the consumers released the previous use (round r - 1)
             if (c == nchunks) {                           // the next tile
                 if (t >= 0) {
                     if (lane == 0) id = atomicAdd(hdr + HDR_TILE, 1u) + gridDim.x;
@@ -542,8 +454,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
                 }
                 if ((j + LS) % kU16Check == 0 || j + LS == W) range_check(gmlast);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[cs]);  // the stage may be refilled once every consumer is done
+            stage_release(cs, 32 * (kU16Cons + 1));  // the stage may be refilled once every consumer is done
             if (++cs == NS) {
                 cs = 0;
                 ++cr;
@@ -599,9 +510,7 @@ bool u16_loads_ok(int n, uint32_t Q) {
     return ((int64_t)kU16Check + 2) * ((int64_t)Q + 1) <= 0x8000;
 }
 
-// The 2-D demand tensor {S columns, n rows} (row stride ld) for the TMA gathers: boxes of 64
-// scenarios x 1 row, out-of-range rows / columns read as zeros.
-static spdp_status make_demand_map(CUtensorMap* map, const uint16_t* demand, int64_t ld, int64_t S, int n) {
+spdp_status make_demand_map(CUtensorMap* map, const uint16_t* demand, int64_t ld, int64_t S, int n, int box_cols) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -613,7 +522,7 @@ static spdp_status make_demand_map(CUtensorMap* map, const uint16_t* demand, int
     if (!encode) return fail(SPDP_E_CUDA, "split_sweep_u16: cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)n};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(uint16_t)};
-    const cuuint32_t box[2] = {(cuuint32_t)kU16Box, 1u};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, 1u};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(demand), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -632,7 +541,7 @@ static spdp_status launch_u16_t(cudaStream_t st, const SweepArgs& a) {
                                      "split_sweep_u16 setup"))
         return e;
     CUtensorMap map;
-    if (spdp_status e = make_demand_map(&map, a.demand, a.ld, a.S, a.n)) return e;
+    if (spdp_status e = make_demand_map(&map, a.demand, a.ld, a.S, a.n, kU16Box)) return e;
     const int64_t ntiles = ((a.S + Cfg::kTile - 1) / Cfg::kTile) * a.T;
     int64_t grid = (int64_t)blocks_per_sm * device_sms();  // (measured: 4-5 CTAs per SM saturate it)
     if (grid > ntiles) grid = ntiles;
@@ -654,16 +563,21 @@ static spdp_status launch_u16_ls(int W, int A0, cudaStream_t st, const SweepArgs
         case 16: return A0 <= 6 ? launch_u16_t<16, 6, 2, LS>(st, a) : A0 <= 8 ? launch_u16_t<16, 8, 2, LS>(st, a)
                                                                               : launch_u16_t<16, 10, 2, LS>(st, a);
         case 20:
-            switch (A0 < 6 ? 6 : (A0 > 12 ? 12 : A0)) {
+            switch (A0 < 6 ? 6 : (A0 > 16 ? 16 : A0)) {
                 case 6: return launch_u16_t<20, 6, 2, LS>(st, a);
                 case 7: return launch_u16_t<20, 7, 2, LS>(st, a);
                 case 8: return launch_u16_t<20, 8, 2, LS>(st, a);
                 case 9: return launch_u16_t<20, 9, 2, LS>(st, a);
                 case 10: return launch_u16_t<20, 10, 2, LS>(st, a);
-                default: return launch_u16_t<20, 12, 2, LS>(st, a);
+                case 11:
+                case 12: return launch_u16_t<20, 12, 2, LS>(st, a);
+                case 13:
+                case 14: return launch_u16_t<20, 14, 2, LS>(st, a);
+                default: return launch_u16_t<20, 16, 2, LS>(st, a);
             }
         case 24: return A0 <= 8 ? launch_u16_t<24, 8, 2, LS>(st, a) : A0 <= 10 ? launch_u16_t<24, 10, 2, LS>(st, a)
-                                                                               : launch_u16_t<24, 12, 2, LS>(st, a);
+                        : A0 <= 12 ? launch_u16_t<24, 12, 2, LS>(st, a) : A0 <= 14 ? launch_u16_t<24, 14, 2, LS>(st, a)
+                                                                        : launch_u16_t<24, 16, 2, LS>(st, a);
         default: return A0 <= 8 ? launch_u16_t<32, 8, 2, LS>(st, a) : launch_u16_t<32, 12, 3, LS>(st, a);
     }
 }
