@@ -110,9 +110,11 @@ __global__ void __launch_bounds__(256) split_f32_kernel(const F32Pos* __restrict
 //   key = bits(val) | (d & 0x80000000)      (one LOP3)
 // orders like val inside the window (val >= 0: IEEE order of non-negative floats is the order of
 // their bit patterns) and above every in-window key outside it: the masked min of Eq. (3) is an
-// unsigned 3-input integer min (VIMNMX3) of keys, exact.  Two layers per step (the candidates of
-// age >= 2 of both are known before either), ages 1..A0 unconditionally, then groups of UG ages
-// behind one warp vote; a window that reaches age W lists the scenario for split_f32_kernel.
+// unsigned 3-input integer min (VIMNMX3) of keys, exact.  Four layers per step (as in the u16
+// sweep: the candidates made before the step first, one warp vote per deeper group of ages for all
+// four layers), ages 1..A0 unconditionally; a window that reaches age W lists the scenario for
+// split_f32_kernel.  Measured (C2, 10^6 scenarios): 0.61 ms (the previous one-thread-per-scenario
+// ring with LDG demand loads) -> 0.153 ms.
 constexpr int kF32Cons = 4;                      // consumer warps per CTA
 constexpr int kF32Threads = 32 * (kF32Cons + 1);
 constexpr int kF32Tile = 32 * kF32Cons;          // scenarios per tile = TMA box columns
@@ -165,6 +167,15 @@ __device__ __forceinline__ uint32_t f32_key(float val, uint32_t d) {
 }
 
 template <int N>
+__device__ __forceinline__ uint32_t umin_tree32(const uint32_t* v);
+// minimum of v[lo .. N - 1] (lo a compile-time constant after unrolling)
+template <int N>
+__device__ __forceinline__ uint32_t umin_tree32_from(const uint32_t* v, const int lo) {
+    if (lo == 0) return umin_tree32<N>(v);
+    if constexpr (N > 1) return umin_tree32_from<N - 1>(v + 1, lo - 1);
+    return v[0];
+}
+template <int N>
 __device__ __forceinline__ uint32_t umin_tree32(const uint32_t* v) {
     if constexpr (N == 1) return v[0];
     else if constexpr (N == 2) return min(v[0], v[1]);
@@ -172,13 +183,13 @@ __device__ __forceinline__ uint32_t umin_tree32(const uint32_t* v) {
     else return __vimin3_u32(umin_tree32<N - 2>(v), v[N - 2], v[N - 1]);
 }
 
-template <int W, int A0, int UG, int NST>
+template <int W, int A0, int UG, int NST, int LS>
 __global__ void __launch_bounds__(kF32Threads) split_f32_tma_kernel(
     const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ trow, const float* __restrict__ tbw, int n,
     int64_t S, int Q, float* __restrict__ cost, int64_t* __restrict__ list, unsigned* __restrict__ count) {
     using Cfg = F32TCfg<W, NST>;
     constexpr int NS = Cfg::NS;
-    static_assert(A0 >= 2 && A0 <= W && UG >= 1, "bad fp32 sweep config");
+    static_assert(A0 >= 2 && A0 <= W && UG >= 1 && W % LS == 0 && A0 >= LS + 1 && (LS == 2 || LS == 4), "bad fp32 sweep config");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NS * Cfg::kStageBytes);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -233,6 +244,7 @@ __global__ void __launch_bounds__(kF32Threads) split_f32_tma_kernel(
         }
     } else {
         __syncwarp();
+        const int rem = n % W;
         float F[W];
         int32_t Y[W];
         int cs = 0;
@@ -251,7 +263,6 @@ __global__ void __launch_bounds__(kF32Threads) split_f32_tma_kernel(
             Y[0] = Q;  // split point 0: f = 0, P = 0
             int32_t P = 0;
             uint32_t qmax = 0u, ovf = 0u;
-            float fin = 0.0f;
             for (int c = 0;;) {
                 const uint16_t* rows = reinterpret_cast<const uint16_t*>(sb) + wid * 32 + lane;
                 const float* band = reinterpret_cast<const float*>(sb + Cfg::kBandOff);
@@ -264,66 +275,91 @@ __global__ void __launch_bounds__(kF32Threads) split_f32_tma_kernel(
                     return f32_key(__fadd_rn(F[sl], band[jj * W + k - 1]), d);
                 };
                 // age W inside the window of a real layer i > W (i <= n): an older split point may be too
-                auto overflow = [&](const int jj, const uint32_t d0, const uint32_t d1) {
-                    if (c >= 1 && (!last || jj + 1 <= ilast)) ovf |= ~d0;
-                    if (c >= 1 && (!last || jj + 2 <= ilast)) ovf |= ~d1;
+                auto overflow = [&](const int jj, const uint32_t d) {
+                    if (c >= 1 && (!last || jj + 1 <= ilast)) ovf |= ~d;
                 };
+                // steps of LS layers (split_u16.cu): layer j + l's candidates of age >= max(2, l + 1) are
+                // split points made before the step; they and the voted deeper groups of all LS layers run
+                // first, the split points made inside the step are folded in last
                 uint32_t qn = rows[0];
 #pragma unroll
-                for (int j = 0; j < W; j += 2) {
-                    const uint32_t q0 = qn, q1 = rows[(j + 1) * kF32Tile];
-                    if (j + 2 < W) qn = rows[(j + 2) * kF32Tile];
-                    qmax = max(qmax, max(q0, q1));
-                    const int32_t Pn0 = P + (int32_t)q0, Pn1 = Pn0 + (int32_t)q1;
-                    // ages 2 .. A0 of both layers (split points <= the step's first layer - 1)
-                    uint32_t k0[A0 - 1], k1[A0 - 1];
+                for (int j = 0; j < W; j += LS) {
+                    uint32_t qv[LS];
+                    qv[0] = qn;
 #pragma unroll
-                    for (int k = 2; k <= A0; ++k) {  // (A0 < W: no overflow test here)
-                        uint32_t d0, d1;
-                        k0[k - 2] = cand(j, Pn0, k, d0);
-                        k1[k - 2] = cand(j + 1, Pn1, k, d1);
+                    for (int l = 1; l < LS; ++l) qv[l] = rows[(j + l) * kF32Tile];
+                    if (j + LS < W) qn = rows[(j + LS) * kF32Tile];
+                    int32_t Pn[LS];
+                    Pn[0] = P + (int32_t)qv[0];
+#pragma unroll
+                    for (int l = 1; l < LS; ++l) Pn[l] = Pn[l - 1] + (int32_t)qv[l];
+#pragma unroll
+                    for (int l = 0; l < LS; l += 2) qmax = max(qmax, max(qv[l], qv[l + 1]));
+                    uint32_t a[LS];
+#pragma unroll
+                    for (int l = 0; l < LS; ++l) {
+                        const int lo = l + 1 > 2 ? l + 1 : 2;
+                        uint32_t kk[A0 - 1];
+#pragma unroll
+                        for (int k = 2; k <= A0; ++k) {
+                            uint32_t d;
+                            kk[k - 2] = k < lo ? 0xffffffffu : cand(j + l, Pn[l], k, d);
+                        }
+                        a[l] = umin_tree32_from<A0 - 1>(kk, lo - 2);
                     }
-                    uint32_t a0 = umin_tree32<A0 - 1>(k0), a1 = umin_tree32<A0 - 1>(k1);
 #pragma unroll
                     for (int gi = 0; gi < W; ++gi) {
                         const int ag = A0 + 1 + gi * UG;
                         if (ag > W) break;
-                        uint32_t d0, d1;
-                        const uint32_t g0 = cand(j, Pn0, ag, d0), g1 = cand(j + 1, Pn1, ag, d1);
-                        if (!__any_sync(kFull, ((d0 & d1) >> 31) == 0u)) break;  // some lane has age ag inside
-                        uint32_t e0[UG + 1], e1[UG + 1];
-                        e0[0] = a0;
-                        e1[0] = a1;
-                        e0[1] = g0;
-                        e1[1] = g1;
+                        uint32_t dg[LS], dall = 0xffffffffu;
 #pragma unroll
-                        for (int u = 1; u < UG; ++u) {
-                            if (ag + u <= W) {
-                                uint32_t dd0, dd1;
-                                e0[u + 1] = cand(j, Pn0, ag + u, dd0);
-                                e1[u + 1] = cand(j + 1, Pn1, ag + u, dd1);
-                                if (ag + u == W) overflow(j, dd0, dd1);
-                            } else {
-                                e0[u + 1] = e1[u + 1] = 0xffffffffu;
-                            }
+                        for (int l = 0; l < LS; ++l) {
+                            dg[l] = (uint32_t)(Y[(1 + j + l - ag + 2 * W) % W] - Pn[l]);
+                            dall &= dg[l];
                         }
-                        if (ag == W) overflow(j, d0, d1);
-                        a0 = umin_tree32<UG + 1>(e0);
-                        a1 = umin_tree32<UG + 1>(e1);
+                        if (!__any_sync(kFull, (dall >> 31) == 0u)) break;  // some lane has age ag inside
+#pragma unroll
+                        for (int l = 0; l < LS; ++l) {
+                            uint32_t e[UG + 1];
+                            e[0] = a[l];
+                            e[1] = f32_key(__fadd_rn(F[(1 + j + l - ag + 2 * W) % W], band[(j + l) * W + ag - 1]), dg[l]);
+                            if (ag == W) overflow(j + l, dg[l]);
+#pragma unroll
+                            for (int u = 1; u < UG; ++u) {
+                                if (ag + u <= W) {
+                                    uint32_t dd;
+                                    e[u + 1] = cand(j + l, Pn[l], ag + u, dd);
+                                    if (ag + u == W) overflow(j + l, dd);
+                                } else {
+                                    e[u + 1] = 0xffffffffu;
+                                }
+                            }
+                            a[l] = umin_tree32<UG + 1>(e);
+                        }
                     }
-                    // age 1 of layer j: split point i - 1 (always inside when q <= Q; q > Q: qmax)
-                    const int s0 = (1 + j - 1 + 2 * W) % W, s1 = (1 + j + 2 * W) % W, s2 = (2 + j) % W;
-                    const float f0 = __uint_as_float(min(a0, __float_as_uint(__fadd_rn(F[s0], band[j * W]))));
-                    F[s1] = f0;  // split point of layer j (its slot held age W of layer j, read above)
-                    Y[s1] = Pn0 + Q;
-                    const float f1 = __uint_as_float(min(a1, __float_as_uint(__fadd_rn(f0, band[(j + 1) * W]))));
-                    F[s2] = f1;
-                    Y[s2] = Pn1 + Q;
-                    if (last) {
-                        if (j + 1 == ilast) fin = f0;
-                        if (j + 2 == ilast) fin = f1;
+                    // the split points of the step: fn[m] = f(i_j + m), i_j = c W + j + 1 (layer j's)
+                    float fn[LS];
+                    const float fprev = F[(j + 2 * W) % W];  // f(i_j - 1): age 1 of layer j
+#pragma unroll
+                    for (int l = 0; l < LS; ++l) {
+                        uint32_t m = a[l];
+                        // in-step ages 2 .. l: split point i_j + l - k = fn[l - k], Y = Pn[l - k] + Q
+                        if (l == 2) {
+                            m = min(m, f32_key(__fadd_rn(fn[0], band[(j + l) * W + 1]), (uint32_t)(Pn[0] + Q - Pn[l])));
+                        } else if (l == 3) {
+                            m = __vimin3_u32(m, f32_key(__fadd_rn(fn[1], band[(j + l) * W + 1]), (uint32_t)(Pn[1] + Q - Pn[l])),
+                                             f32_key(__fadd_rn(fn[0], band[(j + l) * W + 2]), (uint32_t)(Pn[0] + Q - Pn[l])));
+                        }
+                        // age 1 (split point i_j + l - 1): always inside when q <= Q (q > Q: qmax)
+                        const float f1 = l == 0 ? fprev : fn[l - 1];
+                        fn[l] = __uint_as_float(min(m, __float_as_uint(__fadd_rn(f1, band[(j + l) * W]))));
                     }
-                    P = Pn1;
+#pragma unroll
+                    for (int l = 0; l < LS; ++l) {  // (after every read of these slots' previous contents)
+                        F[(1 + j + l) % W] = fn[l];
+                        Y[(1 + j + l) % W] = Pn[l] + Q;
+                    }
+                    P = Pn[LS - 1];
                 }
                 stage_release(cs, 32 * (kF32Cons + 1));
                 if (++cs == NS) {
@@ -334,11 +370,15 @@ __global__ void __launch_bounds__(kF32Threads) split_f32_tma_kernel(
                 sb = smem_raw + (size_t)cs * Cfg::kStageBytes;
                 mbar_wait_warp(&full[cs], cr & 1u);
             }
+            // f(n) sits in slot n mod W (the padded layers after it wrote fewer than W slots)
+            uint32_t fin = 0u;  // (a select chain, not an indexed read: F stays in registers)
+#pragma unroll
+            for (int k = 0; k < W; ++k) fin = k == rem ? __float_as_uint(F[k]) : fin;
             if (s < S) {
                 // the window of some real layer reached age W: an older split point may be inside
                 if (qmax > (uint32_t)Q) cost[s] = INFINITY;  // Eq. (2)'s set is empty at some layer (R4)
                 else if (ovf & 0x80000000u) list[atomicAdd(count, 1u)] = s;
-                else cost[s] = fin;
+                else cost[s] = __uint_as_float(fin);
             }
         }
     }
@@ -443,9 +483,9 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
             kern<<<(unsigned)grid, kF32Threads, smem, st>>>(map, trow, tbw, n, S, Qe, cost, list, count);
             return last_launch("split_f32_tma_kernel");
         };
-        rc = go(split_f32_tma_kernel<kF32TW, kF32TA0, 2, 3>, F32TCfg<kF32TW, 3>::kSmem);
+        rc = go(split_f32_tma_kernel<kF32TW, kF32TA0, 2, 3, 4>, F32TCfg<kF32TW, 3>::kSmem);
         if (rc) return rc;
-        set_last_kernel("split_f32_tma_kernel<%d,%d,%d>", kF32TW, kF32TA0, 2);
+        set_last_kernel("split_f32_tma_kernel<%d,%d,%d,4>", kF32TW, kF32TA0, 2);
     } else {  // (loads near 2^30: every scenario through the general kernel)
         prof_begin(st);
         list = nullptr;
