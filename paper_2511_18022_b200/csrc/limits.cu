@@ -6,7 +6,11 @@
 //   F_0(0) = 0,  F_k(i) = min_{admissible (p, i]} F_{k-1}(p) + t(p, i),
 //   cost = min_{k <= K} F_k(n)   (K <= 0: no fleet limit -> one pass of Eq. (3)).
 // The fleet limit adds the vehicle-count layer dimension to the layered DAG, kept
-// to the band of k that the capacity bounds allow (ring kernel below).  The masks
+// to the band of k that the capacity bounds allow (ring kernel below).  Fleet launches: a classify
+// pass (infeasible scenarios finished; the rest listed by the band width their slack K - kT
+// needs), one ring pass per band width 2 / 4 / 8 / 16 over its list, a warp-per-scenario kernel for
+// slack 16..31 and windows longer than the ring, the general kernel for the rest (C2, K = 27:
+// 3.9 -> 1.37 ms).  The masks
 // mask(i) of Eq. (2) do not depend on k: they are computed once per scenario (two
 // pointers) and reused for every k.
 #include <climits>
@@ -181,8 +185,9 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
                                                                const uint16_t* __restrict__ demand, int64_t S, int Q,
                                                                int Lmax, int K, int32_t* __restrict__ cost,
                                                                spdp_saa_partial* __restrict__ partial,
-                                                               int64_t* __restrict__ list, unsigned* __restrict__ count,
-                                                               int table_in_smem) {
+                                                               int2* __restrict__ list, unsigned* __restrict__ count,
+                                                               int table_in_smem, const int2* __restrict__ in_list,
+                                                               const unsigned* __restrict__ in_count) {
     constexpr bool FLEET = BW > 1;
     extern __shared__ int4 sm4[];
     __shared__ Part red[NT / 32];
@@ -202,15 +207,19 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
     // F of one (slot, thread): BW contiguous ints ([kRing][NT][BW]: one 16-byte load when BW = 4)
     auto F_at = [&](int p, int b) -> int& { return ringF[((p & (kRing - 1)) * NT + tid) * BW + b]; };
     Part acc{0, 0, 0, 0, 0};
-    const int64_t s = (int64_t)blockIdx.x * NT + tid;
+    // the scenario: the thread's own (natural order) or the w-th entry of the classify pass's list for
+    // this band width (its slack already known and in [0, BW): no pre-pass)
+    const int64_t w = (int64_t)blockIdx.x * NT + tid;
+    const bool listed = in_list != nullptr;
+    const int64_t s = listed ? (w < (int64_t)*in_count ? (int64_t)in_list[w].x : S) : w;
     if (s < S) {
         const uint16_t* dcol = demand + s;
         int result = SPDP_INFEASIBLE;
         bool defer = false;
         // capacity pre-pass: any demand above Q (R4) and kT = greedy route count of the whole tour
         bool bad = false;
-        int kT = 0;
-        {
+        int kT = listed ? K - in_list[w].y : 0;
+        if (!listed) {
             int load = Q + 1;
             for (int i = 1; i <= n; ++i) {
                 const int q = dcol[(uint32_t)tb[i].w];
@@ -276,6 +285,15 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
                                 const int c = d ? v[b] : (b ? v[b - 1] : kLimBig);
                                 if (c < kLimBig) best[b] = min(best[b], c + Ap);
                             }
+                        } else if constexpr (BW == 2) {  // (the same select, one 8-byte load)
+                            const int d = kp - K_at(p);
+                            const int2 f2 = *reinterpret_cast<const int2*>(&F_at(p, 0));
+                            const int v[2] = {f2.x, f2.y};
+#pragma unroll
+                            for (int b = 0; b < BW; ++b) {
+                                const int c = d ? v[b] : (b ? v[b - 1] : kLimBig);
+                                if (c < kLimBig) best[b] = min(best[b], c + Ap);
+                            }
                         } else if (FLEET) {
                             const int off = kp - 1 - K_at(p);  // F_{k-1}(p), k = kp + b: band index off + b
 #pragma unroll
@@ -309,8 +327,8 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
                 }
             }
         }
-        if (defer) {
-            list[atomicAdd(count, 1u)] = s;
+        if (defer) {  // (the window outgrew the ring: the warp-per-scenario kernel, any window)
+            list[atomicAdd(count, 1u)] = make_int2((int)s, FLEET ? K - kT : 0);
         } else {
             if (cost) cost[s] = result;
             part_add_cost(acc, result, result != SPDP_INFEASIBLE);
@@ -326,6 +344,184 @@ __global__ void __launch_bounds__(NT) split_limits_ring_kernel(const int4* __res
             atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_hi), (unsigned long long)t.sq_hi);
         }
     }
+}
+
+// Fleet limit, pass 0: one thread per scenario (coalesced column reads): any demand
+// above Q (R4) and kT = the greedy (minimum) route count of the whole tour.  slack = K - kT < 0 (or
+// a demand above Q): infeasible, finished here.  Otherwise the scenario goes to the list of the
+// band width its slack needs (BW = 2, 4, 8, 16: slack < BW) -- or, wider, to the general kernel's
+// list -- so that each ring pass runs warps whose lanes all need (about) the same band and no lane
+// idles on an infeasible scenario (at C2, K = kmin + 2: 72 % infeasible, slack spread over 0..15).
+constexpr int kLimBands = 4;  // band widths 2, 4, 8, 16
+constexpr int kLimWarpBW = 32;  // the warp kernel's band: one lane per vehicle count
+__global__ void __launch_bounds__(256) limits_classify_kernel(const int4* __restrict__ tb, int n,
+                                                              const uint16_t* __restrict__ demand, int64_t S, int Q, int K,
+                                                              int32_t* __restrict__ cost,
+                                                              spdp_saa_partial* __restrict__ partial,
+                                                              int2* __restrict__ blists, int64_t cap,
+                                                              unsigned* __restrict__ bcounts,
+                                                              int64_t* __restrict__ list, unsigned* __restrict__ count,
+                                                              int warp_ok) {
+    // blists: [kLimBands + 1][cap] {scenario, slack} (the last: the warp kernel's), bcounts likewise
+    __shared__ Part red[8];
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    Part acc{0, 0, 0, 0, 0};
+    int cls = -1;  // -1: none (finished or no scenario), 0..3: band list, 4: the warp kernel, 5: the general kernel
+    int slack = 0;
+    if (s < S) {
+        const uint16_t* dcol = demand + s;
+        bool bad = false;
+        int kT = 0, load = Q + 1;
+        for (int i = 1; i <= n; ++i) {
+            const int q = dcol[(uint32_t)__ldg(&tb[i].w)];
+            bad |= q > Q;
+            load += q;
+            if (load > Q) {
+                ++kT;
+                load = q;
+            }
+        }
+        slack = K - kT;
+        if (bad || slack < 0) {
+            if (cost) cost[s] = SPDP_INFEASIBLE;
+            part_add_cost(acc, SPDP_INFEASIBLE, false);
+        } else {
+            cls = slack < 2 ? 0 : slack < 4 ? 1 : slack < 8 ? 2 : slack < 16 ? 3 : (warp_ok && slack < kLimWarpBW) ? 4 : 5;
+        }
+    }
+    // warp-aggregated appends: one atomic per (warp, list)
+#pragma unroll
+    for (int c = 0; c <= kLimBands + 1; ++c) {
+        const unsigned m = __ballot_sync(kFull, cls == c);
+        if (m == 0u) continue;
+        unsigned base = 0u;
+        const int leader = __ffs(m) - 1;
+        if (lane == leader) base = atomicAdd(c <= kLimBands ? &bcounts[c] : count, (unsigned)__popc(m));
+        base = __shfl_sync(kFull, base, leader);
+        if (cls == c) {
+            const unsigned idx = base + (unsigned)__popc(m & ((1u << lane) - 1u));
+            if (c <= kLimBands) blists[(int64_t)c * cap + idx] = make_int2((int)s, slack);
+            else list[idx] = s;
+        }
+    }
+    if (partial) {
+        const Part t = block_sum(acc, red);
+        if (threadIdx.x == 0 && t.n_infeas) atomicAdd(reinterpret_cast<unsigned long long*>(&partial->n_infeas),
+                                                      (unsigned long long)t.n_infeas);
+    }
+}
+
+
+// Fleet limit, the rare cases (slack 16..31, or a window longer than the ring): ONE WARP PER
+// SCENARIO, lane b = vehicle-count offset b (k = kP(i) + b), any window.  Per warp in shared memory
+// the prefix loads P[0..n], kP[0..n] and the band F[0..n][32]; the layer loop and the candidate
+// loop are warp-uniform (the mask two-pointer and the duration test do not depend on k), each lane
+// forms F_{k-1}(p) + t(p, i) for its own k, band entry b - 1 + (kP(i) - kP(p)) (R24, ring kernel).
+__global__ void __launch_bounds__(256) split_limits_warp_kernel(const int4* __restrict__ tb, int n,
+                                                                const uint16_t* __restrict__ demand, int Q, int Lmax,
+                                                                int K, int32_t* __restrict__ cost,
+                                                                spdp_saa_partial* __restrict__ partial,
+                                                                const int2* __restrict__ wlist,
+                                                                const unsigned* __restrict__ wcount) {
+    extern __shared__ int smw[];
+    __shared__ Part red[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int* Pw = smw + (size_t)wid * (n + 1) * (kLimWarpBW + 2);
+    int* Kw = Pw + (n + 1);
+    int* Fw = Kw + (n + 1);
+    Part acc{0, 0, 0, 0, 0};
+    const unsigned total = *wcount;
+    for (unsigned w = blockIdx.x * nw + wid; w < total; w += gridDim.x * nw) {
+        const int2 ent = wlist[w];
+        const int64_t s = ent.x;
+        const uint16_t* dcol = demand + s;
+        // tour-order prefix loads, 32 positions at a time (warp scan)
+        int base = 0;
+        bool bad = false;
+        if (lane == 0) Pw[0] = 0;
+        for (int i0 = 1; i0 <= n; i0 += 32) {
+            const int i = i0 + lane;
+            int q = i <= n ? (int)dcol[(uint32_t)__ldg(&tb[i].w)] : 0;
+            bad |= q > Q;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(kFull, q, o);
+                if (lane >= o) q += v;
+            }
+            if (i <= n) Pw[i] = base + q;
+            base += __shfl_sync(kFull, q, 31);
+        }
+        __syncwarp();
+        if (lane == 0) {  // kP(i): the greedy (minimum) route count of the prefix 1..i
+            int kp = 0, load = Q + 1;
+            Kw[0] = 0;
+            for (int i = 1; i <= n; ++i) {
+                const int q = Pw[i] - Pw[i - 1];
+                load += q;
+                if (load > Q) {
+                    ++kp;
+                    load = q;
+                }
+                Kw[i] = kp;
+            }
+        }
+        __syncwarp();
+        const int slack = K - Kw[n];
+        int result = SPDP_INFEASIBLE;
+        if (!__any_sync(kFull, bad) && slack >= 0) {
+            Fw[lane] = lane == 0 ? 0 : kLimBig;  // F_0(0) = 0
+            int m = 0;
+            for (int i = 1; i <= n; ++i) {
+                const int Pi = Pw[i];
+                while (Pi - Pw[m] > Q) ++m;  // mask(i)
+                const int kpi = Kw[i];
+                const int Bi = __ldg(&tb[i].z);
+                const int thr = Lmax - Bi;
+                int best = kLimBig;
+                __syncwarp();
+                for (int p = i - 1; p >= m; --p) {
+                    const int Ap = __ldg(&tb[p].y);
+                    if (Ap > thr) continue;  // (warp-uniform) the route (p, i] exceeds the duration limit
+                    const int bb = lane - 1 + (kpi - Kw[p]);
+                    if (bb >= 0 && bb <= slack) {
+                        const int f = Fw[p * kLimWarpBW + bb];
+                        if (f < kLimBig) best = min(best, f + Ap);
+                    }
+                }
+                int v = best >= kLimBig ? kLimBig : best + Bi;
+                if (lane > slack || kpi + lane > K) v = kLimBig;
+                Fw[i * kLimWarpBW + lane] = v;
+            }
+            __syncwarp();
+            int r = lane <= slack ? Fw[n * kLimWarpBW + lane] : kLimBig;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r = min(r, __shfl_xor_sync(kFull, r, o));
+            result = r >= kLimBig ? SPDP_INFEASIBLE : r;
+        }
+        if (lane == 0) {
+            if (cost) cost[s] = result;
+            part_add_cost(acc, result, result != SPDP_INFEASIBLE);
+        }
+        __syncwarp();
+    }
+    if (partial) {
+        const Part t = block_sum(acc, red);
+        if (threadIdx.x == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->n_feas), (unsigned long long)t.n_feas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->n_infeas), (unsigned long long)t.n_infeas);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sum), (unsigned long long)t.sum);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_lo), (unsigned long long)t.sq_lo);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&partial->sumsq_hi), (unsigned long long)t.sq_hi);
+        }
+    }
+}
+
+// (n too large for the warp kernel's shared memory) the ring passes' deferrals to the general kernel
+__global__ void limits_wlist_to_general_kernel(const int2* __restrict__ wl, const unsigned* __restrict__ wc,
+                                               int64_t* __restrict__ list, unsigned* __restrict__ count) {
+    for (unsigned w = blockIdx.x * blockDim.x + threadIdx.x; w < *wc; w += gridDim.x * blockDim.x)
+        list[atomicAdd(count, 1u)] = wl[w].x;
 }
 
 // Without a fleet limit: the duration-limited Eq. (3) sweep on a 32-entry REGISTER ring (the
@@ -446,14 +642,15 @@ static size_t ring_smem(int32_t n) {
 
 template <int BW, int NT, int kRing>
 static spdp_status launch_ring(cudaStream_t st, const int4* e, int n, const uint16_t* demand, int64_t S, int Q, int Lmax,
-                               int K, int32_t* cost, spdp_saa_partial* partial, int64_t* list, unsigned* count) {
+                               int K, int32_t* cost, spdp_saa_partial* partial, int2* list, unsigned* count,
+                               const int2* in_list = nullptr, const unsigned* in_count = nullptr, int64_t nwork = -1) {
     const size_t smem = ring_smem<BW, NT, kRing>(n);
     if (spdp_status e = kernel_setup((const void*)split_limits_ring_kernel<BW, NT, kRing>,
                                      (int)ring_smem<BW, NT, kRing>(kLimTableSmemMaxN), -1, 0, 0, nullptr,
                                      "split_limits_ring_kernel setup"))
         return e;
-    split_limits_ring_kernel<BW, NT, kRing><<<(unsigned)ceil_div(S, NT), NT, smem, st>>>(
-        e, n, demand, S, Q, Lmax, K, cost, partial, list, count, n <= kLimTableSmemMaxN ? 1 : 0);
+    split_limits_ring_kernel<BW, NT, kRing><<<(unsigned)ceil_div(nwork < 0 ? S : nwork, NT), NT, smem, st>>>(
+        e, n, demand, S, Q, Lmax, K, cost, partial, list, count, n <= kLimTableSmemMaxN ? 1 : 0, in_list, in_count);
     set_last_kernel("split_limits_ring_kernel<%d,%d>", BW, kRing);
     return last_launch("split_limits_ring_kernel");
 }
@@ -464,7 +661,8 @@ using namespace spdp;
 
 extern "C" size_t spdp_limits_workspace_bytes(int32_t n, int64_t S) {
     if (n < 1 || S < 1) return 0;
-    return lim_table_bytes(n) + lim_scratch_bytes(n) + align_up(sizeof(int64_t) * (size_t)S, 256) + 256;
+    return lim_table_bytes(n) + lim_scratch_bytes(n) + align_up(sizeof(int64_t) * (size_t)S, 256) + 256 +
+           align_up(sizeof(int2) * (size_t)(kLimBands + 1) * (size_t)S, 256) + 256;
 }
 
 extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t* dist, int32_t n,
@@ -494,7 +692,13 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
     if (rc) return rc;
     if (partial && (rc = cuda_check(cudaMemsetAsync(partial, 0, sizeof(spdp_saa_partial), st), "cudaMemsetAsync(partial)")))
         return rc;
+    // band lists of the fleet passes: [kLimBands][S] {scenario, slack} and their counts
+    int2* blists = reinterpret_cast<int2*>(reinterpret_cast<char*>(count) + 256);
+    unsigned* bcounts = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(blists) +
+                                                    align_up(sizeof(int2) * (size_t)(kLimBands + 1) * (size_t)S, 256));
     if ((rc = cuda_check(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
+    if ((rc = cuda_check(cudaMemsetAsync(bcounts, 0, (kLimBands + 1) * sizeof(unsigned), st), "cudaMemsetAsync(bcounts)")))
+        return rc;
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
     const int Lmax = max_duration < 0 ? INT_MAX / 2 : max_duration;
     const bool fleet = max_routes > 0 && max_routes < n;
@@ -503,10 +707,41 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
     // (1) the ring kernel for every scenario; (2) the general kernel for the ones it deferred
     const bool general_only = (flags & SPDP_F_SCRATCH_GLOBAL) != 0;
     if (!general_only) {
-        // fleet: 8 vehicle counts per position on a 16-position ring, 64 threads per CTA (measured at C2:
-        // K = 27 3.9 ms, K = 31 5.4 ms; 4 counts: 3.7 / 7.6 ms -- wider bands defer fewer scenarios)
+        // fleet: the classify pass (infeasible scenarios finished, the rest listed by the band width their
+        // slack needs), then one 16-position-ring pass per band width 2 / 4 / 8 / 16 over its list
+        // (measured at C2, K = 27: one natural-order pass with 8 counts per position 3.9 ms, whose warps
+        // ran every lane at the widest band of the warp, infeasible lanes idle)
         if (fleet) {
-            rc = launch_ring<8, 64, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, list, count);
+            const size_t per_warp = sizeof(int) * (size_t)(n + 1) * (kLimWarpBW + 2);
+            const bool warp_fits = per_warp <= kLimSmemCap;
+            limits_classify_kernel<<<(unsigned)ceil_div(S, 256), 256, 0, st>>>(e, n, demand, S, Qe, K, cost, partial,
+                                                                            blists, S, bcounts, list, count,
+                                                                            warp_fits ? 1 : 0);
+            if ((rc = last_launch("limits_classify_kernel"))) return rc;
+            int2* wl = blists + (int64_t)kLimBands * S;  // the warp kernel's list (+ the ring passes' deferrals)
+            unsigned* wc = bcounts + kLimBands;
+            if (!rc) rc = launch_ring<2, 64, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, wl, wc, blists, bcounts, S);
+            if (!rc) rc = launch_ring<4, 64, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, wl, wc, blists + S,
+                                                 bcounts + 1, S);
+            if (!rc) rc = launch_ring<8, 64, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, wl, wc, blists + 2 * S,
+                                                 bcounts + 2, S);
+            if (!rc) rc = launch_ring<16, 64, 16>(st, e, n, demand, S, Qe, Lmax, K, cost, partial, wl, wc, blists + 3 * S,
+                                                  bcounts + 3, S);
+            if (rc) return rc;
+            if (warp_fits) {
+                int warps = (int)(kLimSmemCap / per_warp);
+                warps = warps > 8 ? 8 : warps;
+                if ((rc = kernel_setup((const void*)split_limits_warp_kernel, (int)kLimSmemCap, -1, 0, 0, nullptr,
+                                       "split_limits_warp_kernel setup")))
+                    return rc;
+                split_limits_warp_kernel<<<(unsigned)(lim_num_sms() * 2), warps * 32, per_warp * warps, st>>>(
+                    e, n, demand, Qe, Lmax, K, cost, partial, wl, wc);
+                if ((rc = last_launch("split_limits_warp_kernel"))) return rc;
+            } else {
+                limits_wlist_to_general_kernel<<<lim_num_sms(), 256, 0, st>>>(wl, wc, list, count);
+                if ((rc = last_launch("limits_wlist_to_general_kernel"))) return rc;
+            }
+            set_last_kernel("split_limits_ring_kernel<2|4|8|16,16>");
         } else {  // duration only (or no limit): the register ring with the per-layer duration bitmask
             limits_dmask_kernel<<<(unsigned)ceil_div(n + 1, 256), 256, 0, st>>>(e, n, Lmax);
             if ((rc = last_launch("limits_dmask_kernel"))) return rc;

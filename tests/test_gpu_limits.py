@@ -42,8 +42,11 @@ def _limits(inst, dem, frac_routes):
     d, t = inst["dist"], inst["tour"]
     trip = int(max(d[0, c] + d[c, 0] for c in t))
     kmin = int(np.ceil(inst["nominal"].astype(np.int64).sum() / inst["Q"]))
+    # kmin + 6: slack spread over the ring passes' band widths 2 / 4 / 8 / 16; kmin + 20: slack 16..31,
+    # the warp-per-scenario kernel; kmin + 40: slack >= 32, the general kernel
     return [(-1, 0), (trip, 0), (int(trip * 1.5), 0), (-1, kmin + frac_routes), (-1, 1),
-            (int(trip * 1.5), kmin + 2 * frac_routes), (-1, kmin + 6)]  # (kmin + 6: bands wider than the ring's)
+            (int(trip * 1.5), kmin + 2 * frac_routes), (-1, kmin + 6), (-1, kmin + 20), (int(trip * 1.5), kmin + 20),
+            (-1, kmin + 40)]
 
 
 @pytest.mark.parametrize("name,S,extra_q,glob", [("C1", 100, 0, False), ("C1", 100, 0, True), ("C2", 2_003, 0, False),
