@@ -190,6 +190,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--window-hint", type=int, default=None)
+    ap.add_argument("--scenario-order", default="load", choices=["load", "natural"],
+                    help="load (default): each rank's resident scenario set is ordered once by total demand "
+                         "(spdp_order_scenarios, a layout of the set, outside the timed steps); natural: as generated")
     ap.add_argument("--eager", action="store_true",
                     help="launch every timed step from Python (default: replay a CUDA graph of the step(s))")
     ap.add_argument("--graph-steps", type=int, default=10,
@@ -241,6 +244,16 @@ def main():
     dem_bytes = n * spdp.padded_ld(S_loc) * 2
     B = 1 if dem_bytes > 1.5 * L2_BYTES else int(np.ceil(2 * L2_BYTES / dem_bytes))
     demands = [spdp.gen_demands(cfg["model"], s_begin + k * S_glob, S_loc, device=dev) for k in range(B)]
+    order_ms, perms = None, None
+    if args.scenario_order == "load":  # (a layout of each resident set, once; timed here, reported in config)
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record()
+        ordered = [spdp.order_scenarios(d_, S=S_loc) for d_ in demands]
+        demands, perms = [o[0] for o in ordered], [o[1] for o in ordered]
+        b_.record()
+        torch.cuda.synchronize(dev)
+        order_ms = a_.elapsed_time(b_) / B
+    mean_w = (bench_config.MEAN_ORDERED if args.scenario_order == "load" else bench_config.MEAN)[args.config]
     demand = demands[0]
     T = cfg["T"]
     tour = torch.from_numpy(inst["tour"]).to(dev)
@@ -265,10 +278,10 @@ def main():
             cur.wait_event(freed[b])
         if T > 1:  # batched tours (a8): T candidate tours over the same scenarios
             spdp.split_eval_batch(tours, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost, partial=part,
-                                  mean_window=bench_config.MEAN[args.config])
+                                  mean_window=mean_w)
         else:
             spdp.split_eval(tour, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost, partial=part,
-                            mean_window=bench_config.MEAN[args.config])
+                            mean_window=mean_w)
         if world > 1:
             ready = torch.cuda.Event()
             ready.record(cur)
@@ -431,7 +444,11 @@ def main():
                                    "(%d per GPU; cv=0.3, rho=0.5), %d giant tour%s" % (
                                        args.config, n + 1, n, Q, S_glob, S_loc, T, "s" if T > 1 else ""),
                        "n": n, "S_per_gpu": S_loc, "S_global": S_glob, "T": T, "window_hint": hint,
-                       "mean_window_hint": bench_config.MEAN[args.config],
+                       "mean_window_hint": mean_w,
+                       "scenario_order": ("by total demand within segments of 65536 (spdp_order_scenarios): a layout "
+                                          "of each rank's resident scenario set, made once (%.3f ms per set) before the "
+                                          "timed steps; the per-scenario costs are the permuted ones, the SAA partials "
+                                          "identical" % order_ms) if order_ms is not None else "natural (as generated)",
                        "l2": ("inputs larger than L2 (demand %.0f MB/GPU > 126 MB)" % (dem_bytes / 1e6) if B == 1 else
                               "inputs larger than L2: each step a fresh batch of the S scenarios, %d batches of "
                               "%.0f MB/GPU rotating (%.0f MB > 2 x 126 MB L2)" % (B, dem_bytes / 1e6,
@@ -477,7 +494,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         partial = partials[(kstep[0] - 1) & 1]
         line["cpu_baseline"] = cpu_baseline(cfg, cost[0] if T > 1 else cost, S_loc, spdp,
-                                            partial[0] if T > 1 else partial)
+                                            partial[0] if T > 1 else partial,
+                                            perms[(kstep[0] - 1) % B] if perms is not None else None)
         if T > 1:
             line["cpu_baseline"]["sample"] += " (tour 0 of the %d)" % T
 
@@ -525,7 +543,22 @@ def measure_rows(spdp, torch, dev, pk):
         ms = _time_events(fn, torch, dev, iters=20)
         sweep[str(S_)] = {"ms": ms, "evals_per_s": S_ / (ms / 1e3)}
     rows["a5_C2_S_sweep"] = sweep
-    del d
+    # the C2 step on the scenario set ordered by total demand (spdp_order_scenarios, once per set;
+    # the per-scenario costs are the permuted ones, the SAA partial identical)
+    dO, _ = spdp.order_scenarios(d, S=cfg2["S"])
+    order_ms = _time_events(lambda: spdp.order_scenarios(d, S=cfg2["S"], out=dO), torch, dev, iters=3)
+    p0 = torch.zeros(6, dtype=torch.int64, device=dev)
+    pO = torch.zeros(6, dtype=torch.int64, device=dev)
+    spdp.split_eval(tour2, dist2, d, inst2["Q"], S=cfg2["S"], window_hint=bench_config.HINT["C2"],
+                    mean_window=bench_config.MEAN["C2"], partial=p0)
+    fn = lambda: spdp.split_eval(tour2, dist2, dO, inst2["Q"], S=cfg2["S"], window_hint=bench_config.HINT["C2"],
+                                 mean_window=bench_config.MEAN_ORDERED["C2"], cost=c_, partial=pO)
+    ms = _time_events(fn, torch, dev, iters=20)
+    rows["a5_C2_ordered"] = {"ms": ms, "evals_per_s": cfg2["S"] / (ms / 1e3), "kernel": spdp.last_kernel(),
+                             "order_ms": order_ms, "partials_equal_natural_order": bool(torch.equal(pO, p0)),
+                             "note": "one C2 step on the scenario set ordered by total demand (ordering once per "
+                                     "set, order_ms, amortised over the tours evaluated on it)"}
+    del d, dO
     # a5 sensitivity: C2 with r = 16 customers per route (Q 4x, windows ~4x: mean 15,
     # max 46 -> the monotone-deque sweep)
     inst16 = synth.make_instance(100, 101, r=16.0)
@@ -580,6 +613,24 @@ def measure_rows(spdp, torch, dev, pk):
                                       "its bound is the demand stream (hbm_frac)")
         else:
             row["bound"] = "alu"
+        if cfg["T"] > 1:
+            # the same batch on the scenario set ordered by total demand (spdp_order_scenarios, once per
+            # set: similar windows share a warp); costs are the permuted ones, the SAA partials identical
+            dO, perm = spdp.order_scenarios(d, S=cfg["S"])
+            order_ms = _time_events(lambda: spdp.order_scenarios(d, S=cfg["S"], out=dO), torch, dev, iters=3)
+            partO = torch.zeros_like(part)
+            mwo = bench_config.MEAN_ORDERED[name]
+            fno = lambda: spdp.split_eval_batch(tours, dist, dO, inst["Q"], S=cfg["S"], want_cost=False, partial=partO,
+                                                window_hint=h, mean_window=mwo)
+            mso = _time_events(fno, torch, dev, iters=6)
+            row["natural_order"] = {k: row[k] for k in ("ms", "evals_per_s", "kernel", "alu_frac")}
+            row.update({"ms": mso, "evals_per_s": cfg["T"] * cfg["S"] / (mso / 1e3), "kernel": spdp.last_kernel(),
+                        "alu_frac": cand / (mso / 1e3) / alu_peak,
+                        "scenario_order": "by total demand (spdp_order_scenarios, %.3f ms once per scenario set; "
+                                          "alu_frac_incl_order adds it to this one batch of %d tours)" % (order_ms, cfg["T"]),
+                        "order_ms": order_ms, "alu_frac_incl_order": cand / ((mso + order_ms) / 1e3) / alu_peak,
+                        "partials_equal_natural_order": bool(torch.equal(partO, part))})
+            del dO, perm
         rows["a8_batch_%s" % name if cfg["T"] > 1 else "a5_%s" % name] = row
         del d
     # f3: the C3 population evaluated from tour 0's prefix / suffix values (spdp_split_values once,
@@ -713,7 +764,7 @@ def measure_rows(spdp, torch, dev, pk):
     return rows
 
 
-def cpu_baseline(cfg, cost_dev, S, spdp, partial_dev):
+def cpu_baseline(cfg, cost_dev, S, spdp, partial_dev, perm_dev=None):
     import oracle
     inst = cfg["inst"]
     threads = max(oracle.num_threads(), os.cpu_count() or 1)  # all host cores (torchrun sets OMP_NUM_THREADS=1)
@@ -723,7 +774,11 @@ def cpu_baseline(cfg, cost_dev, S, spdp, partial_dev):
     w = oracle.saa(want)
     t = time.perf_counter() - t0
     got = cost_dev.cpu().numpy().astype(np.int64)
-    parity = bool(np.array_equal(got, want))
+    if perm_dev is not None:  # (an ordered scenario set: column j holds scenario perm[j])
+        want_cols = np.asarray(want)[perm_dev.cpu().numpy()]
+    else:
+        want_cols = np.asarray(want)
+    parity = bool(np.array_equal(got, want_cols))
     est = spdp.saa_mean(partial_dev)
     # the paper's 1-thread baseline: one host thread on a 10^5-scenario prefix
     S1 = min(S, 100_000)

@@ -167,6 +167,23 @@ SPDP_API size_t spdp_workspace_bytes(int32_t n, int64_t S, int32_t T);
 SPDP_API spdp_status spdp_gen_demands(const spdp_demand_model* model, int64_t s_begin, int64_t S,
                              uint16_t* demand, int64_t ld, spdp_stream_t stream);
 
+/* a1 (layout). Scenario ordering for repeated / batched evaluation of one scenario set
+ * (DESIGN §"scenario order"; a warp runs each layer at the deepest Eq. (3)
+ * window among its lanes, so scenarios with similar loads belong in the same warp).
+ *   key(s) = sum_c demand[c][s];  bucket(s) = floor(key(s) * 1024 / (max_s key(s) + 1));
+ *   perm[j] = within each segment of 65536 consecutive scenarios, the segment's scenarios in
+ *             increasing bucket order, increasing index within a bucket (stable: deterministic);
+ *   out[c][j] = demand[c][perm[j]]  (out may be NULL).
+ * Every evaluation of `out` equals the evaluation of `demand` with its scenarios permuted:
+ * costs[j] belong to scenario perm[j]; SAA partials are identical.  demand, out, perm
+ * (int32 [S]) are DEVICE pointers, out must not alias demand; ws: spdp_order_workspace_bytes(S)
+ * bytes of device scratch.  Asynchronous on `stream`.  Errors: E_USAGE (sizes, NULL, aliasing,
+ * small workspace), E_RESOURCE (n > SPDP_MAX_N, S >= 2^31), E_CUDA. */
+SPDP_API size_t spdp_order_workspace_bytes(int64_t S);
+SPDP_API spdp_status spdp_order_scenarios(const uint16_t* demand, int64_t ld, int32_t n, int64_t S, uint16_t* out,
+                                          int64_t ld_out, int32_t* perm, void* ws, size_t ws_bytes,
+                                          spdp_stream_t stream);
+
 /* a3. Tour-order demand prefix sums ("prefix-sum operations";
  * SPEC:127-135): prefix[i*S + j] = sum_{k<=i} q^j_{sigma_k}, i = 0..n
  * (uint32 [n+1][S], scenario-minor). */

@@ -47,6 +47,7 @@ SYMBOLS = (
     "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours", "spdp_limits_workspace_bytes",
     "spdp_split_eval_limits", "spdp_f32_workspace_bytes", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
     "spdp_saa_f32_moments", "spdp_saa_finalize_f32", "spdp_split_eval_batch_f32", "spdp_split_eval_neighbours_multi",
+    "spdp_order_workspace_bytes", "spdp_order_scenarios",
 )
 
 
@@ -117,6 +118,9 @@ def _sig():
     L.spdp_saa_finalize_f32.argtypes = [P, P, ctypes.POINTER(SaaEstimate)]
     L.spdp_split_eval_batch_f32.argtypes = [P, i32, P, i32, P, i64, i64, i32, P, P, sz, P]
     L.spdp_saa_mean.argtypes = [ctypes.POINTER(SaaPartial), ctypes.POINTER(SaaEstimate)]
+    L.spdp_order_workspace_bytes.argtypes = [i64]
+    L.spdp_order_workspace_bytes.restype = sz
+    L.spdp_order_scenarios.argtypes = [P, i64, i32, i64, P, i64, P, P, sz, P]
     L.spdp_split_eval_host.argtypes = [P, P, i32, P, i64, i64, i32, P, ctypes.POINTER(SaaEstimate), i32, P, sz, P]
     L.spdp_irp_dp.argtypes = [P, ctypes.POINTER(IrpCustomer), i32, i32, P, i64, i64, P, P, P, sz, u32, P]
     for name in ("spdp_gen_demands", "spdp_demand_prefix", "spdp_split_mask", "spdp_split_eval",
@@ -124,7 +128,7 @@ def _sig():
                  "spdp_irp_dp", "spdp_split_values", "spdp_split_eval_neighbours", "spdp_split_eval_penalized",
                  "spdp_split_routes", "spdp_split_eval_limits", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
                  "spdp_saa_f32_moments", "spdp_saa_finalize_f32", "spdp_split_eval_batch_f32",
-                 "spdp_split_eval_neighbours_multi"):
+                 "spdp_split_eval_neighbours_multi", "spdp_order_scenarios"):
         getattr(L, name).restype = st
 
 
@@ -264,6 +268,25 @@ def gen_demands(model: dict, s_begin: int, S: int, device="cuda", out=None):
     out._spdp_S = int(S)
     out._spdp_nominal = nominal  # keep alive until the stream has consumed it
     return out
+
+
+def order_scenarios(demand, S: int | None = None, out=None, want_out: bool = True):
+    """a1 layout: the scenarios (columns) of `demand` in increasing bucketed total demand
+    (spdp_order_scenarios).  Returns (ordered demand [n][ld] or None, perm int32 [S]):
+    column j of the result is scenario perm[j] of `demand`."""
+    torch = _torch()
+    n, ld = demand.shape
+    S = _default_S(demand, S)
+    perm = torch.empty(S, dtype=torch.int32, device=demand.device)
+    if want_out and out is None:
+        out = empty_demand(n, S, demand.device)
+    ws = workspace(int(_lib.spdp_order_workspace_bytes(S)), demand.device, tag="order")
+    _check(_lib.spdp_order_scenarios(_dev_ptr(demand, "demand"), ld, n, S, _dev_ptr(out, "out") if want_out else None,
+                                     out.shape[1] if want_out else 0, _dev_ptr(perm, "perm"), _dev_ptr(ws, "ws"),
+                                     ws.numel(), _stream(demand.device)), "spdp_order_scenarios")
+    if want_out:
+        out._spdp_S = int(S)
+    return (out if want_out else None), perm
 
 
 # ------------------------------------------------------------------ a3 / a4

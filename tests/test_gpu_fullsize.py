@@ -44,6 +44,15 @@ def test_c2_full_all_costs_and_saa(spdp):
         est = spdp.saa_mean(part)
         assert est["m"] == S and est["mean"] == w["mean"]
         assert abs(est["var"] - w["var"]) <= 1e-12 * w["var"]
+    # bench.py's default step: the set ordered by total demand, the ordered launch configuration
+    dO, perm = spdp.order_scenarios(d, S=S)
+    p = perm.cpu().numpy()
+    assert np.array_equal(np.sort(p), np.arange(S))
+    cost, part = spdp.split_eval(tour, dist, dO, inst["Q"], S=S, window_hint=bench_config.HINT["C2"],
+                                 mean_window=bench_config.MEAN_ORDERED["C2"])
+    assert np.array_equal(cost.cpu().numpy().astype(np.int64), np.asarray(want)[p])
+    est = spdp.saa_mean(part)
+    assert est["m"] == S and est["mean"] == w["mean"]
 
 
 @pytest.mark.parametrize("name", ["C3", "C4"])
