@@ -156,6 +156,14 @@ SPDP_API void spdp_set_profile_events(void* start_event, void* stop_event);
  * reports (bench.py's roofline line); never needed for correctness. */
 SPDP_API const char* spdp_last_kernel(void);
 
+/* Debug timeline of the packed-u16 sweep (measurement only): with a non-NULL
+ * DEVICE pointer to a zeroed u64 buffer, every later split_sweep_u16_kernel appends, per tile
+ * and consumer warp, {sm << 16 | warp slot, tile, start ns, end ns} (global timer) as 4 u64
+ * after a u64 record counter at [0] (records start at [2]); the caller sizes the buffer
+ * (2 + 4 x tiles x 4 u64).  NULL switches it off.  Process-wide; returns SPDP_E_CUDA on a
+ * failed symbol copy. */
+SPDP_API spdp_status spdp_debug_timeline(void* buffer);
+
 /* Workspace bytes needed by spdp_split_eval / spdp_split_eval_batch for T tours
  * of n customers over S scenarios (T = 1 for spdp_split_eval). */
 SPDP_API size_t spdp_workspace_bytes(int32_t n, int64_t S, int32_t T);

@@ -9,6 +9,7 @@
 #include <tuple>
 
 #include "common.cuh"
+#include "split_ws.cuh"
 
 namespace spdp {
 
@@ -116,6 +117,8 @@ extern "C" void spdp_set_profile_events(void* start_event, void* stop_event) {
 extern "C" const char* spdp_last_error(void) { return g_err; }
 
 extern "C" const char* spdp_last_kernel(void) { return g_kernel; }
+
+extern "C" spdp_status spdp_debug_timeline(void* buffer) { return spdp::debug_timeline(buffer); }
 
 // a6 finalize.  Exact integer moments, one rounding
 // per reported statistic: mean = sum / m, var = (m sumsq - sum^2) / (m (m-1)).

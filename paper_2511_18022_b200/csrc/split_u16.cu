@@ -59,6 +59,30 @@ constexpr int kU16Threads = 32 * (kU16Cons + 1);  // + 1 producer warp
 constexpr int kU16Box = kU16Cons * 64;            // columns of one TMA box (256 scenarios, 512 B per row)
 constexpr uint32_t kGuard = 0x80008000u;
 
+// Debug timeline (spdp_debug_timeline): when set, lane 0 of every consumer warp appends one record
+// per tile {sm << 16 | warp slot, tile id, start ns, end ns} (global timer) after a u64 counter.
+__device__ unsigned long long* g_timeline = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
+// one record {sm << 16 | warp slot, tile (or 0xfffffff0 CTA start / 0xfffffff1 warp done), t0, now}
+__device__ __forceinline__ void tl_record(unsigned slot, unsigned tile, unsigned long long t0) {
+    const unsigned long long k = atomicAdd(g_timeline, 1ull);
+    unsigned long long* r = g_timeline + 2 + 4 * k;
+    r[0] = ((unsigned long long)smid() << 16) | slot;
+    r[1] = tile;
+    r[2] = t0;
+    r[3] = gtimer();
+}
+static bool g_tl_on = false;  // host: a timeline buffer is set (launch the TL instantiation)
+
 // NP = scenario pairs per lane (64 NP scenarios per consumer warp, NP TMA boxes per row and tile;
 // shared memory per stage: [NP boxes][W rows][256 scenarios] u16, then the W Cg pairs, the header)
 template <int W, int NP, int NST>
@@ -97,6 +121,23 @@ __device__ __forceinline__ uint32_t key_of(uint32_t G, uint32_t d) {
     return k;
 }
 
+// Claim order of a tour's scenario blocks (longest first): spdp_order_scenarios sorts each segment of
+// kOrderSeg scenarios by increasing total demand, i.e. decreasing window length and tile time, so
+// block-claim k takes position p = k / nseg of segment k % nseg: every segment's slowest tiles are
+// claimed first and the persistent schedule ends on the fastest (a ragged last segment of r tiles
+// takes part in the first r positions).  A permutation of 0 .. nb - 1 for any nb; on an unordered
+// set it only changes which CTA takes which tile.
+constexpr uint32_t kOrderSeg = 65536;  // = order.cu kOrdSeg
+__device__ __forceinline__ uint32_t lpt_block(uint32_t k, uint32_t nb, int tile) {
+    const uint32_t per = kOrderSeg / (uint32_t)tile;   // tiles per segment
+    const uint32_t full = nb / per, rem = nb % per;     // full segments, tiles of the ragged last one
+    const uint32_t nseg = full + (rem != 0u);
+    if (k < rem * nseg) return (k % nseg) * per + k / nseg;
+    if (full == 0u) return k;
+    const uint32_t k2 = k - rem * nseg;
+    return (k2 % full) * per + rem + k2 / full;
+}
+
 // Minimum of N packed u16 pairs with ceil((N - 1) / 2) 3-input mins (VIMNMX3.U16x2).
 template <int N>
 __device__ __forceinline__ uint32_t umin_tree(const uint32_t* v) {
@@ -118,7 +159,8 @@ __device__ __forceinline__ uint32_t umin_tree_from(const uint32_t* v, const int 
 // A0: ages scanned unconditionally (age 1 + A0 - 1 masked candidates); then groups of UG ages,
 // each behind a warp vote on its youngest age; the scan of age W also tests for ring overflow.
 // NP: scenario pairs per lane (independent DP chains; one vote and one range check serve all).
-template <int W, int A0, int UG, int NP, int NST, int LS>
+// TL: the debug-timeline instantiation (spdp_debug_timeline; never the production launch).
+template <int W, int A0, int UG, int NP, int NST, int LS, bool TL = false>
 __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::kMaxReg))
     split_sweep_u16_kernel(const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ trows,
                            const int32_t* __restrict__ cgs, const int32_t* __restrict__ g0s,
@@ -142,6 +184,9 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
         fence_mbar_init();
     }
     __syncthreads();
+    if constexpr (TL) {
+        if (tid == 0) tl_record(blockIdx.x * kU16Cons, 0xfffffff0u, gtimer());  // CTA start
+    }
     pdl_wait();  // tables, counters and partial slots come from tour_prep_kernel
 
     // (a vote, not a plain branch on wid: the compiler then knows each role runs whole warps, and the
@@ -164,7 +209,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
                     id = __shfl_sync(kFull, id, 0);
                 }
                 t = id < ntiles ? (int)(id / ntile_s) : -1;
-                b = id < ntiles ? (int)(id - (uint32_t)t * ntile_s) : 0;
+                b = id < ntiles ? (int)lpt_block(id - (uint32_t)t * ntile_s, ntile_s, Cfg::kTile) : 0;
                 trow = reinterpret_cast<const int4*>(trows + (int64_t)(t < 0 ? 0 : t) * trow_stride(n));
                 c = 0;
             }
@@ -258,6 +303,8 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
         if (__all_sync(kFull, th.x < 0)) break;  // (a vote: keeps the warp provably converged)
         const int t = th.x;
         const int64_t s0 = (int64_t)th.y * Cfg::kTile + wid * Cfg::kWarp;  // this warp's 64 NP scenarios
+        unsigned long long tl0 = 0ull;
+        if constexpr (TL) tl0 = gtimer();
         if (__any_sync(kFull, t != acc_t)) {  // a new tour: flush its predecessor's SAA sums, load its constants
             if (slots) flush();
             acc_t = t;
@@ -463,6 +510,9 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
             sb = smem_raw + (size_t)cs * Cfg::kStageBytes;
             mbar_wait_warp(&full[cs], cr & 1u);
         }
+        if constexpr (TL) {
+            if (lane == 0) tl_record(blockIdx.x * kU16Cons + wid, (unsigned)th.y, tl0);
+        }
         const bool ok = tc->ok != 0;
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
@@ -502,7 +552,16 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
         }
     }
     if (slots) flush();
+    if constexpr (TL) {
+        if (lane == 0) tl_record(blockIdx.x * kU16Cons + wid, 0xfffffff1u, gtimer());  // warp done
+    }
     }  // (no early return in either role: the compiler keeps each warp provably converged)
+}
+
+spdp_status debug_timeline(void* p) {
+    unsigned long long* q = static_cast<unsigned long long*>(p);
+    g_tl_on = q != nullptr;
+    return cuda_check(cudaMemcpyToSymbol(g_timeline, &q, sizeof(q)), "spdp_debug_timeline");
 }
 
 bool u16_loads_ok(int n, uint32_t Q) {
@@ -531,11 +590,14 @@ spdp_status make_demand_map(CUtensorMap* map, const uint16_t* demand, int64_t ld
     return SPDP_OK;
 }
 
-template <int W, int A0, int UG, int LS>
+template <int W, int A0, int UG, int LS, bool TL = false>
 static spdp_status launch_u16_t(cudaStream_t st, const SweepArgs& a) {
     constexpr int NP = 1, NST = 3;
+    if constexpr (!TL && W == 20 && A0 == 6) {
+        if (g_tl_on) return launch_u16_t<W, A0, UG, LS, true>(st, a);  // (C2's ordered-set variant only)
+    }
     using Cfg = U16Cfg<W, NP, NST>;
-    auto kern = split_sweep_u16_kernel<W, A0, UG, NP, NST, LS>;
+    auto kern = split_sweep_u16_kernel<W, A0, UG, NP, NST, LS, TL>;
     int blocks_per_sm = 1;
     if (spdp_status e = kernel_setup((const void*)kern, (int)Cfg::kSmem, 100, kU16Threads, Cfg::kSmem, &blocks_per_sm,
                                      "split_sweep_u16 setup"))

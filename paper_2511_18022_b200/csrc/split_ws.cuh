@@ -83,6 +83,7 @@ struct SweepArgs {
 // range check (host side); launch_sweep_u16: W in {16, 20, 24, 32}, mean_w picks the grouping.
 bool u16_loads_ok(int n, uint32_t Q);
 spdp_status launch_sweep_u16(int W, int mean_w, cudaStream_t st, const SweepArgs& a);
+spdp_status debug_timeline(void* p);  // spdp_debug_timeline
 
 // Host launchers (split.cu).
 // tour_prep_kernel over T tours into the workspace (tables, g0, row pointers, Cg
