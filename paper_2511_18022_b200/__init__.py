@@ -42,7 +42,7 @@ SYMBOLS = (
     "spdp_version", "spdp_last_error", "spdp_workspace_bytes", "spdp_gen_demands", "spdp_demand_prefix",
     "spdp_split_mask", "spdp_split_eval", "spdp_split_eval_batch", "spdp_saa_reduce", "spdp_saa_mean",
     "spdp_host_workspace_bytes", "spdp_split_eval_host", "spdp_irp_workspace_bytes", "spdp_irp_dp",
-    "spdp_set_profile_events", "spdp_last_kernel", "spdp_routes_workspace_bytes", "spdp_split_routes",
+    "spdp_set_profile_events", "spdp_last_kernel", "spdp_debug_timeline", "spdp_routes_workspace_bytes", "spdp_split_routes",
     "spdp_split_eval_penalized", "spdp_values_workspace_bytes", "spdp_split_values",
     "spdp_neighbour_workspace_bytes", "spdp_split_eval_neighbours", "spdp_limits_workspace_bytes",
     "spdp_split_eval_limits", "spdp_f32_workspace_bytes", "spdp_split_eval_f32", "spdp_saa_estimate_f32",
@@ -83,6 +83,8 @@ def _sig():
     L.spdp_set_profile_events.restype = None
     L.spdp_last_error.restype = ctypes.c_char_p
     L.spdp_last_kernel.restype = ctypes.c_char_p
+    L.spdp_debug_timeline.argtypes = [ctypes.c_void_p]
+    L.spdp_debug_timeline.restype = ctypes.c_int
     L.spdp_workspace_bytes.argtypes = [i32, i64, i32]
     L.spdp_workspace_bytes.restype = sz
     L.spdp_host_workspace_bytes.argtypes = [i32, i64]
@@ -162,6 +164,12 @@ def set_profile_events(start=None, stop=None):
 def last_kernel() -> str:
     """Name of the sweep kernel the last split call on this thread enqueued (spdp_last_kernel)."""
     return _lib.spdp_last_kernel().decode()
+
+
+def debug_timeline(buf=None):
+    """Debug timeline of the u16 sweep (spdp_debug_timeline): a zeroed int64 CUDA tensor receives
+    per-tile records from later sweeps; None switches it off.  Measurement only."""
+    _check(_lib.spdp_debug_timeline(ctypes.c_void_p(0 if buf is None else buf.data_ptr())), "spdp_debug_timeline")
 
 
 def version() -> int:

@@ -4,7 +4,6 @@ SM-time in the tail.  Also times the sweep alone (profile events) at several S.
 
     python scripts/tail_probe.py [S,...] [natural|ordered]
 """
-import ctypes
 import os
 import statistics
 import sys
@@ -21,9 +20,6 @@ import synth
 dev = torch.device("cuda", 0)
 Ss = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1000000]
 order = sys.argv[2] if len(sys.argv) > 2 else "ordered"
-lib = spdp.lib()
-lib.spdp_debug_timeline.argtypes = [ctypes.c_void_p]
-lib.spdp_debug_timeline.restype = ctypes.c_int
 for S in Ss:
     cfg = synth.config_instance("C2", S=S)
     inst = cfg["inst"]
@@ -57,7 +53,7 @@ for S in Ss:
         S, order, spdp.last_kernel(), 1e3 * statistics.median(ms), 1e3 * statistics.mean(ms), 1e3 * min(ms)), flush=True)
     ntiles = (S + 255) // 256
     buf = torch.zeros(2 + 4 * (ntiles * 4 + 8 * 600), dtype=torch.int64, device=dev)
-    assert lib.spdp_debug_timeline(ctypes.c_void_p(buf.data_ptr())) == 0
+    spdp.debug_timeline(buf)
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st.record()
     en.record()
@@ -65,7 +61,7 @@ for S in Ss:
     run()
     spdp.set_profile_events()
     torch.cuda.synchronize()
-    assert lib.spdp_debug_timeline(ctypes.c_void_p(0)) == 0
+    spdp.debug_timeline()
     run()
     torch.cuda.synchronize()
     nrec = int(buf[0].item())
