@@ -212,86 +212,180 @@ __global__ void __launch_bounds__(256) irp_lane_kernel(const uint8_t* __restrict
     }
 }
 
-// Lane-per-scenario variant with a LAZY demand shift (same results as irp_lane_kernel).
-// Step B of a period moves the whole value function by d and adds h J; instead of
-// rewriting the array, V is kept as
-//     V[J] = A[(J + off) mod B] + alpha J + K        (B = U + 1, per lane)
-// and a period without delivery costs O(d) (the V'[0] term) instead of O(U):
-//     V'[J] = V[J + d] + h J  ==>  off += d,  K += alpha d,  alpha += h,
-//     V'[0] = b d + min_{y <= min(d, top)} (V[y] - b y)   written at A[off'] - K'.
-// A period WITH delivery (band [0, y], X >= U) recomputes W[y] = c y + min_{I <= y}
-// (V[I] - c I) over y = 0..U in place and resets alpha = K = 0.  States above `top`
-// are +inf and never read.  Sentinels: an entry whose value is >= 2^29 (no real
-// value is: host check) is unreachable; reads add alpha J + K >= 0 to a stored
-// value <= 2^30, so nothing overflows int32 and an unreachable entry stays >= 2^29.
+// Lane-per-scenario variant with a LAZY demand shift and an AFFINE TAIL (same results as
+// irp_lane_kernel; DESIGN §6 "IRP").  Per (scenario, customer) the value function is kept as
+//     V[J] = A[(J + off) mod B] + alpha J + K     J in [0, E]   (explicit, B = U + 1, per lane)
+//     V[J] = Ta + Ts J                             J in (E, F]   (affine tail)
+//     V[J] = +inf                                  J in (F, U]
+// Step B (demand d) is exact on this form in O(min(d, E)):
+//     V'[J] = V[J + d] + h J  ==>  off += d, K += alpha d, alpha += h; Ta += Ts d, Ts += h;
+//                                  E -= d (>= 0), F -= d (>= E)
+//     V'[0] = b d + min_{y <= min(d, U)} (V[y] - b y): explicit y by a scan, the tail y in
+//             (E, min(d, F)] at its two ends (affine)             written at A[off'] - K'.
+// Step A (delivery, band [0, y]: X >= U) is W[y] = min(W[y - 1] + c, V[y]) (W[-1] = +inf).  The
+// tail always satisfies V[E + 1] >= V[E] + c and has slope Ts >= c (*) (and +inf above F needs no
+// condition), so for y > E the
+// recursion takes W[y - 1] + c every time: W[y] = W[E] + c (y - E) up to U.  A delivery therefore
+// rewrites only the explicit entries (O(E)), then sets Ta = W[E] - c E, Ts = c, F = U,
+// alpha = K = 0.  (*) holds after a delivery with equality and is kept by step B: a shift adds
+// h >= 0 to every difference, and a new V'[0] (the minimum above includes y = min(d, E) or the
+// tail's first point) never exceeds the value it sits next to.  E never grows: it starts at I0
+// (V_0 = [I0]: nothing above is reachable yet) and loses every period's demand, so once a
+// customer's cumulative demand passes I0 its DP is O(1) per period.  Sentinels: values >= 2^29 are unreachable (host check: every real value is
+// below); explicit unreachable entries are stored as 2^30 and reads add alpha J + K < 2^29.
+//
+// Layout: the ring needs only B = I0 + 1 slots (the explicit region never leaves [0, I0]), per warp
+// [Bmax][32] int32 lane-interleaved (conflict-free), then the task's demands [H][32] u16 staged in
+// one burst of coalesced loads (the per-period reads are then shared-memory hits), and the
+// customer's visit pattern as a bit mask built by two ballots (H <= 64; else read per period).
 __global__ void __launch_bounds__(128) irp_lazy_kernel(const uint8_t* __restrict__ visit,
-                                                       const IrpCust* __restrict__ cust, int H, int M, int Umax,
+                                                       const IrpCust* __restrict__ cust, int H, int M, int Bmax,
                                                        const uint16_t* __restrict__ demand, int64_t ld, int64_t S,
                                                        long long* __restrict__ cost) {
     extern __shared__ int32_t vsm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int32_t* A = vsm + (size_t)wid * (Umax + 1) * 32 + lane;  // A[x] at A[x * 32]
+    const size_t dt_words = (size_t)(H + 1) / 2 * 32;  // the demand tile [H][32] u16 (rounded to 2 rows)
+    const size_t warp_words = (size_t)Bmax * 32 + dt_words;
+    int32_t* A = vsm + (size_t)wid * warp_words + lane;  // A[x] at A[x * 32]
+    uint32_t* dtw = reinterpret_cast<uint32_t*>(vsm + (size_t)wid * warp_words + (size_t)Bmax * 32);
     constexpr int32_t kReal = 1 << 29;                        // values >= kReal are unreachable
     const int64_t ntile = (S + 31) / 32;
+    const int64_t ntask = ntile * M;
+    // the demand tile of a task, [H][32] u16, by cp.async (4 B = 2 scenarios per copy; lanes 0-15 row
+    // t, lanes 16-31 row t + 1; columns at or past ld read as zeros): all H / 2 copies of a lane in
+    // flight at once.  (Staging the next task's tile during this one, in a second buffer with a
+    // persistent grid, measured slower: 0.19-0.20 vs 0.18 ms at C5 -- the extra shared memory costs
+    // more resident warps than the hidden latency gains.)
+    auto stage = [&](int64_t task, uint32_t* buf) {
+        const int64_t tl = task / M;
+        const int mm = (int)(task - tl * M);
+        const int64_t col = tl * 32 + 2 * (lane & 15);
+        for (int t = lane >> 4; t < H; t += 2) {
+            const bool in = col < ld;
+            const uint16_t* src = demand + ((int64_t)t * M + mm) * ld + (in ? col : 0);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(buf + t * 16 + (lane & 15))),
+                         "l"(src), "r"(in ? 4 : 0) : "memory");
+        }
+    };
     // one warp task = (32-scenario tile, customer): M times more independent warps than tiles, so
     // the launch fills every SM several times over; the customer costs are summed with atomics
     // into cost[] (zeroed by the host code)
-    for (int64_t task = (int64_t)blockIdx.x * nw + wid; task < ntile * M; task += (int64_t)gridDim.x * nw) {
+    for (int64_t task = (int64_t)blockIdx.x * nw + wid; task < ntask; task += (int64_t)gridDim.x * nw) {
         const int64_t tile = task / M;
         const int m = (int)(task - tile * M);
         const int64_t s0 = tile * 32;
         const bool live = s0 + lane < S;
         const int64_t s = live ? s0 + lane : S - 1;
-        {
-            const IrpCust p = cust[m];
-            const int U = p.U, B = U + 1;
-            for (int y = 0; y <= U; ++y) A[y * 32] = (y == p.I0) ? 0 : kIrpInf;
-            int off = 0, top = U;
-            int32_t alpha = 0, K = 0;
-            int d = demand[(int64_t)m * ld + s];
-            for (int t = 0; t < H; ++t) {
-                const int dn = (t + 1 < H) ? demand[((int64_t)(t + 1) * M + m) * ld + s] : 0;  // prefetch
-                if (visit[(int64_t)m * H + t] != 0 && p.X > 0) {
-                    // delivery: W[y] = c y + min_{I <= y} (V[I] - c I), y = 0..U, in place (warp-uniform branch)
-                    int32_t run = kIrpInf;
-                    int x = off;
-                    for (int y = 0; y <= U; ++y) {
-                        const int32_t v = (y <= top) ? A[x * 32] + alpha * y + K : kIrpInf;
-                        run = min(run, v - p.c * y);
-                        const int32_t w = run + p.c * y;
-                        A[x * 32] = w >= kReal ? kIrpInf : w;
-                        x = (x + 1 == B) ? 0 : x + 1;
-                    }
-                    alpha = 0;
-                    K = 0;
-                    top = U;
-                }
-                // demand d: V'[0] = b d + min_{y <= min(d, top)} (V[y] - b y); V'[J] = V[J + d] + h J
-                int32_t m0 = kIrpInf;
-                const int ylim = d < top ? d : top;
+        const IrpCust p = cust[m];
+        const int U = p.U, B = p.I0 + 1;
+        __syncwarp();  // (the previous task's reads of the tile are done)
+        stage(task, dtw);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        const uint16_t* dt = reinterpret_cast<const uint16_t*>(dtw) + lane;  // dt[t * 32]
+        const bool vis_lo = lane < H && visit[(int64_t)m * H + lane] != 0;
+        const bool vis_hi = lane + 32 < H && visit[(int64_t)m * H + lane + 32] != 0;
+        const unsigned long long vmask =
+            p.X > 0 ? ((unsigned long long)__ballot_sync(kFull, vis_hi) << 32) | __ballot_sync(kFull, vis_lo) : 0ull;
+        // V_0 = [I0]: explicit [0, I0] (+inf below I0), +inf above (no tail: F = E)
+        for (int y = 0; y <= p.I0; ++y) A[y * 32] = (y == p.I0) ? 0 : kIrpInf;
+        int off = 0, E = p.I0, F = p.I0;  // explicit [0, E], affine tail (E, F]
+        int32_t alpha = 0, K = 0, Ta = 0, Ts = 0;
+        int t = 0;
+        for (; t < H; ++t) {
+            if (__all_sync(kFull, E == 0)) break;  // every lane's explicit region is {0}: register loop below
+            const int d = dt[t * 32];
+            const bool deliver = t < 64 ? ((vmask >> t) & 1ull) != 0ull : (p.X > 0 && visit[(int64_t)m * H + t] != 0);
+            if (deliver) {  // (warp-uniform)
+                int32_t R = kIrpInf;
                 int x = off;
-                for (int y = 0; y <= ylim; ++y) {
-                    m0 = min(m0, A[x * 32] + (alpha - p.b) * y + K);
+#pragma unroll 1
+                for (int y = 0; y <= E; ++y) {
+                    R = min(R + p.c, A[x * 32] + alpha * y + K);
+                    A[x * 32] = R >= kReal ? kIrpInf : R;
                     x = (x + 1 == B) ? 0 : x + 1;
                 }
-                const int dd = d < B ? d : B;  // (a shift by >= B leaves only J = 0; K is then relative)
-                K += alpha * dd;
-                alpha += p.h;
-                off += dd;
-                if (off >= B) off -= B;
-                top = top > d ? top - d : 0;
-                const int32_t v0 = (m0 >= kReal) ? kIrpInf : m0 + p.b * d;
-                A[off * 32] = (v0 >= kReal) ? kIrpInf : v0 - K;
-                d = dn;
+                if (E < U && R < kReal) {  // W[y] = W[E] + c (y - E) for y in (E, U]
+                    Ta = R - p.c * E;
+                    Ts = p.c;
+                    F = U;
+                } else {
+                    F = E;  // (no tail: E == U, or nothing reachable)
+                }
+                alpha = 0;
+                K = 0;
             }
-            int32_t best = kIrpInf;
+            // demand d: V'[0] = b d + min_{y <= min(d, U)} (V[y] - b y); V'[J] = V[J + d] + h J
+            int32_t m0 = kIrpInf;
+            const int ylim = d < E ? d : E;
             int x = off;
-            for (int y = 0; y <= top; ++y) {
+#pragma unroll 1
+            for (int y = 0; y <= ylim; ++y) {
+                m0 = min(m0, A[x * 32] + (alpha - p.b) * y + K);
+                x = (x + 1 == B) ? 0 : x + 1;
+            }
+            if (d > E && F > E) {  // the tail's part of the minimum: an affine function, at its ends
+                const int y2 = d < F ? d : F;
+                m0 = min(m0, Ta + (Ts - p.b) * (E + 1));
+                m0 = min(m0, Ta + (Ts - p.b) * y2);
+            }
+            const int dd = d < B ? d : B;  // (a shift by >= B leaves only J = 0; K is then relative)
+            K += alpha * dd;
+            alpha += p.h;
+            off += dd;
+            if (off >= B) off -= B;
+            const int En = d <= E ? E - d : 0;
+            const int Fn = F - d > En ? F - d : En;
+            if (Fn > En) {  // the tail survives the shift (then d < F <= U: no overflow)
+                Ta += Ts * d;
+                Ts += p.h;
+            }
+            E = En;
+            F = Fn;
+            const int32_t v0 = (m0 >= kReal) ? kIrpInf : m0 + p.b * d;
+            A[off * 32] = (v0 >= kReal) ? kIrpInf : v0 - K;
+        }
+        int32_t best = F > E ? Ta + Ts * (E + 1) : kIrpInf;  // (the tail's minimum: slope Ts >= 0)
+        if (t < H) {
+            // collapsed: E == 0 in every lane, so the explicit part is the one value V0 = V[0] (in a
+            // register) and a period is O(1): the same steps as above with E = 0
+            int32_t V0 = A[off * 32] + K;
+            for (; t < H; ++t) {
+                const int d = dt[t * 32];
+                const bool deliver = t < 64 ? ((vmask >> t) & 1ull) != 0ull : (p.X > 0 && visit[(int64_t)m * H + t] != 0);
+                if (deliver) {
+                    if (U > 0 && V0 < kReal) {  // W[y] = V0 + c y
+                        Ta = V0;
+                        Ts = p.c;
+                        F = U;
+                    } else {
+                        F = 0;
+                    }
+                }
+                int32_t m0 = V0;
+                if (d > 0 && F > 0) {
+                    const int y2 = d < F ? d : F;
+                    m0 = min(m0, min(Ta + (Ts - p.b), Ta + (Ts - p.b) * y2));
+                }
+                const int Fn = F - d > 0 ? F - d : 0;
+                if (Fn > 0) {
+                    Ta += Ts * d;
+                    Ts += p.h;
+                }
+                F = Fn;
+                const int32_t v0 = (m0 >= kReal) ? kIrpInf : m0 + p.b * d;
+                V0 = (v0 >= kReal) ? kIrpInf : v0;
+            }
+            best = min(F > 0 ? Ta + Ts : kIrpInf, V0);
+        } else {
+            int x = off;
+            for (int y = 0; y <= E; ++y) {
                 best = min(best, A[x * 32] + alpha * y + K);
                 x = (x + 1 == B) ? 0 : x + 1;
             }
-            if (live) atomicAdd(reinterpret_cast<unsigned long long*>(&cost[s]), (unsigned long long)(long long)best);
         }
+        if (live) atomicAdd(reinterpret_cast<unsigned long long*>(&cost[s]), (unsigned long long)(long long)best);
     }
 }
 
@@ -374,16 +468,20 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     bool prefix_band = true;  // every customer's delivery band is [0, y] (or empty)
     for (int m = 0; m < M; ++m) prefix_band &= (cust_h[m].X == 0 || cust_h[m].X >= cust_h[m].U);
     const size_t lane_smem_warp = sizeof(int32_t) * 32 * (size_t)(Umax + 1);
+    int I0max = 0;
+    for (int m = 0; m < M; ++m) I0max = cust_h[m].I0 > I0max ? cust_h[m].I0 : I0max;
+    const size_t lazy_smem_warp = sizeof(int32_t) * 32 * ((size_t)(I0max + 1) + (size_t)(H + 1) / 2);
     const int irp_mode = (flags & SPDP_F_IRP_EAGER) ? 1 : 0;  // the eager-shift lane kernel instead of the lazy one
-    if (prefix_band && lane_smem_warp <= 48 * 1024 && irp_mode == 0) {
+    if (prefix_band && lazy_smem_warp <= 48 * 1024 && irp_mode == 0) {
         // lazy-shift lane kernel: 4 warps per CTA, several CTAs per SM
+        // one task per warp (the hardware fills SMs as tasks finish; tasks are short and uneven)
         const int warps = 4;
         if ((rc = kernel_setup((const void*)irp_lazy_kernel, 200 * 1024, 100, 0, 0, nullptr, "irp_lazy setup"))) return rc;
         const int64_t ntask = ((S + 31) / 32) * M;
         const int64_t blocks = (ntask + warps - 1) / warps;
         if ((rc = cuda_check(cudaMemsetAsync(c, 0, sizeof(long long) * (size_t)S, st), "cudaMemsetAsync(cost)"))) return rc;
         prof_begin(st);
-        irp_lazy_kernel<<<(unsigned)blocks, warps * 32, lane_smem_warp * warps, st>>>(dvisit, dcust, H, M, Umax, demand,
+        irp_lazy_kernel<<<(unsigned)blocks, warps * 32, lazy_smem_warp * warps, st>>>(dvisit, dcust, H, M, I0max + 1, demand,
                                                                                      ld, S, c);
         rc = last_launch("irp_lazy_kernel");
         set_last_kernel("irp_lazy_kernel");

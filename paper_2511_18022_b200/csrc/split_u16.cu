@@ -625,7 +625,8 @@ static spdp_status launch_u16_ls(int W, int A0, cudaStream_t st, const SweepArgs
         case 16: return A0 <= 6 ? launch_u16_t<16, 6, 2, LS>(st, a) : A0 <= 8 ? launch_u16_t<16, 8, 2, LS>(st, a)
                                                                               : launch_u16_t<16, 10, 2, LS>(st, a);
         case 20:
-            switch (A0 < 6 ? 6 : (A0 > 16 ? 16 : A0)) {
+            switch (A0 < 5 ? 5 : (A0 > 16 ? 16 : A0)) {
+                case 5: return launch_u16_t<20, 5, 2, LS>(st, a);
                 case 6: return launch_u16_t<20, 6, 2, LS>(st, a);
                 case 7: return launch_u16_t<20, 7, 2, LS>(st, a);
                 case 8: return launch_u16_t<20, 8, 2, LS>(st, a);

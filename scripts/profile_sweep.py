@@ -22,6 +22,7 @@ ap.add_argument("--nbr", action="store_true", help="f3: values of tour 0 + neigh
 ap.add_argument("--granular", action="store_true", help="f3 with the granular one-move population")
 ap.add_argument("--limits", action="store_true", help="f4: duration 1.5 x max trip + fleet ceil(sum mu / Q) + 2")
 ap.add_argument("--f32", action="store_true", help="fp32 mode with unrounded Euclidean costs")
+ap.add_argument("--ordered", action="store_true", help="scenario set ordered by total demand (as bench.py)")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 if a.irp:
@@ -34,6 +35,8 @@ else:
     cfg = synth.config_instance(a.config)
     inst = cfg["inst"]
     d = spdp.gen_demands(cfg["model"], 0, cfg["S"], device=dev)
+    if a.ordered:
+        d, _ = spdp.order_scenarios(d, S=cfg["S"])
     tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
     dist = torch.from_numpy(inst["dist"]).to(dev)
     h = a.hint if a.hint is not None else bench_config.HINT[a.config]
@@ -58,9 +61,9 @@ else:
                                        window_hint=h)
         elif cfg["T"] == 1:
             spdp.split_eval(tours[0].contiguous(), dist, d, inst["Q"], S=cfg["S"], window_hint=h,
-                            mean_window=bench_config.MEAN[a.config])
+                            mean_window=(bench_config.MEAN_ORDERED if a.ordered else bench_config.MEAN)[a.config])
         else:
             spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h,
-                                  mean_window=bench_config.MEAN[a.config])
+                                  mean_window=(bench_config.MEAN_ORDERED if a.ordered else bench_config.MEAN)[a.config])
 torch.cuda.synchronize()
 print("done")

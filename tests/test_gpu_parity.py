@@ -285,6 +285,34 @@ def test_irp_lazy_shift_prefix_band(spdp):
         assert part.cpu().numpy()[2] == int(want.sum())
 
 
+def test_irp_affine_tail_stress(spdp):
+    """The affine-tail representation of the lazy kernel (DESIGN §6 IRP): the explicit region
+    shrinks by every period's demand and deliveries extend W affinely above it, so cover slow
+    collapse (demands 0..3: deliveries on a nearly full explicit region), fast collapse (demands
+    around U), zero costs (c = 0, h = 0 or b = 0), c above b, tiny U, I0 at both ends, and dense
+    and sparse visit patterns -- all against the eager oracle DP."""
+    rng = np.random.default_rng(23)
+    for trial in range(40):
+        H, M = int(rng.integers(1, 31)), int(rng.integers(1, 4))
+        visit = (rng.random((M, H)) < [0.1, 0.5, 0.9][trial % 3]).astype(np.uint8)
+        cust = []
+        for _ in range(M):
+            U = int(rng.integers(0, 6)) if trial % 5 == 0 else int(rng.integers(1, 120))
+            X = 0 if rng.random() < 0.1 else int(rng.integers(U, U + 20))
+            I0 = [0, U, int(rng.integers(0, U + 1))][trial % 3]
+            c = 0 if trial % 7 == 0 else int(rng.integers(0, 40))
+            h = 0 if trial % 4 == 1 else int(rng.integers(0, 6))
+            b = 0 if trial % 6 == 2 else int(rng.integers(0, 50))
+            cust.append([U, X, I0, h, b, c])
+        cust = np.array(cust, dtype=np.int32)
+        S = 129
+        hi = [4, 40, 130][trial % 3]
+        dem = rng.integers(0, hi, size=(H * M, 136)).astype(np.uint16)
+        want = oracle.irp(H, M, visit, cust, dem, S=S)
+        cost, _ = spdp.irp_dp(visit, cust, to_dev(dem), H, M, S=S, want_partial=False)
+        assert np.array_equal(cost.cpu().numpy(), want), "trial %d" % trial
+
+
 # ------------------------------------------------------------------ f2 penalized split
 @pytest.mark.parametrize("name,S,lam", [("C1", 100, 5), ("C2", 20_011, 10), ("C2", 3_001, 0), ("C3", 2_003, 50),
                                         ("C2", 2_003, 10 ** 6)])
