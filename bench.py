@@ -750,17 +750,26 @@ def measure_rows(spdp, torch, dev, pk):
     costb = torch.empty(c5["S"], dtype=torch.int64, device=dev)
     fn = lambda: spdp.irp_dp(irp["visit"], irp["cust"], d, irp["H"], irp["M"], S=c5["S"], cost=costb)
     ms = _time_events(fn, torch, dev, iters=3)
-    # roofline: the demand stream (H M u16 per scenario) + the int64 cost; work = the (scenario,
-    # customer, period) DP stages, each over U + 1 inventory states (the lazy kernel shifts instead of
-    # rewriting the state vector on a no-delivery period, so the states are an upper bound of its work)
+    kern_irp = spdp.last_kernel()
+    # the same DP with the other layouts (same results): eager-shift lanes, and state-parallel lanes
+    # (scenario x customer -> warps, inventory state -> lanes: the "3-D" layout)
+    ms_eager = _time_events(lambda: spdp.irp_dp(irp["visit"], irp["cust"], d, irp["H"], irp["M"], S=c5["S"],
+                                                cost=costb, eager=True), torch, dev, iters=3)
+    ms_states = _time_events(lambda: spdp.irp_dp(irp["visit"], irp["cust"], d, irp["H"], irp["M"], S=c5["S"],
+                                                 cost=costb, states=True), torch, dev, iters=3)
+    # roofline: the demand stream (H M u16 per scenario) + the int64 cost.  The affine-tail kernel's
+    # work per (scenario, customer) is O(I0 + H) (DESIGN §6 IRP), not the eager DP's (U + 1) H state
+    # updates (states_per_s: the eager-equivalent rate); it is issue-bound (ncu: IPC 2.7 of 4,
+    # profiles/r02_ncu_irp_C5.json), and hbm_frac shows how far the data stream is from limiting it
     bytes_irp = irp["H"] * irp["M"] * c5["S"] * 2 + c5["S"] * 8
     U = int(irp["cust"][0, 0])
-    rows["a9_a10_irp_C5"] = {"ms": ms, "scenarios_per_s": c5["S"] / (ms / 1e3), "kernel": spdp.last_kernel(),
+    rows["a9_a10_irp_C5"] = {"ms": ms, "scenarios_per_s": c5["S"] / (ms / 1e3), "kernel": kern_irp,
                              "stages_per_s": c5["S"] * irp["M"] * irp["H"] / (ms / 1e3),
-                             "states_per_s": c5["S"] * irp["M"] * irp["H"] * (U + 1) / (ms / 1e3),
+                             "states_per_s_eager_equivalent": c5["S"] * irp["M"] * irp["H"] * (U + 1) / (ms / 1e3),
                              "bytes_alg": bytes_irp, "hbm_frac": bytes_irp / (ms / 1e3) / (pk["hbm_gbs"] * 1e9),
-                             "bound": "alu (issue): 60 MB of demand against ~10^8 state updates; hbm_frac shows "
-                                      "how far the data stream is from limiting it"}
+                             "eager_lane_ms": ms_eager, "state_parallel_ms": ms_states,
+                             "bound": "issue (ALU): O(I0 + H) integer steps per (scenario, customer) after the "
+                                      "affine-tail reformulation; hbm_frac = the demand stream's share"}
     return rows
 
 

@@ -87,6 +87,9 @@ typedef enum {
                                        average more than 40 % of the tour (the measured crossover) */
 #define SPDP_F_IRP_EAGER 65536u    /* spdp_irp_dp: the eager-shift lane kernel instead of the lazily shifted
                                        value functions (same results) */
+#define SPDP_F_IRP_STATES 131072u  /* spdp_irp_dp: the state-parallel kernel (lanes = inventory states, the
+                                       delivery band a warp prefix-min scan; the general kernel for
+                                       0 < X < U) for every band shape (same results) */
 /* bits 8..15 of flags: the expected MEAN window width i - mask(i) (0 = unknown; with
  * window_hint = 0 it is sampled).  A tuning hint like window_hint: it picks how many
  * candidates the sweep evaluates before its first warp vote, never the result. */
@@ -413,7 +416,8 @@ SPDP_API spdp_status spdp_split_eval_host(const int32_t* tour_h, const int32_t* 
  * U <= 1023 and H (c X + h U + b 65535) < 2^29 per customer (else E_RESOURCE).
  * partial (may be NULL): SAA partial of the S costs (DEVICE pointer); needs the sum of those
  * per-customer bounds below 2^31 (cost^2 must fit the summable int64 halves), else E_RESOURCE.
- * flags: SPDP_F_IRP_EAGER selects the eager-shift kernel (same results). */
+ * flags: SPDP_F_IRP_EAGER selects the eager-shift kernel, SPDP_F_IRP_STATES the state-parallel
+ * one (same results; the default for X == 0 or X >= U is the lazy affine-tail lane kernel). */
 SPDP_API size_t spdp_irp_workspace_bytes(int32_t H, int32_t M, int64_t S);
 SPDP_API spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_customer* cust_h, int32_t H, int32_t M,
                         const uint16_t* demand, int64_t ld, int64_t S, int64_t* cost,

@@ -36,6 +36,7 @@ F_NBR_SMEM = 32
 F_NBR_AUTO = 64
 F_SWEEP = {None: 0, "auto": 0, "int": 2, "f32": 4, "deque": 8, "u16": 128}
 F_IRP_EAGER = 65536  # sweep algorithm flags (spdp.h)
+F_IRP_STATES = 131072
 MAX_N = 16384
 
 SYMBOLS = (
@@ -637,9 +638,10 @@ def split_eval_host(tour_h, dist_h, demand_h, Q: int, S: int | None = None, cost
 
 # ------------------------------------------------------------------ a9 + a10
 def irp_dp(visit, cust, demand, H: int, M: int, S: int | None = None, want_partial: bool = True, cost=None,
-           partial=None, eager: bool = False):
+           partial=None, eager: bool = False, states: bool = False):
     """IRP recourse cost per scenario (int64 [S]); visit u8 [M][H] and cust int32 [M][6] on the host.
-    eager: the eager-shift kernel (SPDP_F_IRP_EAGER; same results)."""
+    eager: the eager-shift kernel (SPDP_F_IRP_EAGER); states: the state-parallel kernel
+    (SPDP_F_IRP_STATES); same results."""
     torch = _torch()
     ld = demand.shape[1]
     S = _default_S(demand, S)
@@ -654,6 +656,7 @@ def irp_dp(visit, cust, demand, H: int, M: int, S: int | None = None, want_parti
     ws = workspace(int(_lib.spdp_irp_workspace_bytes(H, M, S)), dev, tag="irp")
     _check(_lib.spdp_irp_dp(visit.ctypes.data_as(ctypes.c_void_p), carr, H, M, _dev_ptr(demand, "demand"), ld, S,
                             _dev_ptr(cost, "cost"), _dev_ptr(partial, "partial") if want_partial else None,
-                            ctypes.c_void_p(ws.data_ptr()), ws.numel(), F_IRP_EAGER if eager else 0, _stream(dev)),
+                            ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                            (F_IRP_EAGER if eager else 0) | (F_IRP_STATES if states else 0), _stream(dev)),
            "spdp_irp_dp")
     return cost, partial

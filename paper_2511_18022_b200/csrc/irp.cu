@@ -472,7 +472,8 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
     for (int m = 0; m < M; ++m) I0max = cust_h[m].I0 > I0max ? cust_h[m].I0 : I0max;
     const size_t lazy_smem_warp = sizeof(int32_t) * 32 * ((size_t)(I0max + 1) + (size_t)(H + 1) / 2);
     const int irp_mode = (flags & SPDP_F_IRP_EAGER) ? 1 : 0;  // the eager-shift lane kernel instead of the lazy one
-    if (prefix_band && lazy_smem_warp <= 48 * 1024 && irp_mode == 0) {
+    const bool states = (flags & SPDP_F_IRP_STATES) != 0;  // force the state-parallel kernel
+    if (prefix_band && lazy_smem_warp <= 48 * 1024 && irp_mode == 0 && !states) {
         // lazy-shift lane kernel: 4 warps per CTA, several CTAs per SM
         // one task per warp (the hardware fills SMs as tasks finish; tasks are short and uneven)
         const int warps = 4;
@@ -486,7 +487,7 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
         rc = last_launch("irp_lazy_kernel");
         set_last_kernel("irp_lazy_kernel");
         prof_end(st);
-    } else if (prefix_band && lane_smem_warp <= 96 * 1024) {
+    } else if (prefix_band && lane_smem_warp <= 96 * 1024 && !states) {
         int warps = (int)((192 * 1024) / lane_smem_warp);
         warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
         if ((rc = kernel_setup((const void*)irp_lane_kernel, 200 * 1024, 100, 0, 0, nullptr, "irp_lane setup"))) return rc;

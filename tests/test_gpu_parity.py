@@ -202,6 +202,34 @@ def test_irp_parity(spdp):
     assert part.cpu().numpy()[2] == int(want.sum())
 
 
+def test_irp_state_parallel_kernel(spdp):
+    """SPDP_F_IRP_STATES (lanes = inventory states, the "3-D" layout): C5's model on a small S, and
+    random prefix-band and general-band customers, against the oracle."""
+    cfg = synth.irp_config(S=301)
+    irp = cfg["irp"]
+    H, M = irp["H"], irp["M"]
+    dem = oracle.gen_demands(cfg["model"], 0, 301, ld=304)
+    want = oracle.irp(H, M, irp["visit"], irp["cust"], dem, S=301)
+    cost, part = spdp.irp_dp(irp["visit"], irp["cust"], to_dev(dem), H, M, S=301, states=True)
+    assert np.array_equal(cost.cpu().numpy(), want)
+    assert part.cpu().numpy()[2] == int(want.sum())
+    rng = np.random.default_rng(31)
+    for trial in range(8):
+        H, M = int(rng.integers(1, 12)), int(rng.integers(1, 4))
+        visit = rng.integers(0, 2, size=(M, H)).astype(np.uint8)
+        cust = []
+        for _ in range(M):
+            U = int(rng.integers(0, 150))
+            X = int(rng.integers(0, U + 5)) if trial % 2 else int(rng.integers(U, U + 5))
+            cust.append([U, X, int(rng.integers(0, U + 1)), int(rng.integers(0, 4)), int(rng.integers(0, 30)),
+                         int(rng.integers(0, 4))])
+        cust = np.array(cust, dtype=np.int32)
+        dem = rng.integers(0, 60, size=(H * M, 72)).astype(np.uint16)
+        want = oracle.irp(H, M, visit, cust, dem, S=67)
+        cost, _ = spdp.irp_dp(visit, cust, to_dev(dem), H, M, S=67, states=True, want_partial=False)
+        assert np.array_equal(cost.cpu().numpy(), want), "trial %d" % trial
+
+
 def test_irp_random_small(spdp):
     rng = np.random.default_rng(4)
     for trial in range(12):
