@@ -20,6 +20,15 @@ import synth
 dev = torch.device("cuda", 0)
 Ss = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1000000]
 order = sys.argv[2] if len(sys.argv) > 2 else "ordered"
+# event overhead of a trivial kernel (the floor of any event-timed launch)
+_x = torch.zeros(1, device=dev)
+_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+for a, b in _ev:
+    a.record()
+    _x.add_(1)
+    b.record()
+torch.cuda.synchronize()
+print("trivial kernel, event-timed: median %.2f us" % (1e3 * statistics.median(a.elapsed_time(b) for a, b in _ev)))
 for S in Ss:
     cfg = synth.config_instance("C2", S=S)
     inst = cfg["inst"]
@@ -81,7 +90,7 @@ for S in Ss:
         rr = r[slot_ == s_]
         rr = rr[np.argsort(rr[:, 2])]
         gaps.extend((rr[1:, 2] - rr[:-1, 3]).tolist())
-    gaps = np.array(gaps)
+    gaps = np.array(gaps if gaps else [0])
     print("  tile-switch gap: median %.2f p90 %.2f us, total %.1f%% of warp time" % (
         np.median(gaps) / 1e3, np.percentile(gaps, 90) / 1e3, 100.0 * gaps.sum() / (r[:, 3] - r[:, 2]).sum()))
     sm = r[:, 0] >> 16
