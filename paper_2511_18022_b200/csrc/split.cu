@@ -1565,7 +1565,7 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
                 mean_w = (int)((wsum + (unsigned long long)h[HDR_SAMPLE_CNT] * n / 2) / ((unsigned long long)h[HDR_SAMPLE_CNT] * n));
         }
     }
-    const SweepArgs args{rowp, tabs, reinterpret_cast<const int32_t*>(w + L.trow), reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
+    const SweepArgs args{tours, rowp, tabs, reinterpret_cast<const int32_t*>(w + L.trow), reinterpret_cast<const int32_t*>(w + L.cgs), g0, tinfo, n, T, demand, ld, S, Qe,
                          cost, partial ? slots : nullptr, ovf, hdr};
     // fp32 sweep when every load value it forms (P' <= (n + W) min(Q, 65535) for feasible scenarios
     // including the padded layers, Y = P' + Q) is an exact float; the per-tour cost range is checked on

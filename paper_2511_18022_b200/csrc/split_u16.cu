@@ -162,7 +162,8 @@ __device__ __forceinline__ uint32_t umin_tree_from(const uint32_t* v, const int 
 // TL: the debug-timeline instantiation (spdp_debug_timeline; never the production launch).
 template <int W, int A0, int UG, int NP, int NST, int LS, bool TL = false>
 __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::kMaxReg))
-    split_sweep_u16_kernel(const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ trows,
+    split_sweep_u16_kernel(const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ tours,
+                           const int32_t* __restrict__ trows,
                            const int32_t* __restrict__ cgs, const int32_t* __restrict__ g0s,
                            const TourInfo* __restrict__ tinfo, int n, int T, int64_t S, uint32_t Q, U16Consts kc,
                            int32_t* __restrict__ cost, spdp_saa_partial* __restrict__ slots,
@@ -187,7 +188,9 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
     if constexpr (TL) {
         if (tid == 0) tl_record(blockIdx.x * kU16Cons, 0xfffffff0u, gtimer());  // CTA start
     }
-    pdl_wait();  // tables, counters and partial slots come from tour_prep_kernel
+    // (tables, counters and partial slots come from tour_prep_kernel: every role waits for it with
+    // pdl_wait() before its first read of them; the demand matrix and the tours are inputs, complete
+    // before tour_prep_kernel -- a plain launch -- started)
 
     // (a vote, not a plain branch on wid: the compiler then knows each role runs whole warps, and the
     // consumers' warp votes need no divergence checks, BRA.DIV)
@@ -201,6 +204,57 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
         int t = -1, b = 0, c = nchunks, st = 0;
         unsigned r = 0u, id = blockIdx.x;
         const int4* trow = nullptr;
+        // Before the wait for tour_prep_kernel (it triggers this launch at its start): the first tile's
+        // first min(NS, nchunks) chunks of demand rows, with the rows read from the tour itself (the
+        // same clamp as the prep's row table), so the first data is in flight while the prep runs;
+        // their Cg copies follow the wait (the stage's barrier expects both).
+        int pre = 0;
+        if (id < ntiles) {
+            t = (int)(id / ntile_s);
+            b = (int)lpt_block(id - (uint32_t)t * ntile_s, ntile_s, Cfg::kTile);
+            pre = nchunks < NS ? nchunks : NS;
+            // lane j loads the tour entries of rows k W + j of the pre chunks (one round trip for all)
+            const int32_t* tr = tours + (int64_t)t * n;
+            int myrow[NS];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                const int i = k * W + lane;
+                const int cst = (lane < W && k < pre && i < n) ? __ldg(tr + i) : 1;
+                myrow[k] = i < n ? (cst < 1 ? 0 : (cst > n ? n - 1 : cst - 1)) : n;
+            }
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                if (k >= pre) break;
+                unsigned char* sb = smem_raw + (size_t)k * Cfg::kStageBytes;
+                if (lane == 0) {
+                    *reinterpret_cast<int4*>(sb + Cfg::kHdrOff) = make_int4(t, b, k, 0);
+                    mbar_arrive_expect_tx(&full[k], (uint32_t)(Cfg::kRowsBytes + W * 4));
+                }
+#pragma unroll
+                for (int g = 0; g < W / 4; ++g) {
+                    const int r0 = __shfl_sync(kFull, myrow[k], 4 * g), r1 = __shfl_sync(kFull, myrow[k], 4 * g + 1);
+                    const int r2 = __shfl_sync(kFull, myrow[k], 4 * g + 2), r3 = __shfl_sync(kFull, myrow[k], 4 * g + 3);
+                    if (lane == 0)
+#pragma unroll
+                        for (int h = 0; h < NP; ++h)
+                            tma_gather4(sb + h * Cfg::kBoxBytes + g * 4 * Cfg::kRowBytes, &dmap, b * Cfg::kTile + h * kU16Box,
+                                        r0, r1, r2, r3, &full[k]);
+                }
+            }
+            __syncwarp();
+        }
+        pdl_wait();
+        if (pre > 0) {
+            if (lane == 0)
+                for (int k = 0; k < pre; ++k)
+                    bulk_g2s_plain(smem_raw + (size_t)k * Cfg::kStageBytes + Cfg::kCgOff,
+                                   cgs + (int64_t)t * kCgPlanes * cgs_stride + 2 * cgs_stride + k * W, W * 4, &full[k]);
+            __syncwarp();
+            trow = reinterpret_cast<const int4*>(trows + (int64_t)t * trow_stride(n));
+            c = pre;
+            st = pre % NS;
+            r = (unsigned)(pre / NS);
+        }
         for (;;) {
             if (r > 0) stage_acquire(st, 32 * (kU16Cons + 1));  // the consumers released the previous use (round r - 1)
             if (c == nchunks) {                           // the next tile
@@ -246,6 +300,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
     } else {
     // ---------------- consumer warp wid ---------------------------------------------------------
     __syncwarp();
+    pdl_wait();
     const int slot = (blockIdx.x * kU16Cons + wid) % kSlots;
     unsigned* ovf_count = hdr + HDR_OVF_COUNT;
     const int rem = n % W;
@@ -611,7 +666,7 @@ static spdp_status launch_u16_t(cudaStream_t st, const SweepArgs& a) {
     const U16Consts kc{0xffffffffu, 1u, (Q + 0x8000u) * 0x10001u, ((0x10000u - (Q + 1u)) & 0xffffu) * 0x10001u,
                        (0x7fffu - pthr) * 0x10001u};
     prof_begin(st);
-    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kU16Threads), Cfg::kSmem, st, map, a.trows,
+    spdp_status rc = cuda_check(launch_pdl(kern, dim3((unsigned)grid), dim3(kU16Threads), Cfg::kSmem, st, map, a.tours, a.trows,
                                            a.cgs, a.g0, a.tinfo, a.n, a.T, a.S, a.Q, kc, a.cost, a.slots, a.ovf, a.hdr),
                                 "split_sweep_u16_kernel");
     set_last_kernel("split_sweep_u16_kernel<%d,%d,%d,%d>", W, A0, UG, LS);

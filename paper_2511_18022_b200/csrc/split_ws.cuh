@@ -63,6 +63,7 @@ enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
 
 // Arguments of the sweep launchers (split.cu, split_u16.cu).
 struct SweepArgs {
+    const int32_t* tours;  // [T][n] (the u16 sweep reads its first tile's rows from it before the PDL wait)
     const uint16_t* const* rowp;
     const int2* tabs;
     const int32_t* trows;
