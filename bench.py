@@ -707,6 +707,7 @@ def measure_rows(spdp, torch, dev, pk):
     cfg2 = synth.config_instance("C2")
     inst2 = cfg2["inst"]
     d = spdp.gen_demands(cfg2["model"], 0, cfg2["S"], device=dev)
+    d, _ = spdp.order_scenarios(d, S=cfg2["S"])  # (the headline's layout of the resident set)
     xy = np.asarray(inst2["coords"], dtype=np.float64)
     distf = torch.from_numpy(np.ascontiguousarray(np.sqrt(((xy[:, None, :] - xy[None, :, :]) ** 2).sum(-1)))).to(dev)
     tour2 = torch.from_numpy(inst2["tour"]).to(dev)
@@ -715,7 +716,7 @@ def measure_rows(spdp, torch, dev, pk):
                       iters=5)
     est = spdp.saa_estimate_f32(costf)
     rows["a5_f32_C2"] = {"ms": ms, "evals_per_s": cfg2["S"] / (ms / 1e3), "kernel": spdp.last_kernel(),
-                         "saa_mean": est["mean"]}
+                         "saa_mean": est["mean"], "scenario_order": "by total demand (as the headline)"}
     del d
     # f2: penalized split at C2 (lambda = 10 cost units per unit of overload, Q of C2)
     cfg2 = synth.config_instance("C2")

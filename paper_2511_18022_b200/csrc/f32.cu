@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "split_ws.cuh"
 #include "tma.cuh"
 
 namespace spdp {
@@ -114,12 +115,13 @@ __global__ void __launch_bounds__(256) split_f32_kernel(const F32Pos* __restrict
 // sweep: the candidates made before the step first, one warp vote per deeper group of ages for all
 // four layers), ages 1..A0 unconditionally; a window that reaches age W lists the scenario for
 // split_f32_kernel.  Measured (C2, 10^6 scenarios): 0.61 ms (the previous one-thread-per-scenario
-// ring with LDG demand loads) -> 0.153 ms.
+// ring with LDG demand loads) -> 0.153 ms; on a set ordered by total demand with longest-first tile
+// claims (lpt_block) and A0 = 6: 0.130 ms (A0 = 5 / 7 / 8: 0.132 / 0.144 / 0.145 ms).
 constexpr int kF32Cons = 4;                      // consumer warps per CTA
 constexpr int kF32Threads = 32 * (kF32Cons + 1);
 constexpr int kF32Tile = 32 * kF32Cons;          // scenarios per tile = TMA box columns
 constexpr int kF32TW = 20;                       // ring width of the TMA sweep
-constexpr int kF32TA0 = 8;                       // unconditional ages
+constexpr int kF32TA0 = 6;                       // unconditional ages
 
 template <int W, int NST>
 struct F32TCfg {
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(kF32Threads) split_f32_tma_kernel(
                     if (lane == 0) id = atomicAdd(count + 1, 1u) + gridDim.x;
                     id = __shfl_sync(kFull, id, 0);
                 }
-                tile = id < ntiles ? (int)id : -1;
+                tile = id < ntiles ? (int)lpt_block(id, ntiles, kF32Tile) : -1;  // (longest first on an ordered set)
                 c = 0;
             }
             unsigned char* sb = smem_raw + (size_t)st * Cfg::kStageBytes;

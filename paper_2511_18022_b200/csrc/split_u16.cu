@@ -121,23 +121,6 @@ __device__ __forceinline__ uint32_t key_of(uint32_t G, uint32_t d) {
     return k;
 }
 
-// Claim order of a tour's scenario blocks (longest first): spdp_order_scenarios sorts each segment of
-// kOrderSeg scenarios by increasing total demand, i.e. decreasing window length and tile time, so
-// block-claim k takes position p = k / nseg of segment k % nseg: every segment's slowest tiles are
-// claimed first and the persistent schedule ends on the fastest (a ragged last segment of r tiles
-// takes part in the first r positions).  A permutation of 0 .. nb - 1 for any nb; on an unordered
-// set it only changes which CTA takes which tile.
-constexpr uint32_t kOrderSeg = 65536;  // = order.cu kOrdSeg
-__device__ __forceinline__ uint32_t lpt_block(uint32_t k, uint32_t nb, int tile) {
-    const uint32_t per = kOrderSeg / (uint32_t)tile;   // tiles per segment
-    const uint32_t full = nb / per, rem = nb % per;     // full segments, tiles of the ragged last one
-    const uint32_t nseg = full + (rem != 0u);
-    if (k < rem * nseg) return (k % nseg) * per + k / nseg;
-    if (full == 0u) return k;
-    const uint32_t k2 = k - rem * nseg;
-    return (k2 % full) * per + rem + k2 / full;
-}
-
 // Minimum of N packed u16 pairs with ceil((N - 1) / 2) 3-input mins (VIMNMX3.U16x2).
 template <int N>
 __device__ __forceinline__ uint32_t umin_tree(const uint32_t* v) {

@@ -61,6 +61,23 @@ inline WsLayout ws_layout(int32_t n, int64_t S, int32_t T) {
 enum { HDR_OVF_COUNT = 0, HDR_STATUS = 1, HDR_SAMPLE_W = 2, HDR_TILE = 3, HDR_SAMPLE_SUM = 4 /* u64 */, HDR_SAMPLE_CNT = 6 };
 enum { ST_NOT_PERM = 1, ST_NEG_DIST = 2, ST_RANGE = 4 };
 
+// Claim order of a tour's scenario blocks (longest first): spdp_order_scenarios sorts each segment of
+// kOrderSeg scenarios by increasing total demand, i.e. decreasing window length and tile time, so
+// block-claim k takes position p = k / nseg of segment k % nseg: every segment's slowest tiles are
+// claimed first and the persistent schedule ends on the fastest (a ragged last segment of r tiles
+// takes part in the first r positions).  A permutation of 0 .. nb - 1 for any nb; on an unordered
+// set it only changes which CTA takes which tile.
+constexpr uint32_t kOrderSeg = 65536;  // = order.cu kOrdSeg (tile must divide it)
+__device__ __forceinline__ uint32_t lpt_block(uint32_t k, uint32_t nb, int tile) {
+    const uint32_t per = kOrderSeg / (uint32_t)tile;   // tiles per segment
+    const uint32_t full = nb / per, rem = nb % per;     // full segments, tiles of the ragged last one
+    const uint32_t nseg = full + (rem != 0u);
+    if (k < rem * nseg) return (k % nseg) * per + k / nseg;
+    if (full == 0u) return k;
+    const uint32_t k2 = k - rem * nseg;
+    return (k2 % full) * per + rem + k2 / full;
+}
+
 // Arguments of the sweep launchers (split.cu, split_u16.cu).
 struct SweepArgs {
     const int32_t* tours;  // [T][n] (the u16 sweep reads its first tile's rows from it before the PDL wait)
