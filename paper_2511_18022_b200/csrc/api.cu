@@ -123,6 +123,7 @@ extern "C" spdp_status spdp_debug_timeline(void* buffer) { return spdp::debug_ti
 // a6 finalize.  Exact integer moments, one rounding
 // per reported statistic: mean = sum / m, var = (m sumsq - sum^2) / (m (m-1)).
 extern "C" spdp_status spdp_saa_mean(const spdp_saa_partial* p, spdp_saa_estimate* out) {
+    NvtxScope nvtx_("spdp_saa_mean");
     if (!p || !out) return fail(SPDP_E_USAGE, "spdp_saa_mean: NULL pointer");
     if (p->n_feas < 0 || p->n_infeas < 0) return fail(SPDP_E_USAGE, "spdp_saa_mean: negative counts");
     out->m = p->n_feas;
@@ -177,6 +178,7 @@ extern "C" spdp_status spdp_split_eval_host(const int32_t* tour_h, const int32_t
                                             const uint16_t* demand_h, int64_t ld_h, int64_t S, int32_t Q,
                                             int32_t* cost_h, spdp_saa_estimate* est_h, int32_t window_hint, void* ws,
                                             size_t ws_bytes, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval_host");
     if (n < 1 || S < 1) return fail(SPDP_E_USAGE, "spdp_split_eval_host: n and S must be >= 1");
     if (!tour_h || !dist_h || !demand_h || !est_h || !ws) return fail(SPDP_E_USAGE, "spdp_split_eval_host: NULL pointer");
     if (ld_h < S) return fail(SPDP_E_USAGE, "spdp_split_eval_host: ld_h < S");

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <utility>
@@ -13,6 +14,15 @@ namespace spdp {
 
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
+
+// NVTX range around every C-ABI entry point (SURVEY §5 tracing: the calls show up by name on an
+// Nsight Systems timeline; header-only NVTX v3, a no-op without an attached tool).
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+    NvtxScope(const NvtxScope&) = delete;
+    NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 // Thread-local error message (spdp_last_error).
 void set_error(const char* fmt, ...);

@@ -28,15 +28,21 @@ struct F32Pos {
 
 constexpr int kF32SmemMaxN = 4095;  // position table in shared memory up to 128 KB
 
+// (also: the TMA sweep's gather rows trow[i] = demand row of tour position i + 1 (i < n), n past the
+// end, for i < len; and the zeroed list counters count[0..1])
 __global__ void __launch_bounds__(256) f32_prep_kernel(const int32_t* __restrict__ tour, int n,
                                                        const double* __restrict__ dist, int64_t ld,
-                                                       F32Pos* __restrict__ tab) {
+                                                       F32Pos* __restrict__ tab, int32_t* __restrict__ trow, int len,
+                                                       unsigned* __restrict__ count) {
     if (blockIdx.x != 0) return;
     const int64_t N1 = (int64_t)n + 1;
     auto node = [&](int i) -> int {  // customer at 0-based position i, clamped to 1..n
         const int c = tour[i];
         return c < 1 ? 1 : (c > n ? n : c);
     };
+    if (threadIdx.x < 2) count[threadIdx.x] = 0u;
+    if (trow)
+        for (int i = threadIdx.x; i < len; i += blockDim.x) trow[i] = i < n ? node(i) - 1 : n;
     // every position's costs in parallel (Dd temporarily holds the arc into position i)
     for (int i = threadIdx.x; i <= n; i += blockDim.x) {
         if (i == 0) {
@@ -67,36 +73,39 @@ __global__ void __launch_bounds__(256) split_f32_kernel(const F32Pos* __restrict
                                                         const unsigned* __restrict__ count) {
     extern __shared__ F32Pos ftab[];
     const F32Pos* tab = tab_g;
+    const int64_t nw = list ? (int64_t)*count : S;
+    if ((int64_t)blockIdx.x * blockDim.x >= nw) return;  // (block-uniform: before the table copy)
     if (table_in_smem) {
         for (int i = threadIdx.x; i <= n; i += blockDim.x) ftab[i] = tab_g[i];
         __syncthreads();
         tab = ftab;
     }
-    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= (list ? (int64_t)*count : S)) return;
-    const int64_t s = list ? list[w] : w;
-    const uint16_t* dcol = demand + s;
-    float* fc = fsc + s;
-    fc[0] = 0.0f;
-    int P = 0, Pm = 0, m = 0;
-    bool bad = false;
-    for (int i = 1; i <= n && !bad; ++i) {
-        const int q = dcol[tab[i].rowoff];
-        if (q > Q) {  // Eq. (2)'s set is empty from here on (DESIGN R4)
-            bad = true;
-            break;
+    // (list mode: a grid of a few CTAs per SM strides over the listed scenarios)
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = list ? list[w] : w;
+        const uint16_t* dcol = demand + s;
+        float* fc = fsc + s;
+        fc[0] = 0.0f;
+        int P = 0, Pm = 0, m = 0;
+        bool bad = false;
+        for (int i = 1; i <= n && !bad; ++i) {
+            const int q = dcol[tab[i].rowoff];
+            if (q > Q) {  // Eq. (2)'s set is empty from here on (DESIGN R4)
+                bad = true;
+                break;
+            }
+            P += q;
+            while (P - Pm > Q) Pm += dcol[tab[++m].rowoff];  // P(m) = sum_{k<=m} q; stops at m <= i-1
+            const double Di = tab[i].Dd, ci0 = tab[i].ci0;
+            float best = INFINITY;
+            for (int p = i - 1; p >= m; --p) {
+                const double t64 = __dadd_rn(__dadd_rn(tab[p + 1].c0, __dsub_rn(Di, tab[p + 1].Dd)), ci0);
+                best = fminf(best, __fadd_rn(fc[(int64_t)p * S], __double2float_rn(t64)));
+            }
+            fc[(int64_t)i * S] = best;
         }
-        P += q;
-        while (P - Pm > Q) Pm += dcol[tab[++m].rowoff];  // P(m) = sum_{k<=m} q; stops at m <= i-1
-        const double Di = tab[i].Dd, ci0 = tab[i].ci0;
-        float best = INFINITY;
-        for (int p = i - 1; p >= m; --p) {
-            const double t64 = __dadd_rn(__dadd_rn(tab[p + 1].c0, __dsub_rn(Di, tab[p + 1].Dd)), ci0);
-            best = fminf(best, __fadd_rn(fc[(int64_t)p * S], __double2float_rn(t64)));
-        }
-        fc[(int64_t)i * S] = best;
+        cost[s] = bad ? INFINITY : fc[(int64_t)n * S];
     }
-    cost[s] = bad ? INFINITY : fc[(int64_t)n * S];
 }
 
 // ---------------------------------------------------------------- the TMA-fed fp32 ring sweep
@@ -150,17 +159,6 @@ __global__ void f32_bandw_kernel(const F32Pos* __restrict__ tab, int n, int W, f
     tb[idx] = v;
 }
 
-// rows of the TMA gathers: trow[i] = demand row of tour position i + 1 (i < n), n past the end
-__global__ void f32_trow_kernel(const int32_t* __restrict__ tour, int n, int len, int32_t* __restrict__ trow) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= len) return;
-    int r = n;
-    if (i < n) {
-        const int c = tour[i];
-        r = (c < 1 ? 1 : (c > n ? n : c)) - 1;
-    }
-    trow[i] = r;
-}
 
 __device__ __forceinline__ uint32_t f32_key(float val, uint32_t d) {
     uint32_t k;
@@ -437,6 +435,7 @@ extern "C" size_t spdp_f32_workspace_bytes(int32_t n, int64_t S) {
 extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* dist, int32_t n, const uint16_t* demand,
                                            int64_t ld, int64_t S, int32_t Q, float* cost, void* ws, size_t ws_bytes,
                                            spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval_f32");
     const char* fn = "spdp_split_eval_f32";
     if (n < 1) return fail(SPDP_E_USAGE, "%s: n=%d < 1", fn, n);
     if (n > SPDP_MAX_N) return fail(SPDP_E_RESOURCE, "%s: n=%d > SPDP_MAX_N=%d", fn, n, SPDP_MAX_N);
@@ -452,10 +451,6 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     int64_t* list = reinterpret_cast<int64_t*>(w + f32_table_bytes(n));
     unsigned* count = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(list) + align_up(sizeof(int64_t) * (size_t)S, 256));
     float* fsc = reinterpret_cast<float*>(w + f32_table_bytes(n) + f32_list_bytes(S));
-    f32_prep_kernel<<<1, 256, 0, st>>>(tour, n, dist, ld, tab);
-    spdp_status rc = last_launch("f32_prep_kernel");
-    if (rc) return rc;
-    if ((rc = cuda_check(cudaMemsetAsync(count, 0, 2 * sizeof(unsigned), st), "cudaMemsetAsync(count)"))) return rc;
     const int Qe = (int)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
     // the TMA sweep keeps Y = P + Q and P(i) - Y in int32: every load it forms (including the padded
     // layers' zero demands) is at most (n + W) min(Q, 65535) (larger demands make the scenario
@@ -464,10 +459,11 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     const bool tma = ((int64_t)n + kF32TW) * qcap + Qe < (1LL << 30);
     int32_t* trow = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(fsc) + align_up(sizeof(float) * (size_t)(n + 1) * (size_t)S, 256));
     float* tbw = reinterpret_cast<float*>(reinterpret_cast<char*>(trow) + f32_trow_bytes(n));
+    f32_prep_kernel<<<1, 256, 0, st>>>(tour, n, dist, ld, tab, tma ? trow : nullptr, f32_tw_chunks(n) * kF32TW + 4,
+                                       count);
+    spdp_status rc = last_launch("f32_prep_kernel");
+    if (rc) return rc;
     if (tma) {
-        const int len = f32_tw_chunks(n) * kF32TW + 4;
-        f32_trow_kernel<<<(unsigned)ceil_div(len, 256), 256, 0, st>>>(tour, n, len, trow);
-        if ((rc = last_launch("f32_trow_kernel"))) return rc;
         const int64_t nbw = (int64_t)(n + 1 + kF32TW) * kF32TW;
         f32_bandw_kernel<<<(unsigned)ceil_div(nbw, 256), 256, 0, st>>>(tab, n, kF32TW, tbw);
         if ((rc = last_launch("f32_bandw_kernel"))) return rc;
@@ -497,7 +493,9 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
     if ((rc = kernel_setup((const void*)split_f32_kernel, (int)(sizeof(F32Pos) * (kF32SmemMaxN + 1)), -1, 0, 0, nullptr,
                            "split_f32_kernel setup")))
         return rc;
-    split_f32_kernel<<<(unsigned)ceil_div(S, 256), 256, tsm ? sizeof(F32Pos) * (size_t)(n + 1) : 0, st>>>(
+    int64_t fgrid = ceil_div(S, 256);
+    if (list && fgrid > 2 * (int64_t)device_sms()) fgrid = 2 * (int64_t)device_sms();  // (strides over the list)
+    split_f32_kernel<<<(unsigned)fgrid, 256, tsm ? sizeof(F32Pos) * (size_t)(n + 1) : 0, st>>>(
         tab, n, demand, S, Qe, fsc, cost, tsm ? 1 : 0, list, count);
     prof_end(st);
     return last_launch("split_f32_kernel");
@@ -506,6 +504,7 @@ extern "C" spdp_status spdp_split_eval_f32(const int32_t* tour, const double* di
 extern "C" spdp_status spdp_split_eval_batch_f32(const int32_t* tours, int32_t T, const double* dist, int32_t n,
                                                  const uint16_t* demand, int64_t ld, int64_t S, int32_t Q, float* cost,
                                                  void* ws, size_t ws_bytes, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval_batch_f32");
     if (T < 1) return fail(SPDP_E_USAGE, "spdp_split_eval_batch_f32: T=%d < 1", T);
     if (!tours || !cost) return fail(SPDP_E_USAGE, "spdp_split_eval_batch_f32: NULL required pointer");
     // the tours one after the other on the stream (the workspace of one tour is reused)
@@ -519,6 +518,7 @@ extern "C" spdp_status spdp_split_eval_batch_f32(const int32_t* tours, int32_t T
 
 extern "C" spdp_status spdp_saa_f32_moments(const float* cost, int64_t S, double center, double* moments,
                                              spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_saa_f32_moments");
     if (!cost || !moments || S < 1) return fail(SPDP_E_USAGE, "spdp_saa_f32_moments: bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
     spdp_status rc = cuda_check(cudaMemsetAsync(moments, 0, 4 * sizeof(double), st), "cudaMemsetAsync(moments)");
@@ -533,6 +533,7 @@ extern "C" spdp_status spdp_saa_f32_moments(const float* cost, int64_t S, double
 // count and mean; with the pass-2 moments (centred on that mean) also the unbiased variance,
 // standard error and 95 % interval (the sample average of the second-stage costs).
 extern "C" spdp_status spdp_saa_finalize_f32(const double* m1, const double* m2, spdp_saa_estimate* out) {
+    NvtxScope nvtx_("spdp_saa_finalize_f32");
     const char* fn = "spdp_saa_finalize_f32";
     if (!m1 || !out) return fail(SPDP_E_USAGE, "%s: NULL pointer", fn);
     if (!(m1[0] >= 0.0) || !(m1[3] >= 0.0)) return fail(SPDP_E_USAGE, "%s: negative counts", fn);
@@ -552,6 +553,7 @@ extern "C" spdp_status spdp_saa_finalize_f32(const double* m1, const double* m2,
 
 extern "C" spdp_status spdp_saa_estimate_f32(const float* cost, int64_t S, spdp_saa_estimate* out, void* ws,
                                              size_t ws_bytes, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_saa_estimate_f32");
     const char* fn = "spdp_saa_estimate_f32";
     if (!cost || !out || !ws || S < 1) return fail(SPDP_E_USAGE, "%s: bad arguments", fn);
     if (ws_bytes < 64) return fail(SPDP_E_USAGE, "%s: workspace < 64 bytes", fn);

@@ -74,6 +74,7 @@ using namespace spdp;
 
 extern "C" spdp_status spdp_gen_demands(const spdp_demand_model* model, int64_t s_begin, int64_t S,
                                         uint16_t* demand, int64_t ld, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_gen_demands");
     if (!model) return fail(SPDP_E_USAGE, "spdp_gen_demands: model is NULL");
     if (model->n < 1) return fail(SPDP_E_USAGE, "spdp_gen_demands: n=%d < 1", model->n);
     if (S < 0 || s_begin < 0) return fail(SPDP_E_USAGE, "spdp_gen_demands: negative S or s_begin");

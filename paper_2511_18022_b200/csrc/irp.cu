@@ -435,6 +435,7 @@ extern "C" spdp_status spdp_irp_dp(const uint8_t* visit_h, const spdp_irp_custom
                                    const uint16_t* demand, int64_t ld, int64_t S, int64_t* cost,
                                    spdp_saa_partial* partial, void* ws, size_t ws_bytes, uint32_t flags,
                                    spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_irp_dp");
     if (H < 1 || M < 1 || S < 1) return fail(SPDP_E_USAGE, "spdp_irp_dp: H, M, S must be >= 1");
     if (!visit_h || !cust_h || !demand || !cost || !ws) return fail(SPDP_E_USAGE, "spdp_irp_dp: NULL pointer");
     if (ld < S) return fail(SPDP_E_USAGE, "spdp_irp_dp: ld < S");

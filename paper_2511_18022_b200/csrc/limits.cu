@@ -670,6 +670,7 @@ extern "C" spdp_status spdp_split_eval_limits(const int32_t* tour, const int32_t
                                               int32_t max_duration, int32_t max_routes, int32_t* cost,
                                               spdp_saa_partial* partial, void* ws, size_t ws_bytes, uint32_t flags,
                                               spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval_limits");
     const char* fn = "spdp_split_eval_limits";
     if (n < 1) return fail(SPDP_E_USAGE, "%s: n=%d < 1", fn, n);
     if (n > SPDP_MAX_N) return fail(SPDP_E_RESOURCE, "%s: n=%d > SPDP_MAX_N=%d", fn, n, SPDP_MAX_N);

@@ -628,6 +628,7 @@ extern "C" size_t spdp_values_workspace_bytes(int32_t n, int64_t S) {
 extern "C" spdp_status spdp_split_values(const int32_t* tour, const int32_t* dist, int32_t n, const uint16_t* demand,
                                          int64_t ld, int64_t S, int32_t Q, int32_t* fwd, int32_t* bwd, void* ws,
                                          size_t ws_bytes, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_values");
     const char* fn = "spdp_split_values";
     spdp_status rc = check_common(fn, n, S, Q, ld, demand);
     if (rc) return rc;
@@ -723,6 +724,7 @@ extern "C" spdp_status spdp_split_eval_neighbours_multi(const int32_t* parents, 
                                                         int64_t ld, int64_t S, int32_t Q, int32_t* cost,
                                                         spdp_saa_partial* partial, int32_t window_hint, void* ws,
                                                         size_t ws_bytes, uint32_t flags, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval_neighbours_multi");
     const char* fn = "spdp_split_eval_neighbours";
     const int32_t* parent = parents;
     if (P < 1) return fail(SPDP_E_USAGE, "%s: P=%d < 1", fn, P);
@@ -796,6 +798,7 @@ extern "C" spdp_status spdp_split_eval_neighbours(const int32_t* parent, const i
                                                   const uint16_t* demand, int64_t ld, int64_t S, int32_t Q,
                                                   int32_t* cost, spdp_saa_partial* partial, int32_t window_hint,
                                                   void* ws, size_t ws_bytes, uint32_t flags, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval_neighbours");
     return spdp_split_eval_neighbours_multi(parent, 1, nullptr, fwd, bwd, tours, T, dist, n, demand, ld, S, Q, cost,
                                             partial, window_hint, ws, ws_bytes, flags, stream);
 }

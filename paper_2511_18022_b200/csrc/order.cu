@@ -155,6 +155,7 @@ extern "C" size_t spdp_order_workspace_bytes(int64_t S) {
 extern "C" spdp_status spdp_order_scenarios(const uint16_t* demand, int64_t ld, int32_t n, int64_t S, uint16_t* out,
                                             int64_t ld_out, int32_t* perm, void* ws, size_t ws_bytes,
                                             spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_order_scenarios");
     const char* fn = "spdp_order_scenarios";
     if (n < 1 || S < 1) return fail(SPDP_E_USAGE, "%s: n and S must be >= 1", fn);
     if (n > SPDP_MAX_N) return fail(SPDP_E_RESOURCE, "%s: n=%d > SPDP_MAX_N=%d", fn, n, SPDP_MAX_N);

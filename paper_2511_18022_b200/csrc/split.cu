@@ -1672,6 +1672,7 @@ extern "C" spdp_status spdp_split_eval(const int32_t* tour, const int32_t* dist,
                                        int64_t ld, int64_t S, int32_t Q, int32_t* cost, spdp_saa_partial* partial,
                                        int32_t window_hint, void* ws, size_t ws_bytes, uint32_t flags,
                                        spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval");
     return split_common(tour, 1, dist, n, demand, ld, S, Q, cost, partial, window_hint, ws, ws_bytes, flags,
                         (cudaStream_t)stream, "spdp_split_eval");
 }
@@ -1681,6 +1682,7 @@ extern "C" spdp_status spdp_split_eval_penalized(const int32_t* tour, const int3
                                                  int32_t lambda, int32_t* cost, spdp_saa_partial* partial,
                                                  int32_t window_hint, void* ws, size_t ws_bytes, uint32_t flags,
                                                  spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval_penalized");
     if (lambda < 0) return fail(SPDP_E_USAGE, "spdp_split_eval_penalized: lambda=%d < 0", lambda);
     return split_common(tour, 1, dist, n, demand, ld, S, Q, cost, partial, window_hint, ws, ws_bytes, flags,
                         (cudaStream_t)stream, "spdp_split_eval_penalized", lambda);
@@ -1690,6 +1692,7 @@ extern "C" spdp_status spdp_split_eval_batch(const int32_t* tours, int32_t T, co
                                              const uint16_t* demand, int64_t ld, int64_t S, int32_t Q, int32_t* cost,
                                              spdp_saa_partial* partial, int32_t window_hint, void* ws, size_t ws_bytes,
                                              uint32_t flags, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_eval_batch");
     return split_common(tours, T, dist, n, demand, ld, S, Q, cost, partial, window_hint, ws, ws_bytes, flags,
                         (cudaStream_t)stream, "spdp_split_eval_batch");
 }
@@ -1763,6 +1766,7 @@ extern "C" spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dis
                                          int64_t ld, int64_t S, int32_t Q, const int64_t* scen, int32_t K,
                                          int32_t* pred, int32_t* cost, int32_t* nroutes, int32_t* maxload, void* ws,
                                          size_t ws_bytes, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_routes");
     const char* fn = "spdp_split_routes";
     if (n < 1 || S < 1 || Q < 1 || K < 1) return fail(SPDP_E_USAGE, "%s: n, S, Q and K must be >= 1", fn);
     if (n > SPDP_MAX_N) return fail(SPDP_E_RESOURCE, "%s: n=%d > SPDP_MAX_N", fn, n);
@@ -1796,6 +1800,7 @@ extern "C" spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dis
 
 extern "C" spdp_status spdp_demand_prefix(const int32_t* tour, int32_t n, const uint16_t* demand, int64_t ld, int64_t S,
                                           uint32_t* prefix, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_demand_prefix");
     if (n < 1 || S < 1) return fail(SPDP_E_USAGE, "spdp_demand_prefix: n and S must be >= 1");
     if (!tour || !demand || !prefix) return fail(SPDP_E_USAGE, "spdp_demand_prefix: NULL pointer");
     if (ld < S) return fail(SPDP_E_USAGE, "spdp_demand_prefix: ld < S");
@@ -1805,6 +1810,7 @@ extern "C" spdp_status spdp_demand_prefix(const int32_t* tour, int32_t n, const 
 
 extern "C" spdp_status spdp_split_mask(const int32_t* tour, int32_t n, const uint16_t* demand, int64_t ld, int64_t S,
                                        int32_t Q, int32_t* mask, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_split_mask");
     if (n < 1 || S < 1 || Q < 1) return fail(SPDP_E_USAGE, "spdp_split_mask: n, S, Q must be >= 1");
     if (!tour || !demand || !mask) return fail(SPDP_E_USAGE, "spdp_split_mask: NULL pointer");
     if (ld < S) return fail(SPDP_E_USAGE, "spdp_split_mask: ld < S");
@@ -1813,6 +1819,7 @@ extern "C" spdp_status spdp_split_mask(const int32_t* tour, int32_t n, const uin
 }
 
 extern "C" spdp_status spdp_saa_reduce(const int32_t* cost, int64_t S, spdp_saa_partial* partial, spdp_stream_t stream) {
+    NvtxScope nvtx_("spdp_saa_reduce");
     if (S < 0 || !partial || (S > 0 && !cost)) return fail(SPDP_E_USAGE, "spdp_saa_reduce: bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
     spdp_status rc = cuda_check(cudaMemsetAsync(partial, 0, sizeof(spdp_saa_partial), st), "cudaMemsetAsync(partial)");
