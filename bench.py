@@ -638,6 +638,8 @@ def measure_rows(spdp, torch, dev, pk):
     cfg = synth.config_instance("C3")
     inst = cfg["inst"]
     d = spdp.gen_demands(cfg["model"], 0, cfg["S"], device=dev)
+    d, _ = spdp.order_scenarios(d, S=cfg["S"])  # (the scenario set's layout, as in the a8 row: every leg below on it)
+    mw3 = bench_config.MEAN_ORDERED["C3"]
     tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
     parent = tours[0].contiguous()
     dist = torch.from_numpy(inst["dist"]).to(dev)
@@ -664,22 +666,23 @@ def measure_rows(spdp, torch, dev, pk):
                          torch, dev, iters=6)
     kern = spdp.last_kernel()
     ms_bl = _time_events(lambda: spdp.split_eval_batch(ltours, dist, d, inst["Q"], S=cfg["S"], want_cost=False,
-                                                       window_hint=h, mean_window=bench_config.MEAN["C3"]),
+                                                       window_hint=h, mean_window=mw3),
                          torch, dev, iters=6)
     _, lpart = spdp.split_eval_batch(ltours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h)
     # SPDP_F_NBR_AUTO (reads the spans back, one sync): the batched sweep for the C3 population
     ms_auto_c3 = _time_events(lambda: spdp.split_eval_neighbours(parent, fwd, bwd, tours, dist, d, inst["Q"],
                                                                  S=cfg["S"], want_cost=False, partial=part,
                                                                  window_hint=h, auto=True,
-                                                                 mean_window=bench_config.MEAN["C3"]), torch, dev, iters=4)
+                                                                 mean_window=mw3), torch, dev, iters=4)
     ms_auto_gr = _time_events(lambda: spdp.split_eval_neighbours(parent, fwd, bwd, ltours, dist, d, inst["Q"],
                                                                  S=cfg["S"], want_cost=False, partial=part,
                                                                  window_hint=h, auto=True,
-                                                                 mean_window=bench_config.MEAN["C3"]), torch, dev, iters=4)
+                                                                 mean_window=mw3), torch, dev, iters=4)
     rows["f3_neighbours_C3"] = {
         "ms": ms_v + ms_n, "values_ms": ms_v, "neighbours_ms": ms_n, "T": cfg["T"], "S": cfg["S"], "n": cfg["n"],
         "evals_per_s": cfg["T"] * cfg["S"] / ((ms_v + ms_n) / 1e3), "mean_changed_span": span(cfg["tours"]),
         "partials_equal_batch": equal_c3, "kernel": kern, "auto_neighbours_ms": ms_auto_c3,
+        "scenario_order": "by total demand (as the a8 row; values, neighbours and batch all on it)",
         "granular": {"neighbours_ms": ms_nl, "ms": ms_v + ms_nl, "batch_ms": ms_bl, "mean_changed_span": span(lt),
                      "evals_per_s": cfg["T"] * cfg["S"] / ((ms_v + ms_nl) / 1e3), "auto_neighbours_ms": ms_auto_gr,
                      "partials_equal_batch": bool(torch.equal(part, lpart))}}
@@ -701,8 +704,15 @@ def measure_rows(spdp, torch, dev, pk):
         ms = _time_events(fn, torch, dev, iters=3, warm=1)
         f4[tag] = {"ms": ms, "evals_per_s": cfg2["S"] / (ms / 1e3),
                    "infeasible": int(partl[1].item()), "kernel": spdp.last_kernel()}
+    # the same on the scenario set ordered by total demand (the headline's layout): similar vehicle
+    # counts and windows share a warp
+    dO, _ = spdp.order_scenarios(d, S=cfg2["S"])
+    for tag, L, K in (("duration", int(trip * 1.5), 0), ("fleet", -1, kmin + 2), ("both", int(trip * 1.5), kmin + 2)):
+        fn = lambda: spdp.split_eval_limits(tour2, dist2, dO, inst2["Q"], max_duration=L, max_routes=K, S=cfg2["S"],
+                                            cost=costl, partial=partl)
+        f4[tag]["ordered_ms"] = _time_events(fn, torch, dev, iters=3, warm=1)
     rows["f4_limits_C2"] = f4
-    del d
+    del d, dO
     # a5 fp32 mode at C2: real-valued (unrounded Euclidean, fp64) costs, float32 DP (DESIGN R25)
     cfg2 = synth.config_instance("C2")
     inst2 = cfg2["inst"]
@@ -728,9 +738,14 @@ def measure_rows(spdp, torch, dev, pk):
     fn = lambda: spdp.split_eval_penalized(tour2, dist2, d, inst2["Q"], 10, S=cfg2["S"], cost=costp, partial=partp,
                                            window_hint=bench_config.HINT["C2"])
     ms = _time_events(fn, torch, dev, iters=5)
+    kern_f2 = spdp.last_kernel()
+    dO, _ = spdp.order_scenarios(d, S=cfg2["S"])
+    ms_o = _time_events(lambda: spdp.split_eval_penalized(tour2, dist2, dO, inst2["Q"], 10, S=cfg2["S"], cost=costp,
+                                                          partial=partp, window_hint=bench_config.HINT["C2"]),
+                        torch, dev, iters=5)
     rows["f2_penalized_C2"] = {"ms": ms, "lambda": 10, "evals_per_s": cfg2["S"] / (ms / 1e3),
-                               "kernel": spdp.last_kernel()}
-    del d
+                               "kernel": kern_f2, "ordered_ms": ms_o}
+    del d, dO
     # f1: route recovery (spdp_split_routes) for 4096 scenarios of C2 (one thread per scenario)
     cfg2 = synth.config_instance("C2")
     inst2 = cfg2["inst"]
