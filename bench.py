@@ -613,8 +613,8 @@ def measure_rows(spdp, torch, dev, pk):
                                       "its bound is the demand stream (hbm_frac)")
         else:
             row["bound"] = "alu"
-        if cfg["T"] > 1:
-            # the same batch on the scenario set ordered by total demand (spdp_order_scenarios, once per
+        if True:
+            # the same evaluation on the scenario set ordered by total demand (spdp_order_scenarios, once per
             # set: similar windows share a warp); costs are the permuted ones, the SAA partials identical
             dO, perm = spdp.order_scenarios(d, S=cfg["S"])
             order_ms = _time_events(lambda: spdp.order_scenarios(d, S=cfg["S"], out=dO), torch, dev, iters=3)
@@ -623,9 +623,10 @@ def measure_rows(spdp, torch, dev, pk):
             fno = lambda: spdp.split_eval_batch(tours, dist, dO, inst["Q"], S=cfg["S"], want_cost=False, partial=partO,
                                                 window_hint=h, mean_window=mwo)
             mso = _time_events(fno, torch, dev, iters=6)
-            row["natural_order"] = {k: row[k] for k in ("ms", "evals_per_s", "kernel", "alu_frac")}
+            row["natural_order"] = {k: row[k] for k in ("ms", "evals_per_s", "kernel", "alu_frac", "hbm_frac")}
             row.update({"ms": mso, "evals_per_s": cfg["T"] * cfg["S"] / (mso / 1e3), "kernel": spdp.last_kernel(),
                         "alu_frac": cand / (mso / 1e3) / alu_peak,
+                        "hbm_frac": bytes_ / (mso / 1e3) / (pk["hbm_gbs"] * 1e9),
                         "scenario_order": "by total demand (spdp_order_scenarios, %.3f ms once per scenario set; "
                                           "alu_frac_incl_order adds it to this one batch of %d tours)" % (order_ms, cfg["T"]),
                         "order_ms": order_ms, "alu_frac_incl_order": cand / ((mso + order_ms) / 1e3) / alu_peak,
