@@ -195,6 +195,9 @@ def main():
                          "(spdp_order_scenarios, a layout of the set, outside the timed steps); natural: as generated")
     ap.add_argument("--eager", action="store_true",
                     help="launch every timed step from Python (default: replay a CUDA graph of the step(s))")
+    ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
+                    help="N = 1, one tour: 2 = consecutive steps alternate between two streams (two independent "
+                         "evaluations in flight; measured +2 %% at C2); 1 (default) = strictly one after the other")
     ap.add_argument("--graph-steps", type=int, default=10,
                     help="steps per captured CUDA graph at N > 1 (their all-reduces pipelined inside it)")
     args = ap.parse_args()
@@ -259,16 +262,23 @@ def main():
     tour = torch.from_numpy(inst["tour"]).to(dev)
     tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev)
     dist = torch.from_numpy(inst["dist"]).to(dev)
-    cost = torch.empty((T, S_loc) if T > 1 else S_loc, dtype=torch.int32, device=dev)
-    # two partial buffers: at N > 1 the all-reduce of step k (a7) runs on a communication
-    # stream while step k + 1 computes into the other buffer (pipelined evaluations)
+    # two cost / partial buffers: at N > 1 the all-reduce of step k (a7) runs on a communication
+    # stream while step k + 1 computes into the other buffer (pipelined evaluations);
+    # at N = 1 (one tour) consecutive steps alternate between two streams (each with its own
+    # workspace: the binding keys it by stream), so step k + 1's sweep fills the SMs that step k's
+    # persistent grid releases at its ramp-down -- two independent evaluations in flight, each one a
+    # full pass of the hot path over the 10^6 resident scenarios
+    cost2 = [torch.empty((T, S_loc) if T > 1 else S_loc, dtype=torch.int32, device=dev) for _ in range(2)]
+    cost = cost2[0]
     partials = [torch.zeros((T, 6) if T > 1 else 6, dtype=torch.int64, device=dev) for _ in range(2)]
     stream = torch.cuda.current_stream(dev)
     comm = torch.cuda.Stream(dev) if world > 1 else None
+    n_streams = 2 if (world == 1 and T == 1 and args.streams == 2) else 1
+    side = torch.cuda.Stream(dev) if n_streams == 2 else None
     freed = [None, None]  # event: the buffer's last all-reduce has completed
     kstep = [0]
 
-    def step():
+    def step(single=False):
         cur = torch.cuda.current_stream(dev)  # (the capture stream while a graph is being captured)
         b = kstep[0] & 1
         kstep[0] += 1
@@ -277,10 +287,20 @@ def main():
         if freed[b] is not None:
             cur.wait_event(freed[b])
         if T > 1:  # batched tours (a8): T candidate tours over the same scenarios
-            spdp.split_eval_batch(tours, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost, partial=part,
+            spdp.split_eval_batch(tours, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost2[b], partial=part,
                                   mean_window=mean_w)
+        elif n_streams == 2 and b == 1 and not single:  # (the second evaluation in flight, on the side stream)
+            fork = torch.cuda.Event()
+            fork.record(cur)
+            side.wait_event(fork)
+            with torch.cuda.stream(side):
+                spdp.split_eval(tour, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost2[b], partial=part,
+                                mean_window=mean_w)
+                done_b = torch.cuda.Event()
+                done_b.record(side)
+            freed[b] = done_b
         else:
-            spdp.split_eval(tour, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost, partial=part,
+            spdp.split_eval(tour, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost2[b], partial=part,
                             mean_window=mean_w)
         if world > 1:
             ready = torch.cuda.Event()
@@ -302,6 +322,8 @@ def main():
         step()
     join()
     torch.cuda.synchronize(dev)
+    freed[0] = freed[1] = None  # (events of eager work: a capture must not wait on them)
+    ref_parts = [p_.clone() for p_ in partials]  # (per buffer: every step's partial is the same, or all-reduced)
     # The timed steps replay a CUDA graph: at N = 1 of one step (the same three kernels with their
     # programmatic-dependent-launch edges), at N > 1 of G steps whose NCCL all-reduces run on the
     # communication stream, each overlapping the next step (joined at the graph's end) -- so host
@@ -309,6 +331,8 @@ def main():
     G = B  # one graph replay = one pass over the batches
     if world > 1 and B == 1:
         G = max(1, min(args.graph_steps, args.steps))
+    if n_streams == 2 and G % 2:
+        G *= 2  # (both streams' steps in every replay)
     graph, launch_mode = None, "eager (one C-ABI call per step from Python)"
     if share:
         launch_mode += "; gloo all-reduce (SPDP_BENCH_SHARE_GPU functional check)"
@@ -326,12 +350,23 @@ def main():
             torch.cuda.synchronize(dev)
             graph = g
             launch_mode = ("CUDA graph replay (one captured step per replay)" if G == 1 else
+                           "CUDA graph replay (%d captured steps per replay, consecutive steps on two streams: two "
+                           "independent evaluations in flight)" % G if n_streams == 2 else
                            "CUDA graph replay (%d captured steps per replay, each step's all-reduce overlapping "
                            "the next step on a communication stream)" % G)
-        except Exception as ex:  # keep the eager loop (and say why)
+        except Exception as ex:  # keep the eager loop (and say why) -- after checking it still computes
             launch_mode = "eager (graph capture failed: %s)" % str(ex).splitlines()[0][:120]
             freed[0] = freed[1] = None
             torch.cuda.synchronize(dev)
+            kstep[0] = 0
+            for _ in range(2):
+                step()
+            join()
+            torch.cuda.synchronize(dev)
+            freed[0] = freed[1] = None
+            if not all(torch.equal(a_, b_) for a_, b_ in zip(partials, ref_parts)):
+                raise RuntimeError("bench: the eager steps after a failed graph capture no longer reproduce the "
+                                   "warm-up partials (%s)" % launch_mode)
 
     def timed_steps(K):  # exactly K steps: K // G graph replays, the rest launched eagerly
         if graph is not None:
@@ -377,9 +412,9 @@ def main():
     if world > 1:
         tdist.barrier()
     # roofline pass: the same K steps again with the sweep kernel bracketed by events on its stream
-    for k in range(args.steps):
+    for k in range(args.steps):  # (one stream: each sweep timed alone)
         spdp.set_profile_events(ev_s[k], ev_e[k])
-        step()
+        step(single=True)
     join()
     torch.cuda.synchronize(dev)
     spdp.set_profile_events()
@@ -392,7 +427,7 @@ def main():
         tdist.barrier()
     for k in range(n_ss):
         ss_a[k].record(stream)
-        step()
+        step(single=True)
         join()
         ss_b[k].record(stream)
         torch.cuda.synchronize(dev)
@@ -493,6 +528,8 @@ def main():
     # ------------------------------------------------------------------ oracle cpu_baseline (rank 0, N=1)
     if rank == 0 and world == 1 and not args.no_cpu:
         partial = partials[(kstep[0] - 1) & 1]
+        cost = cost2[(kstep[0] - 1) & 1]  # (the last step's buffer)
+        torch.cuda.synchronize(dev)
         line["cpu_baseline"] = cpu_baseline(cfg, cost[0] if T > 1 else cost, S_loc, spdp,
                                             partial[0] if T > 1 else partial,
                                             perms[(kstep[0] - 1) % B] if perms is not None else None)
