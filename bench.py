@@ -272,8 +272,12 @@ def main():
     cost = cost2[0]
     partials = [torch.zeros((T, 6) if T > 1 else 6, dtype=torch.int64, device=dev) for _ in range(2)]
     stream = torch.cuda.current_stream(dev)
-    comm = torch.cuda.Stream(dev) if world > 1 else None
-    n_streams = 2 if (world == 1 and T == 1 and args.streams == 2) else 1
+    # (SPDP_BENCH_FAKE_COMM=1 at N = 1: the N > 1 step structure -- comm stream, double-buffered partials,
+    # G steps per captured graph -- with a capturable stand-in for the all-reduce; a functional check of
+    # the multi-rank capture path on a one-GPU box, its timings mean nothing)
+    fake_comm = world == 1 and os.environ.get("SPDP_BENCH_FAKE_COMM") == "1"
+    comm = torch.cuda.Stream(dev) if (world > 1 or fake_comm) else None
+    n_streams = 2 if (world == 1 and T == 1 and args.streams == 2 and not fake_comm) else 1
     side = torch.cuda.Stream(dev) if n_streams == 2 else None
     freed = [None, None]  # event: the buffer's last all-reduce has completed
     kstep = [0]
@@ -302,12 +306,15 @@ def main():
         else:
             spdp.split_eval(tour, dist, dem, Q, S=S_loc, window_hint=hint, cost=cost2[b], partial=part,
                             mean_window=mean_w)
-        if world > 1:
+        if world > 1 or fake_comm:
             ready = torch.cuda.Event()
             ready.record(cur)
             comm.wait_event(ready)
             with torch.cuda.stream(comm):
-                pdist.allreduce_partials(part)
+                if fake_comm:
+                    part.mul_(1)
+                else:
+                    pdist.allreduce_partials(part)
                 done = torch.cuda.Event()
                 done.record(comm)
             freed[b] = done
@@ -329,7 +336,7 @@ def main():
     # communication stream, each overlapping the next step (joined at the graph's end) -- so host
     # launch overhead (ctypes marshalling, ~tens of us per step in Python) cannot leave the GPU idle.
     G = B  # one graph replay = one pass over the batches
-    if world > 1 and B == 1:
+    if (world > 1 or fake_comm) and B == 1:
         G = max(1, min(args.graph_steps, args.steps))
     if n_streams == 2 and G % 2:
         G *= 2  # (both streams' steps in every replay)
@@ -367,6 +374,9 @@ def main():
             if not all(torch.equal(a_, b_) for a_, b_ in zip(partials, ref_parts)):
                 raise RuntimeError("bench: the eager steps after a failed graph capture no longer reproduce the "
                                    "warm-up partials (%s)" % launch_mode)
+
+    if fake_comm:
+        launch_mode = "SPDP_BENCH_FAKE_COMM functional check (no all-reduce); " + launch_mode
 
     def timed_steps(K):  # exactly K steps: K // G graph replays, the rest launched eagerly
         if graph is not None:
