@@ -832,9 +832,30 @@ def measure_rows(spdp, torch, dev, pk):
                              "states_per_s_eager_equivalent": c5["S"] * irp["M"] * irp["H"] * (U + 1) / (ms / 1e3),
                              "bytes_alg": bytes_irp, "hbm_frac": bytes_irp / (ms / 1e3) / (pk["hbm_gbs"] * 1e9),
                              "eager_lane_ms": ms_eager, "state_parallel_ms": ms_states,
+                             # the eager DP's candidates (band [0, y] on visited periods,
+                             # the demand step's J = 0 minimum), counted exactly from the model, at one
+                             # candidate per ALU lane per clock -- the floor of any eager-DP kernel
+                             "eager_candidates": irp_eager_candidates(irp, c5),
+                             "eager_alu_floor_ms": irp_eager_candidates(irp, c5) / (N_SM * ALU_LANES_PER_SM_CLK *
+                                                                                   pk["sm_max_mhz"] * 1e6) * 1e3,
                              "bound": "issue (ALU): O(I0 + H) integer steps per (scenario, customer) after the "
                                       "affine-tail reformulation; hbm_frac = the demand stream's share"}
     return rows
+
+
+def irp_eager_candidates(irp, c5):
+    """Candidates of the eager IRP DP (SURVEY §8(a9/a10)) over the whole C5 sample, with every state
+    reachable (an upper bound of any state-by-state kernel's work): per (scenario, customer, period),
+    a visited period's band step sum_{y=0..U} (min(y, X) + 1), and the J = 0 step's min(d, U) + 1 --
+    taken at the nominal demand (mu_m) per customer and period (a count of work, not a cost)."""
+    U = int(irp["cust"][0, 0])
+    X = int(irp["cust"][0, 1])
+    band = sum(min(y, X) + 1 for y in range(U + 1))
+    per_sm = 0
+    for m in range(irp["M"]):
+        for t in range(irp["H"]):
+            per_sm += (band if irp["visit"][m, t] else 0) + min(int(irp["mu"][m]), U) + 1
+    return per_sm * c5["S"]
 
 
 def cpu_baseline(cfg, cost_dev, S, spdp, partial_dev, perm_dev=None):
