@@ -834,7 +834,10 @@ __global__ void __launch_bounds__(kSweepThreads, 4)
         uint32_t fy = 0u;          // cached front Y
         auto layer = [&](const uint32_t q, const int cg) {
             qmax = max(qmax, q);
-            const uint32_t Pn = P + q;
+            // (the load advances by min(q, Q): equal for every feasible lane; a lane with q > Q is
+            // infeasible -- qmax tells, its value is discarded -- and the clamp keeps the point just
+            // pushed inside the next window, which ends the front-pop loop below for every lane)
+            const uint32_t Pn = P + min(q, Q);
             const uint32_t ynew = P + Q;
             // push p = L with g(p) = gprev: pop dominated points (g >= gprev) from the back
             for (;;) {
@@ -855,9 +858,11 @@ __global__ void __launch_bounds__(kSweepThreads, 4)
             }
             tl8 += 256u;
             bg = gprev;
-            // pop split points that left the window (Y < P'(L+1)) from the front
+            // pop split points that left the window (Y < P'(L+1)) from the front.  (No size test: the
+            // point just pushed, p = L with Y = P'(L) + Q >= P'(L) + min(q, Q) = P'(L+1), stays in
+            // the window, so it stops the loop.)
             for (;;) {
-                const bool pop = tl8 - hd8 > 256u && fy < Pn;
+                const bool pop = fy < Pn;
                 if (!__any_sync(kFull, pop)) break;
                 const uint32_t nhd = hd8 + (pop ? 256u : 0u);
                 const int2 e = lds_s32x2(dqa + (nhd & kMask));
