@@ -1762,6 +1762,93 @@ __global__ void __launch_bounds__(128) split_routes_kernel(const int2* __restric
     }
 }
 
+// f1 with a warp per scenario (n <= kRoutesWarpMaxN): the prefix loads by a warp scan, the window's
+// lower end by a ballot over 32 positions at a time, the window minimum by two warp reductions
+// (REDUX: the smallest g, then the largest p holding it -- ties go to the largest p, as in the
+// thread-per-scenario kernel above); P and g in shared memory.  Same results.
+constexpr int kRoutesWarpMaxN = 1024;
+__global__ void __launch_bounds__(128) split_routes_warp_kernel(const int2* __restrict__ tab, const int32_t* __restrict__ g0s,
+                                                                int n, const uint16_t* __restrict__ demand, int64_t ld,
+                                                                int64_t S, uint32_t Q, const int64_t* __restrict__ scen,
+                                                                int K, int32_t* __restrict__ pred, int32_t* __restrict__ cost,
+                                                                int32_t* __restrict__ nroutes, int32_t* __restrict__ maxload) {
+    extern __shared__ uint32_t rsm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int k = blockIdx.x * (blockDim.x >> 5) + wid;
+    if (k >= K) return;  // (warp-uniform)
+    const int N1 = n + 1;
+    uint32_t* P = rsm + (size_t)wid * 2 * N1;
+    int32_t* G = reinterpret_cast<int32_t*>(P + N1);
+    int64_t s = scen[k];
+    s = s < 0 ? 0 : (s >= S ? S - 1 : s);  // (the host checks the range; clamp keeps reads in bounds)
+    int32_t* pr = pred + (int64_t)k * N1;
+    uint32_t carry = 0u;  // tour-order prefix, 32 positions per step
+    for (int b = 0; b < n; b += 32) {
+        const int i = b + lane;
+        uint32_t q = i < n ? (uint32_t)demand[(int64_t)tab[i].x * ld + s] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(kFull, q, o);
+            if (lane >= o) q += u;
+        }
+        if (i < n) P[i + 1] = carry + q;
+        carry += __shfl_sync(kFull, q, 31);
+    }
+    if (lane == 0) {
+        P[0] = 0u;
+        G[0] = g0s[0];
+        pr[0] = -1;
+    }
+    __syncwarp();
+    int m = 0;
+    for (int L = 0; L < n; ++L) {
+        const uint32_t Pn = P[L + 1];
+        for (;;) {  // mask(L+1): the first p >= m with Pn - P[p] <= Q (monotone in p), L + 1 if none
+            const int p = m + lane;
+            const bool stop = p > L || Pn - P[p] <= Q;
+            const unsigned bal = __ballot_sync(kFull, stop);
+            if (bal) {
+                m += __ffs(bal) - 1;
+                break;
+            }
+            m += 32;
+        }
+        unsigned best = 0xffffffffu;  // g ^ 0x80000000 (order-preserving); INT_MAX maps to 0xffffffff: unreachable
+        int arg = -1;
+        for (int p0 = m; p0 <= L; p0 += 32) {
+            const int p = p0 + lane;
+            const unsigned key = (unsigned)(p <= L ? G[p] : INT_MAX) ^ 0x80000000u;
+            const unsigned mn = __reduce_min_sync(kFull, key);
+            const unsigned pm = __reduce_max_sync(kFull, key == mn ? (unsigned)(p + 1) : 0u);
+            if (mn != 0xffffffffu && mn <= best) {  // (a later chunk holds larger p: ties go there)
+                best = mn;
+                arg = (int)pm - 1;
+            }
+        }
+        if (lane == 0) {
+            G[L + 1] = (arg < 0) ? INT_MAX : (int32_t)(best ^ 0x80000000u) + tab[L].y;  // tab[n-1].y = B[n]: G[n] = f(n)
+            pr[L + 1] = arg;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        const int f = G[n];
+        cost[k] = (f == INT_MAX) ? SPDP_INFEASIBLE : f;
+        if (nroutes || maxload) {
+            int r = 0;
+            uint32_t ml = 0u;
+            if (f != INT_MAX) {
+                for (int i = n; i > 0; i = pr[i]) {  // walk the optimal routes back from n
+                    ++r;
+                    ml = max(ml, P[i] - P[pr[i]]);
+                }
+            }
+            if (nroutes) nroutes[k] = r;
+            if (maxload) maxload[k] = (int32_t)ml;
+        }
+    }
+}
+
 extern "C" size_t spdp_routes_workspace_bytes(int32_t n, int32_t K) {
     if (n < 1 || K < 1) return 0;
     return ws_layout(n, 1, 1).total + align_up(sizeof(uint32_t) * 2 * (size_t)K * (size_t)(n + 1), 256);
@@ -1798,8 +1885,20 @@ extern "C" spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dis
                                                    reinterpret_cast<int32_t*>(w + L.trow), nullptr, hdr, nullptr, 0);
         if ((rc = last_launch("tour_prep_kernel"))) return rc;
     }
+    if (n <= kRoutesWarpMaxN) {  // a warp per scenario, its P and g in shared memory
+        const size_t smem = sizeof(uint32_t) * 2 * (size_t)(n + 1) * 4;
+        prof_begin(st);
+        split_routes_warp_kernel<<<(unsigned)ceil_div(K, 4), 128, smem, st>>>(tabs, g0, n, demand, ld, S, Qe, scen, K,
+                                                                             pred, cost, nroutes, maxload);
+        prof_end(st);
+        set_last_kernel("split_routes_warp_kernel");
+        return last_launch("split_routes_warp_kernel");
+    }
+    prof_begin(st);
     split_routes_kernel<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(tabs, g0, n, demand, ld, S, Qe, scen, K, pred, cost,
                                                                    nroutes, maxload, Pw, Gw);
+    prof_end(st);
+    set_last_kernel("split_routes_kernel");
     return last_launch("split_routes_kernel");
 }
 

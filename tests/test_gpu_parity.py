@@ -278,6 +278,25 @@ def test_split_routes_pred_exact(spdp, name, S):
         assert rc == cost[k]
 
 
+def test_split_routes_large_n_thread_kernel(spdp):
+    """n above the warp kernel's shared-memory limit (1024): the thread-per-scenario route kernel;
+    pred bit-exact against the oracle (ties -> largest p), route count and max load consistent."""
+    inst = synth.make_instance(1100, 77, r=6.0)
+    model = synth.demand_model(inst["nominal"], inst["Q"], seed=0x5EED00AA)
+    S = 96
+    dem = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
+    scen = np.array([0, 5, 17, 42, 95], dtype=np.int64)
+    want_cost, want_pred = oracle.split(inst["tour"], inst["dist"], dem, inst["Q"], want_pred=True, S=S)
+    cost, pred, nr, ml = spdp.split_routes(to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem), inst["Q"],
+                                           torch.from_numpy(scen).cuda(), S=S)
+    assert np.array_equal(cost.cpu().numpy().astype(np.int64), oracle_cost_as_i32(want_cost[scen]))
+    assert np.array_equal(pred.cpu().numpy(), want_pred[scen])
+    for k, s_ in enumerate(scen):
+        routes = oracle.routes_from_pred(pred.cpu().numpy()[k], inst["tour"])
+        assert len(routes) == int(nr[k].item())
+        assert max(sum(int(dem[c - 1, s_]) for c in r) for r in routes) == int(ml[k].item())
+
+
 def test_split_routes_infeasible(spdp):
     inst = synth.make_instance(6, seed=3)
     Q = inst["Q"]
