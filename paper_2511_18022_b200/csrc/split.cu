@@ -28,6 +28,12 @@
 namespace spdp {
 
 // ---------------------------------------------------------------- a2: tour prep
+// dynamic shared memory of tour_prep_kernel: 37 long longs (warp sums, D[n], block max, ext[5]),
+// the validation bitmap, the Cg of every position
+static inline size_t tour_prep_smem(int n) {
+    return 37 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1) + sizeof(int) * (size_t)n;
+}
+
 // One CTA per tour.  tab[i] = {row of customer s_{i+1}, Cg[i]} (0-based layer i
 // computes f(i+1)); tab[n-1].y = B[n].  g0[t] = c_{0,s_1}.  D is a block scan.
 // Also zeroes the tour's SAA partial and the overflow counter.
@@ -45,9 +51,10 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     long long* dn = wsum + 32;                                             // D[n]
     int* cmx = reinterpret_cast<int*>(dn + 1);                             // block max of the used costs
     // ext: [0] NS = sum of max(0, -Cg), [1] max(0, max Cg), [2] the largest sum of max(0, Cg) over
-    // kU16Check consecutive layers, [3] B[n] (the packed-u16 sweep's range constants, TourInfo)
+    // kU16Check consecutive layers, [3] B[n] (the packed-u16 sweep's range constants, TourInfo), [4] g0
     int* ext = reinterpret_cast<int*>(smem_raw + 34 * sizeof(long long));
-    unsigned* seen = reinterpret_cast<unsigned*>(smem_raw + 36 * sizeof(long long));  // bitmap
+    unsigned* seen = reinterpret_cast<unsigned*>(smem_raw + 37 * sizeof(long long));  // bitmap
+    int* cgsm = reinterpret_cast<int*>(seen + ((n + 32) / 32 + 1));  // Cg of every position (the window sums)
     pdl_trigger();  // the sweep's CTAs may launch now (they wait for this grid's completion)
     const int t = blockIdx.x;
     const int32_t* tour = tours + (int64_t)t * n;
@@ -64,7 +71,7 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
         for (int i = tid; i < kSlots; i += nt) slots[(int64_t)t * kSlots + i] = spdp_saa_partial{0, 0, 0, 0, 0, 0};
     if (tid == 0) {
         *cmx = 0;
-        ext[0] = ext[1] = ext[2] = ext[3] = 0;
+        ext[0] = ext[1] = ext[2] = ext[3] = ext[4] = 0;
         if (partial) partial[t] = spdp_saa_partial{0, 0, 0, 0, 0, 0};  // the finish kernel accumulates
     }
     if (validate) {
@@ -142,6 +149,7 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
             e.y = (int)(D + ca0);       // B[n] = D[n] + c_{s_n,0}
         }
         tab[i] = e;
+        cgsm[i] = e.y;
         cgi[i] = e.y;
         cgi[cs + i] = __float_as_int((float)e.y * 0x1p-24f);
         if (i + 1 < n) {
@@ -171,13 +179,17 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
         rowp[i] = demand;
     }
     for (int i = n + tid; i < trow_stride(n); i += nt) trow[i] = n;  // outside the tensor: zeros
-    if (tid == 0) g0[t] = dist[node(0)];
+    if (lo == 0 && hi > 0) {  // (the thread of position 0: its dist row is in L1)
+        const int g = dist[node(0)];
+        g0[t] = g;
+        ext[4] = g;
+    }
     __syncthreads();
-    {  // the largest sum of max(0, Cg) over kU16Check consecutive layers (plane 0 is complete)
+    {  // the largest sum of max(0, Cg) over kU16Check consecutive layers (cgsm is complete)
         int wmax = 0;
         for (int i = lo; i < min(hi, n - 1); ++i) {
             int sum = 0;
-            for (int k = i; k < min(i + kU16Check, n - 1); ++k) sum += max(0, cgi[k]);
+            for (int k = i; k < min(i + kU16Check, n - 1); ++k) sum += max(0, cgsm[k]);
             wmax = max(wmax, min(sum, 1 << 20));
         }
         if (wmax) atomicMax(&ext[2], wmax);
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(1024) tour_prep_kernel(const int32_t* __restri
     if (tid == 0) {  // g0f = (g0 + OFF) / 2^24
         const long long OFF = *dn, cm = *cmx;
         TourInfo ti;
-        ti.g0f_bits = __float_as_int((float)(dist[node(0)] + OFF) * 0x1p-24f);
+        ti.g0f_bits = __float_as_int((float)(ext[4] + OFF) * 0x1p-24f);
         ti.off = (int)(OFF < INT_MAX ? OFF : INT_MAX);
         // g + OFF <= (2n + 1) cmax + OFF and f(n) + OFF <= 2 n cmax + OFF: all below 2^24
         ti.ok = ((2LL * n + 2) * cm + OFF < (1LL << 24)) ? 1 : 0;
@@ -1627,10 +1639,12 @@ static spdp_status split_common(const int32_t* tours, int32_t T, const int32_t* 
 spdp_status launch_tour_prep(const int32_t* tours, int32_t T, int32_t n, const int32_t* dist,
                              const uint16_t* demand, int64_t ld, char* w, const WsLayout& L,
                              spdp_saa_partial* partial, bool zero_slots, bool validate, cudaStream_t st) {
-    const int threads = n >= 2048 ? 1024 : 256;
-    const size_t smem = 36 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
+    const int threads = n <= 128 ? 128 : (n >= 2048 ? 1024 : 256);
+    const size_t smem = tour_prep_smem(n);
     // (the sweep's shared-memory carveout: no L1 / shared reconfiguration between the kernels of a call)
-    if (spdp_status e = kernel_setup((const void*)tour_prep_kernel, -1, 100, 0, 0, nullptr, "tour_prep setup")) return e;
+    if (spdp_status e = kernel_setup((const void*)tour_prep_kernel, (int)tour_prep_smem(SPDP_MAX_N), 100, 0, 0, nullptr,
+                                     "tour_prep setup"))
+        return e;
     tour_prep_kernel<<<T, threads, smem, st>>>(
         tours, n, dist, reinterpret_cast<int2*>(w + L.tabs), reinterpret_cast<int32_t*>(w + L.g0), demand, ld,
         reinterpret_cast<const uint16_t**>(w + L.rowp), reinterpret_cast<TourInfo*>(w + L.tinfo),
@@ -1878,8 +1892,11 @@ extern "C" spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dis
     const uint32_t Qe = (uint32_t)((int64_t)Q > (int64_t)n * 65535 ? (int64_t)n * 65535 : Q);
     spdp_status rc;
     {
-        const int threads = n >= 2048 ? 1024 : 256;
-        const size_t smem = 36 * sizeof(long long) + sizeof(unsigned) * (size_t)((n + 32) / 32 + 1);
+        const int threads = n <= 128 ? 128 : (n >= 2048 ? 1024 : 256);
+        const size_t smem = tour_prep_smem(n);
+        if ((rc = kernel_setup((const void*)tour_prep_kernel, (int)tour_prep_smem(SPDP_MAX_N), 100, 0, 0, nullptr,
+                               "tour_prep setup")))
+            return rc;
         tour_prep_kernel<<<1, threads, smem, st>>>(tour, n, dist, tabs, g0, demand, ld, rowp, tinfo,
                                                    reinterpret_cast<int32_t*>(w + L.cgs),
                                                    reinterpret_cast<int32_t*>(w + L.trow), nullptr, hdr, nullptr, 0);
