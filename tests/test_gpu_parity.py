@@ -278,6 +278,27 @@ def test_split_routes_pred_exact(spdp, name, S):
         assert rc == cost[k]
 
 
+def test_split_routes_wide_windows(spdp):
+    """The warp route kernel with windows far wider than a warp (Q above the whole tour's load: every
+    split point is a candidate of every layer, up to n = 300), plus a collinear instance (many equal
+    values: the tie rule -- the largest p -- decides pred)."""
+    for n, seed, coll in ((300, 91, False), (150, 92, True)):
+        inst = synth.make_instance(n, seed, r=4.0)
+        if coll:  # all customers on a line through the depot: many ties among split points
+            d = np.abs(np.subtract.outer(np.arange(n + 1), np.arange(n + 1))).astype(np.int32)
+            inst = dict(inst, dist=d)
+        Q = int(inst["nominal"].astype(np.int64).sum() * 3)
+        model = synth.demand_model(inst["nominal"], min(Q, 65535), seed=0x5EED00BB + seed)
+        S = 64
+        dem = oracle.gen_demands(model, 0, S, ld=spdp.padded_ld(S))
+        scen = np.array([0, 7, 31, 63], dtype=np.int64)
+        want_cost, want_pred = oracle.split(inst["tour"], inst["dist"], dem, Q, want_pred=True, S=S)
+        cost, pred, nr, ml = spdp.split_routes(to_dev(inst["tour"]), to_dev(inst["dist"]), to_dev(dem), Q,
+                                               torch.from_numpy(scen).cuda(), S=S)
+        assert np.array_equal(cost.cpu().numpy().astype(np.int64), oracle_cost_as_i32(want_cost[scen])), (n, coll)
+        assert np.array_equal(pred.cpu().numpy(), want_pred[scen]), (n, coll)
+
+
 def test_split_routes_large_n_thread_kernel(spdp):
     """n above the warp kernel's shared-memory limit (1024): the thread-per-scenario route kernel;
     pred bit-exact against the oracle (ties -> largest p), route count and max load consistent."""
