@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(128) irp_lazy_kernel(const uint8_t* __restrict
         const int64_t s = live ? s0 + lane : S - 1;
         const IrpCust p = cust[m];
         const int U = p.U, B = p.I0 + 1;
+        const int32_t* const aend = A + B * 32;  // (one past the last ring slot of this lane)
         __syncwarp();  // (the previous task's reads of the tile are done)
         stage(task, dtw);
         cp_async_commit();
@@ -298,13 +299,15 @@ __global__ void __launch_bounds__(128) irp_lazy_kernel(const uint8_t* __restrict
             const int d = dt[t * 32];
             const bool deliver = t < 64 ? ((vmask >> t) & 1ull) != 0ull : (p.X > 0 && visit[(int64_t)m * H + t] != 0);
             if (deliver) {  // (warp-uniform)
-                int32_t R = kIrpInf;
-                int x = off;
+                int32_t R = kIrpInf, u = K;  // u = alpha y + K
+                int32_t* ap = A + off * 32;  // slot (y + off) mod B, a pointer stepping with wrap
 #pragma unroll 1
                 for (int y = 0; y <= E; ++y) {
-                    R = min(R + p.c, A[x * 32] + alpha * y + K);
-                    A[x * 32] = R >= kReal ? kIrpInf : R;
-                    x = (x + 1 == B) ? 0 : x + 1;
+                    R = min(R + p.c, *ap + u);
+                    *ap = R >= kReal ? kIrpInf : R;
+                    u += alpha;
+                    ap += 32;
+                    if (ap == aend) ap = A;
                 }
                 if (E < U && R < kReal) {  // W[y] = W[E] + c (y - E) for y in (E, U]
                     Ta = R - p.c * E;
@@ -318,12 +321,20 @@ __global__ void __launch_bounds__(128) irp_lazy_kernel(const uint8_t* __restrict
             }
             // demand d: V'[0] = b d + min_{y <= min(d, U)} (V[y] - b y); V'[J] = V[J + d] + h J
             int32_t m0 = kIrpInf;
-            const int ylim = d < E ? d : E;
-            int x = off;
+            {
+                const int ylim = d < E ? d : E;
+                const int32_t du = alpha - p.b;
+                int32_t u = K;  // (alpha - b) y + K
+                const int32_t* ap = A + off * 32;
+                int y = 0;
 #pragma unroll 1
-            for (int y = 0; y <= ylim; ++y) {
-                m0 = min(m0, A[x * 32] + (alpha - p.b) * y + K);
-                x = (x + 1 == B) ? 0 : x + 1;
+                for (; y + 1 <= ylim; y += 2) {  // two states per trip (the loop is per lane: its length is)
+                    const int32_t* ap1 = ap + 32 == aend ? A : ap + 32;
+                    m0 = min(m0, min(*ap + u, *ap1 + u + du));
+                    u += 2 * du;
+                    ap = ap1 + 32 == aend ? A : ap1 + 32;
+                }
+                if (y <= ylim) m0 = min(m0, *ap + u);
             }
             if (d > E && F > E) {  // the tail's part of the minimum: an affine function, at its ends
                 const int y2 = d < F ? d : F;
