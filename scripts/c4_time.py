@@ -3,7 +3,7 @@ import os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth, bench_config, paper_2511_18022_b200 as spdp
 dev = torch.device("cuda")
-cfg = synth.config_instance("C4"); inst = cfg["inst"]
+cfg = synth.config_instance("C4", S=int(sys.argv[1]) if len(sys.argv) > 1 else None); inst = cfg["inst"]
 d = spdp.gen_demands(cfg["model"], 0, cfg["S"], device=dev)
 tour = torch.from_numpy(inst["tour"]).to(dev); dist = torch.from_numpy(inst["dist"]).to(dev)
 part = torch.zeros(6, dtype=torch.int64, device=dev)
