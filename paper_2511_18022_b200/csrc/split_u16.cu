@@ -121,6 +121,26 @@ __device__ __forceinline__ uint32_t key_of(uint32_t G, uint32_t d) {
     return k;
 }
 
+// g[r] for a warp-uniform runtime r < W, as a switch (an indexed branch, not W compare-selects)
+template <int W>
+__device__ __forceinline__ uint32_t ring_slot(const uint32_t (&g)[W], const int r) {
+    switch (r) {
+#define SPDP_RING_CASE(i) \
+    case i:               \
+        if constexpr (i < W) return g[i]; \
+        break;
+        SPDP_RING_CASE(0) SPDP_RING_CASE(1) SPDP_RING_CASE(2) SPDP_RING_CASE(3) SPDP_RING_CASE(4) SPDP_RING_CASE(5)
+        SPDP_RING_CASE(6) SPDP_RING_CASE(7) SPDP_RING_CASE(8) SPDP_RING_CASE(9) SPDP_RING_CASE(10) SPDP_RING_CASE(11)
+        SPDP_RING_CASE(12) SPDP_RING_CASE(13) SPDP_RING_CASE(14) SPDP_RING_CASE(15) SPDP_RING_CASE(16)
+        SPDP_RING_CASE(17) SPDP_RING_CASE(18) SPDP_RING_CASE(19) SPDP_RING_CASE(20) SPDP_RING_CASE(21)
+        SPDP_RING_CASE(22) SPDP_RING_CASE(23) SPDP_RING_CASE(24) SPDP_RING_CASE(25) SPDP_RING_CASE(26)
+        SPDP_RING_CASE(27) SPDP_RING_CASE(28) SPDP_RING_CASE(29) SPDP_RING_CASE(30) SPDP_RING_CASE(31)
+#undef SPDP_RING_CASE
+        default: break;
+    }
+    return 0u;
+}
+
 // Minimum of N packed u16 pairs with ceil((N - 1) / 2) 3-input mins (VIMNMX3.U16x2).
 template <int N>
 __device__ __forceinline__ uint32_t umin_tree(const uint32_t* v) {
@@ -556,12 +576,11 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
         const bool ok = tc->ok != 0;
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
-            uint32_t val = gprev[k];  // rem == 0: the last layer computed position n
-            if (rem != 0) {           // else position n sits in ring slot rem (pushed by the first padded layer)
-#pragma unroll
-                for (int a = 0; a < W; ++a)
-                    if (a == rem) val = G[k][a];
-            }
+            // rem == 0: the last layer computed position n; else position n sits in ring slot rem
+            // (pushed by the first padded layer)
+            const uint32_t val = rem == 0 ? gprev[k] : ring_slot<W>(G[k], rem);
+            int dnf = 0, dni = 0;  // this pair's SAA terms, added to the lane's sums in one update
+            long long dsum = 0, dlo = 0, dhi = 0;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int64_t s = s0 + 64 * k + 2 * lane + h;
@@ -576,18 +595,25 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
                 if (deferred) ovf_list[atomicAdd(ovf_count, 1u)] = ((unsigned long long)t << 40) | (unsigned long long)s;
                 if (cost && live && !deferred) cost[(int64_t)t * S + s] = bad ? SPDP_INFEASIBLE : fval;
                 if (live && !deferred) {
-                    LanePart pa = *accp;
                     if (bad) {
-                        pa.ni += 1;
+                        dni += 1;
                     } else {
                         const unsigned long long sq = (unsigned long long)fval * (unsigned long long)fval;
-                        pa.nf += 1;
-                        pa.sum += fval;
-                        pa.sqlo += (long long)(sq & 0xffffffffull);
-                        pa.sqhi += (long long)(sq >> 32);
+                        dnf += 1;
+                        dsum += fval;
+                        dlo += (long long)(sq & 0xffffffffull);
+                        dhi += (long long)(sq >> 32);
                     }
-                    *accp = pa;
                 }
+            }
+            if (dnf + dni > 0) {
+                LanePart pa = *accp;
+                pa.nf += dnf;
+                pa.ni += dni;
+                pa.sum += dsum;
+                pa.sqlo += dlo;
+                pa.sqhi += dhi;
+                *accp = pa;
             }
         }
     }
