@@ -258,8 +258,10 @@ SPDP_API spdp_status spdp_split_eval_penalized(const int32_t* tour, const int32_
  *   maxload [K] int32 (may be NULL): largest route load (<= Q: the capacity
  *           feasibility of every returned route, checked on the device)
  * Walking pred from i = n back to 0 lists the routes (tour positions
- * pred[i]..i-1, 0-based).  One thread per scenario (latency-oriented: for
- * inspecting a few scenarios, e.g. the worst ones of an SAA sample).
+ * pred[i]..i-1, 0-based).  A warp per scenario for n <= 1024 (window start by ballot,
+ * minimum and its largest argument by warp reductions, P and g in shared memory), one
+ * thread per scenario above (latency-oriented: for inspecting a few thousand scenarios,
+ * e.g. the worst ones of an SAA sample).  Ties go to the largest split point.
  * ws: spdp_routes_workspace_bytes(n, K) bytes of device memory. */
 SPDP_API size_t spdp_routes_workspace_bytes(int32_t n, int32_t K);
 SPDP_API spdp_status spdp_split_routes(const int32_t* tour, const int32_t* dist, int32_t n,
