@@ -381,6 +381,25 @@ def test_irp_affine_tail_stress(spdp):
         assert np.array_equal(cost.cpu().numpy(), want), "trial %d" % trial
 
 
+def test_irp_long_horizon(spdp):
+    """H above 64 periods: the affine-tail kernel's visit pattern beyond its 64-bit ballot mask (read
+    per period), long collapsed phases, and deliveries late in the horizon -- against the oracle."""
+    rng = np.random.default_rng(37)
+    for trial in range(3):
+        H, M = [70, 96, 65][trial], 2
+        visit = (rng.random((M, H)) < [0.3, 0.6, 0.9][trial]).astype(np.uint8)
+        visit[:, -3:] = 1  # deliveries beyond t = 64
+        cust = np.array([[int(rng.integers(1, 60)), 0, 0, 1, 7, 2] for _ in range(M)], dtype=np.int32)
+        for m in range(M):
+            cust[m, 1] = cust[m, 0] + int(rng.integers(0, 5))  # X >= U: the prefix band
+            cust[m, 2] = int(rng.integers(0, cust[m, 0] + 1))
+        S = 97
+        dem = rng.integers(0, 12, size=(H * M, 104)).astype(np.uint16)
+        want = oracle.irp(H, M, visit, cust, dem, S=S)
+        cost, _ = spdp.irp_dp(visit, cust, to_dev(dem), H, M, S=S, want_partial=False)
+        assert np.array_equal(cost.cpu().numpy(), want), "trial %d" % trial
+
+
 # ------------------------------------------------------------------ f2 penalized split
 @pytest.mark.parametrize("name,S,lam", [("C1", 100, 5), ("C2", 20_011, 10), ("C2", 3_001, 0), ("C3", 2_003, 50),
                                         ("C2", 2_003, 10 ** 6)])
