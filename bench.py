@@ -134,6 +134,12 @@ def ncu_traffic(config_name: str):
         return None
 
 
+def workload_str(name, n, Q, S_glob, T):
+    """The workload both arms name in config.workload (the BASELINE configuration)."""
+    return "%s: X-n%d-shaped CVRPSD, n=%d, Q=%d, %d correlated-demand scenarios in all (cv=0.3, rho=0.5), %d giant " \
+           "tour%s" % (name, n + 1, n, Q, S_glob, T, "s" if T > 1 else "")
+
+
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args):
     """The reference arm of this tier: the CPU oracle (plain C, OpenMP over scenarios) on the
@@ -168,8 +174,10 @@ def run_reference(args):
         S_ref, S_full, args.config)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": args.config, "n": cfg["n"], "S_per_step": S_ref, "Q": cfg["Q"]},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": workload_str(args.config, cfg["n"], cfg["Q"], S_full, cfg["T"]) +
+                                   " (the oracle on the host cores; a bounded sample per step)",
+                       "n": cfg["n"], "S_per_step": S_ref, "Q": cfg["Q"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -485,9 +493,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": "%s: X-n%d-shaped CVRPSD, n=%d, Q=%d, %d correlated-demand scenarios in all "
-                                   "(%d per GPU; cv=0.3, rho=0.5), %d giant tour%s" % (
-                                       args.config, n + 1, n, Q, S_glob, S_loc, T, "s" if T > 1 else ""),
+            "config": {"workload": workload_str(args.config, n, Q, S_glob, T) + " (%d per GPU)" % S_loc,
                        "n": n, "S_per_gpu": S_loc, "S_global": S_glob, "T": T, "window_hint": hint,
                        "mean_window_hint": mean_w,
                        "scenario_order": ("by total demand within segments of 65536 (spdp_order_scenarios): a layout "
