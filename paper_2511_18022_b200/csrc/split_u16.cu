@@ -54,9 +54,16 @@
 
 namespace spdp {
 
-constexpr int kU16Cons = 4;                       // consumer warps per CTA, one tile of NP * kU16Box scenarios
+#ifndef SPDP_U16_CONS
+#define SPDP_U16_CONS 4
+#define SPDP_U16_CONS_PER_BOX 4
+#endif
+constexpr int kU16Cons = SPDP_U16_CONS;           // consumer warps per CTA, one tile of NP * 64 kU16Cons scenarios
 constexpr int kU16Threads = 32 * (kU16Cons + 1);  // + 1 producer warp
-constexpr int kU16Box = kU16Cons * 64;            // columns of one TMA box (256 scenarios, 512 B per row)
+constexpr int kU16ConsPerBox = SPDP_U16_CONS_PER_BOX;  // consumer warps per TMA box
+constexpr int kU16Box = kU16ConsPerBox * 64;           // columns of one TMA box (256 scenarios, 512 B per row)
+constexpr int kU16BoxesPerTile = kU16Cons / kU16ConsPerBox;
+static_assert(kU16Cons % kU16ConsPerBox == 0 && kU16Box <= 256, "TMA box: at most 256 columns");
 constexpr uint32_t kGuard = 0x80008000u;
 
 // Debug timeline (spdp_debug_timeline): when set, lane 0 of every consumer warp appends one record
@@ -89,11 +96,12 @@ template <int W, int NP, int NST>
 struct U16Cfg {
     static constexpr int NS = NST;                                          // stages
     static constexpr int kMaxReg = NP == 1 ? (W <= 24 ? 96 : 128) : 128;    // registers: 4 / 3 CTAs per SM
-    static constexpr int kTile = NP * kU16Box;                              // scenarios per tile
+    static constexpr int kTile = NP * kU16Cons * 64;                       // scenarios per tile
     static constexpr int kWarp = NP * 64;                                   // scenarios per consumer warp
     static constexpr int kRowBytes = kU16Box * (int)sizeof(uint16_t);      // 512 B (one box row)
     static constexpr int kBoxBytes = W * kRowBytes;                         // W rows of one box
-    static constexpr int kRowsBytes = NP * kBoxBytes;                       // all boxes
+    static constexpr int kBoxes = NP * kU16BoxesPerTile;                   // boxes per tile
+    static constexpr int kRowsBytes = kBoxes * kBoxBytes;                   // all boxes
     static constexpr int kCgOff = kRowsBytes;                               // W Cg pairs
     static constexpr int kHdrOff = kRowsBytes + W * (int)sizeof(int32_t);   // {tour, block, chunk, 0}
     static constexpr int kStageBytes = (kHdrOff + 16 + 127) / 128 * 128;    // (TMA: 128-B aligned)
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
                     const int r2 = __shfl_sync(kFull, myrow[k], 4 * g + 2), r3 = __shfl_sync(kFull, myrow[k], 4 * g + 3);
                     if (lane == 0)
 #pragma unroll
-                        for (int h = 0; h < NP; ++h)
+                        for (int h = 0; h < Cfg::kBoxes; ++h)
                             tma_gather4(sb + h * Cfg::kBoxBytes + g * 4 * Cfg::kRowBytes, &dmap, b * Cfg::kTile + h * kU16Box,
                                         r0, r1, r2, r3, &full[k]);
                 }
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
 #pragma unroll
                 for (int g = 0; g < W / 4; ++g)
 #pragma unroll
-                    for (int h = 0; h < NP; ++h)
+                    for (int h = 0; h < Cfg::kBoxes; ++h)
                         tma_gather4(sb + h * Cfg::kBoxBytes + g * 4 * Cfg::kRowBytes, &dmap, b * Cfg::kTile + h * kU16Box,
                                     rq[g].x, rq[g].y, rq[g].z, rq[g].w, fb);
                 bulk_g2s_plain(sb + Cfg::kCgOff, cgs + (int64_t)t * kCgPlanes * cgs_stride + 2 * cgs_stride + r0, W * 4,
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
         const int q = NP * wid + k;
-        boff[k] = (q >> 2) * Cfg::kBoxBytes + (q & 3) * 128 + 4 * lane;
+        boff[k] = (q / kU16ConsPerBox) * Cfg::kBoxBytes + (q % kU16ConsPerBox) * 128 + 4 * lane;
     }
 
     uint32_t G[NP][W], Y[NP][W];
