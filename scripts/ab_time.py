@@ -10,7 +10,7 @@ for name in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["C2", "C3"]):
     d = spdp.gen_demands(cfg["model"], 0, cfg["S"], device=dev)
     d, _ = spdp.order_scenarios(d, S=cfg["S"])
     tours = torch.from_numpy(np.ascontiguousarray(cfg["tours"])).to(dev); dist = torch.from_numpy(inst["dist"]).to(dev)
-    h = bench_config.HINT[name]; mw = int(os.environ.get("AB_MW_" + name, bench_config.MEAN_ORDERED[name]))
+    h = int(os.environ.get("AB_HINT_" + name, bench_config.HINT[name])); mw = int(os.environ.get("AB_MW_" + name, bench_config.MEAN_ORDERED[name]))
     part = torch.zeros(cfg["T"], 6, dtype=torch.int64, device=dev)
     fn = lambda: spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], want_cost=False, window_hint=h,
                                        mean_window=mw, partial=part)

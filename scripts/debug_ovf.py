@@ -18,6 +18,6 @@ for name in cfgs:
         for algo in algos:
             spdp.split_eval_batch(tours, dist, d, inst["Q"], S=cfg["S"], window_hint=h, want_cost=False, algo=algo)
             torch.cuda.synchronize()
-            ws = [v for k, v in spdp._WS.items() if k[1] == "split"][0]
+            ws = [v for k, v in spdp._WS.items() if k[-1] == "split"][0]
             hdr = ws[:16].cpu().numpy().view(np.uint32)
             print(name, "hint", h, algo, "ovf_count", hdr[0], "of", cfg["S"] * cfg["T"], flush=True)
