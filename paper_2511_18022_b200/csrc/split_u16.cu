@@ -199,8 +199,9 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
     if constexpr (TL) {
         if (tid == 0) tl_record(blockIdx.x * kU16Cons, 0xfffffff0u, gtimer());  // CTA start
     }
-    // (no early pdl_trigger for split_finish_kernel: its CTAs then sit resident through the whole sweep --
-    // measured +0.4 us per C2 step on one box, 3 runs each)
+    // (the dependent launch of split_finish_kernel is triggered by each producer once every tile is
+    // claimed -- its CTAs then land on SMs the ramp-down frees: -0.6 us per C2 step, 3 interleaved
+    // runs; a trigger at kernel start kept them resident through the whole sweep: +0.4 us)
     // (tables, counters and partial slots come from tour_prep_kernel: every role waits for it with
     // pdl_wait() before its first read of them; the demand matrix and the tours are inputs, complete
     // before tour_prep_kernel -- a plain launch -- started)
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(kU16Threads) __maxnreg__((U16Cfg<W, NP, NST>::
             if (lane == 0) *reinterpret_cast<int4*>(sb + Cfg::kHdrOff) = make_int4(t, b, c, 0);
             if (__any_sync(kFull, t < 0)) {  // no tiles left: an arrival without data tells the consumers to stop
                 if (lane == 0) mbar_arrive(fb);
+                pdl_trigger();  // (every tile is claimed: split_finish_kernel may start launching)
                 break;
             }
             if (lane == 0) {
