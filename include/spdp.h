@@ -77,7 +77,7 @@ typedef enum {
 #define SPDP_F_SWEEP_F32   4u       /* register ring, exact integer-valued fp32, FMA-pipe masking */
 #define SPDP_F_SWEEP_DEQUE 8u       /* monotone-deque sliding-window minimum, O(1) amortised */
 #define SPDP_F_SWEEP_U16 128u       /* register ring, two scenarios per lane in packed u16 halves
-                                       (windows 9..32, 12 (Q + 1) <= 2^15; else as the default) */
+                                       (windows 9..32, 14 (Q + 1) <= 2^15; else as the default) */
 #define SPDP_F_SCRATCH_GLOBAL 16u  /* spdp_split_eval_limits: every scenario through the general kernel
                                        with its DP arrays in the workspace (same results; tests both paths) */
 #define SPDP_F_NBR_SMEM 32u        /* spdp_split_eval_neighbours: the shared-memory-ring kernel instead of

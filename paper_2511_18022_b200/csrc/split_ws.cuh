@@ -21,7 +21,7 @@ struct TourInfo {
 };
 
 // Range-check interval of the packed-u16 sweep (layers); tour_prep_kernel's thr16 assumes it.
-constexpr int kU16Check = 8;
+constexpr int kU16Check = 12;
 
 constexpr int kTabPad = 64;       // padding rows after each tour table
 constexpr int kSlots = 32;  // SAA partial slots per tour (spread the sweep's atomics)
