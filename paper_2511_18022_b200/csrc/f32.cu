@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kF32Threads) split_f32_tma_kernel(
                     cs = 0;
                     ++cr;
                 }
-                if (__all_sync(kFull, ++c >= nchunks)) break;
+                if (++c >= nchunks) break;
                 sb = smem_raw + (size_t)cs * Cfg::kStageBytes;
                 mbar_wait_warp(&full[cs], cr & 1u);
             }

@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(kSweepThreads, F2Cfg<W, MB>::kMinBlocks)
             cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
             cp_async_wait<NS - 1>();  // the next chunk (or the next tile's first chunk) has landed
             __syncwarp();
-            if (__all_sync(kFull, ++c >= nchunks)) break;
+            if (++c >= nchunks) break;
         }
         if (rem != 0) {  // f(n) sits in the slot of position n (pushed by the first padded layer)
 #pragma unroll
@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(kSweepThreads, (W <= 24 ? 3 : (W <= 32 ? 2 : 1
             cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
             cp_async_wait<NS - 1>();
             __syncwarp();
-            if (__all_sync(kFull, ++c >= nchunks)) break;
+            if (++c >= nchunks) break;
         }
         if (rem != 0) {  // f(n) sits in the slot of position n (pushed by the first padded layer)
 #pragma unroll
@@ -904,7 +904,7 @@ __global__ void __launch_bounds__(kSweepThreads, 4)
             cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
             cp_async_wait<NS - 1>();
             __syncwarp();
-            if (__all_sync(kFull, ++c >= nchunks)) break;
+            if (++c >= nchunks) break;
         }
         const bool bad = qmax > Q;
         const int64_t s = s0 + col;
@@ -1044,7 +1044,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3)
             cstage = (cstage + 1 == NS) ? 0 : cstage + 1;
             cp_async_wait<NS - 1>();
             __syncwarp();
-            if (__all_sync(kFull, ++c >= nchunks)) break;
+            if (++c >= nchunks) break;
         }
         if (rem != 0) {  // f(n): the slot of position n (pushed by the first padded layer)
 #pragma unroll
