@@ -852,15 +852,11 @@ __global__ void __launch_bounds__(kSweepThreads, 4)
             const uint32_t Pn = P + min(q, Q);
             const uint32_t ynew = P + Q;
             // push p = L with g(p) = gprev: pop dominated points (g >= gprev) from the back
-            for (;;) {
-                const bool pop = bg >= gprev;
-                if (!__any_sync(kFull, pop)) break;
-                const uint32_t ntl = tl8 - (pop ? 256u : 0u);
+            while (bg >= gprev) {  // (per lane: no vote)
+                const uint32_t ntl = tl8 - 256u;
                 const int nb = lds_s32(dqa + ((ntl - 256u) & kMask));
-                if (pop) {
-                    tl8 = ntl;
-                    bg = (ntl != hd8) ? nb : INT_MIN;
-                }
+                tl8 = ntl;
+                bg = (ntl != hd8) ? nb : INT_MIN;
             }
             ovf |= (tl8 - hd8 == (uint32_t)D * 256u);  // capacity exceeded: the overflow path
             sts_s32x2(dqa + (tl8 & kMask), gprev, (int)ynew);
@@ -873,16 +869,12 @@ __global__ void __launch_bounds__(kSweepThreads, 4)
             // pop split points that left the window (Y < P'(L+1)) from the front.  (No size test: the
             // point just pushed, p = L with Y = P'(L) + Q >= P'(L) + min(q, Q) = P'(L+1), stays in
             // the window, so it stops the loop.)
-            for (;;) {
-                const bool pop = fy < Pn;
-                if (!__any_sync(kFull, pop)) break;
-                const uint32_t nhd = hd8 + (pop ? 256u : 0u);
+            while (fy < Pn) {  // (per lane: no vote)
+                const uint32_t nhd = hd8 + 256u;
                 const int2 e = lds_s32x2(dqa + (nhd & kMask));
-                if (pop) {
-                    hd8 = nhd;
-                    fg = e.x;
-                    fy = (uint32_t)e.y;
-                }
+                hd8 = nhd;
+                fg = e.x;
+                fy = (uint32_t)e.y;
             }
             gprev = fg + cg;  // the front is the window minimum
             P = Pn;
